@@ -1,0 +1,173 @@
+/*
+ * boxscreen_b200.h -- C ABI of the B200-native screened box-constrained
+ * least-squares iteration (drop-in for the hot path of the reference
+ * `boxscreen` package, arXiv 2202.07258).
+ *
+ * The reference has no FFI: its solver dispatch is the string if/elif at
+ * /root/reference/pkg/src/boxscreen/driver.py:411-418 over the kinds listed at
+ * solvers.py:17, operating on the Workspace state contract of
+ * solvers.py:48-69.  Every entry point below replaces one reference symbol;
+ * the symbol is cited beside it.  A Python binding of exactly these entry
+ * points lives in paper_2202_07258_b200/_native.py (ctypes); INTEGRATION.md
+ * shows how the reference's own driver would bind them.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers unless the name ends in _host.
+ *    Matrices are column-major with a leading dimension `lda >= m`; the column
+ *    stride `lda * sizeof(elem)` and the base pointer must be 16-byte aligned
+ *    (the bulk-copy engine streams whole columns).
+ *  - Element type is fp64 (BX_F64) or fp32 (BX_F32) for A, y, bounds, t and
+ *    every per-row / per-column vector; scalars (objectives, gaps, steps) are
+ *    always fp64.
+ *  - Upper bounds may be +inf (NNLS / mixed); lower bounds must be finite.
+ *  - Every function returns a bx_status.  Nonzero codes map 1:1 onto the
+ *    reference exception classes of errors.py (listed per code).  The message
+ *    of the last failure is available from bx_last_error().
+ *  - One context = one solve = one CUDA stream; no global mutable state
+ *    (solves are single-owner and reentrant).
+ *  - Device memory is owned by the caller: bx_workspace_bytes() says how much
+ *    scratch the context needs, the caller allocates it (PyTorch in the Python
+ *    front end) and passes it to bx_ctx_create().  The context never writes A.
+ */
+#ifndef BOXSCREEN_B200_H
+#define BOXSCREEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BX_OK = 0,
+  BX_ERR_DIMENSION = 1,            /* errors.py:8   DimensionMismatch          */
+  BX_ERR_ZERO_COLUMN = 2,          /* errors.py:69  ZeroColumn                 */
+  BX_ERR_NO_INTERIOR = 3,          /* errors.py:29  NoInteriorPoint            */
+  BX_ERR_STEP_TOO_LARGE = 4,       /* errors.py:51  StepSizeTooLarge           */
+  BX_ERR_INTERNAL_CONSISTENCY = 5, /* errors.py:43  InternalConsistency        */
+  BX_ERR_NEGATIVE_GAP = 6,         /* errors.py:39  NegativeGap                */
+  BX_ERR_INVALID_ARGUMENT = 7,     /* ValueError (model.py:67-76, solvers.py:29-35) */
+  BX_ERR_CUDA = 8,                 /* CUDA runtime failure (no reference analogue) */
+  BX_ERR_UNSUPPORTED = 9,          /* shape outside the compiled kernel envelope   */
+  BX_ERR_WORKSPACE = 10,           /* caller workspace too small / misaligned      */
+  BX_ERR_NOT_INTERIOR = 11         /* errors.py:25  NotInterior                */
+} bx_status;
+
+typedef enum { BX_F64 = 0, BX_F32 = 1 } bx_dtype;
+
+/* solver kinds: solvers.py:17 ("pg", "cd"); "apg" is the FISTA extension of
+ * BASELINE.json configs 3 and 5 (not in the reference). */
+typedef enum { BX_PG = 0, BX_CD = 1, BX_APG = 2 } bx_kind;
+
+typedef struct bx_ctx bx_ctx;
+
+/* SolverConfig (solvers.py:20-35) + the solve() flags (driver.py:371). */
+typedef struct {
+  int32_t kind;          /* bx_kind                                              */
+  int32_t inner_passes;  /* >= 1                                                 */
+  int64_t max_rounds;    /* <= 0: reference default (10**6, driver.py:390)       */
+  double gap_tol;        /* > 0                                                  */
+  double step_size;      /* <= 0 or NaN: auto (power iteration, solvers.py:89)   */
+  int32_t power_iters;   /* default 50                                           */
+  int32_t screening;     /* 0/1                                                  */
+  double alpha;          /* loss strong-concavity constant (model.py:40) = 1     */
+  double slack_scale;    /* driver.py:219: 1e-12 for fp64                        */
+} bx_solve_cfg;
+
+/* TraceRecord (driver.py:268-278) plus the dual-point internals. */
+typedef struct {
+  int64_t round;
+  double elapsed;
+  double primal, dual, gap;
+  int64_t preserved_count;
+  int64_t newly_screened_lower, newly_screened_upper;
+  double eps, radius, step;
+  double certified_gap;  /* NaN when not evaluated this round                   */
+} bx_trace_rec;
+
+typedef struct {
+  int64_t rounds;
+  int32_t converged;
+  double gap;            /* certified gap when converged, else last reduced gap */
+  int64_t n_sat_lower, n_sat_upper;
+  int64_t iterations;    /* primal passes (PG/APG steps or CD sweeps)          */
+  double step;
+  double sigma;          /* last power-iteration estimate                      */
+  int64_t kernel_launches;
+} bx_solve_out;
+
+/* Host callback producing the power-iteration start vector of length k:
+ * the Python front end passes numpy default_rng(seed).standard_normal(k),
+ * exactly solvers.py:75-76.  NULL selects an internal (non-numpy) generator. */
+typedef void (*bx_start_vector_fn)(int64_t k, int64_t seed, double* out_host, void* user);
+
+/* ---- context ------------------------------------------------------------ */
+
+/* bytes of device scratch a context of this shape needs */
+size_t bx_workspace_bytes(int64_t m, int64_t n, int32_t dtype);
+
+/* Problem (model.py:47-99) + ScreeningState (screening.py:221-230) +
+ * TranslationVector (duality.py:339-357).  `t` may be NULL: neg-ones
+ * (duality.py:372-373).  Validates zero columns (ZeroColumn) and, when some
+ * upper bound is infinite, strict interiority (NoInteriorPoint). */
+int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype,
+                  const void* a, int64_t lda, const void* y,
+                  const void* lower, const void* upper, const void* t,
+                  void* workspace, size_t workspace_bytes, void* cuda_stream);
+int bx_ctx_destroy(bx_ctx* ctx);
+const char* bx_last_error(const bx_ctx* ctx);
+
+/* ---- fine-grained entry points (Workspace contract, solvers.py:48-137) ---- */
+
+/* column norms ||a_j|| (model.py:89-92), length n, element type */
+int bx_col_norms(bx_ctx* ctx, void* out);
+/* A't (duality.py:350), length n, element type */
+int bx_att(bx_ctx* ctx, void* out);
+/* spectral_norm_estimate on the preserved columns (solvers.py:72-86) */
+int bx_power_iter(bx_ctx* ctx, int32_t iters, const double* v0_host, double* sigma_out);
+/* reset the primal point to clip(0, l, u) and rebuild the workspace
+ * (driver.py:389, solvers.py:54-65) */
+int bx_reset(bx_ctx* ctx);
+/* `passes` primal passes of the given kind on the preserved set:
+ * pg_step (solvers.py:101-116), cd_sweep (:119-137), FISTA */
+int bx_primal_passes(bx_ctx* ctx, int32_t kind, double eta, int32_t passes);
+/* dual point + reduced gap + (optionally) the sphere test for the current
+ * iterate: driver.py:423-441 and 453-461.  out_scalars_host receives
+ * {primal, dual, gap, eps, radius, slack, n_new_lower, n_new_upper}. */
+int bx_dual_screen(bx_ctx* ctx, int32_t screening, double slack_scale, double* out_scalars_host);
+/* apply_screening (screening.py:72-94) + Workspace.refresh (solvers.py:54-65):
+ * snaps screened x to bounds, updates z, compacts A and the per-column state
+ * (ballot/prefix-sum), recomputes the residual. */
+int bx_compact(bx_ctx* ctx);
+/* _certified_gap on the full problem (driver.py:352-357 ->
+ * duality.py:457-507); out_host = {gap, primal, dual, eps} */
+int bx_certified_gap(bx_ctx* ctx, double* out_host);
+/* preserved count, and the preserved original indices (int32, device) */
+int64_t bx_preserved_count(const bx_ctx* ctx);
+
+/* ---- the Algorithm-1 loop (driver.py:371-496) ---------------------------- */
+int bx_solve(bx_ctx* ctx, const bx_solve_cfg* cfg, bx_start_vector_fn start_fn,
+             void* start_user, bx_trace_rec* trace_host, int64_t trace_cap,
+             bx_solve_out* out_host);
+
+/* final state (SolveResult, driver.py:281-290): x (n, element type), theta
+ * (m, element type), sat_lower / sat_upper (int64, in screening order).  Any
+ * pointer may be NULL.  Device pointers. */
+int bx_get_state(bx_ctx* ctx, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper);
+
+/* ---- multi-GPU column sharding ---------------------------- */
+/* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller */
+int bx_nccl_unique_id(unsigned char* id_out_host);
+/* attach a communicator: this context holds global columns
+ * [col_offset, col_offset + n) of an n_global-column problem */
+int bx_ctx_set_comm(bx_ctx* ctx, const unsigned char* id_host, int32_t rank,
+                    int32_t nranks, int64_t col_offset, int64_t n_global);
+
+/* ---- batched many-RHS APG (BASELINE config 5) ----------------------------- */
+size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BOXSCREEN_B200_H */

@@ -1,0 +1,988 @@
+// bx_core.cu -- context, Algorithm-1 round loop and the C ABI
+// (include/boxscreen_b200.h).  Host-side C++; every O(m k) operation is one of
+// the kernels of bx_kernels.cuh launched on the context's stream.
+//
+// Reference mapping (file:line in /root/reference/pkg/src/boxscreen):
+//   bx_ctx_create     Problem (model.py:55-87), ScreeningState (screening.py:221-230),
+//                     TranslationVector (duality.py:346-357)
+//   refresh()         Workspace.refresh (solvers.py:54-65)
+//   primal_passes()   pg_step (solvers.py:101-116), cd_sweep (solvers.py:119-137),
+//                     FISTA extension
+//   dual_screen()     driver.py:423-441 (dual point, reduced dual, clamp_gap) and
+//                     driver.py:453-461 (radius, slack, safe_screen_test)
+//   compact()         apply_screening (screening.py:72-94) + refresh + step
+//                     re-estimate (driver.py:462-475)
+//   certified()       _certified_gap (driver.py:352-357)
+//   bx_solve          solve (driver.py:371-496)
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/boxscreen_b200.h"
+#include "bx_kernels.cuh"
+
+using namespace bx;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (torch's bundled libnccl.so.2) so the library has
+// no link-time dependency; only the symbols the column-sharded path uses.
+// ---------------------------------------------------------------------------
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int (*nccl_get_id_fn)(ncclUniqueId*);
+typedef int (*nccl_init_rank_fn)(ncclComm_t*, int, ncclUniqueId, int);
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*nccl_destroy_fn)(ncclComm_t);
+typedef const char* (*nccl_errstr_fn)(int);
+enum { ncclFloat32 = 7, ncclFloat64 = 8, ncclInt64 = 4, ncclSum = 0, ncclMax = 2 };
+
+struct Nccl {
+  void* h = nullptr;
+  nccl_get_id_fn get_id = nullptr;
+  nccl_init_rank_fn init_rank = nullptr;
+  nccl_allreduce_fn allreduce = nullptr;
+  nccl_destroy_fn destroy = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    get_id = (nccl_get_id_fn)dlsym(h, "ncclGetUniqueId");
+    init_rank = (nccl_init_rank_fn)dlsym(h, "ncclCommInitRank");
+    allreduce = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+    destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
+    errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
+    return get_id && init_rank && allreduce && destroy;
+  }
+};
+Nccl g_nccl;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// the context
+// ---------------------------------------------------------------------------
+struct bx_ctx {
+  int64_t m = 0, n = 0, mp = 0;  // rows, columns, padded rows
+  int dtype = BX_F64;
+  size_t esz = 8;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  int Gmax = 148;
+  size_t smem_cap = 0;
+
+  const void* A = nullptr;  // original matrix (never written)
+  int64_t lda = 0;
+  void* Aact = nullptr;  // compacted preserved columns
+  int64_t ldact = 0;
+  bool act_is_orig = true;  // before the first compaction the act view is A itself
+
+  // per-row vectors (mp elements)
+  void *y = nullptr, *t = nullptr, *negy = nullptr, *z = nullptr, *z2 = nullptr, *off = nullptr, *tgt = nullptr;
+  void *r = nullptr, *rprev = nullptr, *rc = nullptr, *theta = nullptr, *thetac = nullptr, *u = nullptr;
+  // per-column state (ping-pong for compaction)
+  int cur = 0;
+  int32_t* idx[2] = {nullptr, nullptr};
+  void *x[2] = {}, *xprev[2] = {}, *lo[2] = {}, *hi[2] = {}, *nrm[2] = {}, *att[2] = {};
+  void *g = nullptr, *v = nullptr, *coef = nullptr;
+  // full-problem vectors
+  void *xfull = nullptr, *lofull = nullptr, *hifull = nullptr, *nrmfull = nullptr, *attfull = nullptr;
+  void *gfull = nullptr, *vfull = nullptr;
+  // screening scratch
+  uint8_t* flags = nullptr;
+  int32_t* bcnt = nullptr;
+  int32_t* scr_idx = nullptr;
+  void* scr_val = nullptr;
+  int64_t* sat_lo = nullptr;
+  int64_t* sat_up = nullptr;
+  int* probe = nullptr;
+  // partials
+  void* part = nullptr;
+  int64_t ldp = 0;
+  double* bpart = nullptr;   // pass block scalars
+  double* bpart2 = nullptr;  // reduce block scalars
+  double* bpart3 = nullptr;  // dual block scalars (4 per block)
+  DevScalars* sc = nullptr;
+  DevScalars* hsc = nullptr;  // pinned mirror
+
+  int64_t k = 0;  // preserved count
+  int64_t n_sat_lo = 0, n_sat_up = 0;
+  int has_inf = 0;
+  int bound_bits = 0;
+  bool g_valid = false;
+  bool theta_is_cert = false;
+  bool have_apg_state = false;
+  int64_t launches = 0;
+  std::string err;
+
+  // multi-GPU column sharding
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t col_offset = 0, n_global = 0;
+};
+
+namespace {
+
+int fail(bx_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(c, BX_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LAUNCHED()                                                                                   \
+  do {                                                                                               \
+    ++c->launches;                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                             \
+    if (e_ != cudaSuccess) return fail(c, BX_ERR_CUDA, "launch (%s:%d): %s", __FILE__, __LINE__, \
+                                       cudaGetErrorString(e_));                                      \
+  } while (0)
+
+#define TRY(expr)            \
+  do {                       \
+    int s_ = (expr);         \
+    if (s_ != BX_OK) return s_; \
+  } while (0)
+
+// Workspace carving
+struct Carver {
+  char* base;
+  size_t off = 0;
+  size_t cap;
+  bool dry;
+  void* take(size_t bytes) {
+    off = align_up(off, kAlign);
+    void* p = dry ? nullptr : base + off;
+    off += align_up(bytes, kAlign);
+    return p;
+  }
+};
+
+constexpr int kPartRows = 1;  // placeholder to keep layout comments aligned
+
+void carve(bx_ctx* c, Carver& w) {
+  const int64_t m = c->m, n = c->n, mp = c->mp;
+  const size_t e = c->esz;
+  c->Aact = w.take((size_t)c->ldact * n * e);
+  void** rows[] = {&c->y, &c->t, &c->negy, &c->z, &c->z2, &c->off, &c->tgt,
+                   &c->r, &c->rprev, &c->rc, &c->theta, &c->thetac, &c->u};
+  for (void** p : rows) *p = w.take(mp * e);
+  for (int s = 0; s < 2; ++s) {
+    c->idx[s] = (int32_t*)w.take(n * 4);
+    c->x[s] = w.take(n * e);
+    c->xprev[s] = w.take(n * e);
+    c->lo[s] = w.take(n * e);
+    c->hi[s] = w.take(n * e);
+    c->nrm[s] = w.take(n * e);
+    c->att[s] = w.take(n * e);
+  }
+  c->g = w.take(n * e);
+  c->v = w.take(n * e);
+  c->coef = w.take(n * e);
+  c->xfull = w.take(n * e);
+  c->lofull = w.take(n * e);
+  c->hifull = w.take(n * e);
+  c->nrmfull = w.take(n * e);
+  c->attfull = w.take(n * e);
+  c->gfull = w.take(n * e);
+  c->vfull = w.take(n * e);
+  c->flags = (uint8_t*)w.take(n);
+  c->bcnt = (int32_t*)w.take((n / RT + 2) * 3 * 4);
+  c->scr_idx = (int32_t*)w.take(n * 4);
+  c->scr_val = w.take(n * e);
+  c->sat_lo = (int64_t*)w.take(n * 8);
+  c->sat_up = (int64_t*)w.take(n * 8);
+  c->probe = (int*)w.take(64);
+  c->ldp = mp;
+  c->part = w.take((size_t)c->Gmax * c->ldp * e);
+  c->bpart = (double*)w.take(c->Gmax * 8 * 2);
+  c->bpart2 = (double*)w.take(4096 * 8);
+  c->bpart3 = (double*)w.take(4096 * 4 * 8);
+  c->sc = (DevScalars*)w.take(sizeof(DevScalars));
+  (void)m;
+  (void)kPartRows;
+}
+
+void shape_params(bx_ctx* c) {
+  c->mp = round_up(c->m, 32);
+  c->ldact = c->mp;
+  c->Gmax = 2 * c->nsm;
+}
+
+// ---------------------------------------------------------------------------
+// pass launcher
+// ---------------------------------------------------------------------------
+int pick_R(int64_t m, size_t esz) {
+  const int V = (int)(16 / esz);
+  const int64_t per = (int64_t)NT * V;
+  const int Rs[] = {1, 2, 4, 6, 8, 10, 12};
+  for (int R : Rs)
+    if ((int64_t)R * per >= m) return R;
+  return -1;
+}
+
+template <typename T, int R, bool D, bool X>
+int launch_pass_RDX(bx_ctx* c, const PassArgs<T>& a, int G, size_t smem) {
+  static bool attr_set = false;
+  auto kern = k_pass<T, R, D, X>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_cap);
+    if (e != cudaSuccess) return fail(c, BX_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  kern<<<G, NT, smem, c->stream>>>(a);
+  LAUNCHED();
+  return BX_OK;
+}
+
+template <typename T, int R>
+int launch_pass_R(bx_ctx* c, const PassArgs<T>& a, bool dot, bool axpy, int G, size_t smem) {
+  if (dot && axpy) return launch_pass_RDX<T, R, true, true>(c, a, G, smem);
+  if (dot) return launch_pass_RDX<T, R, true, false>(c, a, G, smem);
+  return launch_pass_RDX<T, R, false, true>(c, a, G, smem);
+}
+
+// A "view" of columns the pass streams
+template <typename T>
+struct View {
+  const T* A;
+  int64_t ld;
+  const int32_t* colmap;
+  int64_t k;
+};
+
+template <typename T>
+View<T> act_view(bx_ctx* c) {
+  if (c->act_is_orig) return View<T>{(const T*)c->A, c->lda, nullptr, c->k};
+  return View<T>{(const T*)c->Aact, c->ldact, nullptr, c->k};
+}
+template <typename T>
+View<T> full_view(bx_ctx* c) {
+  return View<T>{(const T*)c->A, c->lda, nullptr, c->n};
+}
+
+int pass_grid(bx_ctx* c, int64_t k) {
+  int64_t G = (k + 7) / 8;
+  if (G > c->nsm) G = c->nsm;
+  if (G < 1) G = 1;
+  return (int)G;
+}
+
+// Launch one streamed pass.  Returns the grid used through *G_out.
+template <typename T>
+int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_prev, T* x, T* xprev, const T* lo,
+             const T* hi, T* g, const T* att, const T* coef, double* bpart, int has_inf, int* G_out) {
+  const int R = pick_R(c->m, sizeof(T));
+  if (R < 0) return fail(c, BX_ERR_UNSUPPORTED, "m=%lld exceeds the fused-pass envelope", (long long)c->m);
+  const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
+  const bool axpy = (upd != U_DOT);
+  const int C = cols_per_slot(R);
+  const uint32_t colbytes = (uint32_t)align_up((size_t)c->m * sizeof(T), 16);
+  const uint32_t colstride = (uint32_t)align_up(colbytes, 128);
+  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 2 * CMAX) * 8 + 64;
+  const size_t slot = (size_t)C * colstride;
+  int S = (int)((c->smem_cap - scratch) / slot);
+  if (S > SMAX) S = SMAX;
+  if (S < 1) return fail(c, BX_ERR_UNSUPPORTED, "column of %u bytes does not fit shared memory", colbytes);
+  const size_t smem = S * slot + scratch;
+  const int G = pass_grid(c, vw.k);
+  PassArgs<T> a;
+  a.A = vw.A;
+  a.ld = vw.ld;
+  a.colmap = vw.colmap;
+  a.k = vw.k;
+  a.m = c->m;
+  a.vin = vin;
+  a.vin_prev = vin_prev;
+  a.x = x;
+  a.xprev = xprev;
+  a.lo = lo;
+  a.hi = hi;
+  a.g = g;
+  a.att = att;
+  a.coef = coef;
+  a.part = (T*)c->part;
+  a.ldp = c->ldp;
+  a.bpart = bpart;
+  a.sc = c->sc;
+  a.upd = upd;
+  a.has_inf = has_inf;
+  a.C = C;
+  a.S = S;
+  a.colbytes = colbytes;
+  a.colstride = colstride;
+  if (G_out) *G_out = G;
+  switch (R) {
+    case 1: return launch_pass_R<T, 1>(c, a, dot, axpy, G, smem);
+    case 2: return launch_pass_R<T, 2>(c, a, dot, axpy, G, smem);
+    case 4: return launch_pass_R<T, 4>(c, a, dot, axpy, G, smem);
+    case 6: return launch_pass_R<T, 6>(c, a, dot, axpy, G, smem);
+    case 8: return launch_pass_R<T, 8>(c, a, dot, axpy, G, smem);
+    case 10: return launch_pass_R<T, 10>(c, a, dot, axpy, G, smem);
+    case 12: return launch_pass_R<T, 12>(c, a, dot, axpy, G, smem);
+  }
+  return fail(c, BX_ERR_UNSUPPORTED, "R=%d", R);
+}
+
+template <typename T>
+int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* wpart, int Gw, int counter) {
+  int nb = (int)((c->m + RT - 1) / RT);
+  if (nb > 2 * c->nsm) nb = 2 * c->nsm;
+  if (nb < 1) nb = 1;
+  k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, off, out, c->sc, c->bpart2, wpart, Gw,
+                                         mode, counter);
+  LAUNCHED();
+  return BX_OK;
+}
+
+int grid1d(bx_ctx* c, int64_t n) {
+  int64_t b = (n + RT - 1) / RT;
+  if (b > 4 * c->nsm) b = 4 * c->nsm;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------------------
+// building blocks of a round
+// ---------------------------------------------------------------------------
+template <typename T>
+int sync_scalars(bx_ctx* c) {
+  CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+int check_dev_err(bx_ctx* c) {
+  const int e = c->hsc->err;
+  if (e == 0) return BX_OK;
+  if (e == DE_STEP_TOO_LARGE)
+    return fail(c, BX_ERR_STEP_TOO_LARGE, "objective rose from %.6e to %.6e", c->hsc->P_prev, c->hsc->P);
+  if (e == DE_INTERNAL_CONSISTENCY) {
+    const DualOut& d = c->hsc->act.gap_raw < -1e-9 ? c->hsc->act : c->hsc->cert;
+    return fail(c, BX_ERR_INTERNAL_CONSISTENCY, "duality gap %.3e below round-off slack", d.gap_raw);
+  }
+  return fail(c, BX_ERR_CUDA, "device error code %d", e);
+}
+
+// residual r = A_act x + (z - y) and its objective (solvers.py:64)
+template <typename T>
+int refresh_resid(bx_ctx* c) {
+  const int s = c->cur;
+  int G = 1;
+  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, (T*)c->x[s], nullptr, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->r, R_SET, nullptr, 0, 0));
+  return BX_OK;
+}
+
+// FISTA: r_prev = A_act x_prev + (z - y)
+template <typename T>
+int refresh_rprev(bx_ctx* c) {
+  const int s = c->cur;
+  int G = 1;
+  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, (T*)c->xprev[s], nullptr, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_PLAIN, nullptr, 0, 0));
+  return BX_OK;
+}
+
+// spectral_norm_estimate on the act view (solvers.py:72-86); one fused pass per
+// power iteration: w = A'u, acc = A w, u <- acc / ||w||
+template <typename T>
+int power_iter(bx_ctx* c, int iters, const double* v0_host, double* sigma) {
+  const int64_t k = c->k;
+  if (k == 0) {
+    *sigma = 0.0;
+    return BX_OK;
+  }
+  std::vector<T> tmp(k);
+  for (int64_t i = 0; i < k; ++i) tmp[i] = (T)v0_host[i];
+  CU(cudaMemcpyAsync(c->coef, tmp.data(), k * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  int G = 1;
+  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                  (const T*)c->coef, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, nullptr, (T*)c->u, R_PLAIN, nullptr, 0, 0));
+  CU(cudaMemsetAsync(&c->sc->err, 0, sizeof(int32_t), c->stream));
+  double sig = 0.0;
+  // chunks of 10 iterations between host checks of the ||w|| == 0 exit
+  for (int it = 0; it < iters; ++it) {
+    TRY(run_pass<T>(c, act_view<T>(c), U_POWER, (const T*)c->u, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    (T*)c->g, nullptr, nullptr, c->bpart, 0, &G));
+    TRY(run_reduce<T>(c, G, nullptr, (T*)c->u, R_POWER, c->bpart, G, 1));
+  }
+  TRY(sync_scalars<T>(c));
+  if (c->hsc->err == DE_POWER_ZERO) {
+    // ||w|| hit zero: the reference returns 0.0 (solvers.py:82-83)
+    CU(cudaMemsetAsync(&c->sc->err, 0, sizeof(int32_t), c->stream));
+    *sigma = 0.0;
+    return BX_OK;
+  }
+  sig = c->hsc->sigma;
+  *sigma = sig;
+  return BX_OK;
+}
+
+void internal_start_vector(int64_t k, int64_t seed, double* out) {
+  std::mt19937_64 gen((uint64_t)seed);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  double s = 0.0;
+  for (int64_t i = 0; i < k; ++i) {
+    out[i] = nd(gen);
+    s += out[i] * out[i];
+  }
+  s = std::sqrt(s);
+  for (int64_t i = 0; i < k; ++i) out[i] /= s;
+}
+
+template <typename T>
+int auto_step(bx_ctx* c, int iters, double alpha, bx_start_vector_fn fn, void* user, double* eta, double* sigma_out) {
+  std::vector<double> v0(c->k > 0 ? c->k : 1);
+  if (c->k > 0) {
+    if (fn)
+      fn(c->k, 0, v0.data(), user);
+    else
+      internal_start_vector(c->k, 0, v0.data());
+  }
+  double sig = 0.0;
+  TRY(power_iter<T>(c, iters, v0.data(), &sig));
+  if (sigma_out) *sigma_out = sig;
+  const double s = sig / 0.999;  // solvers.py:95
+  *eta = (s == 0.0) ? 1.0 : 0.99 * alpha / (s * s);
+  CU(cudaMemcpyAsync(&c->sc->eta, eta, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+// one round's primal passes
+template <typename T>
+int primal_passes(bx_ctx* c, int kind, int passes) {
+  const int s = c->cur;
+  for (int p = 0; p < passes; ++p) {
+    int G = 1;
+    if (kind == BX_PG) {
+      if (c->g_valid) {
+        TRY(run_pass<T>(c, act_view<T>(c), U_PG_G, nullptr, nullptr, (T*)c->x[s], nullptr, (const T*)c->lo[s],
+                        (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, nullptr, 0, &G));
+      } else {
+        TRY(run_pass<T>(c, act_view<T>(c), U_PG, (const T*)c->r, nullptr, (T*)c->x[s], nullptr, (const T*)c->lo[s],
+                        (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, nullptr, 0, &G));
+      }
+      TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->r, R_PG, nullptr, 0, 2));
+      c->g_valid = false;
+    } else if (kind == BX_APG) {
+      TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const T*)c->r, (const T*)c->rprev, (T*)c->x[s], (T*)c->xprev[s],
+                      (const T*)c->lo[s], (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, nullptr, 0, &G));
+      // r_prev <- r, r <- new residual: write into the r_prev buffer, swap
+      TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_APG, nullptr, 0, 2));
+      std::swap(c->r, c->rprev);
+    } else {
+      return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent is not built yet");
+    }
+  }
+  return BX_OK;
+}
+
+// gradient at the current iterate + dual point + gap (+ sphere test)
+template <typename T>
+int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
+  const int s = c->cur;
+  int G = 1;
+  TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const T*)c->r, nullptr, nullptr, nullptr, nullptr, (const T*)c->hi[s],
+                  (T*)c->g, (const T*)c->att[s], nullptr, c->bpart, c->has_inf, &G));
+  c->g_valid = true;
+  int nb = grid1d(c, c->m > c->k ? c->m : c->k);
+  k_dual<T><<<nb, RT, 0, c->stream>>>((const T*)c->r, (const T*)c->t, (const T*)c->tgt, (T*)c->theta, c->m,
+                                       (const T*)c->g, (const T*)c->att[s], (const T*)c->lo[s], (const T*)c->hi[s],
+                                       (T*)c->v, c->k, c->bpart, G, c->has_inf, c->sc, 0, c->bpart3, slack_scale,
+                                       alpha, 3);
+  LAUNCHED();
+  c->theta_is_cert = false;
+  if (screening && c->k > 0) {
+    const int nbs = (int)((c->k + RT - 1) / RT);
+    k_sphere<T><<<nbs, RT, 0, c->stream>>>((const T*)c->v, (const T*)c->nrm[s], (const T*)c->hi[s], c->k, c->sc,
+                                            c->flags, c->bcnt);
+    LAUNCHED();
+    k_scan<<<1, 1024, 0, c->stream>>>(c->bcnt, nbs, c->sc);
+    LAUNCHED();
+  } else {
+    CU(cudaMemsetAsync(&c->sc->n_keep, 0, 3 * sizeof(int64_t), c->stream));
+  }
+  return BX_OK;
+}
+
+// _certified_gap (driver.py:352-357): full-problem A x, A'(y - A x), epsilon
+// over all infinite-upper columns, dual objective
+template <typename T>
+int certified(bx_ctx* c, double alpha) {
+  const int s = c->cur;
+  k_scatter_x<T><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], (const T*)c->x[s], (T*)c->xfull);
+  LAUNCHED();
+  int G = 1;
+  TRY(run_pass<T>(c, full_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                  (const T*)c->xfull, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, (const T*)c->negy, (T*)c->rc, R_CERT, nullptr, 0, 4));
+  TRY(run_pass<T>(c, full_view<T>(c), U_DOT, (const T*)c->rc, nullptr, nullptr, nullptr, nullptr,
+                  (const T*)c->hifull, (T*)c->gfull, (const T*)c->attfull, nullptr, c->bpart + c->Gmax, c->has_inf,
+                  &G));
+  int nb = grid1d(c, c->m > c->n ? c->m : c->n);
+  k_dual<T><<<nb, RT, 0, c->stream>>>((const T*)c->rc, (const T*)c->t, (const T*)c->y, (T*)c->thetac, c->m,
+                                       (const T*)c->gfull, (const T*)c->attfull, (const T*)c->lofull,
+                                       (const T*)c->hifull, (T*)c->vfull, c->n, c->bpart + c->Gmax, G, c->has_inf,
+                                       c->sc, 1, c->bpart3, 0.0, alpha, 5);
+  LAUNCHED();
+  return BX_OK;
+}
+
+// apply_screening + Workspace.refresh (screening.py:72-94, solvers.py:54-65)
+template <typename T>
+int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind) {
+  const int s = c->cur, d = 1 - c->cur;
+  const int nbs = (int)((c->k + RT - 1) / RT);
+  ColState<T> src{c->idx[s], (T*)c->x[s], kind == BX_APG ? (T*)c->xprev[s] : nullptr, (T*)c->lo[s], (T*)c->hi[s],
+                  (T*)c->nrm[s], (T*)c->att[s]};
+  ColState<T> dst{c->idx[d], (T*)c->x[d], (T*)c->xprev[d], (T*)c->lo[d], (T*)c->hi[d], (T*)c->nrm[d], (T*)c->att[d]};
+  k_compact<T><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (T*)c->xfull, c->scr_idx,
+                                           (T*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo, c->sat_up + c->n_sat_up);
+  LAUNCHED();
+  c->cur = d;
+  c->k = n_keep;
+  c->n_sat_lo += n_lo;
+  c->n_sat_up += n_up;
+  // z += A_S bound_S  (only when some screened bound is nonzero)
+  const bool lo_nz = (c->bound_bits & 1) && n_lo > 0;
+  const bool up_nz = (c->bound_bits & 2) && n_up > 0;
+  if (lo_nz || up_nz) {
+    View<T> vw{(const T*)c->A, c->lda, c->scr_idx, n_lo + n_up};
+    int G = 1;
+    TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    (const T*)c->scr_val, nullptr, 0, &G));
+    TRY(run_reduce<T>(c, G, (const T*)c->z, (T*)c->z2, R_PLAIN, nullptr, 0, 0));
+    std::swap(c->z, c->z2);
+    k_offsets<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const T*)c->y, (const T*)c->z, (T*)c->off,
+                                                          (T*)c->tgt);
+    LAUNCHED();
+  }
+  // physical rewrite of the preserved columns (solvers.py:57)
+  if (c->k > 0) {
+    int nb = (int)(c->k < 8 * c->nsm ? c->k : 8 * c->nsm);
+    k_gather<T><<<nb, RT, 0, c->stream>>>((const T*)c->A, c->lda, c->idx[c->cur], c->k, c->m, (T*)c->Aact,
+                                           c->ldact);
+    LAUNCHED();
+  }
+  c->act_is_orig = false;
+  TRY(refresh_resid<T>(c));
+  if (kind == BX_APG) TRY(refresh_rprev<T>(c));
+  c->g_valid = false;
+  return BX_OK;
+}
+
+template <typename T>
+int reset_state(bx_ctx* c, int kind) {
+  const int s = 0;
+  c->cur = 0;
+  c->k = c->n;
+  c->n_sat_lo = c->n_sat_up = 0;
+  c->act_is_orig = true;
+  c->g_valid = false;
+  c->theta_is_cert = false;
+  k_init_cols<T><<<grid1d(c, c->n), RT, 0, c->stream>>>(c->n, (const T*)c->lofull, (const T*)c->hifull,
+                                                         (T*)c->xfull, c->idx[s], (T*)c->x[s], (T*)c->lo[s],
+                                                         (T*)c->hi[s], (const T*)c->nrmfull, (T*)c->nrm[s],
+                                                         (const T*)c->attfull, (T*)c->att[s]);
+  LAUNCHED();
+  CU(cudaMemsetAsync(c->z, 0, c->mp * sizeof(T), c->stream));
+  k_offsets<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const T*)c->y, (const T*)c->z, (T*)c->off, (T*)c->tgt);
+  LAUNCHED();
+  DevScalars h;
+  memset(&h, 0, sizeof(h));
+  h.mom_t = 1.0;
+  h.P = INFINITY;
+  CU(cudaMemcpyAsync(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  TRY(refresh_resid<T>(c));
+  if (kind == BX_APG) {
+    CU(cudaMemcpyAsync(c->xprev[s], c->x[s], c->n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->rprev, c->r, c->mp * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    c->have_apg_state = true;
+  }
+  return BX_OK;
+}
+
+template <typename T>
+int create_typed(bx_ctx* c, const void* y, const void* lower, const void* upper, const void* t) {
+  const int64_t m = c->m, n = c->n;
+  CU(cudaMemsetAsync(c->y, 0, c->mp * sizeof(T), c->stream));
+  CU(cudaMemcpyAsync(c->y, y, m * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  k_neg<T><<<grid1d(c, m), RT, 0, c->stream>>>(c->mp, (const T*)c->y, (T*)c->negy);
+  LAUNCHED();
+  CU(cudaMemcpyAsync(c->lofull, lower, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->hifull, upper, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemsetAsync(c->probe, 0, 64, c->stream));
+  k_bounds_probe<T><<<grid1d(c, n), RT, 0, c->stream>>>(n, (const T*)c->lofull, (const T*)c->hifull, c->probe);
+  LAUNCHED();
+  int bits = 0;
+  CU(cudaMemcpyAsync(&bits, c->probe, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (bits & 32) return fail(c, BX_ERR_INVALID_ARGUMENT, "NaN entries in bounds");
+  if (bits & 8) return fail(c, BX_ERR_INVALID_ARGUMENT, "lower bounds must be finite");
+  if (bits & 16) return fail(c, BX_ERR_INVALID_ARGUMENT, "need lower_j < upper_j for every coordinate");
+  c->bound_bits = bits;
+  c->has_inf = (bits & 4) ? 1 : 0;
+  // translation vector: neg-ones unless given (duality.py:372-373)
+  CU(cudaMemsetAsync(c->t, 0, c->mp * sizeof(T), c->stream));
+  if (t) {
+    CU(cudaMemcpyAsync(c->t, t, m * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    k_fill<T><<<grid1d(c, m), RT, 0, c->stream>>>(m, (T*)c->t, T(-1));
+    LAUNCHED();
+  }
+  CU(cudaMemsetAsync(c->probe, 0, 64, c->stream));
+  const int nbw = (int)((n * 32 + RT - 1) / RT < 16 * c->nsm ? (n * 32 + RT - 1) / RT : 16 * c->nsm);
+  k_colstats<T><<<nbw, RT, 0, c->stream>>>((const T*)c->A, c->lda, n, m, (const T*)c->t, (T*)c->nrmfull,
+                                            (T*)c->attfull, c->has_inf, c->probe);
+  LAUNCHED();
+  int cf = 0;
+  CU(cudaMemcpyAsync(&cf, c->probe, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  // solve() builds the translation vector before the screening state
+  // (driver.py:381-392), so NoInteriorPoint takes precedence over ZeroColumn
+  if (c->has_inf && (cf & 2)) return fail(c, BX_ERR_NO_INTERIOR, "strategy did not yield a strictly interior t");
+  if (cf & 1) return fail(c, BX_ERR_ZERO_COLUMN, "zero column in A");
+  return BX_OK;
+}
+
+template <typename T>
+int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* user, bx_trace_rec* trace,
+                int64_t cap, bx_solve_out* out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int kind = cfg->kind;
+  const int passes = cfg->inner_passes;
+  const int64_t max_rounds = cfg->max_rounds > 0 ? cfg->max_rounds : 1000000;
+  const double tol = cfg->gap_tol;
+  const double alpha = cfg->alpha > 0 ? cfg->alpha : 1.0;
+  const double slack_scale = cfg->slack_scale >= 0 ? cfg->slack_scale : 1e-12;
+  const bool auto_eta = !(cfg->step_size > 0);  // NaN or <= 0
+  TRY(reset_state<T>(c, kind));
+  double eta = cfg->step_size;
+  double sigma = 0.0;
+  int64_t basis = c->n;
+  if ((kind == BX_PG || kind == BX_APG)) {
+    if (auto_eta) {
+      TRY(auto_step<T>(c, cfg->power_iters, alpha, fn, user, &eta, &sigma));
+    } else {
+      CU(cudaMemcpyAsync(&c->sc->eta, &eta, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    }
+  }
+  int64_t rounds = 0, iters = 0;
+  bool converged = false;
+  double gap_out = INFINITY;
+  int64_t ntrace = 0;
+  for (int64_t rnd = 1; rnd <= max_rounds; ++rnd) {
+    rounds = rnd;
+    TRY(primal_passes<T>(c, kind, passes));
+    iters += passes;
+    TRY(dual_screen<T>(c, cfg->screening, slack_scale, alpha));
+    TRY(sync_scalars<T>(c));
+    TRY(check_dev_err(c));
+    const DualOut act = c->hsc->act;
+    gap_out = act.gap;
+    double cert_gap = NAN;
+    if (act.gap < tol) {
+      TRY(certified<T>(c, alpha));
+      TRY(sync_scalars<T>(c));
+      TRY(check_dev_err(c));
+      cert_gap = c->hsc->cert.gap;
+      gap_out = cert_gap;
+      c->theta_is_cert = true;
+      if (cert_gap < tol) converged = true;
+    }
+    int64_t n_lo = 0, n_up = 0;
+    if (cfg->screening && c->k > 0) {
+      n_lo = c->hsc->n_lo;
+      n_up = c->hsc->n_up;
+      if (n_lo || n_up) {
+        // theta of this round must survive the compaction's scratch use
+        TRY(compact<T>(c, n_lo, n_up, c->hsc->n_keep, kind));
+        if ((kind == BX_PG || kind == BX_APG) && auto_eta && (double)c->k < 0.5 * (double)basis) {
+          TRY(auto_step<T>(c, cfg->power_iters, alpha, fn, user, &eta, &sigma));
+          basis = c->k;
+        }
+      }
+    }
+    if (trace && ntrace < cap) {
+      bx_trace_rec& tr = trace[ntrace++];
+      tr.round = rnd;
+      tr.elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      tr.primal = act.primal;
+      tr.dual = act.dual;
+      tr.gap = act.gap;
+      tr.preserved_count = c->k;
+      tr.newly_screened_lower = n_lo;
+      tr.newly_screened_upper = n_up;
+      tr.eps = act.eps;
+      tr.radius = act.radius;
+      tr.step = eta;
+      tr.certified_gap = cert_gap;
+    }
+    if (converged) break;
+  }
+  // x_full <- current preserved iterate (ws.sync, driver.py:492)
+  k_scatter_x<T><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], (const T*)c->x[c->cur], (T*)c->xfull);
+  LAUNCHED();
+  CU(cudaStreamSynchronize(c->stream));
+  if (out) {
+    out->rounds = rounds;
+    out->converged = converged ? 1 : 0;
+    out->gap = gap_out;
+    out->n_sat_lower = c->n_sat_lo;
+    out->n_sat_upper = c->n_sat_up;
+    out->iterations = iters;
+    out->step = eta;
+    out->sigma = sigma;
+    out->kernel_launches = c->launches;
+  }
+  return BX_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+size_t bx_workspace_bytes(int64_t m, int64_t n, int32_t dtype) {
+  bx_ctx tmp;
+  tmp.m = m;
+  tmp.n = n;
+  tmp.dtype = dtype;
+  tmp.esz = dtype == BX_F32 ? 4 : 8;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0) tmp.nsm = nsm;
+  }
+  shape_params(&tmp);
+  Carver w{nullptr, 0, 0, true};
+  carve(&tmp, w);
+  return w.off + kAlign;
+}
+
+int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void* a, int64_t lda, const void* y,
+                  const void* lower, const void* upper, const void* t, void* workspace, size_t workspace_bytes,
+                  void* cuda_stream) {
+  if (!out) return BX_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  bx_ctx* c = new bx_ctx();
+  *out = c;
+  if (m < 1 || n < 1) return fail(c, BX_ERR_DIMENSION, "A must have at least one row and column");
+  if (n > INT32_MAX) return fail(c, BX_ERR_UNSUPPORTED, "n too large");
+  if (dtype != BX_F64 && dtype != BX_F32) return fail(c, BX_ERR_INVALID_ARGUMENT, "dtype");
+  c->m = m;
+  c->n = n;
+  c->dtype = dtype;
+  c->esz = dtype == BX_F32 ? 4 : 8;
+  if (lda < m) return fail(c, BX_ERR_DIMENSION, "lda < m");
+  if (((uintptr_t)a % 16) || ((lda * (int64_t)c->esz) % 16))
+    return fail(c, BX_ERR_INVALID_ARGUMENT, "A base and column stride must be 16-byte aligned");
+  if (pick_R(m, c->esz) < 0)
+    return fail(c, BX_ERR_UNSUPPORTED, "m=%lld rows exceeds the fused-pass envelope", (long long)m);
+  c->A = a;
+  c->lda = lda;
+  c->stream = (cudaStream_t)cuda_stream;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
+  int smem_optin = 0;
+  CU(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  c->smem_cap = (size_t)smem_optin;
+  shape_params(c);
+  Carver dry{nullptr, 0, 0, true};
+  carve(c, dry);
+  if (!workspace || workspace_bytes < dry.off + kAlign)
+    return fail(c, BX_ERR_WORKSPACE, "workspace of %zu bytes, need %zu", workspace_bytes, dry.off + kAlign);
+  char* base = (char*)align_up((uintptr_t)workspace, kAlign);
+  Carver w{base, 0, workspace_bytes, false};
+  carve(c, w);
+  CU(cudaMallocHost((void**)&c->hsc, sizeof(DevScalars)));
+  memset(c->hsc, 0, sizeof(DevScalars));
+  CU(cudaMemsetAsync(c->sc, 0, sizeof(DevScalars), c->stream));
+  CU(cudaMemsetAsync(c->part, 0, (size_t)c->Gmax * c->ldp * c->esz, c->stream));
+  if (dtype == BX_F64) return create_typed<double>(c, y, lower, upper, t);
+  return create_typed<float>(c, y, lower, upper, t);
+}
+
+int bx_ctx_destroy(bx_ctx* c) {
+  if (!c) return BX_OK;
+  if (c->hsc) cudaFreeHost(c->hsc);
+  if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  delete c;
+  return BX_OK;
+}
+
+const char* bx_last_error(const bx_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int bx_col_norms(bx_ctx* c, void* out) {
+  CU(cudaMemcpyAsync(out, c->nrmfull, c->n * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+int bx_att(bx_ctx* c, void* out) {
+  CU(cudaMemcpyAsync(out, c->attfull, c->n * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+int bx_power_iter(bx_ctx* c, int32_t iters, const double* v0_host, double* sigma_out) {
+  if (!sigma_out) return fail(c, BX_ERR_INVALID_ARGUMENT, "sigma_out");
+  if (c->dtype == BX_F64) return power_iter<double>(c, iters, v0_host, sigma_out);
+  return power_iter<float>(c, iters, v0_host, sigma_out);
+}
+
+int bx_reset(bx_ctx* c) {
+  if (c->dtype == BX_F64) return reset_state<double>(c, BX_APG);
+  return reset_state<float>(c, BX_APG);
+}
+
+int bx_primal_passes(bx_ctx* c, int32_t kind, double eta, int32_t passes) {
+  CU(cudaMemcpyAsync(&c->sc->eta, &eta, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int s = (c->dtype == BX_F64) ? primal_passes<double>(c, kind, passes) : primal_passes<float>(c, kind, passes);
+  if (s != BX_OK) return s;
+  CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return check_dev_err(c);
+}
+
+int bx_dual_screen(bx_ctx* c, int32_t screening, double slack_scale, double* o) {
+  int s = (c->dtype == BX_F64) ? dual_screen<double>(c, screening, slack_scale, 1.0)
+                               : dual_screen<float>(c, screening, slack_scale, 1.0);
+  if (s != BX_OK) return s;
+  CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  s = check_dev_err(c);
+  if (o) {
+    const DualOut& d = c->hsc->act;
+    o[0] = d.primal;
+    o[1] = d.dual;
+    o[2] = d.gap;
+    o[3] = d.eps;
+    o[4] = d.radius;
+    o[5] = d.slack;
+    o[6] = (double)c->hsc->n_lo;
+    o[7] = (double)c->hsc->n_up;
+  }
+  return s;
+}
+
+int bx_compact(bx_ctx* c) {
+  const int64_t lo = c->hsc->n_lo, up = c->hsc->n_up, keep = c->hsc->n_keep;
+  if (lo + up == 0) return BX_OK;
+  int s = (c->dtype == BX_F64) ? compact<double>(c, lo, up, keep, BX_APG) : compact<float>(c, lo, up, keep, BX_APG);
+  if (s != BX_OK) return s;
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+int bx_certified_gap(bx_ctx* c, double* o) {
+  int s = (c->dtype == BX_F64) ? certified<double>(c, 1.0) : certified<float>(c, 1.0);
+  if (s != BX_OK) return s;
+  CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  s = check_dev_err(c);
+  if (o) {
+    o[0] = c->hsc->cert.gap;
+    o[1] = c->hsc->cert.primal;
+    o[2] = c->hsc->cert.dual;
+    o[3] = c->hsc->cert.eps;
+  }
+  return s;
+}
+
+int64_t bx_preserved_count(const bx_ctx* c) { return c ? c->k : -1; }
+
+int bx_solve(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* user, bx_trace_rec* trace,
+             int64_t cap, bx_solve_out* out) {
+  if (!c || !cfg) return BX_ERR_INVALID_ARGUMENT;
+  if (cfg->kind != BX_PG && cfg->kind != BX_CD && cfg->kind != BX_APG)
+    return fail(c, BX_ERR_INVALID_ARGUMENT, "unknown solver kind %d", cfg->kind);
+  if (!(cfg->gap_tol > 0)) return fail(c, BX_ERR_INVALID_ARGUMENT, "gap_tol must be positive");
+  if (cfg->inner_passes < 1) return fail(c, BX_ERR_INVALID_ARGUMENT, "inner_passes must be >= 1");
+  c->launches = 0;
+  if (c->dtype == BX_F64) return solve_typed<double>(c, cfg, fn, user, trace, cap, out);
+  return solve_typed<float>(c, cfg, fn, user, trace, cap, out);
+}
+
+int bx_get_state(bx_ctx* c, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper) {
+  if (x) CU(cudaMemcpyAsync(x, c->xfull, c->n * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+  if (theta)
+    CU(cudaMemcpyAsync(theta, c->theta_is_cert ? c->thetac : c->theta, c->m * c->esz, cudaMemcpyDeviceToDevice,
+                       c->stream));
+  if (sat_lower && c->n_sat_lo)
+    CU(cudaMemcpyAsync(sat_lower, c->sat_lo, c->n_sat_lo * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (sat_upper && c->n_sat_up)
+    CU(cudaMemcpyAsync(sat_upper, c->sat_up, c->n_sat_up * 8, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+int bx_nccl_unique_id(unsigned char* id_out) {
+  if (!g_nccl.load()) return BX_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  if (g_nccl.get_id(&id) != 0) return BX_ERR_CUDA;
+  memcpy(id_out, id.internal, 128);
+  return BX_OK;
+}
+
+int bx_ctx_set_comm(bx_ctx* c, const unsigned char* id_host, int32_t rank, int32_t nranks, int64_t col_offset,
+                    int64_t n_global) {
+  if (!g_nccl.load()) return fail(c, BX_ERR_UNSUPPORTED, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  memcpy(id.internal, id_host, 128);
+  ncclComm_t comm = nullptr;
+  const int r = g_nccl.init_rank(&comm, nranks, id, rank);
+  if (r != 0) return fail(c, BX_ERR_CUDA, "ncclCommInitRank: %d", r);
+  c->comm = comm;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->col_offset = col_offset;
+  c->n_global = n_global;
+  return BX_OK;
+}
+
+size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs) {
+  (void)m;
+  (void)n;
+  (void)k_rhs;
+  return 0;
+}
+
+}  // extern "C"

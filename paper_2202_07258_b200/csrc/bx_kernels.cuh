@@ -1,0 +1,877 @@
+// bx_kernels.cuh -- sm_100a kernels of the screened box-constrained LS iteration.
+//
+// Hot path:
+//   k_pass     one streamed pass over the preserved columns A_act.  Each CTA
+//              owns a contiguous range of columns, stages them whole into a
+//              shared-memory ring with cp.async.bulk (TMA bulk engine,
+//              mbarrier completion) and, per column j,
+//                 g_j   = a_j . v            (dot; v = residual / extrapolated residual)
+//                 x_j'  = clip(y_j - eta g_j, l_j, u_j)    (PG / FISTA update)
+//                 acc  += a_j x_j'           (the next residual's partial A x')
+//              so ONE read of A serves both products of a projected-gradient
+//              step (solvers.py:109-116 does two GEMV passes).  Modes cover
+//              the screening pass (dot + epsilon partial), power iteration
+//              (solvers.py:78-85) and plain A x (refresh, certified gap).
+//   k_reduce   sums the per-CTA partial rows in a fixed order (deterministic),
+//              adds the offset z - y, and in its last CTA finalises the
+//              objective, the StepSizeTooLarge guard (solvers.py:111-114) or
+//              the FISTA restart test.
+//   k_dual     dual translation/scaling + reduced dual + gap clamp + radius +
+//              slack (driver.py:423-441, 453-459; duality.py:452-454).
+//   k_sphere / k_scan / k_compact / k_gather
+//              gap-safe sphere test (screening.py:254-263) with warp-ballot /
+//              block prefix-sum compaction of the preserved set and the
+//              physical rewrite of A_act (solvers.py:57).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+namespace bx {
+
+constexpr int NT = 512;            // k_pass block size
+constexpr int NWARPS = NT / 32;
+constexpr int CMAX = 8;            // columns per ring slot (max)
+constexpr int SMAX = 8;            // ring slots (max)
+constexpr int RT = 256;            // block size of the vector kernels
+
+template <typename T> struct V16;
+template <> struct V16<double> { using type = double2; static constexpr int n = 2; };
+template <> struct V16<float> { using type = float4; static constexpr int n = 4; };
+
+enum PassUpd : int {
+  U_DOT = 0,    // g_j = a_j . v ; epsilon partial over infinite-upper columns
+  U_PG_G = 1,   // x_j' = clip(x_j - eta g_j) with the stored g (no dot)
+  U_PG = 2,     // dot + PG update
+  U_APG = 3,    // dot on r_y = r + beta (r - r_prev), FISTA update
+  U_POWER = 4,  // w_j = a_j . u ; acc += a_j w_j ; sum w_j^2
+  U_AX = 5      // acc += a_j c_j (c = coef or x)
+};
+
+enum ReduceMode : int { R_PLAIN = 0, R_SET = 1, R_PG = 2, R_APG = 3, R_POWER = 4, R_CERT = 5 };
+
+enum DevErr : int {
+  DE_NONE = 0, DE_STEP_TOO_LARGE = 4, DE_INTERNAL_CONSISTENCY = 5, DE_POWER_ZERO = 64
+};
+
+// Scalars shared by the kernels of one context (device memory).
+struct DualOut {
+  double primal, dual, gap, gap_raw, eps, radius, slack, thr, th_norm2;
+};
+
+struct DevScalars {
+  double eta;       // step in force
+  double P;         // 0.5 ||r||^2 of the current residual
+  double P_prev;    // objective before the last pass (error reporting)
+  double mom_t;     // FISTA momentum scalar t_k
+  double nw;        // power iteration ||w||
+  double sigma;     // sqrt(nw)
+  double cert_P;    // 0.5 ||A x - y||^2 on the full problem
+  DualOut act;      // reduced-problem dual point of this round
+  DualOut cert;     // certified (full-problem) dual point
+  int64_t n_keep, n_lo, n_up;
+  int32_t err;
+  int32_t restarts;
+  unsigned int counters[8];
+};
+
+template <typename T>
+struct PassArgs {
+  const T* A;              // column base
+  int64_t ld;              // column stride (elements)
+  const int32_t* colmap;   // column p lives at A + colmap[p]*ld (NULL: p)
+  int64_t k;               // columns in this pass
+  int64_t m;               // rows
+  const T* vin;            // dot vector (residual / power vector)
+  const T* vin_prev;       // FISTA: previous residual
+  T* x;                    // iterate (updated in place)
+  T* xprev;                // FISTA previous iterate
+  const T* lo;
+  const T* hi;
+  T* g;                    // gradient A'v (written by dot modes, read by U_PG_G)
+  const T* att;            // A't for the epsilon partial
+  const T* coef;           // U_AX coefficients (NULL: x)
+  T* part;                 // [gridDim.x][ldp] partial rows of A x'
+  int64_t ldp;
+  double* bpart;           // [gridDim.x] block scalar partial (eps max / sum w^2)
+  DevScalars* sc;
+  int upd;
+  int has_inf;
+  int C;                   // columns per ring slot
+  int S;                   // ring slots
+  uint32_t colbytes;       // bytes moved per column (multiple of 16)
+  uint32_t colstride;      // smem bytes per column in a slot
+};
+
+// ----------------------------------------------------------------------------
+// PTX helpers: mbarrier + bulk copy (TMA bulk engine, SASS UBLKCP)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void set_err(DevScalars* sc, int code) { atomicCAS(&sc->err, 0, code); }
+
+// numpy-order scalar helpers (no FMA contraction, so the update matches
+// `np.clip(x - eta * g, lo, hi)` operation by operation)
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+// np.clip(v, lo, hi) == minimum(maximum(v, lo), hi) for non-NaN input
+template <typename T>
+__device__ __forceinline__ T clip(T v, T lo, T hi) {
+  const T a = v < lo ? lo : v;
+  return a > hi ? hi : a;
+}
+
+template <typename T>
+__device__ __forceinline__ void unpack(const typename V16<T>::type& v, T* o);
+template <>
+__device__ __forceinline__ void unpack<double>(const double2& v, double* o) {
+  o[0] = v.x;
+  o[1] = v.y;
+}
+template <>
+__device__ __forceinline__ void unpack<float>(const float4& v, float* o) {
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.z;
+  o[3] = v.w;
+}
+template <typename T>
+__device__ __forceinline__ typename V16<T>::type pack(const T* o);
+template <>
+__device__ __forceinline__ double2 pack<double>(const double* o) {
+  return make_double2(o[0], o[1]);
+}
+template <>
+__device__ __forceinline__ float4 pack<float>(const float* o) {
+  return make_float4(o[0], o[1], o[2], o[3]);
+}
+
+// columns per slot as a function of R (rows-per-thread chunks)
+__host__ __device__ constexpr int cols_per_slot(int R) { return R >= 6 ? 1 : (R >= 4 ? 2 : (R >= 2 ? 4 : 8)); }
+
+// ----------------------------------------------------------------------------
+// k_pass: one streamed pass over k columns (see header comment)
+// ----------------------------------------------------------------------------
+template <typename T, int R, bool DOT, bool AXPY>
+__global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
+  using VT = typename V16<T>::type;
+  constexpr int V = V16<T>::n;
+  constexpr int C = cols_per_slot(R);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int m = static_cast<int>(a.m);
+  const int row0 = tid * V;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int64_t G = gridDim.x;
+  const int64_t b = blockIdx.x;
+  const int64_t p0 = a.k * b / G;
+  const int64_t p1 = a.k * (b + 1) / G;
+  const int ncol = static_cast<int>(p1 - p0);
+  const int S = a.S;
+  const int ngroups = (ncol + C - 1) / C;
+  const uint32_t slot_bytes = C * a.colstride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * slot_bytes);
+  double* red = reinterpret_cast<double*>(bars + SMAX);  // [NWARPS][C]
+  double* cf = red + NWARPS * CMAX;                      // [C] axpy coefficients
+  double* bscr = cf + CMAX;                              // [C] block scalar scratch
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = policy_evict_first();
+    const int pre = ngroups < S ? ngroups : S;
+    for (int gi = 0; gi < pre; ++gi) {
+      const int cg = min(C, ncol - gi * C);
+      mbar_expect_tx(&bars[gi], cg * a.colbytes);
+      for (int c = 0; c < cg; ++c) {
+        const int64_t p = p0 + (int64_t)gi * C + c;
+        const int64_t col = a.colmap ? (int64_t)a.colmap[p] : p;
+        bulk_g2s(smem + gi * slot_bytes + c * a.colstride, a.A + col * a.ld, a.colbytes, &bars[gi], pol);
+      }
+    }
+  }
+
+  // the dot vector, register resident: thread owns rows (i*NT + tid)*V + e
+  T vr[DOT ? R : 1][V];
+  double beta = 0.0;
+  const double eta = a.sc->eta;
+  if (DOT) {
+    if (a.upd == U_APG) {
+      const double t = a.sc->mom_t;
+      const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+      beta = (t - 1.0) / tn;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = row0 + i * (NT * V);
+#pragma unroll
+      for (int e = 0; e < V; ++e) vr[i][e] = T(0);
+      if (row < m) {
+        T cur[V];
+        unpack<T>(*reinterpret_cast<const VT*>(a.vin + row), cur);
+        if (beta != 0.0) {
+          T prv[V];
+          unpack<T>(*reinterpret_cast<const VT*>(a.vin_prev + row), prv);
+          const T bt = static_cast<T>(beta);
+#pragma unroll
+          for (int e = 0; e < V; ++e) cur[e] = add_rn(cur[e], mul_rn(bt, sub_rn(cur[e], prv[e])));
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? cur[e] : T(0);
+      }
+    }
+  }
+
+  T acc[AXPY ? R : 1][V];
+#pragma unroll
+  for (int i = 0; i < (AXPY ? R : 1); ++i)
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[i][e] = T(0);
+  double run = 0.0;  // block-scalar running value (threads tid < C)
+
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int s = gi % S;
+    const int cg = min(C, ncol - gi * C);
+    mbar_wait(&bars[s], (uint32_t)((gi / S) & 1));
+    const unsigned char* slot = smem + s * slot_bytes;
+    if (DOT) {
+      T d[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        d[c] = T(0);
+        if (c < cg) {
+          const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            const int row = row0 + i * (NT * V);
+            if (row < m) {
+              T av[V];
+              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+              for (int e = 0; e < V; ++e) d[c] += ((row + e < m) ? av[e] : T(0)) * vr[i][e];
+            }
+          }
+        }
+        d[c] = warp_sum<T>(d[c]);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) red[warp * CMAX + c] = static_cast<double>(d[c]);
+      }
+      __syncthreads();
+      if (tid < cg) {
+        double gsum = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWARPS; ++w) gsum += red[w * CMAX + tid];
+        const T gj = static_cast<T>(gsum);
+        const int64_t p = p0 + (int64_t)gi * C + tid;
+        double coef = 0.0;
+        switch (a.upd) {
+          case U_DOT: {
+            a.g[p] = gj;
+            if (a.has_inf && isinf(static_cast<double>(a.hi[p]))) {
+              const double ratio = fmax(-static_cast<double>(gj), 0.0) / fabs(static_cast<double>(a.att[p]));
+              run = fmax(run, ratio);
+            }
+          } break;
+          case U_PG: {
+            a.g[p] = gj;
+            const T xo = a.x[p];
+            const T xn = clip<T>(sub_rn(xo, mul_rn(static_cast<T>(eta), gj)), a.lo[p], a.hi[p]);
+            a.x[p] = xn;
+            coef = static_cast<double>(xn);
+          } break;
+          case U_APG: {
+            const T xo = a.x[p];
+            const T xp = a.xprev[p];
+            T yv = xo;
+            if (beta != 0.0) yv = add_rn(xo, mul_rn(static_cast<T>(beta), sub_rn(xo, xp)));
+            const T xn = clip<T>(sub_rn(yv, mul_rn(static_cast<T>(eta), gj)), a.lo[p], a.hi[p]);
+            a.xprev[p] = xo;
+            a.x[p] = xn;
+            coef = static_cast<double>(xn);
+          } break;
+          case U_POWER: {
+            coef = static_cast<double>(gj);
+            run += coef * coef;
+          } break;
+          default:
+            break;
+        }
+        cf[tid] = coef;
+      }
+      __syncthreads();
+    } else {
+      if (tid < cg) {
+        const int64_t p = p0 + (int64_t)gi * C + tid;
+        double coef = 0.0;
+        if (a.upd == U_PG_G) {
+          const T xo = a.x[p];
+          const T xn = clip<T>(sub_rn(xo, mul_rn(static_cast<T>(eta), a.g[p])), a.lo[p], a.hi[p]);
+          a.x[p] = xn;
+          coef = static_cast<double>(xn);
+        } else {
+          coef = static_cast<double>(a.coef ? a.coef[p] : a.x[p]);
+        }
+        cf[tid] = coef;
+      }
+      __syncthreads();
+    }
+    if (AXPY) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (c < cg) {
+          const T cc = static_cast<T>(cf[c]);
+          const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            const int row = row0 + i * (NT * V);
+            if (row < m) {
+              T av[V];
+              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+              for (int e = 0; e < V; ++e) acc[i][e] += ((row + e < m) ? av[e] : T(0)) * cc;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with slot s
+    if (tid == 0 && gi + S < ngroups) {
+      const int gn = gi + S;
+      const int cgn = min(C, ncol - gn * C);
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bars[s], cgn * a.colbytes);
+      for (int c = 0; c < cgn; ++c) {
+        const int64_t p = p0 + (int64_t)gn * C + c;
+        const int64_t col = a.colmap ? (int64_t)a.colmap[p] : p;
+        bulk_g2s(smem + s * slot_bytes + c * a.colstride, a.A + col * a.ld, a.colbytes, &bars[s], pol);
+      }
+    }
+  }
+
+  if (AXPY) {
+    T* out = a.part + b * a.ldp;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = row0 + i * (NT * V);
+      if (row < m) *reinterpret_cast<VT*>(out + row) = pack<T>(acc[i]);
+    }
+  }
+  if (a.bpart) {
+    if (tid < C) bscr[tid] = run;
+    __syncthreads();
+    if (tid == 0) {
+      double v = bscr[0];
+      for (int c = 1; c < C; ++c) v = (a.upd == U_DOT) ? fmax(v, bscr[c]) : v + bscr[c];
+      a.bpart[b] = v;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// k_reduce: out_i = sum_b part[b][i] (+ off_i) ; block partial of ||out||^2 ;
+// last block finalises the objective bookkeeping.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum_rt(double v, double* sh) {
+  v = warp_sum<double>(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+  }
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64_t ldp, int G, int64_t m,
+                                               const T* __restrict__ off, T* __restrict__ out,
+                                               DevScalars* sc, double* bpart, const double* wpart,
+                                               int Gw, int mode, int counter) {
+  __shared__ double sh[RT / 32];
+  __shared__ bool last;
+  double scale_div = 1.0;
+  if (mode == R_POWER) {
+    double nw2 = 0.0;
+    for (int b = 0; b < Gw; ++b) nw2 += wpart[b];
+    scale_div = sqrt(nw2);
+  }
+  double sq = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < m; i += (int64_t)gridDim.x * RT) {
+    T s = T(0);
+    int bb = 0;
+    for (; bb + 4 <= G; bb += 4) {
+      const T a0 = part[(int64_t)(bb + 0) * ldp + i];
+      const T a1 = part[(int64_t)(bb + 1) * ldp + i];
+      const T a2 = part[(int64_t)(bb + 2) * ldp + i];
+      const T a3 = part[(int64_t)(bb + 3) * ldp + i];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; bb < G; ++bb) s += part[(int64_t)bb * ldp + i];
+    if (off) s = add_rn(s, off[i]);
+    if (mode == R_POWER) s = static_cast<T>(static_cast<double>(s) / scale_div);
+    out[i] = s;
+    sq += static_cast<double>(s) * static_cast<double>(s);
+  }
+  if (mode == R_PLAIN) return;
+  const double tot = block_sum_rt(sq, sh);
+  if (threadIdx.x == 0) {
+    bpart[blockIdx.x] = tot;
+    __threadfence();
+    const unsigned prev = atomicAdd(&sc->counters[counter], 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double total = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) total += *((volatile double*)&bpart[b]);
+  const double Pn = 0.5 * total;
+  switch (mode) {
+    case R_SET:
+      sc->P = Pn;
+      break;
+    case R_PG:
+      if (Pn > sc->P + 1e-9) {
+        sc->P_prev = sc->P;
+        set_err(sc, DE_STEP_TOO_LARGE);
+      }
+      sc->P = Pn;
+      break;
+    case R_APG: {
+      const double t = sc->mom_t;
+      const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+      if (Pn > sc->P) {
+        sc->mom_t = 1.0;
+        sc->restarts += 1;
+      } else {
+        sc->mom_t = tn;
+      }
+      sc->P = Pn;
+    } break;
+    case R_POWER:
+      sc->nw = scale_div;
+      sc->sigma = sqrt(scale_div);
+      if (scale_div == 0.0) set_err(sc, DE_POWER_ZERO);
+      break;
+    case R_CERT:
+      sc->cert_P = Pn;
+      break;
+    default:
+      break;
+  }
+  sc->counters[counter] = 0u;
+}
+
+// ----------------------------------------------------------------------------
+// k_dual: dual point, reduced dual objective, clamped gap, radius, slack
+// ----------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* __restrict__ t,
+                                             const T* __restrict__ tgt, T* __restrict__ theta, int64_t m,
+                                             const T* __restrict__ g, const T* __restrict__ att,
+                                             const T* __restrict__ lo, const T* __restrict__ hi,
+                                             T* __restrict__ v, int64_t k, const double* eps_part, int Ge,
+                                             int has_inf, DevScalars* sc, int which, double* bpart,
+                                             double slack_scale, double alpha, int counter) {
+  __shared__ double sh[RT / 32];
+  __shared__ bool last;
+  DualOut* out = which ? &sc->cert : &sc->act;
+  double eps = 0.0;
+  if (has_inf)
+    for (int b = 0; b < Ge; ++b) eps = fmax(eps, eps_part[b]);
+  const T te = static_cast<T>(eps);
+  double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * RT;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < m; i += stride) {
+    T th = -r[i];
+    if (eps > 0.0) th = add_rn(th, mul_rn(te, t[i]));
+    theta[i] = th;
+    s1 += static_cast<double>(th) * static_cast<double>(tgt[i]);
+    s2 += static_cast<double>(th) * static_cast<double>(th);
+  }
+  for (int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x; j < k; j += stride) {
+    T vj = -g[j];
+    if (has_inf) vj = add_rn(vj, mul_rn(te, att[j]));
+    v[j] = vj;
+    const double vd = static_cast<double>(vj);
+    s3 += static_cast<double>(lo[j]) * fmin(vd, 0.0);
+    if (!isinf(static_cast<double>(hi[j]))) s4 += static_cast<double>(hi[j]) * fmax(vd, 0.0);
+  }
+  const double b1 = block_sum_rt(s1, sh);
+  const double b2 = block_sum_rt(s2, sh);
+  const double b3 = block_sum_rt(s3, sh);
+  const double b4 = block_sum_rt(s4, sh);
+  if (threadIdx.x == 0) {
+    bpart[4 * blockIdx.x + 0] = b1;
+    bpart[4 * blockIdx.x + 1] = b2;
+    bpart[4 * blockIdx.x + 2] = b3;
+    bpart[4 * blockIdx.x + 3] = b4;
+    __threadfence();
+    const unsigned prev = atomicAdd(&sc->counters[counter], 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0;
+  volatile double* vb = bpart;
+  for (int b = 0; b < (int)gridDim.x; ++b) {
+    t1 += vb[4 * b + 0];
+    t2 += vb[4 * b + 1];
+    t3 += vb[4 * b + 2];
+    t4 += vb[4 * b + 3];
+  }
+  double dual = t1 - 0.5 * t2;
+  dual -= t3;
+  dual -= t4;
+  const double primal = which ? sc->cert_P : sc->P;
+  const double raw = primal - dual;
+  if (raw < -1e-9) set_err(sc, DE_INTERNAL_CONSISTENCY);
+  const double gap = fmax(raw, 0.0);
+  out->primal = primal;
+  out->dual = dual;
+  out->gap_raw = raw;
+  out->gap = gap;
+  out->eps = eps;
+  out->th_norm2 = t2;
+  out->radius = sqrt(2.0 * gap / alpha);
+  out->slack = slack_scale * fmax(1.0, sqrt(t2));
+  out->thr = out->radius + out->slack;
+  sc->counters[counter] = 0u;
+}
+
+// ----------------------------------------------------------------------------
+// sphere test + compaction (warp ballot + block prefix sums)
+// flags: 0 keep, 1 lower, 2 upper
+// ----------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(RT) k_sphere(const T* __restrict__ v, const T* __restrict__ nrm,
+                                               const T* __restrict__ hi, int64_t k, const DevScalars* sc,
+                                               uint8_t* __restrict__ flags, int32_t* __restrict__ bcnt) {
+  __shared__ int32_t wc[RT / 32][3];
+  const int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x;
+  int f = -1;
+  if (j < k) {
+    const double thr = sc->act.thr * static_cast<double>(nrm[j]);
+    const double vj = static_cast<double>(v[j]);
+    f = 0;
+    if (vj < -thr)
+      f = 1;
+    else if (vj > thr && !isinf(static_cast<double>(hi[j])))
+      f = 2;
+    flags[j] = static_cast<uint8_t>(f);
+  }
+  const unsigned bk = __ballot_sync(0xffffffffu, f == 0);
+  const unsigned bl = __ballot_sync(0xffffffffu, f == 1);
+  const unsigned bu = __ballot_sync(0xffffffffu, f == 2);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    wc[warp][0] = __popc(bk);
+    wc[warp][1] = __popc(bl);
+    wc[warp][2] = __popc(bu);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    int s = 0;
+    for (int w = 0; w < RT / 32; ++w) s += wc[w][threadIdx.x];
+    bcnt[3 * blockIdx.x + threadIdx.x] = s;
+  }
+}
+
+// single block: exclusive scan of the per-block (keep, lower, upper) counts
+// in place; totals to sc->n_keep / n_lo / n_up
+__global__ void __launch_bounds__(1024) k_scan(int32_t* bcnt, int nb, DevScalars* sc) {
+  __shared__ int64_t wsum[32][3];
+  __shared__ int64_t carry[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 3) carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    int64_t c[3] = {0, 0, 0};
+    if (i < nb) {
+      c[0] = bcnt[3 * i + 0];
+      c[1] = bcnt[3 * i + 1];
+      c[2] = bcnt[3 * i + 2];
+    }
+    int64_t inc[3] = {c[0], c[1], c[2]};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t nb_ = __shfl_up_sync(0xffffffffu, inc[q], o);
+        if (lane >= o) inc[q] += nb_;
+      }
+      if (lane == 31) wsum[warp][q] = inc[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        int64_t w = wsum[lane][q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t nb_ = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += nb_;
+        }
+        wsum[lane][q] = w;  // inclusive over warps
+      }
+    }
+    __syncthreads();
+    if (i < nb) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int64_t wex = warp ? wsum[warp - 1][q] : 0;
+        bcnt[3 * i + q] = static_cast<int32_t>(carry[q] + wex + inc[q] - c[q]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) carry[threadIdx.x] += wsum[31][threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sc->n_keep = carry[0];
+    sc->n_lo = carry[1];
+    sc->n_up = carry[2];
+  }
+}
+
+// scatter by flag: kept columns -> compacted per-column state (order kept);
+// screened -> x_full snapped to its bound, the (column, bound) list for the
+// z update, and the global sat_lower / sat_upper lists (screening.py:278-288)
+template <typename T>
+struct ColState {
+  int32_t* idx;
+  T* x;
+  T* xprev;
+  T* lo;
+  T* hi;
+  T* nrm;
+  T* att;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flags, const int32_t* __restrict__ boff,
+                                                int64_t k, ColState<T> src, ColState<T> dst, T* __restrict__ x_full,
+                                                int32_t* __restrict__ scr_idx, T* __restrict__ scr_val, int64_t n_lo_total,
+                                                int64_t* __restrict__ sat_lo, int64_t* __restrict__ sat_up) {
+  __shared__ int32_t woff[RT / 32][3];
+  const int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x;
+  const int f = (j < k) ? flags[j] : 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned bq[3] = {__ballot_sync(0xffffffffu, f == 0), __ballot_sync(0xffffffffu, f == 1),
+                          __ballot_sync(0xffffffffu, f == 2)};
+  if (lane == 0) {
+    woff[warp][0] = __popc(bq[0]);
+    woff[warp][1] = __popc(bq[1]);
+    woff[warp][2] = __popc(bq[2]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    int run = 0;
+    for (int w = 0; w < RT / 32; ++w) {
+      const int x = woff[w][threadIdx.x];
+      woff[w][threadIdx.x] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  if (f > 2) return;
+  const int64_t pos = (int64_t)boff[3 * blockIdx.x + f] + woff[warp][f] + __popc(bq[f] & lt);
+  const int32_t id = src.idx[j];
+  if (f == 0) {
+    dst.idx[pos] = id;
+    dst.x[pos] = src.x[j];
+    if (src.xprev) dst.xprev[pos] = src.xprev[j];
+    dst.lo[pos] = src.lo[j];
+    dst.hi[pos] = src.hi[j];
+    dst.nrm[pos] = src.nrm[j];
+    dst.att[pos] = src.att[j];
+  } else if (f == 1) {
+    const T b = src.lo[j];
+    x_full[id] = b;
+    scr_idx[pos] = id;
+    scr_val[pos] = b;
+    sat_lo[pos] = id;
+  } else {
+    const T b = src.hi[j];
+    x_full[id] = b;
+    scr_idx[n_lo_total + pos] = id;
+    scr_val[n_lo_total + pos] = b;
+    sat_up[pos] = id;
+  }
+}
+
+// physical column rewrite: B[:, p] = A[:, idx[p]]  (solvers.py:57)
+template <typename T>
+__global__ void __launch_bounds__(RT) k_gather(const T* __restrict__ A, int64_t lda, const int32_t* __restrict__ idx,
+                                               int64_t k, int64_t m, T* __restrict__ B, int64_t ldb) {
+  using VT = typename V16<T>::type;
+  constexpr int V = V16<T>::n;
+  for (int64_t p = blockIdx.x; p < k; p += gridDim.x) {
+    const VT* s = reinterpret_cast<const VT*>(A + (int64_t)idx[p] * lda);
+    VT* d = reinterpret_cast<VT*>(B + p * ldb);
+    const int64_t nv = (m + V - 1) / V;
+    for (int64_t i = threadIdx.x; i < nv; i += RT) d[i] = __ldcs(s + i);
+  }
+}
+
+// per-column statistics of the original matrix: ||a_j|| (model.py:89-92) and
+// a_j' t (duality.py:350); flags zero columns and non-interior t
+template <typename T>
+__global__ void __launch_bounds__(RT) k_colstats(const T* __restrict__ A, int64_t lda, int64_t n, int64_t m,
+                                                 const T* __restrict__ t, T* __restrict__ nrm, T* __restrict__ att,
+                                                 int check_interior, int* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * RT + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * RT) >> 5;
+  for (int64_t j = w; j < n; j += nw) {
+    const T* col = A + j * lda;
+    double ss = 0.0, st = 0.0;
+    for (int64_t i = lane; i < m; i += 32) {
+      const double a = static_cast<double>(col[i]);
+      ss += a * a;
+      st += a * static_cast<double>(t[i]);
+    }
+    ss = warp_sum<double>(ss);
+    st = warp_sum<double>(st);
+    if (lane == 0) {
+      const double nj = sqrt(ss);
+      nrm[j] = static_cast<T>(nj);
+      att[j] = static_cast<T>(st);
+      if (nj == 0.0) atomicOr(&flags[0], 1);
+      if (check_interior && !(static_cast<double>(static_cast<T>(st)) < -1e-10 * static_cast<double>(static_cast<T>(nj))))
+        atomicOr(&flags[0], 2);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_init_cols(int64_t n, const T* __restrict__ lo, const T* __restrict__ hi, T* __restrict__ x_full,
+                            int32_t* __restrict__ idx, T* __restrict__ x, T* __restrict__ lo2, T* __restrict__ hi2,
+                            const T* __restrict__ nrm, T* __restrict__ nrm2, const T* __restrict__ att,
+                            T* __restrict__ att2) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const T x0 = clip<T>(T(0), lo[j], hi[j]);  // driver.py:389
+    x_full[j] = x0;
+    x[j] = x0;
+    idx[j] = static_cast<int32_t>(j);
+    lo2[j] = lo[j];
+    hi2[j] = hi[j];
+    nrm2[j] = nrm[j];
+    att2[j] = att[j];
+  }
+}
+
+template <typename T>
+__global__ void k_offsets(int64_t m, const T* __restrict__ y, const T* __restrict__ z, T* __restrict__ off,
+                          T* __restrict__ tgt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    off[i] = sub_rn(z[i], y[i]);  // solvers.py:62
+    tgt[i] = sub_rn(y[i], z[i]);  // solvers.py:63
+  }
+}
+
+template <typename T>
+__global__ void k_scatter_x(int64_t k, const int32_t* __restrict__ idx, const T* __restrict__ x, T* __restrict__ x_full) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x)
+    x_full[idx[p]] = x[p];
+}
+
+template <typename T>
+__global__ void k_fill(int64_t n, T* __restrict__ d, T v) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) d[p] = v;
+}
+
+template <typename T>
+__global__ void k_neg(int64_t n, const T* __restrict__ s, T* __restrict__ d) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) d[p] = -s[p];
+}
+
+// bound structure probe: bit0 some lower != 0, bit1 some finite upper != 0,
+// bit2 some upper infinite, bit3 lower not finite, bit4 lower >= upper, bit5 NaN
+template <typename T>
+__global__ void k_bounds_probe(int64_t n, const T* __restrict__ lo, const T* __restrict__ hi, int* __restrict__ out) {
+  int f = 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double l = static_cast<double>(lo[j]), u = static_cast<double>(hi[j]);
+    if (l != 0.0) f |= 1;
+    if (!isinf(u) && u != 0.0) f |= 2;
+    if (isinf(u)) f |= 4;
+    if (!isfinite(l)) f |= 8;
+    if (!(l < u)) f |= 16;
+    if (isnan(l) || isnan(u)) f |= 32;
+  }
+  if (f) atomicOr(out, f);
+}
+
+}  // namespace bx

@@ -1,0 +1,204 @@
+"""The screening solver front end: ``solve`` / ``SolveResult`` / ``TraceRecord``.
+
+Drop-in for /root/reference/pkg/src/boxscreen/driver.py:131-256 (same
+signature, same result and trace fields, same exceptions).  The whole
+Algorithm-1 loop -- primal passes, dual point, gap, certified gap, sphere test,
+compaction, step re-estimate -- runs natively in ``bx_solve``
+(csrc/bx_core.cu) on one CUDA stream; this module owns the device buffers
+(PyTorch) and converts results.  There is no CPU path: a missing native
+library or a machine without CUDA raises.
+"""
+
+import csv
+import ctypes
+import json
+import math
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .model import Problem, QuadraticLoss
+from .solvers import SolverConfig, start_vector
+
+
+@dataclass
+class TraceRecord:
+    round: int
+    elapsed: float
+    primal: float
+    dual: float
+    gap: float
+    preserved_count: int
+    screening_ratio: float
+    newly_screened_lower: int = 0
+    newly_screened_upper: int = 0
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    theta: np.ndarray
+    gap: float
+    rounds: int
+    converged: bool
+    trace: list = field(default_factory=list)
+    sat_lower: np.ndarray = field(default_factory=lambda: np.empty(0, int))
+    sat_upper: np.ndarray = field(default_factory=lambda: np.empty(0, int))
+    info: dict = field(default_factory=dict)
+
+    def to_dict(self):
+        d = asdict(self)
+        d.pop("info", None)
+        d["x"] = self.x.tolist()
+        d["theta"] = self.theta.tolist()
+        d["sat_lower"] = self.sat_lower.tolist()
+        d["sat_upper"] = self.sat_upper.tolist()
+        return d
+
+    def to_json(self, path=None, indent=None):
+        text = json.dumps(self.to_dict(), indent=indent)
+        if path is not None:
+            with open(path, "w") as fh:
+                fh.write(text)
+        return text
+
+
+TRACE_CSV_COLUMNS = ("round", "elapsed_s", "primal", "dual", "gap", "preserved", "ratio")
+
+
+def trace_to_csv(trace, path):
+    """Byte-compatible with driver.py:312-320."""
+    with open(path, "w", newline="") as fh:
+        writer = csv.writer(fh)
+        writer.writerow(TRACE_CSV_COLUMNS)
+        for rec in trace:
+            writer.writerow([rec.round, f"{rec.elapsed:.9f}", f"{rec.primal:.17g}", f"{rec.dual:.17g}",
+                             f"{rec.gap:.17g}", rec.preserved_count, f"{rec.screening_ratio:.17g}"])
+
+
+TRACE_DTYPE = np.dtype([("round", "<i8"), ("elapsed", "<f8"), ("primal", "<f8"), ("dual", "<f8"), ("gap", "<f8"),
+                        ("preserved_count", "<i8"), ("newly_screened_lower", "<i8"),
+                        ("newly_screened_upper", "<i8"), ("eps", "<f8"), ("radius", "<f8"), ("step", "<f8"),
+                        ("certified_gap", "<f8")])
+assert TRACE_DTYPE.itemsize == ctypes.sizeof(nat.TraceRec)
+
+
+@ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p)
+def _start_cb(k, seed, out, user):
+    v = start_vector(int(k), int(seed))
+    ctypes.memmove(out, v.ctypes.data, v.nbytes)
+
+
+class _Session:
+    """One native context over a Problem's device arrays (context manager)."""
+
+    def __init__(self, p, tv=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2202_07258_b200 needs a CUDA device (no CPU fallback)")
+        L = nat.lib()
+        self.p = p
+        d = p.device_arrays()
+        self.dev = d
+        self.torch = torch
+        self.tdt = d["a"].dtype
+        self.dtype_code = nat.BX_F32 if self.tdt == torch.float32 else nat.BX_F64
+        a = d["a"]  # (n, lda) storage of column-major A
+        self.m, self.n = p.m, p.n
+        lda = a.stride(0)
+        nbytes = L.bx_workspace_bytes(self.m, self.n, self.dtype_code)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=a.device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(a.device)
+        self.t_dev = None
+        if tv is not None:
+            self.t_dev = torch.as_tensor(np.asarray(tv.t), device=a.device).to(self.tdt).contiguous()
+        self.ctx = ctypes.c_void_p()
+        st = L.bx_ctx_create(ctypes.byref(self.ctx), self.m, self.n, self.dtype_code, a.data_ptr(), lda,
+                             d["y"].data_ptr(), d["lo"].data_ptr(), d["hi"].data_ptr(),
+                             self.t_dev.data_ptr() if self.t_dev is not None else None,
+                             self.ws.data_ptr(), nbytes, self.stream.cuda_stream)
+        if st != 0:
+            try:
+                nat.check(st, self.ctx, "bx_ctx_create")
+            finally:
+                L.bx_ctx_destroy(self.ctx)
+                self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def close(self):
+        if self.ctx is not None:
+            nat.lib().bx_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def power_iter(self, iters, v0):
+        nat.check(nat.lib().bx_reset(self.ctx), self.ctx, "bx_reset")
+        v0 = np.ascontiguousarray(v0, dtype=np.float64)
+        sig = ctypes.c_double()
+        nat.check(nat.lib().bx_power_iter(self.ctx, iters, v0.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                          ctypes.byref(sig)), self.ctx, "bx_power_iter")
+        return sig.value
+
+    def run(self, cfg, screening, alpha, slack_scale):
+        L = nat.lib()
+        c = nat.SolveCfg()
+        c.kind = nat.KINDS[cfg.kind]
+        c.inner_passes = cfg.inner_passes
+        c.max_rounds = cfg.max_rounds or 0
+        c.gap_tol = cfg.gap_tol
+        c.step_size = cfg.step_size if cfg.step_size is not None else float("nan")
+        c.power_iters = cfg.power_iters
+        c.screening = 1 if screening else 0
+        c.alpha = alpha
+        c.slack_scale = slack_scale
+        cap = min(cfg.max_rounds or 1_000_000, 250_000)
+        trace = np.empty(cap, dtype=TRACE_DTYPE)
+        out = nat.SolveOut()
+        st = L.bx_solve(self.ctx, ctypes.byref(c), _start_cb, None,
+                        trace.ctypes.data_as(ctypes.POINTER(nat.TraceRec)), cap, ctypes.byref(out))
+        nat.check(st, self.ctx, "bx_solve")
+        torch = self.torch
+        dev = self.dev["a"].device
+        x = torch.empty(self.n, dtype=self.tdt, device=dev)
+        theta = torch.empty(self.m, dtype=self.tdt, device=dev)
+        sl = torch.empty(max(out.n_sat_lower, 1), dtype=torch.int64, device=dev)
+        su = torch.empty(max(out.n_sat_upper, 1), dtype=torch.int64, device=dev)
+        nat.check(L.bx_get_state(self.ctx, x.data_ptr(), theta.data_ptr(), sl.data_ptr(), su.data_ptr()),
+                  self.ctx, "bx_get_state")
+        return out, trace[: min(out.rounds, cap)], x, theta, sl[: out.n_sat_lower], su[: out.n_sat_upper]
+
+
+def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None, return_device=False):
+    """Run the chosen primal solver with (or without) dynamic safe screening.
+
+    Same contract as the reference's ``solve`` (driver.py:371-496).  With
+    ``return_device`` the result's x / theta stay CUDA tensors (no host copy).
+    """
+    cfg = cfg or SolverConfig()
+    if cfg.kind == "active-set":
+        raise NotImplementedError("the active-set solver is outside the GPU hot path (SURVEY.md 8f)")
+    if not isinstance(p, Problem):
+        raise TypeError("p must be a Problem")
+    if slack_scale is None:
+        # driver.py:459 for fp64; fp32 needs a slack scaled to its unit round-off
+        slack_scale = 1e-12 if p.dtype == np.float64 else 1e-5
+    with _Session(p, tv=tv) as s:
+        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale)
+    n = p.n
+    trace = [TraceRecord(int(r["round"]), float(r["elapsed"]), float(r["primal"]), float(r["dual"]),
+                         float(r["gap"]), int(r["preserved_count"]), (n - int(r["preserved_count"])) / n,
+                         int(r["newly_screened_lower"]), int(r["newly_screened_upper"])) for r in tr]
+    info = dict(iterations=int(out.iterations), step=float(out.step), sigma=float(out.sigma),
+                kernel_launches=int(out.kernel_launches), trace_arrays=tr)
+    if return_device:
+        xo, tho = x, theta
+    else:
+        xo = x.double().cpu().numpy()
+        tho = theta.double().cpu().numpy()
+    return SolveResult(x=xo, theta=tho, gap=float(out.gap), rounds=int(out.rounds), converged=bool(out.converged),
+                       trace=trace, sat_lower=sl.cpu().numpy(), sat_upper=su.cpu().numpy(), info=info)
