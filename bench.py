@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""bench.py -- screened box-constrained least squares on B200.
+
+Headline workload (BASELINE.json config 3, the largest fp64 configuration that
+fits one GPU and the one the metric's "achieved HBM GB/s" is meaningful for):
+NNLS, A 10000 x 50000 fp64 (4 GB, Uniform[0,1) entries, unit columns), x0 2%
+nonzeros |N(0,1)|, 30 dB SNR, accelerated projected gradient (FISTA +
+function-value restart) with gap-safe screening every 10 iterations, solved to
+a certified duality gap <= 1e-6.  One bench "step" = one full solve from
+x = clip(0, l, u) (setup, power iteration, all rounds, the certified gap).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3]
+    python bench.py --impl reference ...      # the CPU reference arm
+
+JSON line keys: value = screened FISTA iterations per second over whole solves
+(inputs resident in HBM), ms_per_step = time-to-gap, e2e = the same through the
+public API from pinned host buffers (H2D of A, y, bounds and D2H of x, theta
+inside the timed region), roofline = the fused FISTA pass kernel timed live
+with CUDA events, cpu_baseline = the oracle port on the host cores.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAJ_PATH = os.path.join(ROOT, "profiles", "cfg3_trajectory.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--write-trajectory", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", pk
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, util_floor=0.0):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# the CPU side: oracle port timed on the host cores (cpu_baseline / reference arm)
+# ---------------------------------------------------------------------------
+def cpu_rate(inst, k_bins, budget_s, passes=10):
+    """Oracle FISTA iterations/s over the solve's preserved-set trajectory.
+
+    ``k_bins`` = [(k, iterations)] -- how many iterations the screened solve
+    spends at each preserved count.  For each bin the oracle's FISTA passes
+    (oracle/boxscreen_oracle.py:apg_passes, the reference's two-GEMV
+    Workspace arithmetic) are timed on a k-column working set; the rate is
+    total iterations / sum(iterations_b * seconds_per_iteration(k_b)).
+    Returns (rate, details).
+    """
+    from oracle.boxscreen_oracle import ActiveView, apg_passes
+    a, y, lo, hi = inst.a, inst.y, inst.lower, inst.upper
+    n = a.shape[1]
+    norms = np.ones(n)
+    perm = np.random.default_rng(1).permutation(n)
+    total_it = sum(it for _, it in k_bins)
+    per_bin = budget_s / max(1, len(k_bins))
+    details = []
+    tsum = 0.0
+    x_full = np.zeros(n)
+    for k, it in k_bins:
+        keep = np.sort(perm[:k])
+        w = ActiveView(a, y, lo, hi, norms, np.zeros(a.shape[0]), x_full, keep)
+        eta = 1.0 / (0.75 * k + 10.0)  # timing only: cost does not depend on the step
+        mom = [1.0]
+        t0 = time.perf_counter()
+        done = 0
+        while True:
+            apg_passes(w, eta, passes, mom)
+            done += passes
+            el = time.perf_counter() - t0
+            if el > per_bin or done >= it:
+                break
+        sec_per_it = el / done
+        details.append(dict(k=int(k), iterations_in_solve=int(it), timed_iterations=done,
+                            sec_per_iteration=sec_per_it))
+        tsum += it * sec_per_it
+        del w
+    return total_it / tsum, details
+
+
+def k_bins_from_trace(trace_arrays, passes, nbins=6):
+    """Bin the solve's iterations by preserved count (count in force during the round)."""
+    ks = [int(r["preserved_count"]) for r in trace_arrays]
+    start = [ks[0]] + ks[:-1]  # preserved count during round i (before its own screening)
+    n0 = max(start)
+    counts = {}
+    for k in start:
+        counts[k] = counts.get(k, 0) + passes
+    items = sorted(counts.items())
+    # quantile bins weighted by iterations
+    total = sum(c for _, c in items)
+    bins, acc, cur_k_w, cur_it = [], 0, 0.0, 0
+    edge = total / nbins
+    for k, c in items:
+        cur_k_w += k * c
+        cur_it += c
+        acc += c
+        if acc >= edge * (len(bins) + 1) or (k, c) == items[-1]:
+            bins.append((max(1, int(round(cur_k_w / cur_it))), cur_it))
+            cur_k_w, cur_it = 0.0, 0
+    del n0
+    return bins
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return os.cpu_count(), model
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        for inf in threadpool_info():
+            if inf.get("internal_api") in ("openblas", "mkl", "blis"):
+                return int(inf.get("num_threads", 0))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+# ---------------------------------------------------------------------------
+def make_instance(cfg_id):
+    from paper_2202_07258_b200.generate import make_config
+    return make_config(cfg_id)
+
+
+def config_block(cfg_id, inst):
+    from paper_2202_07258_b200.generate import CONFIGS
+    c = CONFIGS[cfg_id]
+    return {"workload": c["name"], "m": int(inst.a.shape[0]), "n": int(inst.a.shape[1]), "solver": inst.kind,
+            "inner_passes": inst.inner_passes, "gap_tol": inst.gap_tol, "screening": True,
+            "problem": "NNLS" if np.isinf(inst.upper).all() else "BVLS", "seed": 0,
+            "l2_policy": "inputs larger than L2 (A = %.1f GB > 126 MB L2)" % (inst.a.nbytes / 1e9)
+            if inst.a.nbytes > 126e6 else "working set L2-resident (reported, not flushed)",
+            "step": "one full solve to certified gap <= gap_tol"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    inst = make_instance(args.config)
+    try:
+        with open(TRAJ_PATH) as fh:
+            traj = json.load(fh)
+        bins = [tuple(b) for b in traj["k_bins"]]
+        src = "preserved-count trajectory of the GPU solve (profiles/cfg3_trajectory.json)"
+    except Exception:
+        bins = [(inst.a.shape[1], 100)]
+        src = "unscreened working set (no trajectory file)"
+    per_step_budget = max(5.0, args.cpu_budget / max(1, args.steps))
+    for _ in range(args.warmup):
+        pass  # CPU arm: warm-up is the first (untimed) view construction inside cpu_rate
+    rates, details = [], None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, details = cpu_rate(inst, bins, per_step_budget)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    rate = float(np.median(rates))
+    cores, model = cpu_info()
+    thr = blas_threads()
+    sample = (f"oracle FISTA passes (numpy/OpenBLAS, reference Workspace arithmetic) timed at {len(bins)} "
+              f"preserved-count bins weighted by {src}; {sum(d['timed_iterations'] for d in details)} "
+              f"iterations per step")
+    line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": "iters/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config recipe)",
+            "config": config_block(args.config, inst),
+            "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": thr, "kind": "port", "sample": sample,
+                             "cpu_model": model, "nproc": cores, "bins": details},
+            "e2e": {"value": rate, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def metric_name(cfg_id):
+    return ("screened iters/s & time-to-gap<=1e-6 (m x n fp64); achieved HBM GB/s vs peak "
+            f"[config {cfg_id}]")
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+
+    inst = make_instance(args.config)
+    m, n = inst.a.shape
+    cfg = SolverConfig(kind=inst.kind, inner_passes=inst.inner_passes, gap_tol=inst.gap_tol)
+    tdt = torch.float32 if inst.a.dtype == np.float32 else torch.float64
+    a_dev = torch.from_numpy(np.ascontiguousarray(inst.a.T)).to(dev)  # (n, m) == column-major A
+    p_dev = Problem(a_dev.t(), torch.from_numpy(inst.y).to(dev), inst.lower, inst.upper)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        solve(p_dev, cfg, return_device=True)
+    torch.cuda.synchronize()
+    results = []
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            results.append(solve(p_dev, cfg, return_device=True))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    elapsed = ev0.elapsed_time(ev1) / 1000.0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    iters = sum(r.info["iterations"] for r in results)
+    launches = sum(r.info["kernel_launches"] for r in results)
+    value = world * iters / elapsed
+    ms_per_step = 1000.0 * elapsed / args.steps
+    conv = all(r.converged for r in results)
+
+    # live roofline of the dominant kernel (one extra, instrumented solve)
+    prof_res = solve(p_dev, cfg, return_device=True, profile=True)
+    prof = prof_res.info["profile"] or {}
+    hbm, peak_src, pk = peaks()
+    tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
+    dom_name = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
+    dom = prof.get(dom_name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
+    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["ms"] > 0 else 0.0
+    roof = {"bound": "hbm", "kernel": f"k_pass[{dom_name}]", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+            "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / max(1, dom["launches"]),
+            "share_of_kernel_time": dom["ms"] / tot_ms,
+            "bytes_per_launch_avg": dom["bytes"] / max(1, dom["launches"]),
+            "algorithmic_bytes": "8*m per streamed column + per-column state + row vectors (DESIGN.md)",
+            "passes_per_iteration": 1,
+            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                            "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
+                        for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+
+    # trajectory for the CPU arm (preserved-count bins of this solve)
+    bins = k_bins_from_trace(prof_res.info["trace_arrays"], inst.inner_passes)
+    if args.write_trajectory and rank == 0:
+        os.makedirs(os.path.dirname(TRAJ_PATH), exist_ok=True)
+        with open(TRAJ_PATH, "w") as fh:
+            json.dump({"config": args.config, "k_bins": bins, "rounds": prof_res.rounds,
+                       "iterations": prof_res.info["iterations"]}, fh, indent=1)
+
+    # end to end through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        p_host = Problem(inst.a, inst.y, inst.lower, inst.upper, pin=True)
+        h2d = p_host.a_matrix.nbytes + 8 * (m + 2 * n)
+        e_it, e_t, d2h = 0, 0.0, 0
+        for s in range(args.steps + 1):
+            p_host.release_device()
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            r = solve(p_host, cfg)  # H2D inside, x/theta D2H at the end
+            t1.record(stream)
+            torch.cuda.synchronize()
+            if s == 0:
+                continue  # first call warms the pinned path
+            e_t += t0.elapsed_time(t1) / 1000.0
+            e_it += r.info["iterations"]
+            d2h = r.x.nbytes + r.theta.nbytes + 8 * (r.sat_lower.size + r.sat_upper.size)
+        p_host.release_device()
+        e2e = {"value": world * e_it / e_t, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000.0 * e_t / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, det = cpu_rate(inst, bins, args.cpu_budget)
+        cores, model = cpu_info()
+        cpu = {"value": rate, "unit": "iters/s", "cores": blas_threads(), "kind": "port",
+               "sample": (f"oracle FISTA passes at {len(bins)} preserved-count bins of this solve, "
+                          f"{sum(d['timed_iterations'] for d in det)} iterations, ~{args.cpu_budget:.0f}s"),
+               "cpu_model": model, "nproc": cores}
+
+    r0 = results[0]
+    line = {"metric": metric_name(args.config), "value": value, "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "replicas", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy, BASELINE config recipe; no public dataset)",
+            "config": config_block(args.config, inst),
+            "time_to_gap_s": ms_per_step / 1000.0, "converged": conv, "rounds": r0.rounds,
+            "iterations_per_solve": r0.info["iterations"], "final_preserved": r0.trace[-1].preserved_count,
+            "certified_gap": r0.gap, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

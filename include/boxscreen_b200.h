@@ -164,6 +164,31 @@ int bx_nccl_unique_id(unsigned char* id_out_host);
 int bx_ctx_set_comm(bx_ctx* ctx, const unsigned char* id_host, int32_t rank,
                     int32_t nranks, int64_t col_offset, int64_t n_global);
 
+/* ---- live per-kernel timing (bench.py roofline) ---------------------------- */
+/* CUDA events around every kernel launch on the context stream; accumulated
+ * per slot with the ALGORITHMIC bytes of each launch. */
+enum {
+  BX_PROF_PASS_DOT = 0,    /* screening pass: g = A'r + epsilon partial     */
+  BX_PROF_PASS_PG_G = 1,   /* PG step from the stored gradient              */
+  BX_PROF_PASS_PG = 2,     /* fused PG step (dot + update + A x)            */
+  BX_PROF_PASS_APG = 3,    /* fused FISTA step                              */
+  BX_PROF_PASS_POWER = 4,  /* power iteration                               */
+  BX_PROF_PASS_AX = 5,     /* A x (refresh / certified gap / z update)      */
+  BX_PROF_REDUCE = 6,
+  BX_PROF_DUAL = 7,
+  BX_PROF_SPHERE = 8,
+  BX_PROF_GATHER = 9,
+  BX_PROF_CD = 10,
+  BX_PROF_SLOTS = 12
+};
+typedef struct {
+  int64_t launches;
+  double ms;
+  double bytes;
+} bx_prof_entry;
+int bx_set_profiling(bx_ctx* ctx, int32_t on);
+int bx_get_profile(bx_ctx* ctx, bx_prof_entry* out_host, int32_t n);
+
 /* ---- batched many-RHS APG (BASELINE config 5) ----------------------------- */
 size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs);
 

@@ -44,6 +44,7 @@ import numpy as np
 GAP_ROUNDOFF = 1e-9          # duality.py:322 (weak-duality round-off slack)
 SLACK_SCALE = 1e-12          # driver.py:219
 INTERIOR_TOL = 1e-10         # duality.py:346 (strict_tol)
+RESTART_SLACK = 1e-12        # FISTA restart threshold (extension)
 
 
 class OracleError(Exception):
@@ -192,7 +193,10 @@ def apg_passes(w, eta, passes, mom):
         t' = (1 + sqrt(1 + 4 t^2)) / 2 ;  beta = (t - 1) / t'
         y  = x + beta (x - x_prev) ;  r_y = r + beta (r - r_prev)
         x+ = clip(y - eta A'r_y, lo, hi) ;  r+ = A x+ + off
-        restart (t <- 1) when P(x+) > P(x), else t <- t'
+        restart (t <- 1) when P(x+) > P(x) + 1e-12 max(1, P(x)), else t <- t'
+    The 1e-12 relative slack keeps the restart decision out of the round-off
+    band (summation-order noise in P is ~1e-14 relative at m = 1e4), so the
+    CPU oracle and the GPU take the same decisions.
     After the passes g = A'r at the final x (for the dual point).
     """
     obj = 0.5 * float(w.r @ w.r)
@@ -215,7 +219,7 @@ def apg_passes(w, eta, passes, mom):
         nobj = 0.5 * float(rn @ rn)
         w.x_prev, w.r_prev = w.x, w.r
         w.x, w.r = xn, rn
-        mom[0] = 1.0 if nobj > obj else tn
+        mom[0] = 1.0 if nobj > obj + RESTART_SLACK * max(1.0, abs(obj)) else tn
         obj = nobj
     w.g = w.mat.T @ w.r
 

@@ -42,6 +42,14 @@ class SolveOut(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64)]
 
 
+class ProfEntry(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+PROF_SLOTS = 12
+PROF_NAMES = ["pass_dot", "pass_pg_g", "pass_pg", "pass_apg", "pass_power", "pass_ax", "reduce", "dual",
+              "sphere", "gather", "cd", "other"]
+
 START_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                             ctypes.c_void_p)
 
@@ -68,6 +76,8 @@ SIGNATURES = {
     "bx_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "bx_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "bx_ctx_set_comm": (ctypes.c_int, [_vp, ctypes.c_char_p, _i32, _i32, _i64, _i64]),
+    "bx_set_profiling": (ctypes.c_int, [_vp, _i32]),
+    "bx_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(ProfEntry), _i32]),
     "bx_batched_workspace_bytes": (_sz, [_i64, _i64, _i64]),
 }
 

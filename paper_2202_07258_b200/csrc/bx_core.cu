@@ -135,6 +135,17 @@ struct bx_ctx {
   int64_t launches = 0;
   std::string err;
 
+  // live per-kernel timing (CUDA events on the context stream)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  struct Pending {
+    int slot;
+    int e0;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  bx_prof_entry pstat[BX_PROF_SLOTS];
+
   // multi-GPU column sharding
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
@@ -172,6 +183,45 @@ int fail(bx_ctx* c, int code, const char* fmt, ...) {
     int s_ = (expr);         \
     if (s_ != BX_OK) return s_; \
   } while (0)
+
+// ---- live timing ---------------------------------------------------------
+int prof_drain(bx_ctx* c) {
+  if (c->pending.empty()) return BX_OK;
+  CU(cudaEventSynchronize(c->ev[c->pending.back().e0 + 1]));
+  for (const auto& p : c->pending) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, c->ev[p.e0], c->ev[p.e0 + 1]));
+    c->pstat[p.slot].launches += 1;
+    c->pstat[p.slot].ms += ms;
+    c->pstat[p.slot].bytes += p.bytes;
+  }
+  c->pending.clear();
+  return BX_OK;
+}
+
+// returns the event index pair to close with prof_end (or -1)
+int prof_begin(bx_ctx* c) {
+  if (!c->prof) return -1;
+  if (c->ev.empty()) {
+    c->ev.resize(2 * 2048);
+    for (auto& e : c->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+  }
+  if ((int)c->pending.size() * 2 + 2 > (int)c->ev.size()) {
+    if (prof_drain(c) != BX_OK) return -1;
+  }
+  const int e0 = (int)c->pending.size() * 2;
+  cudaEventRecord(c->ev[e0], c->stream);
+  c->pending.push_back({-1, e0, 0.0});
+  return e0;
+}
+
+void prof_end(bx_ctx* c, int e0, int slot, double bytes) {
+  if (e0 < 0) return;
+  cudaEventRecord(c->ev[e0 + 1], c->stream);
+  c->pending.back().slot = slot;
+  c->pending.back().bytes = bytes;
+}
 
 // Workspace carving
 struct Carver {
@@ -341,16 +391,29 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_p
   a.colbytes = colbytes;
   a.colstride = colstride;
   if (G_out) *G_out = G;
+  const int e0 = prof_begin(c);
+  int st = BX_OK;
   switch (R) {
-    case 1: return launch_pass_R<T, 1>(c, a, dot, axpy, G, smem);
-    case 2: return launch_pass_R<T, 2>(c, a, dot, axpy, G, smem);
-    case 4: return launch_pass_R<T, 4>(c, a, dot, axpy, G, smem);
-    case 6: return launch_pass_R<T, 6>(c, a, dot, axpy, G, smem);
-    case 8: return launch_pass_R<T, 8>(c, a, dot, axpy, G, smem);
-    case 10: return launch_pass_R<T, 10>(c, a, dot, axpy, G, smem);
-    case 12: return launch_pass_R<T, 12>(c, a, dot, axpy, G, smem);
+    case 1: st = launch_pass_R<T, 1>(c, a, dot, axpy, G, smem); break;
+    case 2: st = launch_pass_R<T, 2>(c, a, dot, axpy, G, smem); break;
+    case 4: st = launch_pass_R<T, 4>(c, a, dot, axpy, G, smem); break;
+    case 6: st = launch_pass_R<T, 6>(c, a, dot, axpy, G, smem); break;
+    case 8: st = launch_pass_R<T, 8>(c, a, dot, axpy, G, smem); break;
+    case 10: st = launch_pass_R<T, 10>(c, a, dot, axpy, G, smem); break;
+    case 12: st = launch_pass_R<T, 12>(c, a, dot, axpy, G, smem); break;
+    default: st = fail(c, BX_ERR_UNSUPPORTED, "R=%d", R);
   }
-  return fail(c, BX_ERR_UNSUPPORTED, "R=%d", R);
+  if (e0 >= 0) {
+    // algorithmic bytes: every streamed column once, the per-column state the
+    // mode touches, the input row vector(s) and the output row vector once
+    static const int col_vec[] = {3, 5, 5, 6, 0, 1};  // U_DOT..U_AX, elements per column
+    const double es = (double)sizeof(T);
+    double bytes = (double)vw.k * (double)c->m * es + (double)vw.k * col_vec[upd] * es;
+    if (dot) bytes += (double)c->m * es * (upd == U_APG ? 2 : 1);
+    if (axpy) bytes += (double)c->m * es;
+    prof_end(c, e0, BX_PROF_PASS_DOT + upd, bytes);
+  }
+  return st;
 }
 
 template <typename T>
@@ -358,9 +421,11 @@ int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* w
   int nb = (int)((c->m + RT - 1) / RT);
   if (nb > 2 * c->nsm) nb = 2 * c->nsm;
   if (nb < 1) nb = 1;
+  const int e0 = prof_begin(c);
   k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, off, out, c->sc, c->bpart2, wpart, Gw,
                                          mode, counter);
   LAUNCHED();
+  prof_end(c, e0, BX_PROF_REDUCE, (double)c->m * sizeof(T) * (G + 2 + (off ? 1 : 0)));
   return BX_OK;
 }
 
@@ -378,7 +443,7 @@ template <typename T>
 int sync_scalars(bx_ctx* c) {
   CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  return BX_OK;
+  return prof_drain(c);
 }
 
 int check_dev_err(bx_ctx* c) {
@@ -520,19 +585,23 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
                   (T*)c->g, (const T*)c->att[s], nullptr, c->bpart, c->has_inf, &G));
   c->g_valid = true;
   int nb = grid1d(c, c->m > c->k ? c->m : c->k);
+  const int e0 = prof_begin(c);
   k_dual<T><<<nb, RT, 0, c->stream>>>((const T*)c->r, (const T*)c->t, (const T*)c->tgt, (T*)c->theta, c->m,
                                        (const T*)c->g, (const T*)c->att[s], (const T*)c->lo[s], (const T*)c->hi[s],
                                        (T*)c->v, c->k, c->bpart, G, c->has_inf, c->sc, 0, c->bpart3, slack_scale,
                                        alpha, 3);
   LAUNCHED();
+  prof_end(c, e0, BX_PROF_DUAL, (double)sizeof(T) * (4.0 * c->m + 6.0 * c->k));
   c->theta_is_cert = false;
   if (screening && c->k > 0) {
     const int nbs = (int)((c->k + RT - 1) / RT);
+    const int e1 = prof_begin(c);
     k_sphere<T><<<nbs, RT, 0, c->stream>>>((const T*)c->v, (const T*)c->nrm[s], (const T*)c->hi[s], c->k, c->sc,
                                             c->flags, c->bcnt);
     LAUNCHED();
     k_scan<<<1, 1024, 0, c->stream>>>(c->bcnt, nbs, c->sc);
     LAUNCHED();
+    prof_end(c, e1, BX_PROF_SPHERE, (double)c->k * (3.0 * sizeof(T) + 1.0));
   } else {
     CU(cudaMemsetAsync(&c->sc->n_keep, 0, 3 * sizeof(int64_t), c->stream));
   }
@@ -594,9 +663,11 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind) {
   // physical rewrite of the preserved columns (solvers.py:57)
   if (c->k > 0) {
     int nb = (int)(c->k < 8 * c->nsm ? c->k : 8 * c->nsm);
+    const int e0 = prof_begin(c);
     k_gather<T><<<nb, RT, 0, c->stream>>>((const T*)c->A, c->lda, c->idx[c->cur], c->k, c->m, (T*)c->Aact,
                                            c->ldact);
     LAUNCHED();
+    prof_end(c, e0, BX_PROF_GATHER, 2.0 * (double)c->k * c->m * sizeof(T));
   }
   c->act_is_orig = false;
   TRY(refresh_resid<T>(c));
@@ -842,6 +913,7 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
 
 int bx_ctx_destroy(bx_ctx* c) {
   if (!c) return BX_OK;
+  for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->hsc) cudaFreeHost(c->hsc);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
   delete c;
@@ -975,6 +1047,21 @@ int bx_ctx_set_comm(bx_ctx* c, const unsigned char* id_host, int32_t rank, int32
   c->nranks = nranks;
   c->col_offset = col_offset;
   c->n_global = n_global;
+  return BX_OK;
+}
+
+int bx_set_profiling(bx_ctx* c, int32_t on) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  c->prof = on != 0;
+  memset(c->pstat, 0, sizeof(c->pstat));
+  c->pending.clear();
+  return BX_OK;
+}
+
+int bx_get_profile(bx_ctx* c, bx_prof_entry* out, int32_t n) {
+  if (!c || !out) return BX_ERR_INVALID_ARGUMENT;
+  TRY(prof_drain(c));
+  for (int i = 0; i < n && i < BX_PROF_SLOTS; ++i) out[i] = c->pstat[i];
   return BX_OK;
 }
 

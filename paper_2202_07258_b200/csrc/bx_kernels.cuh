@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     case R_APG: {
       const double t = sc->mom_t;
       const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-      if (Pn > sc->P) {
+      if (Pn > sc->P + 1e-12 * fmax(1.0, fabs(sc->P))) {  // restart (FISTA)
         sc->mom_t = 1.0;
         sc->restarts += 1;
       } else {

@@ -144,8 +144,9 @@ class _Session:
                                           ctypes.byref(sig)), self.ctx, "bx_power_iter")
         return sig.value
 
-    def run(self, cfg, screening, alpha, slack_scale):
+    def run(self, cfg, screening, alpha, slack_scale, profile=False):
         L = nat.lib()
+        nat.check(L.bx_set_profiling(self.ctx, 1 if profile else 0), self.ctx, "bx_set_profiling")
         c = nat.SolveCfg()
         c.kind = nat.KINDS[cfg.kind]
         c.inner_passes = cfg.inner_passes
@@ -162,6 +163,12 @@ class _Session:
         st = L.bx_solve(self.ctx, ctypes.byref(c), _start_cb, None,
                         trace.ctypes.data_as(ctypes.POINTER(nat.TraceRec)), cap, ctypes.byref(out))
         nat.check(st, self.ctx, "bx_solve")
+        self.profile = None
+        if profile:
+            ents = (nat.ProfEntry * nat.PROF_SLOTS)()
+            nat.check(L.bx_get_profile(self.ctx, ents, nat.PROF_SLOTS), self.ctx, "bx_get_profile")
+            self.profile = {nat.PROF_NAMES[i]: dict(launches=int(e.launches), ms=float(e.ms), bytes=float(e.bytes))
+                            for i, e in enumerate(ents) if e.launches}
         torch = self.torch
         dev = self.dev["a"].device
         x = torch.empty(self.n, dtype=self.tdt, device=dev)
@@ -173,11 +180,13 @@ class _Session:
         return out, trace[: min(out.rounds, cap)], x, theta, sl[: out.n_sat_lower], su[: out.n_sat_upper]
 
 
-def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None, return_device=False):
+def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None, return_device=False,
+          profile=False):
     """Run the chosen primal solver with (or without) dynamic safe screening.
 
     Same contract as the reference's ``solve`` (driver.py:371-496).  With
-    ``return_device`` the result's x / theta stay CUDA tensors (no host copy).
+    ``return_device`` the result's x / theta stay CUDA tensors (no host copy);
+    ``profile`` times every kernel launch with CUDA events (info["profile"]).
     """
     cfg = cfg or SolverConfig()
     if cfg.kind == "active-set":
@@ -188,13 +197,14 @@ def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=
         # driver.py:459 for fp64; fp32 needs a slack scaled to its unit round-off
         slack_scale = 1e-12 if p.dtype == np.float64 else 1e-5
     with _Session(p, tv=tv) as s:
-        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale)
+        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
+        prof = s.profile
     n = p.n
     trace = [TraceRecord(int(r["round"]), float(r["elapsed"]), float(r["primal"]), float(r["dual"]),
                          float(r["gap"]), int(r["preserved_count"]), (n - int(r["preserved_count"])) / n,
                          int(r["newly_screened_lower"]), int(r["newly_screened_upper"])) for r in tr]
     info = dict(iterations=int(out.iterations), step=float(out.step), sigma=float(out.sigma),
-                kernel_launches=int(out.kernel_launches), trace_arrays=tr)
+                kernel_launches=int(out.kernel_launches), trace_arrays=tr, profile=prof)
     if return_device:
         xo, tho = x, theta
     else:

@@ -1,5 +1,7 @@
 """GPU parity: the CUDA path through the C ABI vs the CPU oracle, round by round."""
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -24,7 +26,7 @@ def _solve_both(a, y, lo, hi, kind, passes=10, tol=1e-8, screening=True, max_rou
 @pytest.mark.parametrize("kind", ["pg", "apg"])
 @pytest.mark.parametrize("screening", [True, False])
 def test_small_trajectories(family, kind, screening):
-    rng = np.random.default_rng(hash((family, kind, screening)) % 2**32)
+    rng = np.random.default_rng(zlib.crc32(f"{family}-{kind}-{screening}".encode()))
     for _ in range(4):
         n = int(rng.integers(3, 31))
         m = int(rng.integers(n, 61))
