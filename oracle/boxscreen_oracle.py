@@ -246,12 +246,14 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
     hi = np.broadcast_to(np.asarray(hi, dtype=float), (n,)).copy()
     inf_mask = np.isinf(hi)
     norms = column_norms(a)
-    if np.any(norms == 0.0):
-        raise OracleError("ZeroColumn", f"zero column at {int(np.argmin(norms))}")
     att_full = None
     if inf_mask.any():
+        # the translation vector is built before the screening state
+        # (driver.py:381-392), so NoInteriorPoint precedes ZeroColumn
         t = -np.ones(m) if t is None else np.asarray(t, dtype=float).ravel()
         att_full = translation_att(a, t, norms)
+    if np.any(norms == 0.0):
+        raise OracleError("ZeroColumn", f"zero column at {int(np.argmin(norms))}")
     if kind not in ("pg", "cd", "apg"):
         raise ValueError(kind)
     x_full = np.clip(np.zeros(n), lo, hi)

@@ -418,8 +418,9 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_p
 
 template <typename T>
 int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* wpart, int Gw, int counter) {
-  int nb = (int)((c->m + RT - 1) / RT);
-  if (nb > 2 * c->nsm) nb = 2 * c->nsm;
+  const int64_t rb = 32 * (16 / (int64_t)sizeof(T));
+  int nb = (int)((c->m + rb - 1) / rb);
+  if (nb > 4 * c->nsm) nb = 4 * c->nsm;
   if (nb < 1) nb = 1;
   const int e0 = prof_begin(c);
   k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, off, out, c->sc, c->bpart2, wpart, Gw,

@@ -447,59 +447,19 @@ __device__ __forceinline__ double block_sum_rt(double v, double* sh) {
   return t;  // valid in thread 0
 }
 
+// Blocks own RB = 32*V consecutive rows; the 8 warps split the G partial rows
+// (warp w sums partials w, w+8, ...), then the 8 slice sums are combined in
+// warp order -- a fixed summation order, so results are deterministic.
+constexpr int RED_SLICES = RT / 32;
+
 template <typename T>
-__global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64_t ldp, int G, int64_t m,
-                                               const T* __restrict__ off, T* __restrict__ out,
-                                               DevScalars* sc, double* bpart, const double* wpart,
-                                               int Gw, int mode, int counter) {
-  __shared__ double sh[RT / 32];
-  __shared__ bool last;
-  double scale_div = 1.0;
-  if (mode == R_POWER) {
-    double nw2 = 0.0;
-    for (int b = 0; b < Gw; ++b) nw2 += wpart[b];
-    scale_div = sqrt(nw2);
-  }
-  double sq = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < m; i += (int64_t)gridDim.x * RT) {
-    T s = T(0);
-    int bb = 0;
-    for (; bb + 4 <= G; bb += 4) {
-      const T a0 = part[(int64_t)(bb + 0) * ldp + i];
-      const T a1 = part[(int64_t)(bb + 1) * ldp + i];
-      const T a2 = part[(int64_t)(bb + 2) * ldp + i];
-      const T a3 = part[(int64_t)(bb + 3) * ldp + i];
-      s += a0;
-      s += a1;
-      s += a2;
-      s += a3;
-    }
-    for (; bb < G; ++bb) s += part[(int64_t)bb * ldp + i];
-    if (off) s = add_rn(s, off[i]);
-    if (mode == R_POWER) s = static_cast<T>(static_cast<double>(s) / scale_div);
-    out[i] = s;
-    sq += static_cast<double>(s) * static_cast<double>(s);
-  }
-  if (mode == R_PLAIN) return;
-  const double tot = block_sum_rt(sq, sh);
-  if (threadIdx.x == 0) {
-    bpart[blockIdx.x] = tot;
-    __threadfence();
-    const unsigned prev = atomicAdd(&sc->counters[counter], 1u);
-    last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  double total = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) total += *((volatile double*)&bpart[b]);
-  const double Pn = 0.5 * total;
+__device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, double Pn, double scale_div) {
   switch (mode) {
     case R_SET:
       sc->P = Pn;
       break;
     case R_PG:
-      if (Pn > sc->P + 1e-9) {
+      if (Pn > sc->P + 1e-9) {  // solvers.py:111-114
         sc->P_prev = sc->P;
         set_err(sc, DE_STEP_TOO_LARGE);
       }
@@ -527,6 +487,86 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     default:
       break;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64_t ldp, int G, int64_t m,
+                                               const T* __restrict__ off, T* __restrict__ out,
+                                               DevScalars* sc, double* bpart, const double* wpart,
+                                               int Gw, int mode, int counter) {
+  using VT = typename V16<T>::type;
+  constexpr int V = V16<T>::n;
+  constexpr int RB = 32 * V;
+  __shared__ T sl[RED_SLICES][RB];
+  __shared__ double sh[RT / 32];
+  __shared__ double s_div;
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (mode == R_POWER && warp == 0) {
+    double nw2 = 0.0;
+    for (int b = lane; b < Gw; b += 32) nw2 += wpart[b];
+    // fixed-shape tree: deterministic
+    nw2 = warp_sum<double>(nw2);
+    if (lane == 0) s_div = sqrt(nw2);
+  }
+  double sq = 0.0;
+  for (int64_t r0 = (int64_t)blockIdx.x * RB; r0 < m; r0 += (int64_t)gridDim.x * RB) {
+    const int64_t row = r0 + lane * V;
+    T acc[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] = T(0);
+    if (row < m) {
+      int bb = warp;
+      for (; bb + 3 * RED_SLICES < G; bb += 4 * RED_SLICES) {
+        T q0[V], q1[V], q2[V], q3[V];
+        unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)bb * ldp + row), q0);
+        unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)(bb + RED_SLICES) * ldp + row), q1);
+        unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)(bb + 2 * RED_SLICES) * ldp + row), q2);
+        unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)(bb + 3 * RED_SLICES) * ldp + row), q3);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] += q0[e] + q1[e] + q2[e] + q3[e];
+      }
+      for (; bb < G; bb += RED_SLICES) {
+        T q[V];
+        unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)bb * ldp + row), q);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] += q[e];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) sl[warp][lane * V + e] = acc[e];
+    __syncthreads();
+    if (mode == R_POWER) {
+      // all threads read the divisor after the first barrier
+    }
+    for (int q = threadIdx.x; q < RB; q += RT) {
+      const int64_t i = r0 + q;
+      if (i < m) {
+        T s = sl[0][q];
+#pragma unroll
+        for (int w = 1; w < RED_SLICES; ++w) s += sl[w][q];
+        if (off) s = add_rn(s, off[i]);
+        if (mode == R_POWER) s = static_cast<T>(static_cast<double>(s) / s_div);
+        out[i] = s;
+        sq += static_cast<double>(s) * static_cast<double>(s);
+      }
+    }
+    __syncthreads();
+  }
+  if (mode == R_PLAIN) return;
+  const double tot = block_sum_rt(sq, sh);
+  if (threadIdx.x == 0) {
+    bpart[blockIdx.x] = tot;
+    __threadfence();
+    const unsigned prev = atomicAdd(&sc->counters[counter], 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double total = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) total += *((volatile double*)&bpart[b]);
+  finalize_objective<T>(sc, mode, 0.5 * total, mode == R_POWER ? s_div : 0.0);
   sc->counters[counter] = 0u;
 }
 
@@ -541,39 +581,57 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
                                              T* __restrict__ v, int64_t k, const double* eps_part, int Ge,
                                              int has_inf, DevScalars* sc, int which, double* bpart,
                                              double slack_scale, double alpha, int counter) {
-  __shared__ double sh[RT / 32];
+  __shared__ double sh[RT / 32][4];
+  __shared__ double s_eps;
   __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   DualOut* out = which ? &sc->cert : &sc->act;
-  double eps = 0.0;
-  if (has_inf)
-    for (int b = 0; b < Ge; ++b) eps = fmax(eps, eps_part[b]);
+  if (warp == 0) {
+    double e = 0.0;
+    if (has_inf)
+      for (int b = lane; b < Ge; b += 32) e = fmax(e, eps_part[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) s_eps = e;  // max is order independent: exact
+  }
+  __syncthreads();
+  const double eps = s_eps;
   const T te = static_cast<T>(eps);
   double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
   const int64_t stride = (int64_t)gridDim.x * RT;
   for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < m; i += stride) {
-    T th = -r[i];
-    if (eps > 0.0) th = add_rn(th, mul_rn(te, t[i]));
+    T th = -r[i];  // driver.py:424
+    if (eps > 0.0) th = add_rn(th, mul_rn(te, t[i]));  // driver.py:434-435
     theta[i] = th;
     s1 += static_cast<double>(th) * static_cast<double>(tgt[i]);
     s2 += static_cast<double>(th) * static_cast<double>(th);
   }
   for (int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x; j < k; j += stride) {
-    T vj = -g[j];
-    if (has_inf) vj = add_rn(vj, mul_rn(te, att[j]));
+    T vj = -g[j];  // driver.py:425
+    if (has_inf) vj = add_rn(vj, mul_rn(te, att[j]));  // driver.py:436
     v[j] = vj;
     const double vd = static_cast<double>(vj);
     s3 += static_cast<double>(lo[j]) * fmin(vd, 0.0);
     if (!isinf(static_cast<double>(hi[j]))) s4 += static_cast<double>(hi[j]) * fmax(vd, 0.0);
   }
-  const double b1 = block_sum_rt(s1, sh);
-  const double b2 = block_sum_rt(s2, sh);
-  const double b3 = block_sum_rt(s3, sh);
-  const double b4 = block_sum_rt(s4, sh);
+  s1 = warp_sum<double>(s1);
+  s2 = warp_sum<double>(s2);
+  s3 = warp_sum<double>(s3);
+  s4 = warp_sum<double>(s4);
+  if (lane == 0) {
+    sh[warp][0] = s1;
+    sh[warp][1] = s2;
+    sh[warp][2] = s3;
+    sh[warp][3] = s4;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double a = 0.0;
+    for (int w = 0; w < RT / 32; ++w) a += sh[w][threadIdx.x];
+    bpart[4 * blockIdx.x + threadIdx.x] = a;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    bpart[4 * blockIdx.x + 0] = b1;
-    bpart[4 * blockIdx.x + 1] = b2;
-    bpart[4 * blockIdx.x + 2] = b3;
-    bpart[4 * blockIdx.x + 3] = b4;
     __threadfence();
     const unsigned prev = atomicAdd(&sc->counters[counter], 1u);
     last = (prev == gridDim.x - 1);
@@ -589,12 +647,13 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
     t3 += vb[4 * b + 2];
     t4 += vb[4 * b + 3];
   }
+  // _reduced_dual (driver.py:360-368) / eval_dual (duality.py:401-422)
   double dual = t1 - 0.5 * t2;
   dual -= t3;
   dual -= t4;
   const double primal = which ? sc->cert_P : sc->P;
   const double raw = primal - dual;
-  if (raw < -1e-9) set_err(sc, DE_INTERNAL_CONSISTENCY);
+  if (raw < -1e-9) set_err(sc, DE_INTERNAL_CONSISTENCY);  // clamp_gap, duality.py:452
   const double gap = fmax(raw, 0.0);
   out->primal = primal;
   out->dual = dual;
@@ -602,8 +661,8 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
   out->gap = gap;
   out->eps = eps;
   out->th_norm2 = t2;
-  out->radius = sqrt(2.0 * gap / alpha);
-  out->slack = slack_scale * fmax(1.0, sqrt(t2));
+  out->radius = sqrt(2.0 * gap / alpha);                 // screening.py:11-15
+  out->slack = slack_scale * fmax(1.0, sqrt(t2));        // driver.py:459
   out->thr = out->radius + out->slack;
   sc->counters[counter] = 0u;
 }

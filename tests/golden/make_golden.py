@@ -1,0 +1,178 @@
+"""Generate the golden fixtures from the REAL reference package.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference (`boxscreen` from
+/root/reference/pkg/src), runs its `solve` on seeded inputs and stores inputs
+(or the seed that regenerates them) and outputs as compressed .npz files next
+to this script.  The GPU box never reads /root/reference: tests load these
+fixtures instead.
+
+Fixtures
+  small_cases.npz     36 small instances (nnls/bvls/mixed x pg/cd x screening
+                      on/off x 3 seeds): inputs, per-round trace, final state
+  kat_cases.npz       known-answer cases from the reference test-suite shapes
+  optimum_cases.npz   high-accuracy optima (active set, certified gap 1e-12)
+                      for solution-level pinning of the FISTA extension
+  cfg1_trace.npz      BASELINE config 1 at full size (1000 x 2000, PG, 10
+                      passes/round, gap 1e-6): the reference's whole trajectory
+  cfg2_trace.npz      BASELINE config 2 at full size (2000 x 4000, CD, gap 1e-7)
+"""
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, REF)
+
+import boxscreen as bs  # noqa: E402  (the reference)
+
+from conftest import small_instance  # noqa: E402
+from paper_2202_07258_b200.generate import make_config  # noqa: E402
+
+
+def trace_arrays(res):
+    tr = res.trace
+    return dict(primal=np.array([r.primal for r in tr]), dual=np.array([r.dual for r in tr]),
+                gap=np.array([r.gap for r in tr]), preserved=np.array([r.preserved_count for r in tr], np.int32),
+                new_lower=np.array([r.newly_screened_lower for r in tr], np.int32),
+                new_upper=np.array([r.newly_screened_upper for r in tr], np.int32))
+
+
+def digest(*arrs):
+    h = hashlib.sha256()
+    for a in arrs:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def small_cases():
+    out = {}
+    i = 0
+    for family in ("nnls", "bvls", "mixed"):
+        for kind in ("pg", "cd"):
+            for seed in range(3):
+                rng = np.random.default_rng(1000 + 17 * seed + (0 if family == "nnls" else 7 if family == "bvls" else 13))
+                n = int(rng.integers(3, 31))
+                m = int(rng.integers(n, 61))
+                a, y, lo, hi = small_instance(rng, m, n, family)
+                p = bs.Problem(a, y, lo, hi)
+                for screening in (True, False):
+                    res = bs.solve(p, bs.SolverConfig(kind=kind, gap_tol=1e-8, inner_passes=10),
+                                   screening=screening)
+                    key = f"c{i:03d}"
+                    meta = np.array([family, kind, str(int(screening))])
+                    out[key + "_meta"] = meta
+                    out[key + "_a"] = a
+                    out[key + "_y"] = y
+                    out[key + "_lo"] = lo
+                    out[key + "_hi"] = hi
+                    for k, v in trace_arrays(res).items():
+                        out[f"{key}_tr_{k}"] = v
+                    out[key + "_x"] = res.x
+                    out[key + "_theta"] = res.theta
+                    out[key + "_final"] = np.array([res.gap, res.rounds, float(res.converged)])
+                    out[key + "_sat_lower"] = np.asarray(res.sat_lower, np.int64)
+                    out[key + "_sat_upper"] = np.asarray(res.sat_upper, np.int64)
+                    i += 1
+    out["count"] = np.array(i)
+    np.savez_compressed(os.path.join(HERE, "small_cases.npz"), **out)
+    print("small_cases:", i)
+
+
+def kat_cases():
+    """Known answers on the reference suite's tiny shapes, recomputed by the reference."""
+    cases = [
+        ("nnls1d_immediate", [[1.0]], [-1.0], 0.0, np.inf, "cd", 1),   # test_driver.py:15-22
+        ("box1d_step1", [[1.0]], [3.0], 0.0, 1.0, "pg", 1),            # test_solvers.py:78-83
+        ("nnls1d_cd", [[1.0]], [2.0], 0.0, np.inf, "cd", 1),           # test_solvers.py:108-113
+        ("identity_nnls", np.eye(2), [1.0, -1.0], 0.0, np.inf, "pg", 10),
+        ("identity_box", np.eye(2), [0.5, 0.5], -1.0, 1.0, "pg", 1),    # test_solvers.py:70-76
+    ]
+    out = {}
+    for name, a, y, lo, hi, kind, passes in cases:
+        a = np.asarray(a, float)
+        n = a.shape[1]
+        p = bs.Problem(a, y, lo, hi)
+        step = 1.0 if name == "box1d_step1" else None
+        res = bs.solve(p, bs.SolverConfig(kind=kind, inner_passes=passes, step_size=step, gap_tol=1e-6),
+                       screening=True)
+        out[name + "_a"] = a
+        out[name + "_y"] = np.asarray(y, float)
+        out[name + "_lo"] = np.broadcast_to(np.asarray(lo, float), (n,)).copy()
+        out[name + "_hi"] = np.broadcast_to(np.asarray(hi, float), (n,)).copy()
+        out[name + "_kind"] = np.array(kind)
+        out[name + "_passes"] = np.array(passes)
+        out[name + "_step"] = np.array(np.nan if step is None else step)
+        out[name + "_x"] = res.x
+        out[name + "_final"] = np.array([res.gap, res.rounds, float(res.converged)])
+        out[name + "_ratio"] = np.array(res.trace[-1].screening_ratio)
+    out["names"] = np.array([c[0] for c in cases])
+    np.savez_compressed(os.path.join(HERE, "kat_cases.npz"), **out)
+    print("kat_cases:", len(cases))
+
+
+def optimum_cases():
+    out = {}
+    names = []
+    for i in range(6):
+        rng = np.random.default_rng(500 + i)
+        fam = ("nnls", "mixed", "bvls")[i % 3]
+        n = int(rng.integers(5, 25))
+        m = int(rng.integers(n + 5, 60))
+        a, y, lo, hi = small_instance(rng, m, n, fam)
+        p = bs.Problem(a, y, lo, hi)
+        res = bs.solve(p, bs.SolverConfig(kind="active-set", gap_tol=1e-12), screening=False)
+        assert res.converged
+        key = f"o{i}"
+        names.append(key)
+        out[key + "_a"] = a
+        out[key + "_y"] = y
+        out[key + "_lo"] = lo
+        out[key + "_hi"] = hi
+        out[key + "_x"] = res.x
+        r = a @ res.x - y
+        out[key + "_obj"] = np.array(0.5 * float(r @ r))
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "optimum_cases.npz"), **out)
+    print("optimum_cases:", len(names))
+
+
+def full_config(cfg_id, fname):
+    inst = make_config(cfg_id)
+    p = bs.Problem(inst.a, inst.y, inst.lower, inst.upper)
+    t0 = time.time()
+    res = bs.solve(p, bs.SolverConfig(kind=inst.kind, inner_passes=inst.inner_passes, gap_tol=inst.gap_tol),
+                   screening=True)
+    el = time.time() - t0
+    out = {f"tr_{k}": v for k, v in trace_arrays(res).items()}
+    out.update(x=res.x, theta=res.theta, final=np.array([res.gap, res.rounds, float(res.converged)]),
+               sat_lower=np.asarray(res.sat_lower, np.int64), sat_upper=np.asarray(res.sat_upper, np.int64),
+               input_sha256=np.array(digest(inst.a, inst.y)), elapsed=np.array(el),
+               step=np.array(bs.auto_step_size(inst.a, 1.0)))
+    np.savez_compressed(os.path.join(HERE, fname), **out)
+    print(fname, "rounds", res.rounds, "converged", res.converged, "elapsed %.1fs" % el)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["small", "kat", "optimum", "cfg2", "cfg1"]
+    if "small" in which:
+        small_cases()
+    if "kat" in which:
+        kat_cases()
+    if "optimum" in which:
+        optimum_cases()
+    if "cfg2" in which:
+        full_config(2, "cfg2_trace.npz")
+    if "cfg1" in which:
+        full_config(1, "cfg1_trace.npz")
