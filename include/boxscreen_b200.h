@@ -84,6 +84,8 @@ typedef struct {
   int64_t newly_screened_lower, newly_screened_upper;
   double eps, radius, step;
   double certified_gap;  /* NaN when not evaluated this round                   */
+  int64_t restarts;      /* FISTA restarts so far (cumulative)                  */
+  double momentum;       /* FISTA t_k after the round                            */
 } bx_trace_rec;
 
 typedef struct {
@@ -95,6 +97,7 @@ typedef struct {
   double step;
   double sigma;          /* last power-iteration estimate                      */
   int64_t kernel_launches;
+  int64_t restarts;
 } bx_solve_out;
 
 /* Host callback producing the power-iteration start vector of length k:

@@ -32,14 +32,14 @@ class TraceRec(ctypes.Structure):
                 ("preserved_count", ctypes.c_int64), ("newly_screened_lower", ctypes.c_int64),
                 ("newly_screened_upper", ctypes.c_int64), ("eps", ctypes.c_double),
                 ("radius", ctypes.c_double), ("step", ctypes.c_double),
-                ("certified_gap", ctypes.c_double)]
+                ("certified_gap", ctypes.c_double), ("restarts", ctypes.c_int64), ("momentum", ctypes.c_double)]
 
 
 class SolveOut(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("converged", ctypes.c_int32), ("gap", ctypes.c_double),
                 ("n_sat_lower", ctypes.c_int64), ("n_sat_upper", ctypes.c_int64),
                 ("iterations", ctypes.c_int64), ("step", ctypes.c_double), ("sigma", ctypes.c_double),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("restarts", ctypes.c_int64)]
 
 
 class ProfEntry(ctypes.Structure):

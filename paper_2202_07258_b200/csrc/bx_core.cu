@@ -274,7 +274,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->probe = (int*)w.take(64);
   c->ldp = mp;
   c->part = w.take((size_t)c->Gmax * c->ldp * e);
-  c->bpart = (double*)w.take(c->Gmax * 8 * 2);
+  c->bpart = (double*)w.take(c->Gmax * 8 * 4);
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
   c->sc = (DevScalars*)w.take(sizeof(DevScalars));
@@ -350,7 +350,8 @@ int pass_grid(bx_ctx* c, int64_t k) {
 // Launch one streamed pass.  Returns the grid used through *G_out.
 template <typename T>
 int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_prev, T* x, T* xprev, const T* lo,
-             const T* hi, T* g, const T* att, const T* coef, double* bpart, int has_inf, int* G_out) {
+             const T* hi, T* g, const T* att, const T* coef, double* bpart, int has_inf, int* G_out,
+             const T* nrm = nullptr) {
   const int R = pick_R(c->m, sizeof(T));
   if (R < 0) return fail(c, BX_ERR_UNSUPPORTED, "m=%lld exceeds the fused-pass envelope", (long long)c->m);
   const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
@@ -358,7 +359,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_p
   const int C = cols_per_slot(R);
   const uint32_t colbytes = (uint32_t)align_up((size_t)c->m * sizeof(T), 16);
   const uint32_t colstride = (uint32_t)align_up(colbytes, 128);
-  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 2 * CMAX) * 8 + 64;
+  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 3 * CMAX) * 8 + 64;
   const size_t slot = (size_t)C * colstride;
   int S = (int)((c->smem_cap - scratch) / slot);
   if (S > SMAX) S = SMAX;
@@ -379,6 +380,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_p
   a.hi = hi;
   a.g = g;
   a.att = att;
+  a.nrm = nrm;
   a.coef = coef;
   a.part = (T*)c->part;
   a.ldp = c->ldp;
@@ -566,9 +568,10 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
       c->g_valid = false;
     } else if (kind == BX_APG) {
       TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const T*)c->r, (const T*)c->rprev, (T*)c->x[s], (T*)c->xprev[s],
-                      (const T*)c->lo[s], (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, nullptr, 0, &G));
+                      (const T*)c->lo[s], (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, c->bpart, 0, &G,
+                      (const T*)c->nrm[s]));
       // r_prev <- r, r <- new residual: write into the r_prev buffer, swap
-      TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_APG, nullptr, 0, 2));
+      TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_APG, c->bpart, G, 2));
       std::swap(c->r, c->rprev);
     } else {
       return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent is not built yet");
@@ -823,6 +826,8 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       tr.radius = act.radius;
       tr.step = eta;
       tr.certified_gap = cert_gap;
+      tr.restarts = c->hsc->restarts;
+      tr.momentum = c->hsc->mom_t;
     }
     if (converged) break;
   }
@@ -840,6 +845,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     out->step = eta;
     out->sigma = sigma;
     out->kernel_launches = c->launches;
+    out->restarts = c->hsc->restarts;
   }
   return BX_OK;
 }

@@ -90,6 +90,7 @@ struct PassArgs {
   const T* hi;
   T* g;                    // gradient A'v (written by dot modes, read by U_PG_G)
   const T* att;            // A't for the epsilon partial
+  const T* nrm;            // ||a_j|| (FISTA restart slack)
   const T* coef;           // U_AX coefficients (NULL: x)
   T* part;                 // [gridDim.x][ldp] partial rows of A x'
   int64_t ldp;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * slot_bytes);
   double* red = reinterpret_cast<double*>(bars + SMAX);  // [NWARPS][C]
   double* cf = red + NWARPS * CMAX;                      // [C] axpy coefficients
-  double* bscr = cf + CMAX;                              // [C] block scalar scratch
+  double* bscr = cf + CMAX;                              // [2][CMAX] block scalar scratch
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -288,7 +289,8 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   for (int i = 0; i < (AXPY ? R : 1); ++i)
 #pragma unroll
     for (int e = 0; e < V; ++e) acc[i][e] = T(0);
-  double run = 0.0;  // block-scalar running value (threads tid < C)
+  double run = 0.0;   // block-scalar running value (threads tid < C)
+  double run2 = 0.0;  // second block scalar (FISTA restart slack)
 
   for (int gi = 0; gi < ngroups; ++gi) {
     const int s = gi % S;
@@ -351,6 +353,11 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
             a.xprev[p] = xo;
             a.x[p] = xn;
             coef = static_cast<double>(xn);
+            // gradient restart test g_y'(x+ - x) and its round-off scale
+            // sum ||a_j|| |x+ - x| (FISTA)
+            const double dxj = static_cast<double>(xn) - static_cast<double>(xo);
+            run += static_cast<double>(gj) * dxj;
+            run2 += static_cast<double>(a.nrm[p]) * fabs(dxj);
           } break;
           case U_POWER: {
             coef = static_cast<double>(gj);
@@ -420,12 +427,23 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     }
   }
   if (a.bpart) {
-    if (tid < C) bscr[tid] = run;
+    if (tid < C) {
+      bscr[tid] = run;
+      bscr[CMAX + tid] = run2;
+    }
     __syncthreads();
     if (tid == 0) {
-      double v = bscr[0];
-      for (int c = 1; c < C; ++c) v = (a.upd == U_DOT) ? fmax(v, bscr[c]) : v + bscr[c];
-      a.bpart[b] = v;
+      double v = bscr[0], v2 = bscr[CMAX];
+      for (int c = 1; c < C; ++c) {
+        v = (a.upd == U_DOT) ? fmax(v, bscr[c]) : v + bscr[c];
+        v2 += bscr[CMAX + c];
+      }
+      if (a.upd == U_APG) {
+        a.bpart[2 * b] = v;
+        a.bpart[2 * b + 1] = v2;
+      } else {
+        a.bpart[b] = v;
+      }
     }
   }
 }
@@ -453,7 +471,8 @@ __device__ __forceinline__ double block_sum_rt(double v, double* sh) {
 constexpr int RED_SLICES = RT / 32;
 
 template <typename T>
-__device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, double Pn, double scale_div) {
+__device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, double Pn, double scale_div,
+                                                   double gdot, double gscale) {
   switch (mode) {
     case R_SET:
       sc->P = Pn;
@@ -468,7 +487,9 @@ __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, dou
     case R_APG: {
       const double t = sc->mom_t;
       const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-      if (Pn > sc->P + 1e-12 * fmax(1.0, fabs(sc->P))) {  // restart (FISTA)
+      const double s_f = 1e-12 * fmax(1.0, fabs(sc->P));
+      const double s_g = 1e-12 * sqrt(2.0 * sc->P) * gscale;
+      if (Pn > sc->P + s_f || gdot > s_g) {  // function / gradient restart (FISTA)
         sc->mom_t = 1.0;
         sc->restarts += 1;
       } else {
@@ -562,11 +583,21 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last || warp != 0) return;
   __threadfence();
-  double total = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) total += *((volatile double*)&bpart[b]);
-  finalize_objective<T>(sc, mode, 0.5 * total, mode == R_POWER ? s_div : 0.0);
+  // last block: warp 0 folds the block partials (lane-strided + fixed tree)
+  double total = 0.0, gdot = 0.0, gscale = 0.0;
+  for (int b = lane; b < (int)gridDim.x; b += 32) total += __ldcg(&bpart[b]);
+  if (mode == R_APG && wpart)
+    for (int b = lane; b < Gw; b += 32) {
+      gdot += __ldcg(&wpart[2 * b]);
+      gscale += __ldcg(&wpart[2 * b + 1]);
+    }
+  total = warp_sum<double>(total);
+  gdot = warp_sum<double>(gdot);
+  gscale = warp_sum<double>(gscale);
+  if (lane != 0) return;
+  finalize_objective<T>(sc, mode, 0.5 * total, mode == R_POWER ? s_div : 0.0, gdot, gscale);
   sc->counters[counter] = 0u;
 }
 
@@ -637,16 +668,20 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last || warp != 0) return;
   __threadfence();
   double t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0;
-  volatile double* vb = bpart;
-  for (int b = 0; b < (int)gridDim.x; ++b) {
-    t1 += vb[4 * b + 0];
-    t2 += vb[4 * b + 1];
-    t3 += vb[4 * b + 2];
-    t4 += vb[4 * b + 3];
+  for (int b = lane; b < (int)gridDim.x; b += 32) {
+    t1 += __ldcg(&bpart[4 * b + 0]);
+    t2 += __ldcg(&bpart[4 * b + 1]);
+    t3 += __ldcg(&bpart[4 * b + 2]);
+    t4 += __ldcg(&bpart[4 * b + 3]);
   }
+  t1 = warp_sum<double>(t1);
+  t2 = warp_sum<double>(t2);
+  t3 = warp_sum<double>(t3);
+  t4 = warp_sum<double>(t4);
+  if (lane != 0) return;
   // _reduced_dual (driver.py:360-368) / eval_dual (duality.py:401-422)
   double dual = t1 - 0.5 * t2;
   dual -= t3;

@@ -80,7 +80,7 @@ def trace_to_csv(trace, path):
 TRACE_DTYPE = np.dtype([("round", "<i8"), ("elapsed", "<f8"), ("primal", "<f8"), ("dual", "<f8"), ("gap", "<f8"),
                         ("preserved_count", "<i8"), ("newly_screened_lower", "<i8"),
                         ("newly_screened_upper", "<i8"), ("eps", "<f8"), ("radius", "<f8"), ("step", "<f8"),
-                        ("certified_gap", "<f8")])
+                        ("certified_gap", "<f8"), ("restarts", "<i8"), ("momentum", "<f8")])
 assert TRACE_DTYPE.itemsize == ctypes.sizeof(nat.TraceRec)
 
 
@@ -204,7 +204,7 @@ def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=
                          float(r["gap"]), int(r["preserved_count"]), (n - int(r["preserved_count"])) / n,
                          int(r["newly_screened_lower"]), int(r["newly_screened_upper"])) for r in tr]
     info = dict(iterations=int(out.iterations), step=float(out.step), sigma=float(out.sigma),
-                kernel_launches=int(out.kernel_launches), trace_arrays=tr, profile=prof)
+                kernel_launches=int(out.kernel_launches), restarts=int(out.restarts), trace_arrays=tr, profile=prof)
     if return_device:
         xo, tho = x, theta
     else:
