@@ -1,0 +1,283 @@
+// bx_cd.cuh -- cyclic coordinate descent (reference solvers.py:119-137) on one
+// thread-block cluster.
+//
+// The reference sweeps the preserved columns in original-index order; for each
+// column k: step = a_k'r / ||a_k||^2, x_k' = clip(x_k - step, l_k, u_k),
+// r += (x_k' - x_k) a_k when the move is nonzero.  Sequential in k, so the GPU
+// version is "block-exact": the columns are cut into blocks J of B <= 32
+// consecutive preserved columns and, per block,
+//    d_J   = A_J' r                   (parallel dots, split over the cluster)
+//    for i in J (in order):  c_i = d_i + sum_{l<i, l in J} G_il delta_l
+//                            step = c_i / ||a_i||^2 ; x_i' = clip(...) ; delta_i
+//    r    += A_J delta_J              (parallel axpy)
+// with the Gram blocks G_JJ = A_J'A_J precomputed (k_gram).  In exact
+// arithmetic this is the reference's sweep step for step; only the rounding
+// of a_i'r differs (a block dot + Gram corrections instead of a fresh dot).
+//
+// Layout: a cluster of NC CTAs splits the m rows; each CTA keeps its rows of r
+// in registers and its rows of A_J in shared memory (double buffered,
+// prefetched with cp.async while the previous block's update runs).  The B
+// partial dots of every CTA are combined through distributed shared memory in
+// rank order (deterministic), then every CTA runs the (tiny) sequential update
+// redundantly, so one cluster barrier per block is the only synchronisation.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "bx_kernels.cuh"
+
+namespace bx {
+
+namespace cg = cooperative_groups;
+
+constexpr int CD_NT = 256;   // threads per CTA
+constexpr int CD_B = 32;     // columns per block (one warp lane each)
+constexpr int CD_RMAX = 4;   // rows per thread held in registers (m <= NC*CD_NT*CD_RMAX)
+
+template <typename T>
+struct CdArgs {
+  const T* A;        // compacted preserved columns, column stride ld
+  int64_t ld;
+  int64_t m;
+  int64_t k;         // preserved columns
+  T* x;              // preserved iterate, read in even passes
+  T* x2;             // written in even passes, read in odd (ping-pong: every
+                     // CTA reads x_j while rank 0 publishes the new value)
+  const T* lo;
+  const T* hi;
+  const T* nrm;      // ||a_j||  (sq = nrm^2, as solvers.py:60)
+  const T* gram;     // [nblocks][B][B] Gram blocks
+  T* r;              // residual (in/out, m)
+  DevScalars* sc;
+  int passes;
+  int rows_per_cta;  // multiple of 2
+};
+
+// cp.async 16-byte global->shared copy (LDGSTS)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <typename T>
+__device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, int64_t blk, int64_t row0, int nrows) {
+  // dst[c * rows_pad + i] = A[row0 + i, 32*blk + c]
+  const int64_t c0 = blk * CD_B;
+  const int nc = (int)min((int64_t)CD_B, a.k - c0);
+  constexpr int V = 16 / sizeof(T);
+  const int nvec = (nrows + V - 1) / V;  // rows_per_cta is a multiple of V
+  const int rows_pad = a.rows_per_cta;
+  for (int q = threadIdx.x; q < nc * nvec; q += CD_NT) {
+    const int c = q / nvec, v = q - c * nvec;
+    cp_async16(dst + (int64_t)c * rows_pad + v * V, a.A + (c0 + c) * a.ld + row0 + v * V);
+  }
+  cp_async_commit();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int NC = (int)cluster.num_blocks();
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int rows_pad = a.rows_per_cta;
+  T* abuf0 = reinterpret_cast<T*>(smem);
+  T* abuf1 = abuf0 + CD_B * rows_pad;
+  double* part = reinterpret_cast<double*>(abuf1 + CD_B * rows_pad);  // [2][CD_B] partial dots
+  double* gbuf = part + 2 * CD_B;                                       // [CD_B][CD_B] Gram block
+  double* delta = gbuf + CD_B * CD_B;                                   // [CD_B]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row0 = (int64_t)rank * rows_pad;
+  const int nrows = (int)max((int64_t)0, min((int64_t)rows_pad, a.m - row0));
+
+  // residual rows in registers: thread owns rows tid + q*CD_NT
+  T rr[CD_RMAX];
+#pragma unroll
+  for (int q = 0; q < CD_RMAX; ++q) {
+    const int i = tid + q * CD_NT;
+    rr[q] = (i < nrows) ? a.r[row0 + i] : T(0);
+  }
+  const int64_t nblk = (a.k + CD_B - 1) / CD_B;
+  int64_t it = 0;  // global block counter (selects buffers)
+  if (nblk > 0 && nrows > 0) cd_prefetch(a, abuf0, 0, row0, nrows);
+  for (int pass = 0; pass < a.passes; ++pass) {
+    for (int64_t blk = 0; blk < nblk; ++blk, ++it) {
+      T* cur = (it & 1) ? abuf1 : abuf0;
+      T* nxt = (it & 1) ? abuf0 : abuf1;
+      const int64_t c0 = blk * CD_B;
+      const int nc = (int)min((int64_t)CD_B, a.k - c0);
+      if (nrows > 0) cp_async_wait_all();
+      // Gram block for the sequential update
+      const T* gsrc = a.gram + blk * CD_B * CD_B;
+      for (int q = tid; q < CD_B * CD_B; q += CD_NT) gbuf[q] = static_cast<double>(gsrc[q]);
+      __syncthreads();
+      // prefetch the next block while this one is processed
+      {
+        int64_t nb = blk + 1, np = pass;
+        if (nb == nblk) {
+          nb = 0;
+          ++np;
+        }
+        if (np < a.passes && nrows > 0) cd_prefetch(a, nxt, nb, row0, nrows);
+      }
+      // partial dots: every thread multiplies its register rows with the block's
+      // columns; a butterfly transpose-reduction leaves column c's warp sum in
+      // lane c (31 shuffles instead of 32 x 5)
+      double* mypart = part + (it & 1) * CD_B;
+      {
+        double pd[CD_B];
+#pragma unroll
+        for (int c = 0; c < CD_B; ++c) pd[c] = 0.0;
+#pragma unroll
+        for (int q = 0; q < CD_RMAX; ++q) {
+          const int i = tid + q * CD_NT;
+          if (i < nrows) {
+            const double rv = static_cast<double>(rr[q]);
+#pragma unroll
+            for (int c = 0; c < CD_B; ++c)
+              if (c < nc) pd[c] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * rv;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const bool upper = (lane & o) != 0;
+#pragma unroll
+          for (int q = 0; q < o; ++q) {
+            const double send = upper ? pd[q] : pd[q + o];
+            const double keep = upper ? pd[q + o] : pd[q];
+            pd[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        __shared__ double wpart[CD_NT / 32][CD_B];
+        wpart[warp][lane] = pd[0];
+        __syncthreads();
+        if (tid < CD_B) {
+          double s = 0.0;
+          for (int w = 0; w < CD_NT / 32; ++w) s += wpart[w][tid];
+          mypart[tid] = s;
+        }
+      }
+      cluster.sync();  // every CTA's partial dots are visible
+      // combine partial dots of all CTAs in rank order, then the sequential
+      // block update on warp 0 (lane = column), redundantly in every CTA
+      if (warp == 0) {
+        double cdot = 0.0;
+        if (lane < nc) {
+          for (int q = 0; q < NC; ++q) {
+            const double* rp = cluster.map_shared_rank(part + (it & 1) * CD_B, q);
+            cdot += rp[lane];
+          }
+        }
+        const int64_t j = c0 + lane;
+        const T* xin = (pass & 1) ? a.x2 : a.x;
+        T* xout = (pass & 1) ? a.x : a.x2;
+        T xj = T(0), loj = T(0), hij = T(0);
+        double sq = 1.0;
+        if (lane < nc) {
+          xj = xin[j];
+          loj = a.lo[j];
+          hij = a.hi[j];
+          const double nj = static_cast<double>(a.nrm[j]);
+          sq = nj * nj;  // solvers.py:60 (col_norms ** 2)
+        }
+        double dl = 0.0;
+        for (int i = 0; i < nc; ++i) {
+          double di = 0.0;
+          if (lane == i) {
+            const T step = static_cast<T>(cdot / sq);                  // solvers.py:131
+            T nv = xj - step;                                           // solvers.py:132
+            nv = nv < loj ? loj : nv;
+            nv = nv > hij ? hij : nv;
+            const T dt = nv - xj;                                       // solvers.py:133
+            if (dt != T(0)) {
+              di = static_cast<double>(dt);
+              xj = nv;
+            }
+            dl = di;
+          }
+          di = __shfl_sync(0xffffffffu, di, i);
+          if (di != 0.0 && lane > i && lane < nc) cdot += gbuf[lane * CD_B + i] * di;
+        }
+        delta[lane] = dl;
+        if (lane < nc && rank == 0) xout[j] = xj;
+      }
+      __syncthreads();
+      // r += A_J delta_J on this CTA's rows
+#pragma unroll
+      for (int q = 0; q < CD_RMAX; ++q) {
+        const int i = tid + q * CD_NT;
+        if (i < nrows) {
+          T acc = rr[q];
+          for (int c = 0; c < nc; ++c) {
+            const double dc = delta[c];
+            if (dc != 0.0) acc += cur[(int64_t)c * rows_pad + i] * static_cast<T>(dc);
+          }
+          rr[q] = acc;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // write back the residual rows and the objective 0.5 ||r||^2
+  double sq = 0.0;
+#pragma unroll
+  for (int q = 0; q < CD_RMAX; ++q) {
+    const int i = tid + q * CD_NT;
+    if (i < nrows) {
+      a.r[row0 + i] = rr[q];
+      sq += static_cast<double>(rr[q]) * static_cast<double>(rr[q]);
+    }
+  }
+  sq = warp_sum<double>(sq);
+  __shared__ double wsq[CD_NT / 32];
+  if (lane == 0) wsq[warp] = sq;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < CD_NT / 32; ++w) s += wsq[w];
+    part[0] = s;
+  }
+  cluster.sync();
+  if (rank == 0 && tid == 0) {
+    double tot = 0.0;
+    for (int q = 0; q < NC; ++q) tot += *cluster.map_shared_rank(part, q);
+    a.sc->P = 0.5 * tot;
+  }
+  cluster.sync();  // keep smem alive until rank 0 has read it
+}
+
+// Gram blocks G_JJ = A_J' A_J for consecutive blocks of CD_B preserved columns
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram(const T* __restrict__ A, int64_t ld, int64_t m, int64_t k,
+                                              T* __restrict__ gram) {
+  __shared__ T tile[CD_B][129];  // 128-row chunk of the block's columns (+1 pad)
+  const int64_t blk = blockIdx.x;
+  const int64_t c0 = blk * CD_B;
+  const int nc = (int)min((int64_t)CD_B, k - c0);
+  // thread -> 4 (i, l) pairs of the 32x32 block
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t r0 = 0; r0 < m; r0 += 128) {
+    const int nr = (int)min((int64_t)128, m - r0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < CD_B * 128; q += 256) {
+      const int c = q / 128, i = q % 128;
+      tile[c][i] = (c < nc && i < nr) ? A[(c0 + c) * ld + r0 + i] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = threadIdx.x * 4 + u;
+      const int i = p / CD_B, l = p % CD_B;
+      double s = 0.0;
+      for (int rr = 0; rr < nr; ++rr) s += static_cast<double>(tile[i][rr]) * static_cast<double>(tile[l][rr]);
+      acc[u] += s;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int p = threadIdx.x * 4 + u;
+    gram[blk * CD_B * CD_B + p] = static_cast<T>(acc[u]);
+  }
+}
+
+}  // namespace bx

@@ -28,6 +28,7 @@
 
 #include "../../include/boxscreen_b200.h"
 #include "bx_kernels.cuh"
+#include "bx_cd.cuh"
 
 using namespace bx;
 
@@ -105,6 +106,8 @@ struct bx_ctx {
   int32_t* idx[2] = {nullptr, nullptr};
   void *x[2] = {}, *xprev[2] = {}, *lo[2] = {}, *hi[2] = {}, *nrm[2] = {}, *att[2] = {};
   void *g = nullptr, *v = nullptr, *coef = nullptr;
+  void* gram = nullptr;  // CD Gram blocks [ceil(n/32)][32][32]
+  bool gram_dirty = true;
   // full-problem vectors
   void *xfull = nullptr, *lofull = nullptr, *hifull = nullptr, *nrmfull = nullptr, *attfull = nullptr;
   void *gfull = nullptr, *vfull = nullptr;
@@ -258,6 +261,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->g = w.take(n * e);
   c->v = w.take(n * e);
   c->coef = w.take(n * e);
+  c->gram = w.take((size_t)((n + CD_B - 1) / CD_B) * CD_B * CD_B * e);
   c->xfull = w.take(n * e);
   c->lofull = w.take(n * e);
   c->hifull = w.take(n * e);
@@ -550,6 +554,70 @@ int auto_step(bx_ctx* c, int iters, double alpha, bx_start_vector_fn fn, void* u
   return BX_OK;
 }
 
+// cyclic coordinate descent sweeps on one thread-block cluster (bx_cd.cuh)
+template <typename T>
+int cd_sweeps(bx_ctx* c, int passes) {
+  const int s = c->cur;
+  View<T> vw = act_view<T>(c);
+  if (c->k == 0) return BX_OK;
+  constexpr int V = 16 / sizeof(T);
+  int NC = 8;
+  int64_t rows = round_up((c->m + NC - 1) / NC, V);
+  const size_t fixed = (2 * CD_B + CD_B * CD_B + CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
+  auto smem_for = [&](int64_t r) { return 2 * CD_B * (size_t)r * sizeof(T) + fixed; };
+  if (rows > CD_NT * CD_RMAX || smem_for(rows) > c->smem_cap) {
+    NC = 16;
+    rows = round_up((c->m + NC - 1) / NC, V);
+  }
+  if (rows > CD_NT * CD_RMAX || smem_for(rows) > c->smem_cap)
+    return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent: m=%lld exceeds the cluster envelope", (long long)c->m);
+  if (c->gram_dirty) {
+    const int nblk = (int)((c->k + CD_B - 1) / CD_B);
+    const int e0 = prof_begin(c);
+    k_gram<T><<<nblk, 256, 0, c->stream>>>(vw.A, vw.ld, c->m, c->k, (T*)c->gram);
+    LAUNCHED();
+    prof_end(c, e0, BX_PROF_CD, (double)c->k * c->m * sizeof(T));
+    c->gram_dirty = false;
+  }
+  CdArgs<T> a;
+  a.A = vw.A;
+  a.ld = vw.ld;
+  a.m = c->m;
+  a.k = c->k;
+  a.x = (T*)c->x[s];
+  a.x2 = (T*)c->coef;
+  a.lo = (const T*)c->lo[s];
+  a.hi = (const T*)c->hi[s];
+  a.nrm = (const T*)c->nrm[s];
+  a.gram = (const T*)c->gram;
+  a.r = (T*)c->r;
+  a.sc = c->sc;
+  a.passes = passes;
+  a.rows_per_cta = (int)rows;
+  const size_t smem = smem_for(rows);
+  CU(cudaFuncSetAttribute(k_cd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaFuncSetAttribute(k_cd<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(NC, 1, 1);
+  lc.blockDim = dim3(CD_NT, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = NC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const int e0 = prof_begin(c);
+  CU(cudaLaunchKernelEx(&lc, k_cd<T>, a));
+  LAUNCHED();
+  prof_end(c, e0, BX_PROF_CD, 2.0 * (double)passes * c->k * c->m * sizeof(T));
+  if (passes & 1) CU(cudaMemcpyAsync(c->x[s], c->coef, c->k * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  c->g_valid = false;
+  return BX_OK;
+}
+
 // one round's primal passes
 template <typename T>
 int primal_passes(bx_ctx* c, int kind, int passes) {
@@ -574,7 +642,7 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
       TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_APG, c->bpart, G, 2));
       std::swap(c->r, c->rprev);
     } else {
-      return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent is not built yet");
+      return cd_sweeps<T>(c, passes);  // all sweeps in one launch
     }
   }
   return BX_OK;
@@ -674,6 +742,7 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind) {
     prof_end(c, e0, BX_PROF_GATHER, 2.0 * (double)c->k * c->m * sizeof(T));
   }
   c->act_is_orig = false;
+  c->gram_dirty = true;
   TRY(refresh_resid<T>(c));
   if (kind == BX_APG) TRY(refresh_rprev<T>(c));
   c->g_valid = false;
@@ -687,6 +756,7 @@ int reset_state(bx_ctx* c, int kind) {
   c->k = c->n;
   c->n_sat_lo = c->n_sat_up = 0;
   c->act_is_orig = true;
+  c->gram_dirty = true;
   c->g_valid = false;
   c->theta_is_cert = false;
   k_init_cols<T><<<grid1d(c, c->n), RT, 0, c->stream>>>(c->n, (const T*)c->lofull, (const T*)c->hifull,

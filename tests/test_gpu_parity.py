@@ -23,7 +23,7 @@ def _solve_both(a, y, lo, hi, kind, passes=10, tol=1e-8, screening=True, max_rou
 
 
 @pytest.mark.parametrize("family", ["nnls", "bvls", "mixed"])
-@pytest.mark.parametrize("kind", ["pg", "apg"])
+@pytest.mark.parametrize("kind", ["pg", "apg", "cd"])
 @pytest.mark.parametrize("screening", [True, False])
 def test_small_trajectories(family, kind, screening):
     rng = np.random.default_rng(zlib.crc32(f"{family}-{kind}-{screening}".encode()))
@@ -75,7 +75,7 @@ def test_zero_column_and_interior():
         solve(Problem(a, np.zeros(2), 0.0, 1.0), SolverConfig(kind="pg"))
 
 
-@pytest.mark.parametrize("cfg_id,m,n,rounds", [(1, 1000, 2000, 300), (3, 1000, 5000, 200)])
+@pytest.mark.parametrize("cfg_id,m,n,rounds", [(1, 1000, 2000, 300), (3, 1000, 5000, 200), (2, 500, 1000, 60)])
 def test_baseline_recipe_prefix(cfg_id, m, n, rounds):
     """BASELINE config recipes at oracle-friendly sizes: first rounds round-by-round."""
     from paper_2202_07258_b200.generate import make_config
