@@ -126,7 +126,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # the CPU side: oracle port timed on the host cores (cpu_baseline / reference arm)
 # ---------------------------------------------------------------------------
-def cpu_rate(inst, k_bins, budget_s, passes=10):
+def cpu_rate(inst, k_bins, budget_s, passes=None):
     """Oracle FISTA iterations/s over the solve's preserved-set trajectory.
 
     ``k_bins`` = [(k, iterations)] -- how many iterations the screened solve
@@ -136,8 +136,15 @@ def cpu_rate(inst, k_bins, budget_s, passes=10):
     total iterations / sum(iterations_b * seconds_per_iteration(k_b)).
     Returns (rate, details).
     """
-    from oracle.boxscreen_oracle import ActiveView, apg_passes
+    from oracle.boxscreen_oracle import ActiveView, apg_passes, cd_passes, pg_passes
     a, y, lo, hi = inst.a, inst.y, inst.lower, inst.upper
+    passes = passes or inst.inner_passes
+    if inst.kind == "pg":
+        step_fn = lambda w, eta, p, mom: pg_passes(w, eta, p)  # noqa: E731
+    elif inst.kind == "cd":
+        step_fn = lambda w, eta, p, mom: cd_passes(w, p)  # noqa: E731
+    else:
+        step_fn = apg_passes
     n = a.shape[1]
     norms = np.ones(n)
     perm = np.random.default_rng(1).permutation(n)
@@ -149,12 +156,12 @@ def cpu_rate(inst, k_bins, budget_s, passes=10):
     for k, it in k_bins:
         keep = np.sort(perm[:k])
         w = ActiveView(a, y, lo, hi, norms, np.zeros(a.shape[0]), x_full, keep)
-        eta = 1.0 / (0.75 * k + 10.0)  # timing only: cost does not depend on the step
+        eta = 0.5 / (0.75 * k + 10.0)  # timing only: cost does not depend on the step
         mom = [1.0]
         t0 = time.perf_counter()
         done = 0
         while True:
-            apg_passes(w, eta, passes, mom)
+            step_fn(w, eta, passes, mom)
             done += passes
             el = time.perf_counter() - t0
             if el > per_bin or done >= it:
@@ -390,7 +397,8 @@ def run_ours(args):
     r0 = results[0]
     line = {"metric": metric_name(args.config), "value": value, "unit": "iters/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if world == 1 else "replicas", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if world == 1 else "replicas", "vs_baseline": None,
+            "dtype": "f32" if inst.a.dtype == np.float32 else "f64",
             "data": "synthetic (seeded numpy, BASELINE config recipe; no public dataset)",
             "config": config_block(args.config, inst),
             "time_to_gap_s": ms_per_step / 1000.0, "converged": conv, "rounds": r0.rounds,
