@@ -167,6 +167,14 @@ int bx_nccl_unique_id(unsigned char* id_out_host);
 int bx_ctx_set_comm(bx_ctx* ctx, const unsigned char* id_host, int32_t rank,
                     int32_t nranks, int64_t col_offset, int64_t n_global);
 
+/* in-process rank group: ranks are threads of one process sharing a GPU or
+ * several; the allreduce is host-barrier + device sum (test transport of the
+ * column-sharded path; production uses NCCL through bx_ctx_set_comm) */
+typedef struct bx_group bx_group;
+int bx_group_create(bx_group** out, int32_t nranks);
+int bx_group_destroy(bx_group* group);
+int bx_ctx_set_group(bx_ctx* ctx, bx_group* group, int32_t rank, int64_t col_offset, int64_t n_global);
+
 /* ---- live per-kernel timing (bench.py roofline) ---------------------------- */
 /* CUDA events around every kernel launch on the context stream; accumulated
  * per slot with the ALGORITHMIC bytes of each launch. */

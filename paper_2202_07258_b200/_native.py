@@ -76,6 +76,9 @@ SIGNATURES = {
     "bx_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "bx_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "bx_ctx_set_comm": (ctypes.c_int, [_vp, ctypes.c_char_p, _i32, _i32, _i64, _i64]),
+    "bx_group_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i32]),
+    "bx_group_destroy": (ctypes.c_int, [_vp]),
+    "bx_ctx_set_group": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64]),
     "bx_set_profiling": (ctypes.c_int, [_vp, _i32]),
     "bx_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(ProfEntry), _i32]),
     "bx_batched_workspace_bytes": (_sz, [_i64, _i64, _i64]),

@@ -18,6 +18,8 @@
 #include <dlfcn.h>
 
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -35,6 +37,7 @@ using namespace bx;
 namespace {
 
 constexpr size_t kAlign = 256;
+constexpr int kMaxRanks = 256;
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
@@ -51,7 +54,7 @@ typedef int (*nccl_init_rank_fn)(ncclComm_t*, int, ncclUniqueId, int);
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*nccl_destroy_fn)(ncclComm_t);
 typedef const char* (*nccl_errstr_fn)(int);
-enum { ncclFloat32 = 7, ncclFloat64 = 8, ncclInt64 = 4, ncclSum = 0, ncclMax = 2 };
+enum { ncclInt32 = 2, ncclFloat32 = 7, ncclFloat64 = 8, ncclInt64 = 4, ncclSum = 0, ncclMax = 2 };
 
 struct Nccl {
   void* h = nullptr;
@@ -79,6 +82,82 @@ struct Nccl {
 Nccl g_nccl;
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// collectives of the column-sharded path.  dtype/op use the
+// NCCL enums; the in-process group is the test transport on one GPU: ranks
+// are threads of one process, each with its own stream, and synchronise only
+// through host barriers (no kernel ever waits on another).
+// ---------------------------------------------------------------------------
+struct bx_group {
+  int n = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  std::vector<const void*> ptrs;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long my = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my; });
+    }
+  }
+};
+
+struct Comm {
+  virtual ~Comm() {}
+  // in-place allreduce of count elements on `stream`; returns 0 on success
+  virtual int allreduce(void* buf, size_t count, int dtype, int op, cudaStream_t stream, std::string& err) = 0;
+};
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm && g_nccl.destroy) g_nccl.destroy(comm);
+  }
+  int allreduce(void* buf, size_t count, int dtype, int op, cudaStream_t stream, std::string& err) override {
+    const int r = g_nccl.allreduce(buf, buf, count, dtype, op, comm, stream);
+    if (r != 0) err = std::string("ncclAllReduce: ") + (g_nccl.errstr ? g_nccl.errstr(r) : "error");
+    return r;
+  }
+};
+
+struct LocalComm : Comm {
+  bx_group* g = nullptr;
+  int rank = 0;
+  void* tmp = nullptr;          // device scratch, >= count * 8 bytes
+  const void** dptrs = nullptr; // device array of n pointers
+  std::vector<const void*> snap;
+  int allreduce(void* buf, size_t count, int dtype, int op, cudaStream_t stream, std::string& err) override {
+    const int dt = dtype == ncclFloat64 ? 0 : dtype == ncclFloat32 ? 1 : dtype == ncclInt64 ? 2 : 3;
+    const int o = op == ncclMax ? 1 : 0;
+    const size_t es = (dt == 1 || dt == 3) ? 4 : 8;
+    if (cudaStreamSynchronize(stream) != cudaSuccess) {
+      err = "LocalComm: stream sync";
+      return 1;
+    }
+    g->ptrs[rank] = buf;
+    g->barrier();
+    snap = g->ptrs;
+    cudaMemcpyAsync(dptrs, snap.data(), g->n * sizeof(void*), cudaMemcpyHostToDevice, stream);
+    int nb = (int)((count + 255) / 256);
+    if (nb > 1024) nb = 1024;
+    if (nb < 1) nb = 1;
+    bx::k_group_reduce<<<nb, 256, 0, stream>>>(tmp, dptrs, g->n, (int64_t)count, dt, o);
+    if (cudaStreamSynchronize(stream) != cudaSuccess) {
+      err = "LocalComm: reduce";
+      return 1;
+    }
+    g->barrier();  // every rank has read every buffer
+    cudaMemcpyAsync(buf, tmp, count * es, cudaMemcpyDeviceToDevice, stream);
+    return 0;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // the context
@@ -150,9 +229,17 @@ struct bx_ctx {
   bx_prof_entry pstat[BX_PROF_SLOTS];
 
   // multi-GPU column sharding
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;
   int rank = 0, nranks = 1;
   int64_t col_offset = 0, n_global = 0;
+  void* rloc = nullptr;    // this rank's A x partial rows (mp elements)
+  double* scal = nullptr;  // small cross-rank scalar buffers [16]
+  double* dsum = nullptr;  // dual sums [8]
+  int64_t* kvec = nullptr; // per-rank preserved counts [kMaxRanks]
+  void* grp_tmp = nullptr;
+  const void** grp_ptrs = nullptr;
+  int val_bits = 0, col_bits = 0;  // validation flags recorded at create
+  bool sharded() const { return comm != nullptr && nranks > 1; }
 };
 
 namespace {
@@ -186,6 +273,19 @@ int fail(bx_ctx* c, int code, const char* fmt, ...) {
     int s_ = (expr);         \
     if (s_ != BX_OK) return s_; \
   } while (0)
+
+// ---- collectives ---------------------------------------------------------
+int allreduce(bx_ctx* c, void* buf, size_t count, int dtype, int op) {
+  if (!c->sharded()) return BX_OK;
+  std::string e;
+  if (c->comm->allreduce(buf, count, dtype, op, c->stream, e) != 0) return fail(c, BX_ERR_CUDA, "%s", e.c_str());
+  ++c->launches;
+  return BX_OK;
+}
+template <typename T>
+constexpr int nccl_type() {
+  return sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+}
 
 // ---- live timing ---------------------------------------------------------
 int prof_drain(bx_ctx* c) {
@@ -282,6 +382,12 @@ void carve(bx_ctx* c, Carver& w) {
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
   c->sc = (DevScalars*)w.take(sizeof(DevScalars));
+  c->rloc = w.take(mp * e);
+  c->scal = (double*)w.take(16 * 8);
+  c->dsum = (double*)w.take(8 * 8);
+  c->kvec = (int64_t*)w.take(kMaxRanks * 8);
+  c->grp_tmp = w.take(mp * 8 + 4096);
+  c->grp_ptrs = (const void**)w.take(kMaxRanks * 8);
   (void)m;
   (void)kPartRows;
 }
@@ -428,6 +534,25 @@ int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* w
   int nb = (int)((c->m + rb - 1) / rb);
   if (nb > 4 * c->nsm) nb = 4 * c->nsm;
   if (nb < 1) nb = 1;
+  if (c->sharded()) {
+    // phase A: this rank's partial rows; block scalars folded; both summed
+    // over ranks (NCCL allreduce); phase B: offset, objective, mode logic
+    k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, nullptr, (T*)c->rloc, c->sc,
+                                           c->bpart2, nullptr, 0, R_PLAIN, counter);
+    LAUNCHED();
+    const int stride = (mode == R_APG) ? 2 : 1;
+    if (wpart && Gw > 0) {
+      k_fold<<<1, 32, 0, c->stream>>>(wpart, Gw, stride, 0, c->scal);
+      LAUNCHED();
+    }
+    TRY(allreduce(c, c->rloc, (size_t)c->m, nccl_type<T>(), ncclSum));
+    if (wpart && Gw > 0) TRY(allreduce(c, c->scal, (size_t)stride, ncclFloat64, ncclSum));
+    k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->rloc, c->ldp, 1, c->m, off, out, c->sc, c->bpart2,
+                                           (wpart && Gw > 0) ? c->scal : nullptr, (wpart && Gw > 0) ? 1 : 0, mode,
+                                           counter);
+    LAUNCHED();
+    return BX_OK;
+  }
   const int e0 = prof_begin(c);
   k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, off, out, c->sc, c->bpart2, wpart, Gw,
                                          mode, counter);
@@ -490,15 +615,15 @@ int refresh_rprev(bx_ctx* c) {
 // spectral_norm_estimate on the act view (solvers.py:72-86); one fused pass per
 // power iteration: w = A'u, acc = A w, u <- acc / ||w||
 template <typename T>
-int power_iter(bx_ctx* c, int iters, const double* v0_host, double* sigma) {
+int power_iter(bx_ctx* c, int iters, const double* v0_host, double* sigma, int64_t k_global) {
   const int64_t k = c->k;
-  if (k == 0) {
+  if (k_global == 0) {
     *sigma = 0.0;
     return BX_OK;
   }
-  std::vector<T> tmp(k);
+  std::vector<T> tmp(k > 0 ? k : 1);
   for (int64_t i = 0; i < k; ++i) tmp[i] = (T)v0_host[i];
-  CU(cudaMemcpyAsync(c->coef, tmp.data(), k * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  if (k > 0) CU(cudaMemcpyAsync(c->coef, tmp.data(), k * sizeof(T), cudaMemcpyHostToDevice, c->stream));
   int G = 1;
   TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                   (const T*)c->coef, nullptr, 0, &G));
@@ -535,17 +660,44 @@ void internal_start_vector(int64_t k, int64_t seed, double* out) {
   for (int64_t i = 0; i < k; ++i) out[i] /= s;
 }
 
+// preserved counts of all ranks -> (global count, this rank's offset in the
+// global preserved order; ranks own contiguous column blocks)
+int global_k(bx_ctx* c, int64_t* kg, int64_t* pos) {
+  if (!c->sharded()) {
+    *kg = c->k;
+    *pos = 0;
+    return BX_OK;
+  }
+  std::vector<int64_t> kv(c->nranks, 0);
+  kv[c->rank] = c->k;
+  CU(cudaMemcpyAsync(c->kvec, kv.data(), c->nranks * 8, cudaMemcpyHostToDevice, c->stream));
+  TRY(allreduce(c, c->kvec, (size_t)c->nranks, ncclInt64, ncclSum));
+  CU(cudaMemcpyAsync(kv.data(), c->kvec, c->nranks * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  *kg = 0;
+  *pos = 0;
+  for (int r = 0; r < c->nranks; ++r) {
+    if (r < c->rank) *pos += kv[r];
+    *kg += kv[r];
+  }
+  return BX_OK;
+}
+
 template <typename T>
 int auto_step(bx_ctx* c, int iters, double alpha, bx_start_vector_fn fn, void* user, double* eta, double* sigma_out) {
-  std::vector<double> v0(c->k > 0 ? c->k : 1);
-  if (c->k > 0) {
+  int64_t kg = 0, pos = 0;
+  TRY(global_k(c, &kg, &pos));
+  // the start vector is drawn over the GLOBAL preserved set in original order
+  // (solvers.py:75-76) and this rank takes its slice
+  std::vector<double> v0(kg > 0 ? kg : 1);
+  if (kg > 0) {
     if (fn)
-      fn(c->k, 0, v0.data(), user);
+      fn(kg, 0, v0.data(), user);
     else
-      internal_start_vector(c->k, 0, v0.data());
+      internal_start_vector(kg, 0, v0.data());
   }
   double sig = 0.0;
-  TRY(power_iter<T>(c, iters, v0.data(), &sig));
+  TRY(power_iter<T>(c, iters, v0.data() + pos, &sig, kg));
   if (sigma_out) *sigma_out = sig;
   const double s = sig / 0.999;  // solvers.py:95
   *eta = (s == 0.0) ? 1.0 : 0.99 * alpha / (s * s);
@@ -648,6 +800,34 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
   return BX_OK;
 }
 
+// epsilon (max over ranks), theta, reduced dual, gap, radius (k_dual [+ fin])
+template <typename T>
+int dual_point(bx_ctx* c, int which, const T* r, const T* tgt, T* theta, const T* g, const T* att, const T* lo,
+               const T* hi, T* v, int64_t k, const double* eps_part, int Ge, double slack_scale, double alpha) {
+  const double* ep = eps_part;
+  int ge = Ge;
+  if (c->sharded()) {
+    k_fold<<<1, 32, 0, c->stream>>>(eps_part, Ge, 1, 1, c->scal + 8);
+    LAUNCHED();
+    TRY(allreduce(c, c->scal + 8, 1, ncclFloat64, ncclMax));
+    ep = c->scal + 8;
+    ge = 1;
+  }
+  int nb = grid1d(c, c->m > k ? c->m : k);
+  const int e0 = prof_begin(c);
+  k_dual<T><<<nb, RT, 0, c->stream>>>(r, (const T*)c->t, tgt, theta, c->m, g, att, lo, hi, v, k, ep, ge, c->has_inf,
+                                       c->sc, which, c->bpart3, slack_scale, alpha, which ? 5 : 3,
+                                       c->sharded() ? c->dsum : nullptr);
+  LAUNCHED();
+  prof_end(c, e0, BX_PROF_DUAL, (double)sizeof(T) * (4.0 * c->m + 6.0 * k));
+  if (c->sharded()) {
+    TRY(allreduce(c, c->dsum + 2, 2, ncclFloat64, ncclSum));  // bound terms are per-rank
+    k_dual_fin<<<1, 32, 0, c->stream>>>(c->dsum, c->sc, which, slack_scale, alpha);
+    LAUNCHED();
+  }
+  return BX_OK;
+}
+
 // gradient at the current iterate + dual point + gap (+ sphere test)
 template <typename T>
 int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
@@ -656,14 +836,8 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
   TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const T*)c->r, nullptr, nullptr, nullptr, nullptr, (const T*)c->hi[s],
                   (T*)c->g, (const T*)c->att[s], nullptr, c->bpart, c->has_inf, &G));
   c->g_valid = true;
-  int nb = grid1d(c, c->m > c->k ? c->m : c->k);
-  const int e0 = prof_begin(c);
-  k_dual<T><<<nb, RT, 0, c->stream>>>((const T*)c->r, (const T*)c->t, (const T*)c->tgt, (T*)c->theta, c->m,
-                                       (const T*)c->g, (const T*)c->att[s], (const T*)c->lo[s], (const T*)c->hi[s],
-                                       (T*)c->v, c->k, c->bpart, G, c->has_inf, c->sc, 0, c->bpart3, slack_scale,
-                                       alpha, 3);
-  LAUNCHED();
-  prof_end(c, e0, BX_PROF_DUAL, (double)sizeof(T) * (4.0 * c->m + 6.0 * c->k));
+  TRY(dual_point<T>(c, 0, (const T*)c->r, (const T*)c->tgt, (T*)c->theta, (const T*)c->g, (const T*)c->att[s],
+                    (const T*)c->lo[s], (const T*)c->hi[s], (T*)c->v, c->k, c->bpart, G, slack_scale, alpha));
   c->theta_is_cert = false;
   if (screening && c->k > 0) {
     const int nbs = (int)((c->k + RT - 1) / RT);
@@ -675,8 +849,9 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
     LAUNCHED();
     prof_end(c, e1, BX_PROF_SPHERE, (double)c->k * (3.0 * sizeof(T) + 1.0));
   } else {
-    CU(cudaMemsetAsync(&c->sc->n_keep, 0, 3 * sizeof(int64_t), c->stream));
+    CU(cudaMemsetAsync(&c->sc->n_keep, 0, 6 * sizeof(int64_t), c->stream));
   }
+  if (screening && c->sharded()) TRY(allreduce(c, &c->sc->g_keep, 3, ncclInt64, ncclSum));
   return BX_OK;
 }
 
@@ -694,34 +869,48 @@ int certified(bx_ctx* c, double alpha) {
   TRY(run_pass<T>(c, full_view<T>(c), U_DOT, (const T*)c->rc, nullptr, nullptr, nullptr, nullptr,
                   (const T*)c->hifull, (T*)c->gfull, (const T*)c->attfull, nullptr, c->bpart + c->Gmax, c->has_inf,
                   &G));
-  int nb = grid1d(c, c->m > c->n ? c->m : c->n);
-  k_dual<T><<<nb, RT, 0, c->stream>>>((const T*)c->rc, (const T*)c->t, (const T*)c->y, (T*)c->thetac, c->m,
-                                       (const T*)c->gfull, (const T*)c->attfull, (const T*)c->lofull,
-                                       (const T*)c->hifull, (T*)c->vfull, c->n, c->bpart + c->Gmax, G, c->has_inf,
-                                       c->sc, 1, c->bpart3, 0.0, alpha, 5);
-  LAUNCHED();
+  TRY(dual_point<T>(c, 1, (const T*)c->rc, (const T*)c->y, (T*)c->thetac, (const T*)c->gfull,
+                    (const T*)c->attfull, (const T*)c->lofull, (const T*)c->hifull, (T*)c->vfull, c->n,
+                    c->bpart + c->Gmax, G, 0.0, alpha));
   return BX_OK;
 }
 
 // apply_screening + Workspace.refresh (screening.py:72-94, solvers.py:54-65)
 template <typename T>
-int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind) {
+int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, bool z_update) {
   const int s = c->cur, d = 1 - c->cur;
   const int nbs = (int)((c->k + RT - 1) / RT);
+  if (n_lo + n_up == 0) {
+    // nothing screened on this rank: keep its columns, join the collectives
+    if (z_update) {
+      View<T> vw{(const T*)c->A, c->lda, c->scr_idx, 0};
+      int G = 1;
+      TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      (const T*)c->scr_val, nullptr, 0, &G));
+      TRY(run_reduce<T>(c, G, (const T*)c->z, (T*)c->z2, R_PLAIN, nullptr, 0, 0));
+      std::swap(c->z, c->z2);
+      k_offsets<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const T*)c->y, (const T*)c->z, (T*)c->off,
+                                                            (T*)c->tgt);
+      LAUNCHED();
+    }
+    TRY(refresh_resid<T>(c));
+    if (kind == BX_APG) TRY(refresh_rprev<T>(c));
+    c->g_valid = false;
+    return BX_OK;
+  }
   ColState<T> src{c->idx[s], (T*)c->x[s], kind == BX_APG ? (T*)c->xprev[s] : nullptr, (T*)c->lo[s], (T*)c->hi[s],
                   (T*)c->nrm[s], (T*)c->att[s]};
   ColState<T> dst{c->idx[d], (T*)c->x[d], (T*)c->xprev[d], (T*)c->lo[d], (T*)c->hi[d], (T*)c->nrm[d], (T*)c->att[d]};
   k_compact<T><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (T*)c->xfull, c->scr_idx,
-                                           (T*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo, c->sat_up + c->n_sat_up);
+                                           (T*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo, c->sat_up + c->n_sat_up,
+                                           c->col_offset);
   LAUNCHED();
   c->cur = d;
   c->k = n_keep;
   c->n_sat_lo += n_lo;
   c->n_sat_up += n_up;
   // z += A_S bound_S  (only when some screened bound is nonzero)
-  const bool lo_nz = (c->bound_bits & 1) && n_lo > 0;
-  const bool up_nz = (c->bound_bits & 2) && n_up > 0;
-  if (lo_nz || up_nz) {
+  if (z_update) {
     View<T> vw{(const T*)c->A, c->lda, c->scr_idx, n_lo + n_up};
     int G = 1;
     TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
@@ -812,15 +1001,34 @@ int create_typed(bx_ctx* c, const void* y, const void* lower, const void* upper,
   CU(cudaMemsetAsync(c->probe, 0, 64, c->stream));
   const int nbw = (int)((n * 32 + RT - 1) / RT < 16 * c->nsm ? (n * 32 + RT - 1) / RT : 16 * c->nsm);
   k_colstats<T><<<nbw, RT, 0, c->stream>>>((const T*)c->A, c->lda, n, m, (const T*)c->t, (T*)c->nrmfull,
-                                            (T*)c->attfull, c->has_inf, c->probe);
+                                            (T*)c->attfull, 1, c->probe);
   LAUNCHED();
   int cf = 0;
   CU(cudaMemcpyAsync(&cf, c->probe, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  // solve() builds the translation vector before the screening state
+  // reported by bx_solve (after agreeing across ranks): the reference raises
+  // these from solve(), driver.py:381-392
+  c->col_bits = cf;
+  return BX_OK;
+}
+
+// data validation agreed over ranks: every rank raises the same error and the
+// global bound structure (some u infinite, nonzero bounds) drives every rank
+int validate(bx_ctx* c) {
+  // {some u infinite, some lower != 0, some finite upper != 0, zero column, t not interior}
+  int f[5] = {c->has_inf, c->bound_bits & 1, (c->bound_bits >> 1) & 1, c->col_bits & 1, (c->col_bits >> 1) & 1};
+  if (c->sharded()) {
+    CU(cudaMemcpyAsync(c->probe, f, sizeof(f), cudaMemcpyHostToDevice, c->stream));
+    TRY(allreduce(c, c->probe, 5, ncclInt32, ncclMax));
+    CU(cudaMemcpyAsync(f, c->probe, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  c->has_inf = f[0] ? 1 : 0;
+  c->bound_bits = (c->bound_bits & ~3) | (f[1] ? 1 : 0) | (f[2] ? 2 : 0);
+  // the translation vector is built before the screening state
   // (driver.py:381-392), so NoInteriorPoint takes precedence over ZeroColumn
-  if (c->has_inf && (cf & 2)) return fail(c, BX_ERR_NO_INTERIOR, "strategy did not yield a strictly interior t");
-  if (cf & 1) return fail(c, BX_ERR_ZERO_COLUMN, "zero column in A");
+  if (c->has_inf && f[4]) return fail(c, BX_ERR_NO_INTERIOR, "strategy did not yield a strictly interior t");
+  if (f[3]) return fail(c, BX_ERR_ZERO_COLUMN, "zero column in A");
   return BX_OK;
 }
 
@@ -835,10 +1043,14 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   const double alpha = cfg->alpha > 0 ? cfg->alpha : 1.0;
   const double slack_scale = cfg->slack_scale >= 0 ? cfg->slack_scale : 1e-12;
   const bool auto_eta = !(cfg->step_size > 0);  // NaN or <= 0
+  if (kind == BX_CD && c->sharded())
+    return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent is sequential: replicas only, no column sharding");
+  TRY(validate(c));
   TRY(reset_state<T>(c, kind));
   double eta = cfg->step_size;
   double sigma = 0.0;
-  int64_t basis = c->n;
+  int64_t kg = c->sharded() ? c->n_global : c->n;  // global preserved count
+  int64_t basis = kg;
   if ((kind == BX_PG || kind == BX_APG)) {
     if (auto_eta) {
       TRY(auto_step<T>(c, cfg->power_iters, alpha, fn, user, &eta, &sigma));
@@ -870,15 +1082,16 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       if (cert_gap < tol) converged = true;
     }
     int64_t n_lo = 0, n_up = 0;
-    if (cfg->screening && c->k > 0) {
-      n_lo = c->hsc->n_lo;
-      n_up = c->hsc->n_up;
+    if (cfg->screening && kg > 0) {
+      n_lo = c->hsc->g_lo;
+      n_up = c->hsc->g_up;
       if (n_lo || n_up) {
-        // theta of this round must survive the compaction's scratch use
-        TRY(compact<T>(c, n_lo, n_up, c->hsc->n_keep, kind));
-        if ((kind == BX_PG || kind == BX_APG) && auto_eta && (double)c->k < 0.5 * (double)basis) {
+        const bool z_update = ((c->bound_bits & 1) && n_lo > 0) || ((c->bound_bits & 2) && n_up > 0);
+        TRY(compact<T>(c, c->hsc->n_lo, c->hsc->n_up, c->hsc->n_keep, kind, z_update));
+        kg = c->hsc->g_keep;
+        if ((kind == BX_PG || kind == BX_APG) && auto_eta && (double)kg < 0.5 * (double)basis) {
           TRY(auto_step<T>(c, cfg->power_iters, alpha, fn, user, &eta, &sigma));
-          basis = c->k;
+          basis = kg;
         }
       }
     }
@@ -889,7 +1102,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       tr.primal = act.primal;
       tr.dual = act.dual;
       tr.gap = act.gap;
-      tr.preserved_count = c->k;
+      tr.preserved_count = kg;
       tr.newly_screened_lower = n_lo;
       tr.newly_screened_upper = n_up;
       tr.eps = act.eps;
@@ -992,7 +1205,7 @@ int bx_ctx_destroy(bx_ctx* c) {
   if (!c) return BX_OK;
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->hsc) cudaFreeHost(c->hsc);
-  if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  delete c->comm;
   delete c;
   return BX_OK;
 }
@@ -1013,8 +1226,8 @@ int bx_att(bx_ctx* c, void* out) {
 
 int bx_power_iter(bx_ctx* c, int32_t iters, const double* v0_host, double* sigma_out) {
   if (!sigma_out) return fail(c, BX_ERR_INVALID_ARGUMENT, "sigma_out");
-  if (c->dtype == BX_F64) return power_iter<double>(c, iters, v0_host, sigma_out);
-  return power_iter<float>(c, iters, v0_host, sigma_out);
+  if (c->dtype == BX_F64) return power_iter<double>(c, iters, v0_host, sigma_out, c->k);
+  return power_iter<float>(c, iters, v0_host, sigma_out, c->k);
 }
 
 int bx_reset(bx_ctx* c) {
@@ -1055,7 +1268,9 @@ int bx_dual_screen(bx_ctx* c, int32_t screening, double slack_scale, double* o) 
 int bx_compact(bx_ctx* c) {
   const int64_t lo = c->hsc->n_lo, up = c->hsc->n_up, keep = c->hsc->n_keep;
   if (lo + up == 0) return BX_OK;
-  int s = (c->dtype == BX_F64) ? compact<double>(c, lo, up, keep, BX_APG) : compact<float>(c, lo, up, keep, BX_APG);
+  const bool zu = ((c->bound_bits & 1) && lo > 0) || ((c->bound_bits & 2) && up > 0);
+  int s = (c->dtype == BX_F64) ? compact<double>(c, lo, up, keep, BX_APG, zu)
+                               : compact<float>(c, lo, up, keep, BX_APG, zu);
   if (s != BX_OK) return s;
   CU(cudaStreamSynchronize(c->stream));
   return BX_OK;
@@ -1113,15 +1328,51 @@ int bx_nccl_unique_id(unsigned char* id_out) {
 
 int bx_ctx_set_comm(bx_ctx* c, const unsigned char* id_host, int32_t rank, int32_t nranks, int64_t col_offset,
                     int64_t n_global) {
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return fail(c, BX_ERR_INVALID_ARGUMENT, "rank %d of %d", rank, nranks);
   if (!g_nccl.load()) return fail(c, BX_ERR_UNSUPPORTED, "libnccl.so.2 not found");
   ncclUniqueId id;
   memcpy(id.internal, id_host, 128);
-  ncclComm_t comm = nullptr;
-  const int r = g_nccl.init_rank(&comm, nranks, id, rank);
-  if (r != 0) return fail(c, BX_ERR_CUDA, "ncclCommInitRank: %d", r);
-  c->comm = comm;
+  NcclComm* nc = new NcclComm();
+  const int r = g_nccl.init_rank(&nc->comm, nranks, id, rank);
+  if (r != 0) {
+    delete nc;
+    return fail(c, BX_ERR_CUDA, "ncclCommInitRank: %d", r);
+  }
+  delete c->comm;
+  c->comm = nc;
   c->rank = rank;
   c->nranks = nranks;
+  c->col_offset = col_offset;
+  c->n_global = n_global;
+  return BX_OK;
+}
+
+int bx_group_create(bx_group** out, int32_t nranks) {
+  if (!out || nranks < 1 || nranks > kMaxRanks) return BX_ERR_INVALID_ARGUMENT;
+  bx_group* g = new bx_group();
+  g->n = nranks;
+  g->ptrs.assign(nranks, nullptr);
+  *out = g;
+  return BX_OK;
+}
+
+int bx_group_destroy(bx_group* g) {
+  delete g;
+  return BX_OK;
+}
+
+int bx_ctx_set_group(bx_ctx* c, bx_group* g, int32_t rank, int64_t col_offset, int64_t n_global) {
+  if (!c || !g || rank < 0 || rank >= g->n) return BX_ERR_INVALID_ARGUMENT;
+  LocalComm* lc = new LocalComm();
+  lc->g = g;
+  lc->rank = rank;
+  lc->tmp = c->grp_tmp;
+  lc->dptrs = c->grp_ptrs;
+  delete c->comm;
+  c->comm = lc;
+  c->rank = rank;
+  c->nranks = g->n;
   c->col_offset = col_offset;
   c->n_global = n_global;
   return BX_OK;

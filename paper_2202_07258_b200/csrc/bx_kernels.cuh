@@ -69,7 +69,8 @@ struct DevScalars {
   double cert_P;    // 0.5 ||A x - y||^2 on the full problem
   DualOut act;      // reduced-problem dual point of this round
   DualOut cert;     // certified (full-problem) dual point
-  int64_t n_keep, n_lo, n_up;
+  int64_t n_keep, n_lo, n_up;  // this rank's sphere-test counts
+  int64_t g_keep, g_lo, g_up;  // summed over ranks (== local on one GPU)
   int32_t err;
   int32_t restarts;
   unsigned int counters[8];
@@ -604,6 +605,29 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
 // ----------------------------------------------------------------------------
 // k_dual: dual point, reduced dual objective, clamped gap, radius, slack
 // ----------------------------------------------------------------------------
+// _reduced_dual (driver.py:360-368) / eval_dual (duality.py:401-422), clamp_gap
+// (duality.py:452), radius (screening.py:11-15), slack (driver.py:459)
+__device__ __forceinline__ void dual_finalize(DevScalars* sc, int which, double t1, double t2, double t3, double t4,
+                                              double eps, double slack_scale, double alpha) {
+  DualOut* out = which ? &sc->cert : &sc->act;
+  double dual = t1 - 0.5 * t2;
+  dual -= t3;
+  dual -= t4;
+  const double primal = which ? sc->cert_P : sc->P;
+  const double raw = primal - dual;
+  if (raw < -1e-9) set_err(sc, DE_INTERNAL_CONSISTENCY);
+  const double gap = fmax(raw, 0.0);
+  out->primal = primal;
+  out->dual = dual;
+  out->gap_raw = raw;
+  out->gap = gap;
+  out->eps = eps;
+  out->th_norm2 = t2;
+  out->radius = sqrt(2.0 * gap / alpha);
+  out->slack = slack_scale * fmax(1.0, sqrt(t2));
+  out->thr = out->radius + out->slack;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* __restrict__ t,
                                              const T* __restrict__ tgt, T* __restrict__ theta, int64_t m,
@@ -611,12 +635,11 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
                                              const T* __restrict__ lo, const T* __restrict__ hi,
                                              T* __restrict__ v, int64_t k, const double* eps_part, int Ge,
                                              int has_inf, DevScalars* sc, int which, double* bpart,
-                                             double slack_scale, double alpha, int counter) {
+                                             double slack_scale, double alpha, int counter, double* sums_out) {
   __shared__ double sh[RT / 32][4];
   __shared__ double s_eps;
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  DualOut* out = which ? &sc->cert : &sc->act;
   if (warp == 0) {
     double e = 0.0;
     if (has_inf)
@@ -682,24 +705,24 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
   t3 = warp_sum<double>(t3);
   t4 = warp_sum<double>(t4);
   if (lane != 0) return;
-  // _reduced_dual (driver.py:360-368) / eval_dual (duality.py:401-422)
-  double dual = t1 - 0.5 * t2;
-  dual -= t3;
-  dual -= t4;
-  const double primal = which ? sc->cert_P : sc->P;
-  const double raw = primal - dual;
-  if (raw < -1e-9) set_err(sc, DE_INTERNAL_CONSISTENCY);  // clamp_gap, duality.py:452
-  const double gap = fmax(raw, 0.0);
-  out->primal = primal;
-  out->dual = dual;
-  out->gap_raw = raw;
-  out->gap = gap;
-  out->eps = eps;
-  out->th_norm2 = t2;
-  out->radius = sqrt(2.0 * gap / alpha);                 // screening.py:11-15
-  out->slack = slack_scale * fmax(1.0, sqrt(t2));        // driver.py:459
-  out->thr = out->radius + out->slack;
   sc->counters[counter] = 0u;
+  if (sums_out) {
+    // column-sharded: the bound terms t3, t4 are this rank's share; the host
+    // allreduces them and k_dual_fin finalises (t1, t2 come from the
+    // replicated residual and are identical on every rank)
+    sums_out[0] = t1;
+    sums_out[1] = t2;
+    sums_out[2] = t3;
+    sums_out[3] = t4;
+    sums_out[4] = eps;
+    return;
+  }
+  dual_finalize(sc, which, t1, t2, t3, t4, eps, slack_scale, alpha);
+}
+
+__global__ void k_dual_fin(const double* sums, DevScalars* sc, int which, double slack_scale, double alpha) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    dual_finalize(sc, which, sums[0], sums[1], sums[2], sums[3], sums[4], slack_scale, alpha);
 }
 
 // ----------------------------------------------------------------------------
@@ -792,9 +815,9 @@ __global__ void __launch_bounds__(1024) k_scan(int32_t* bcnt, int nb, DevScalars
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    sc->n_keep = carry[0];
-    sc->n_lo = carry[1];
-    sc->n_up = carry[2];
+    sc->n_keep = sc->g_keep = carry[0];
+    sc->n_lo = sc->g_lo = carry[1];
+    sc->n_up = sc->g_up = carry[2];
   }
 }
 
@@ -816,7 +839,8 @@ template <typename T>
 __global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flags, const int32_t* __restrict__ boff,
                                                 int64_t k, ColState<T> src, ColState<T> dst, T* __restrict__ x_full,
                                                 int32_t* __restrict__ scr_idx, T* __restrict__ scr_val, int64_t n_lo_total,
-                                                int64_t* __restrict__ sat_lo, int64_t* __restrict__ sat_up) {
+                                                int64_t* __restrict__ sat_lo, int64_t* __restrict__ sat_up,
+                                                int64_t col_offset) {
   __shared__ int32_t woff[RT / 32][3];
   const int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x;
   const int f = (j < k) ? flags[j] : 3;
@@ -855,13 +879,13 @@ __global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flag
     x_full[id] = b;
     scr_idx[pos] = id;
     scr_val[pos] = b;
-    sat_lo[pos] = id;
+    sat_lo[pos] = col_offset + id;
   } else {
     const T b = src.hi[j];
     x_full[id] = b;
     scr_idx[n_lo_total + pos] = id;
     scr_val[n_lo_total + pos] = b;
-    sat_up[pos] = id;
+    sat_up[pos] = col_offset + id;
   }
 }
 
@@ -966,6 +990,63 @@ __global__ void k_bounds_probe(int64_t n, const T* __restrict__ lo, const T* __r
     if (isnan(l) || isnan(u)) f |= 32;
   }
   if (f) atomicOr(out, f);
+}
+
+// column-sharded helpers -----------------------------------------------------
+// fold per-block scalar partials into out[0..stride): sum (op 0) or max (op 1),
+// lane-strided + fixed-shape tree (deterministic)
+__global__ void k_fold(const double* __restrict__ in, int G, int stride, int op, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int q = 0; q < stride; ++q) {
+    double v = 0.0;
+    for (int b = lane; b < G; b += 32) {
+      const double x = __ldcg(&in[b * stride + q]);
+      v = op ? fmax(v, x) : v + x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, v, o);
+      v = op ? fmax(v, y) : v + y;
+    }
+    if (lane == 0) out[q] = v;
+  }
+}
+
+// in-process rank group (tests on one GPU): out = reduce over ranks of
+// ptrs[r][0..count) in rank order.  dtype: 0 f64, 1 f32, 2 i64, 3 i32; op: 0 sum, 1 max
+__global__ void k_group_reduce(void* __restrict__ out, const void* const* __restrict__ ptrs, int n, int64_t count,
+                               int dtype, int op) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    if (dtype == 0) {
+      double v = static_cast<const double*>(ptrs[0])[i];
+      for (int r = 1; r < n; ++r) {
+        const double x = static_cast<const double*>(ptrs[r])[i];
+        v = op ? fmax(v, x) : v + x;
+      }
+      static_cast<double*>(out)[i] = v;
+    } else if (dtype == 1) {
+      float v = static_cast<const float*>(ptrs[0])[i];
+      for (int r = 1; r < n; ++r) {
+        const float x = static_cast<const float*>(ptrs[r])[i];
+        v = op ? fmaxf(v, x) : v + x;
+      }
+      static_cast<float*>(out)[i] = v;
+    } else if (dtype == 2) {
+      long long v = static_cast<const long long*>(ptrs[0])[i];
+      for (int r = 1; r < n; ++r) {
+        const long long x = static_cast<const long long*>(ptrs[r])[i];
+        v = op ? (x > v ? x : v) : v + x;
+      }
+      static_cast<long long*>(out)[i] = v;
+    } else {
+      int v = static_cast<const int*>(ptrs[0])[i];
+      for (int r = 1; r < n; ++r) {
+        const int x = static_cast<const int*>(ptrs[r])[i];
+        v = op ? (x > v ? x : v) : v + x;
+      }
+      static_cast<int*>(out)[i] = v;
+    }
+  }
 }
 
 }  // namespace bx

@@ -1,0 +1,105 @@
+"""Column-sharded solves (BASELINE configs 3 and 4).
+
+Each rank owns a contiguous block of columns (its own A shard, per-column
+state and compaction); y, t, z and the residual are replicated.  Per FISTA /
+PG step the native loop allreduces the m-vector of partial A x (SUM), per
+round the epsilon of the dual translation (MAX), the bound terms of the dual
+objective (SUM) and the screening counts (SUM); power iteration and the
+certified gap follow the same pattern (csrc/bx_core.cu, run_reduce /
+dual_point / global_k).  Two transports behind one C++ interface:
+
+* NCCL (``solve_distributed``): one process per GPU under torchrun; the
+  128-byte unique id travels over the caller's torch.distributed group.
+* in-process group (``solve_group``): ranks are threads of one process with
+  their own streams, synchronised by host barriers only -- the test transport
+  that runs the exact sharded code path on a single GPU.
+
+Coordinate descent is sequential and is not sharded (replicas only).
+"""
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native as nat
+from .driver import _Session, _default_slack, _result
+from .model import Problem, QuadraticLoss
+from .solvers import SolverConfig
+
+
+def column_blocks(n, world):
+    """Contiguous, balanced column blocks [(c0, c1)] for ``world`` ranks."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    return [(n * r // world, n * (r + 1) // world) for r in range(world)]
+
+
+def shard(p, c0, c1):
+    """Problem over columns [c0, c1) of p, sharing p's device storage."""
+    d = p.device_arrays()
+    return Problem.from_device_storage(d["a"][c0:c1], p.m, d["y"], d["lo"][c0:c1], d["hi"][c0:c1])
+
+
+def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None,
+                return_shards=False):
+    """Column-sharded solve with ``nranks`` ranks as threads on the current GPU."""
+    import torch
+    cfg = cfg or SolverConfig()
+    slack_scale = _default_slack(p) if slack_scale is None else slack_scale
+    L = nat.lib()
+    group = ctypes.c_void_p()
+    nat.check(L.bx_group_create(ctypes.byref(group), nranks), None, "bx_group_create")
+    blocks = column_blocks(p.n, nranks)
+    sessions, results, errors = [], [None] * nranks, [None] * nranks
+    try:
+        for r, (c0, c1) in enumerate(blocks):
+            s = _Session(shard(p, c0, c1), tv=tv, stream=torch.cuda.Stream())
+            s.attach_group(group, r, c0, p.n)
+            sessions.append(s)
+
+        def work(r):
+            try:
+                results[r] = sessions[r].run(cfg, screening, loss.alpha, slack_scale)
+            except BaseException as e:  # surfaced below
+                errors[r] = e
+
+        threads = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for e in errors:
+            if e is not None:
+                raise e
+    finally:
+        for s in sessions:
+            s.close()
+        L.bx_group_destroy(group)
+    if return_shards:
+        return results
+    out, tr, _, theta, _, _ = results[0]
+    x = torch.cat([res[2] for res in results])
+    sl = torch.cat([res[4] for res in results])
+    su = torch.cat([res[5] for res in results])
+    return _result(p.n, out, tr, x, theta, sl, su, None, False)
+
+
+def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, tv=None, loss=QuadraticLoss,
+                      slack_scale=None, return_device=True, pg=None):
+    """This rank's part of an NCCL column-sharded solve (call on every rank of
+    the torch.distributed group ``pg``).  Returns the rank-local result: x is
+    the shard's block, trace / gap / theta are global."""
+    import torch.distributed as dist
+    cfg = cfg or SolverConfig()
+    slack_scale = _default_slack(p_shard) if slack_scale is None else slack_scale
+    rank, world = dist.get_rank(pg), dist.get_world_size(pg)
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        nat.check(nat.lib().bx_nccl_unique_id(uid), None, "bx_nccl_unique_id")
+    box = [uid.raw if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=pg)
+    with _Session(p_shard, tv=tv) as s:
+        s.attach_nccl(box[0], rank, world, col_offset, n_global)
+        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale)
+    return _result(n_global, out, tr, x, theta, sl, su, None, return_device, n_total=n_global)

@@ -125,6 +125,14 @@ class _Session:
                 L.bx_ctx_destroy(self.ctx)
                 self.ctx = None
 
+    def attach_group(self, group, rank, col_offset, n_global):
+        nat.check(nat.lib().bx_ctx_set_group(self.ctx, group, rank, col_offset, n_global), self.ctx,
+                  "bx_ctx_set_group")
+
+    def attach_nccl(self, uid, rank, nranks, col_offset, n_global):
+        nat.check(nat.lib().bx_ctx_set_comm(self.ctx, uid, rank, nranks, col_offset, n_global), self.ctx,
+                  "bx_ctx_set_comm")
+
     def __enter__(self):
         return self
 
@@ -180,6 +188,27 @@ class _Session:
         return out, trace[: min(out.rounds, cap)], x, theta, sl[: out.n_sat_lower], su[: out.n_sat_upper]
 
 
+def _result(p_n, out, tr, x, theta, sl, su, prof, return_device, n_total=None):
+    n = n_total or p_n
+    trace = [TraceRecord(int(r["round"]), float(r["elapsed"]), float(r["primal"]), float(r["dual"]),
+                         float(r["gap"]), int(r["preserved_count"]), (n - int(r["preserved_count"])) / n,
+                         int(r["newly_screened_lower"]), int(r["newly_screened_upper"])) for r in tr]
+    info = dict(iterations=int(out.iterations), step=float(out.step), sigma=float(out.sigma),
+                kernel_launches=int(out.kernel_launches), restarts=int(out.restarts), trace_arrays=tr, profile=prof)
+    if return_device:
+        xo, tho = x, theta
+    else:
+        xo = x.double().cpu().numpy()
+        tho = theta.double().cpu().numpy()
+    return SolveResult(x=xo, theta=tho, gap=float(out.gap), rounds=int(out.rounds), converged=bool(out.converged),
+                       trace=trace, sat_lower=sl.cpu().numpy(), sat_upper=su.cpu().numpy(), info=info)
+
+
+def _default_slack(p):
+    # driver.py:459 for fp64; fp32 needs a slack scaled to its unit round-off
+    return 1e-12 if p.dtype == np.float64 else 1e-5
+
+
 def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None, return_device=False,
           profile=False):
     """Run the chosen primal solver with (or without) dynamic safe screening.
@@ -194,21 +223,8 @@ def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=
     if not isinstance(p, Problem):
         raise TypeError("p must be a Problem")
     if slack_scale is None:
-        # driver.py:459 for fp64; fp32 needs a slack scaled to its unit round-off
-        slack_scale = 1e-12 if p.dtype == np.float64 else 1e-5
+        slack_scale = _default_slack(p)
     with _Session(p, tv=tv) as s:
         out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
         prof = s.profile
-    n = p.n
-    trace = [TraceRecord(int(r["round"]), float(r["elapsed"]), float(r["primal"]), float(r["dual"]),
-                         float(r["gap"]), int(r["preserved_count"]), (n - int(r["preserved_count"])) / n,
-                         int(r["newly_screened_lower"]), int(r["newly_screened_upper"])) for r in tr]
-    info = dict(iterations=int(out.iterations), step=float(out.step), sigma=float(out.sigma),
-                kernel_launches=int(out.kernel_launches), restarts=int(out.restarts), trace_arrays=tr, profile=prof)
-    if return_device:
-        xo, tho = x, theta
-    else:
-        xo = x.double().cpu().numpy()
-        tho = theta.double().cpu().numpy()
-    return SolveResult(x=xo, theta=tho, gap=float(out.gap), rounds=int(out.rounds), converged=bool(out.converged),
-                       trace=trace, sat_lower=sl.cpu().numpy(), sat_upper=su.cpu().numpy(), info=info)
+    return _result(p.n, out, tr, x, theta, sl, su, prof, return_device)

@@ -117,6 +117,31 @@ class Problem:
         self.j_inf = np.flatnonzero(self.j_inf_mask)
         self._pinned = None
 
+    @classmethod
+    def from_device_storage(cls, storage, m, y, lower, upper):
+        """Wrap CUDA storage that already has the C-ABI layout: ``storage`` is
+        (n, lda) row-major == column-major A with leading dimension lda >= m
+        (e.g. a column block ``full_storage[c0:c1]`` of a larger problem)."""
+        import torch
+        p = cls.__new__(cls)
+        n = storage.shape[0]
+        tdt = storage.dtype
+        p.dtype = np.dtype(np.float32) if tdt == torch.float32 else np.dtype(np.float64)
+        p.m, p.n = int(m), int(n)
+        dev = storage.device
+        lo = torch.as_tensor(lower, dtype=tdt, device=dev).broadcast_to((n,)).contiguous()
+        hi = torch.as_tensor(upper, dtype=tdt, device=dev).broadcast_to((n,)).contiguous()
+        yv = torch.as_tensor(y, device=dev).to(tdt).reshape(-1).contiguous()
+        p._dev = dict(a=storage, y=yv, lo=lo, hi=hi, device=dev)
+        p.a_matrix = None
+        p.y = None
+        p.lower = lo.double().cpu().numpy()
+        p.upper = hi.double().cpu().numpy()
+        p.j_inf_mask = np.isinf(p.upper)
+        p.j_inf = np.flatnonzero(p.j_inf_mask)
+        p._pinned = None
+        return p
+
     @staticmethod
     def _device_layout(a):
         """(m, n) tensor -> (n, lda) row-major storage == column-major A with a
