@@ -284,6 +284,112 @@ def metric_name(cfg_id):
             f"[config {cfg_id}]")
 
 
+def roofline_block(prof):
+    hbm, peak_src, _ = peaks()
+    prof = prof or {}
+    tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
+    dom_name = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
+    dom = prof.get(dom_name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
+    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["ms"] > 0 else 0.0
+    return {"bound": "hbm", "kernel": f"k_pass[{dom_name}]", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+            "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / max(1, dom["launches"]),
+            "share_of_kernel_time": dom["ms"] / tot_ms,
+            "bytes_per_launch_avg": dom["bytes"] / max(1, dom["launches"]),
+            "algorithmic_bytes": "8*m per streamed column + per-column state + row vectors (DESIGN.md)",
+            "passes_per_iteration": 1,
+            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                            "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
+                        for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+
+
+def run_sharded(args, rank, world, dev):
+    """Configs 3 / 4 over `world` GPUs: NCCL column sharding (csrc/bx_core.cu)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2202_07258_b200 import Problem, SolverConfig
+    from paper_2202_07258_b200.distributed import column_blocks, solve_distributed
+    from paper_2202_07258_b200.generate import CONFIGS, sparse_nnls_block
+    c = CONFIGS[args.config]
+    m = c["m"]
+    n = c["n"] if args.config == 3 else 62500 * world  # config 4: 62,500 columns per GPU (weak)
+    c0, c1 = column_blocks(n, world)[rank]
+
+    def reduce_sum(v):
+        t = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+        dist.all_reduce(t)
+        return t.cpu().numpy()
+
+    dt = np.float32 if args.config == 4 else np.float64
+    a_blk, y, lo, hi, _ = sparse_nnls_block(m, n, c["density"], c["snr"], c0, c1, reduce_sum, dtype=dt)
+    a_dev = torch.from_numpy(np.ascontiguousarray(a_blk.T)).to(dev)
+    tdt = a_dev.dtype
+    p = Problem.from_device_storage(a_dev, m, torch.from_numpy(y).to(dev).to(tdt), lo, hi)
+    cfg = SolverConfig(kind=c["kind"], inner_passes=c["inner_passes"], gap_tol=c["gap_tol"])
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        solve_distributed(p, c0, n, cfg)
+    torch.cuda.synchronize()
+    results = []
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            results.append(solve_distributed(p, c0, n, cfg))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    el = torch.tensor([ev0.elapsed_time(ev1) / 1000.0], device=dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    elapsed = float(el.item())
+    iters = sum(r.info["iterations"] for r in results)
+    launches = sum(r.info["kernel_launches"] for r in results)
+    prof_res = solve_distributed(p, c0, n, cfg, profile=True)
+    roof = roofline_block(prof_res.info["profile"])
+    e2e = None
+    if not args.no_e2e:
+        p_host = Problem(a_blk, y, lo, hi, dtype=dt, pin=True)
+        h2d = p_host.a_matrix.nbytes + y.nbytes + lo.nbytes + hi.nbytes
+        e_it, e_t = 0, 0.0
+        for s_ in range(args.steps + 1):
+            p_host.release_device()
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            r = solve_distributed(p_host, c0, n, cfg, return_device=False)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            tt = torch.tensor([t0.elapsed_time(t1) / 1000.0], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if s_ == 0:
+                continue
+            e_t += float(tt.item())
+            e_it += r.info["iterations"]
+        e2e = {"value": e_it / e_t, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(8 * (c1 - c0) + 8 * m), "ms_per_step": 1000.0 * e_t / args.steps,
+               "note": "per-rank bytes; every rank uploads its own column block"}
+    r0 = results[0]
+    line = {"metric": metric_name(args.config), "value": iters / elapsed, "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / args.steps,
+            "higher_is_better": True, "scaling": "strong" if args.config == 3 else "weak", "vs_baseline": None,
+            "dtype": "f32" if dt == np.float32 else "f64",
+            "data": "synthetic (seeded numpy, BASELINE config recipe; per-rank column blocks of the same draw)",
+            "config": {"workload": c["name"], "m": m, "n": n, "solver": c["kind"], "inner_passes": c["inner_passes"],
+                       "gap_tol": c["gap_tol"], "screening": True, "parallelism": f"column-sharded x{world} (NCCL)",
+                       "l2_policy": "inputs larger than L2", "step": "one full solve to certified gap <= gap_tol"},
+            "time_to_gap_s": elapsed / args.steps, "converged": all(r.converged for r in results),
+            "rounds": r0.rounds, "iterations_per_solve": r0.info["iterations"],
+            "final_preserved": r0.trace[-1].preserved_count, "certified_gap": r0.gap, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": None, "e2e": e2e, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -292,6 +398,8 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+        if args.config in (3, 4):
+            return run_sharded(args, rank, world, dev)
     from paper_2202_07258_b200 import Problem, SolverConfig, solve
 
     inst = make_instance(args.config)
@@ -330,28 +438,13 @@ def run_ours(args):
         elapsed = float(t.item())
     iters = sum(r.info["iterations"] for r in results)
     launches = sum(r.info["kernel_launches"] for r in results)
-    value = world * iters / elapsed
+    value = world * iters / elapsed  # replicas (configs 1, 2): every rank solves the whole problem
     ms_per_step = 1000.0 * elapsed / args.steps
     conv = all(r.converged for r in results)
 
     # live roofline of the dominant kernel (one extra, instrumented solve)
     prof_res = solve(p_dev, cfg, return_device=True, profile=True)
-    prof = prof_res.info["profile"] or {}
-    hbm, peak_src, pk = peaks()
-    tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
-    dom_name = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
-    dom = prof.get(dom_name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
-    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["ms"] > 0 else 0.0
-    roof = {"bound": "hbm", "kernel": f"k_pass[{dom_name}]", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-            "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / max(1, dom["launches"]),
-            "share_of_kernel_time": dom["ms"] / tot_ms,
-            "bytes_per_launch_avg": dom["bytes"] / max(1, dom["launches"]),
-            "algorithmic_bytes": "8*m per streamed column + per-column state + row vectors (DESIGN.md)",
-            "passes_per_iteration": 1,
-            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                            "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
-                        for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+    roof = roofline_block(prof_res.info["profile"])
 
     # trajectory for the CPU arm (preserved-count bins of this solve)
     bins = k_bins_from_trace(prof_res.info["trace_arrays"], inst.inner_passes)

@@ -86,7 +86,7 @@ def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLo
 
 
 def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, tv=None, loss=QuadraticLoss,
-                      slack_scale=None, return_device=True, pg=None):
+                      slack_scale=None, return_device=True, pg=None, profile=False):
     """This rank's part of an NCCL column-sharded solve (call on every rank of
     the torch.distributed group ``pg``).  Returns the rank-local result: x is
     the shard's block, trace / gap / theta are global."""
@@ -101,5 +101,6 @@ def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, t
     dist.broadcast_object_list(box, src=0, group=pg)
     with _Session(p_shard, tv=tv) as s:
         s.attach_nccl(box[0], rank, world, col_offset, n_global)
-        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale)
-    return _result(n_global, out, tr, x, theta, sl, su, None, return_device, n_total=n_global)
+        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
+        prof = s.profile
+    return _result(n_global, out, tr, x, theta, sl, su, prof, return_device, n_total=n_global)

@@ -70,6 +70,28 @@ def sparse_nnls(m, n, density, snr_db, seed=0, dtype=np.float64):
     return a, y, np.zeros(n), np.full(n, np.inf), x0
 
 
+def sparse_nnls_block(m, n, density, snr_db, c0, c1, reduce_sum, seed=0, dtype=np.float64):
+    """Columns [c0, c1) of ``sparse_nnls(m, n, ...)`` without drawing the rest:
+    the A stream is advanced to column c0 (PCG64 draws one 64-bit word per
+    double), so the block's columns are bit-identical to the full draw.  The
+    clean signal A x0 is the sum of the ranks' partial products, formed by the
+    caller's ``reduce_sum`` (an allreduce); y therefore equals the full draw's y
+    up to summation order.  Returns (A_block F-order, y, lower, upper, x0)."""
+    rng_a, rng_x, rng_e = _streams(seed, 3)
+    rng_a.bit_generator.advance(c0 * m)
+    a = _unit_columns(rng_a.random((c1 - c0, m), dtype=np.float64).T)
+    k = max(1, int(round(density * n)))
+    x0 = np.zeros(n)
+    sup = rng_x.choice(n, size=k, replace=False)
+    x0[sup] = np.abs(rng_x.standard_normal(k))
+    clean = reduce_sum(a @ x0[c0:c1])
+    sigma = np.linalg.norm(clean) / np.sqrt(m) * 10.0 ** (-snr_db / 20.0)
+    y = clean + sigma * rng_e.standard_normal(m)
+    if dtype != np.float64:
+        a = np.asfortranarray(a.astype(dtype))
+    return a, y, np.zeros(c1 - c0), np.full(c1 - c0, np.inf), x0
+
+
 def box_bvls(m, n, snr_db, seed=0):
     """N(0,1/m) entries, unit columns, x0 40% at 0, 40% at 1, 20% U(0,1) (config 2)."""
     rng_a, rng_x, rng_e = _streams(seed, 3)
