@@ -16,9 +16,10 @@
  *    Matrices are column-major with a leading dimension `lda >= m`; the column
  *    stride `lda * sizeof(elem)` and the base pointer must be 16-byte aligned
  *    (the bulk-copy engine streams whole columns).
- *  - Element type is fp64 (BX_F64) or fp32 (BX_F32) for A, y, bounds, t and
- *    every per-row / per-column vector; scalars (objectives, gaps, steps) are
- *    always fp64.
+ *  - A is stored in fp64 (BX_F64) or fp32 (BX_F32, BASELINE config 4: half the
+ *    streamed bytes, products accumulated in fp32 per CTA); y, bounds, t, the
+ *    iterate and every other vector and scalar are fp64 (so fp32 storage never
+ *    limits the precision of x -- DESIGN.md, "fp32").
  *  - Upper bounds may be +inf (NNLS / mixed); lower bounds must be finite.
  *  - Every function returns a bx_status.  Nonzero codes map 1:1 onto the
  *    reference exception classes of errors.py (listed per code).  The message
@@ -73,6 +74,8 @@ typedef struct {
   int32_t screening;     /* 0/1                                                  */
   double alpha;          /* loss strong-concavity constant (model.py:40) = 1     */
   double slack_scale;    /* driver.py:219: 1e-12 for fp64                        */
+  int32_t relative_gap;  /* 1: stop when gap <= gap_tol * max(1, P) (fp32 rule,
+                            DESIGN.md); 0: absolute gap (reference rule)        */
 } bx_solve_cfg;
 
 /* TraceRecord (driver.py:268-278) plus the dual-point internals. */
@@ -123,9 +126,9 @@ const char* bx_last_error(const bx_ctx* ctx);
 
 /* ---- fine-grained entry points (Workspace contract, solvers.py:48-137) ---- */
 
-/* column norms ||a_j|| (model.py:89-92), length n, element type */
+/* column norms ||a_j|| (model.py:89-92), length n, fp64 */
 int bx_col_norms(bx_ctx* ctx, void* out);
-/* A't (duality.py:350), length n, element type */
+/* A't (duality.py:350), length n, fp64 */
 int bx_att(bx_ctx* ctx, void* out);
 /* spectral_norm_estimate on the preserved columns (solvers.py:72-86) */
 int bx_power_iter(bx_ctx* ctx, int32_t iters, const double* v0_host, double* sigma_out);
@@ -154,8 +157,8 @@ int bx_solve(bx_ctx* ctx, const bx_solve_cfg* cfg, bx_start_vector_fn start_fn,
              void* start_user, bx_trace_rec* trace_host, int64_t trace_cap,
              bx_solve_out* out_host);
 
-/* final state (SolveResult, driver.py:281-290): x (n, element type), theta
- * (m, element type), sat_lower / sat_upper (int64, in screening order).  Any
+/* final state (SolveResult, driver.py:281-290): x (n, fp64), theta
+ * (m, fp64), sat_lower / sat_upper (int64, in screening order).  Any
  * pointer may be NULL.  Device pointers. */
 int bx_get_state(bx_ctx* ctx, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper);
 

@@ -23,7 +23,7 @@ class SolveCfg(ctypes.Structure):
                 ("max_rounds", ctypes.c_int64), ("gap_tol", ctypes.c_double),
                 ("step_size", ctypes.c_double), ("power_iters", ctypes.c_int32),
                 ("screening", ctypes.c_int32), ("alpha", ctypes.c_double),
-                ("slack_scale", ctypes.c_double)]
+                ("slack_scale", ctypes.c_double), ("relative_gap", ctypes.c_int32)]
 
 
 class TraceRec(ctypes.Structure):

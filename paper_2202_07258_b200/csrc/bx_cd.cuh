@@ -39,14 +39,14 @@ struct CdArgs {
   int64_t ld;
   int64_t m;
   int64_t k;         // preserved columns
-  T* x;              // preserved iterate, read in even passes
-  T* x2;             // written in even passes, read in odd (ping-pong: every
+  double* x;         // preserved iterate, read in even passes
+  double* x2;        // written in even passes, read in odd (ping-pong: every
                      // CTA reads x_j while rank 0 publishes the new value)
-  const T* lo;
-  const T* hi;
-  const T* nrm;      // ||a_j||  (sq = nrm^2, as solvers.py:60)
-  const T* gram;     // [nblocks][B][B] Gram blocks
-  T* r;              // residual (in/out, m)
+  const double* lo;
+  const double* hi;
+  const double* nrm; // ||a_j||  (sq = nrm^2, as solvers.py:60)
+  const double* gram;  // [nblocks][B][B] Gram blocks (fp64)
+  double* r;         // residual (in/out, m)
   DevScalars* sc;
   int passes;
   int rows_per_cta;  // multiple of 2
@@ -91,11 +91,11 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   const int nrows = (int)max((int64_t)0, min((int64_t)rows_pad, a.m - row0));
 
   // residual rows in registers: thread owns rows tid + q*CD_NT
-  T rr[CD_RMAX];
+  double rr[CD_RMAX];
 #pragma unroll
   for (int q = 0; q < CD_RMAX; ++q) {
     const int i = tid + q * CD_NT;
-    rr[q] = (i < nrows) ? a.r[row0 + i] : T(0);
+    rr[q] = (i < nrows) ? a.r[row0 + i] : 0.0;
   }
   const int64_t nblk = (a.k + CD_B - 1) / CD_B;
   int64_t it = 0;  // global block counter (selects buffers)
@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       const int nc = (int)min((int64_t)CD_B, a.k - c0);
       if (nrows > 0) cp_async_wait_all();
       // Gram block for the sequential update
-      const T* gsrc = a.gram + blk * CD_B * CD_B;
-      for (int q = tid; q < CD_B * CD_B; q += CD_NT) gbuf[q] = static_cast<double>(gsrc[q]);
+      const double* gsrc = a.gram + blk * CD_B * CD_B;
+      for (int q = tid; q < CD_B * CD_B; q += CD_NT) gbuf[q] = gsrc[q];
       __syncthreads();
       // prefetch the next block while this one is processed
       {
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         for (int q = 0; q < CD_RMAX; ++q) {
           const int i = tid + q * CD_NT;
           if (i < nrows) {
-            const double rv = static_cast<double>(rr[q]);
+            const double rv = rr[q];
 #pragma unroll
             for (int c = 0; c < CD_B; ++c)
               if (c < nc) pd[c] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * rv;
@@ -169,28 +169,28 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           }
         }
         const int64_t j = c0 + lane;
-        const T* xin = (pass & 1) ? a.x2 : a.x;
-        T* xout = (pass & 1) ? a.x : a.x2;
-        T xj = T(0), loj = T(0), hij = T(0);
+        const double* xin = (pass & 1) ? a.x2 : a.x;
+        double* xout = (pass & 1) ? a.x : a.x2;
+        double xj = 0.0, loj = 0.0, hij = 0.0;
         double sq = 1.0;
         if (lane < nc) {
           xj = xin[j];
           loj = a.lo[j];
           hij = a.hi[j];
-          const double nj = static_cast<double>(a.nrm[j]);
+          const double nj = a.nrm[j];
           sq = nj * nj;  // solvers.py:60 (col_norms ** 2)
         }
         double dl = 0.0;
         for (int i = 0; i < nc; ++i) {
           double di = 0.0;
           if (lane == i) {
-            const T step = static_cast<T>(cdot / sq);                  // solvers.py:131
-            T nv = xj - step;                                           // solvers.py:132
+            const double step = cdot / sq;                             // solvers.py:131
+            double nv = xj - step;                                      // solvers.py:132
             nv = nv < loj ? loj : nv;
             nv = nv > hij ? hij : nv;
-            const T dt = nv - xj;                                       // solvers.py:133
-            if (dt != T(0)) {
-              di = static_cast<double>(dt);
+            const double dt = nv - xj;                                  // solvers.py:133
+            if (dt != 0.0) {
+              di = dt;
               xj = nv;
             }
             dl = di;
@@ -207,10 +207,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       for (int q = 0; q < CD_RMAX; ++q) {
         const int i = tid + q * CD_NT;
         if (i < nrows) {
-          T acc = rr[q];
+          double acc = rr[q];
           for (int c = 0; c < nc; ++c) {
             const double dc = delta[c];
-            if (dc != 0.0) acc += cur[(int64_t)c * rows_pad + i] * static_cast<T>(dc);
+            if (dc != 0.0) acc += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * dc;
           }
           rr[q] = acc;
         }
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     const int i = tid + q * CD_NT;
     if (i < nrows) {
       a.r[row0 + i] = rr[q];
-      sq += static_cast<double>(rr[q]) * static_cast<double>(rr[q]);
+      sq += rr[q] * rr[q];
     }
   }
   sq = warp_sum<double>(sq);
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
 // Gram blocks G_JJ = A_J' A_J for consecutive blocks of CD_B preserved columns
 template <typename T>
 __global__ void __launch_bounds__(256) k_gram(const T* __restrict__ A, int64_t ld, int64_t m, int64_t k,
-                                              T* __restrict__ gram) {
+                                              double* __restrict__ gram) {
   __shared__ T tile[CD_B][129];  // 128-row chunk of the block's columns (+1 pad)
   const int64_t blk = blockIdx.x;
   const int64_t c0 = blk * CD_B;
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) k_gram(const T* __restrict__ A, int64_t l
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int p = threadIdx.x * 4 + u;
-    gram[blk * CD_B * CD_B + p] = static_cast<T>(acc[u]);
+    gram[blk * CD_B * CD_B + p] = acc[u];
   }
 }
 

@@ -239,7 +239,9 @@ struct bx_ctx {
   void* grp_tmp = nullptr;
   const void** grp_ptrs = nullptr;
   int val_bits = 0, col_bits = 0;  // validation flags recorded at create
-  bool sharded() const { return comm != nullptr && nranks > 1; }
+  // an attached communicator always takes the collective code path (even
+  // with one rank, which is how the NCCL plumbing is exercised on one GPU)
+  bool sharded() const { return comm != nullptr; }
 };
 
 namespace {
@@ -344,8 +346,9 @@ constexpr int kPartRows = 1;  // placeholder to keep layout comments aligned
 
 void carve(bx_ctx* c, Carver& w) {
   const int64_t m = c->m, n = c->n, mp = c->mp;
-  const size_t e = c->esz;
-  c->Aact = w.take((size_t)c->ldact * n * e);
+  const size_t e = 8;       // every vector is fp64
+  const size_t ea = c->esz; // storage type of A
+  c->Aact = w.take((size_t)c->ldact * n * ea);
   void** rows[] = {&c->y, &c->t, &c->negy, &c->z, &c->z2, &c->off, &c->tgt,
                    &c->r, &c->rprev, &c->rc, &c->theta, &c->thetac, &c->u};
   for (void** p : rows) *p = w.take(mp * e);
@@ -361,7 +364,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->g = w.take(n * e);
   c->v = w.take(n * e);
   c->coef = w.take(n * e);
-  c->gram = w.take((size_t)((n + CD_B - 1) / CD_B) * CD_B * CD_B * e);
+  c->gram = w.take((size_t)((n + CD_B - 1) / CD_B) * CD_B * CD_B * 8);
   c->xfull = w.take(n * e);
   c->lofull = w.take(n * e);
   c->hifull = w.take(n * e);
@@ -377,7 +380,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->sat_up = (int64_t*)w.take(n * 8);
   c->probe = (int*)w.take(64);
   c->ldp = mp;
-  c->part = w.take((size_t)c->Gmax * c->ldp * e);
+  c->part = w.take((size_t)c->Gmax * c->ldp * ea);
   c->bpart = (double*)w.take(c->Gmax * 8 * 4);
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
@@ -459,9 +462,9 @@ int pass_grid(bx_ctx* c, int64_t k) {
 
 // Launch one streamed pass.  Returns the grid used through *G_out.
 template <typename T>
-int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_prev, T* x, T* xprev, const T* lo,
-             const T* hi, T* g, const T* att, const T* coef, double* bpart, int has_inf, int* G_out,
-             const T* nrm = nullptr) {
+int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
+             double* xprev, const double* lo, const double* hi, double* g, const double* att, const double* coef,
+             double* bpart, int has_inf, int* G_out, const double* nrm = nullptr) {
   const int R = pick_R(c->m, sizeof(T));
   if (R < 0) return fail(c, BX_ERR_UNSUPPORTED, "m=%lld exceeds the fused-pass envelope", (long long)c->m);
   const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
@@ -529,7 +532,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const T* vin, const T* vin_p
 }
 
 template <typename T>
-int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* wpart, int Gw, int counter) {
+int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const double* wpart, int Gw, int counter) {
   const int64_t rb = 32 * (16 / (int64_t)sizeof(T));
   int nb = (int)((c->m + rb - 1) / rb);
   if (nb > 4 * c->nsm) nb = 4 * c->nsm;
@@ -537,7 +540,7 @@ int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* w
   if (c->sharded()) {
     // phase A: this rank's partial rows; block scalars folded; both summed
     // over ranks (NCCL allreduce); phase B: offset, objective, mode logic
-    k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, nullptr, (T*)c->rloc, c->sc,
+    k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, nullptr, (double*)c->rloc, c->sc,
                                            c->bpart2, nullptr, 0, R_PLAIN, counter);
     LAUNCHED();
     const int stride = (mode == R_APG) ? 2 : 1;
@@ -545,9 +548,10 @@ int run_reduce(bx_ctx* c, int G, const T* off, T* out, int mode, const double* w
       k_fold<<<1, 32, 0, c->stream>>>(wpart, Gw, stride, 0, c->scal);
       LAUNCHED();
     }
-    TRY(allreduce(c, c->rloc, (size_t)c->m, nccl_type<T>(), ncclSum));
+    TRY(allreduce(c, c->rloc, (size_t)c->m, ncclFloat64, ncclSum));
+    const int nb2 = (int)(((c->m + 63) / 64) < 4 * c->nsm ? (c->m + 63) / 64 : 4 * c->nsm);
     if (wpart && Gw > 0) TRY(allreduce(c, c->scal, (size_t)stride, ncclFloat64, ncclSum));
-    k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->rloc, c->ldp, 1, c->m, off, out, c->sc, c->bpart2,
+    k_reduce<double><<<nb2, RT, 0, c->stream>>>((const double*)c->rloc, c->ldp, 1, c->m, off, out, c->sc, c->bpart2,
                                            (wpart && Gw > 0) ? c->scal : nullptr, (wpart && Gw > 0) ? 1 : 0, mode,
                                            counter);
     LAUNCHED();
@@ -582,7 +586,7 @@ int check_dev_err(bx_ctx* c) {
   const int e = c->hsc->err;
   if (e == 0) return BX_OK;
   if (e == DE_STEP_TOO_LARGE)
-    return fail(c, BX_ERR_STEP_TOO_LARGE, "objective rose from %.6e to %.6e", c->hsc->P_prev, c->hsc->P);
+    return fail(c, BX_ERR_STEP_TOO_LARGE, "objective rose from %.6e to %.6e", c->hsc->err_v1, c->hsc->err_v2);
   if (e == DE_INTERNAL_CONSISTENCY) {
     const DualOut& d = c->hsc->act.gap_raw < -1e-9 ? c->hsc->act : c->hsc->cert;
     return fail(c, BX_ERR_INTERNAL_CONSISTENCY, "duality gap %.3e below round-off slack", d.gap_raw);
@@ -595,9 +599,9 @@ template <typename T>
 int refresh_resid(bx_ctx* c) {
   const int s = c->cur;
   int G = 1;
-  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, (T*)c->x[s], nullptr, nullptr, nullptr, nullptr,
+  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, (double*)c->x[s], nullptr, nullptr, nullptr, nullptr,
                   nullptr, nullptr, nullptr, 0, &G));
-  TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->r, R_SET, nullptr, 0, 0));
+  TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_SET, nullptr, 0, 0));
   return BX_OK;
 }
 
@@ -606,9 +610,9 @@ template <typename T>
 int refresh_rprev(bx_ctx* c) {
   const int s = c->cur;
   int G = 1;
-  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, (T*)c->xprev[s], nullptr, nullptr, nullptr, nullptr,
+  TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, (double*)c->xprev[s], nullptr, nullptr, nullptr, nullptr,
                   nullptr, nullptr, nullptr, 0, &G));
-  TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_PLAIN, nullptr, 0, 0));
+  TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->rprev, R_PLAIN, nullptr, 0, 0));
   return BX_OK;
 }
 
@@ -621,20 +625,18 @@ int power_iter(bx_ctx* c, int iters, const double* v0_host, double* sigma, int64
     *sigma = 0.0;
     return BX_OK;
   }
-  std::vector<T> tmp(k > 0 ? k : 1);
-  for (int64_t i = 0; i < k; ++i) tmp[i] = (T)v0_host[i];
-  if (k > 0) CU(cudaMemcpyAsync(c->coef, tmp.data(), k * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  if (k > 0) CU(cudaMemcpyAsync(c->coef, v0_host, k * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   int G = 1;
   TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                  (const T*)c->coef, nullptr, 0, &G));
-  TRY(run_reduce<T>(c, G, nullptr, (T*)c->u, R_PLAIN, nullptr, 0, 0));
+                  (const double*)c->coef, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, nullptr, (double*)c->u, R_PLAIN, nullptr, 0, 0));
   CU(cudaMemsetAsync(&c->sc->err, 0, sizeof(int32_t), c->stream));
   double sig = 0.0;
   // chunks of 10 iterations between host checks of the ||w|| == 0 exit
   for (int it = 0; it < iters; ++it) {
-    TRY(run_pass<T>(c, act_view<T>(c), U_POWER, (const T*)c->u, nullptr, nullptr, nullptr, nullptr, nullptr,
-                    (T*)c->g, nullptr, nullptr, c->bpart, 0, &G));
-    TRY(run_reduce<T>(c, G, nullptr, (T*)c->u, R_POWER, c->bpart, G, 1));
+    TRY(run_pass<T>(c, act_view<T>(c), U_POWER, (const double*)c->u, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    (double*)c->g, nullptr, nullptr, c->bpart, 0, &G));
+    TRY(run_reduce<T>(c, G, nullptr, (double*)c->u, R_POWER, c->bpart, G, 1));
   }
   TRY(sync_scalars<T>(c));
   if (c->hsc->err == DE_POWER_ZERO) {
@@ -726,7 +728,7 @@ int cd_sweeps(bx_ctx* c, int passes) {
   if (c->gram_dirty) {
     const int nblk = (int)((c->k + CD_B - 1) / CD_B);
     const int e0 = prof_begin(c);
-    k_gram<T><<<nblk, 256, 0, c->stream>>>(vw.A, vw.ld, c->m, c->k, (T*)c->gram);
+    k_gram<T><<<nblk, 256, 0, c->stream>>>(vw.A, vw.ld, c->m, c->k, (double*)c->gram);
     LAUNCHED();
     prof_end(c, e0, BX_PROF_CD, (double)c->k * c->m * sizeof(T));
     c->gram_dirty = false;
@@ -736,13 +738,13 @@ int cd_sweeps(bx_ctx* c, int passes) {
   a.ld = vw.ld;
   a.m = c->m;
   a.k = c->k;
-  a.x = (T*)c->x[s];
-  a.x2 = (T*)c->coef;
-  a.lo = (const T*)c->lo[s];
-  a.hi = (const T*)c->hi[s];
-  a.nrm = (const T*)c->nrm[s];
-  a.gram = (const T*)c->gram;
-  a.r = (T*)c->r;
+  a.x = (double*)c->x[s];
+  a.x2 = (double*)c->coef;
+  a.lo = (const double*)c->lo[s];
+  a.hi = (const double*)c->hi[s];
+  a.nrm = (const double*)c->nrm[s];
+  a.gram = (const double*)c->gram;
+  a.r = (double*)c->r;
   a.sc = c->sc;
   a.passes = passes;
   a.rows_per_cta = (int)rows;
@@ -765,7 +767,7 @@ int cd_sweeps(bx_ctx* c, int passes) {
   CU(cudaLaunchKernelEx(&lc, k_cd<T>, a));
   LAUNCHED();
   prof_end(c, e0, BX_PROF_CD, 2.0 * (double)passes * c->k * c->m * sizeof(T));
-  if (passes & 1) CU(cudaMemcpyAsync(c->x[s], c->coef, c->k * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  if (passes & 1) CU(cudaMemcpyAsync(c->x[s], c->coef, c->k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   c->g_valid = false;
   return BX_OK;
 }
@@ -778,20 +780,20 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
     int G = 1;
     if (kind == BX_PG) {
       if (c->g_valid) {
-        TRY(run_pass<T>(c, act_view<T>(c), U_PG_G, nullptr, nullptr, (T*)c->x[s], nullptr, (const T*)c->lo[s],
-                        (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, nullptr, 0, &G));
+        TRY(run_pass<T>(c, act_view<T>(c), U_PG_G, nullptr, nullptr, (double*)c->x[s], nullptr, (const double*)c->lo[s],
+                        (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G));
       } else {
-        TRY(run_pass<T>(c, act_view<T>(c), U_PG, (const T*)c->r, nullptr, (T*)c->x[s], nullptr, (const T*)c->lo[s],
-                        (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, nullptr, 0, &G));
+        TRY(run_pass<T>(c, act_view<T>(c), U_PG, (const double*)c->r, nullptr, (double*)c->x[s], nullptr, (const double*)c->lo[s],
+                        (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G));
       }
-      TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->r, R_PG, nullptr, 0, 2));
+      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_PG, nullptr, 0, 2));
       c->g_valid = false;
     } else if (kind == BX_APG) {
-      TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const T*)c->r, (const T*)c->rprev, (T*)c->x[s], (T*)c->xprev[s],
-                      (const T*)c->lo[s], (const T*)c->hi[s], (T*)c->g, nullptr, nullptr, c->bpart, 0, &G,
-                      (const T*)c->nrm[s]));
+      TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const double*)c->r, (const double*)c->rprev, (double*)c->x[s], (double*)c->xprev[s],
+                      (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, c->bpart, 0, &G,
+                      (const double*)c->nrm[s]));
       // r_prev <- r, r <- new residual: write into the r_prev buffer, swap
-      TRY(run_reduce<T>(c, G, (const T*)c->off, (T*)c->rprev, R_APG, c->bpart, G, 2));
+      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->rprev, R_APG, c->bpart, G, 2));
       std::swap(c->r, c->rprev);
     } else {
       return cd_sweeps<T>(c, passes);  // all sweeps in one launch
@@ -802,8 +804,9 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
 
 // epsilon (max over ranks), theta, reduced dual, gap, radius (k_dual [+ fin])
 template <typename T>
-int dual_point(bx_ctx* c, int which, const T* r, const T* tgt, T* theta, const T* g, const T* att, const T* lo,
-               const T* hi, T* v, int64_t k, const double* eps_part, int Ge, double slack_scale, double alpha) {
+int dual_point(bx_ctx* c, int which, const double* r, const double* tgt, double* theta, const double* g,
+               const double* att, const double* lo, const double* hi, double* v, int64_t k, const double* eps_part,
+               int Ge, double slack_scale, double alpha) {
   const double* ep = eps_part;
   int ge = Ge;
   if (c->sharded()) {
@@ -815,11 +818,11 @@ int dual_point(bx_ctx* c, int which, const T* r, const T* tgt, T* theta, const T
   }
   int nb = grid1d(c, c->m > k ? c->m : k);
   const int e0 = prof_begin(c);
-  k_dual<T><<<nb, RT, 0, c->stream>>>(r, (const T*)c->t, tgt, theta, c->m, g, att, lo, hi, v, k, ep, ge, c->has_inf,
+  k_dual<double><<<nb, RT, 0, c->stream>>>(r, (const double*)c->t, tgt, theta, c->m, g, att, lo, hi, v, k, ep, ge, c->has_inf,
                                        c->sc, which, c->bpart3, slack_scale, alpha, which ? 5 : 3,
                                        c->sharded() ? c->dsum : nullptr);
   LAUNCHED();
-  prof_end(c, e0, BX_PROF_DUAL, (double)sizeof(T) * (4.0 * c->m + 6.0 * k));
+  prof_end(c, e0, BX_PROF_DUAL, 8.0 * (4.0 * c->m + 6.0 * k));
   if (c->sharded()) {
     TRY(allreduce(c, c->dsum + 2, 2, ncclFloat64, ncclSum));  // bound terms are per-rank
     k_dual_fin<<<1, 32, 0, c->stream>>>(c->dsum, c->sc, which, slack_scale, alpha);
@@ -833,21 +836,21 @@ template <typename T>
 int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
   const int s = c->cur;
   int G = 1;
-  TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const T*)c->r, nullptr, nullptr, nullptr, nullptr, (const T*)c->hi[s],
-                  (T*)c->g, (const T*)c->att[s], nullptr, c->bpart, c->has_inf, &G));
+  TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr, (const double*)c->hi[s],
+                  (double*)c->g, (const double*)c->att[s], nullptr, c->bpart, c->has_inf, &G));
   c->g_valid = true;
-  TRY(dual_point<T>(c, 0, (const T*)c->r, (const T*)c->tgt, (T*)c->theta, (const T*)c->g, (const T*)c->att[s],
-                    (const T*)c->lo[s], (const T*)c->hi[s], (T*)c->v, c->k, c->bpart, G, slack_scale, alpha));
+  TRY(dual_point<T>(c, 0, (const double*)c->r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g, (const double*)c->att[s],
+                    (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->v, c->k, c->bpart, G, slack_scale, alpha));
   c->theta_is_cert = false;
   if (screening && c->k > 0) {
     const int nbs = (int)((c->k + RT - 1) / RT);
     const int e1 = prof_begin(c);
-    k_sphere<T><<<nbs, RT, 0, c->stream>>>((const T*)c->v, (const T*)c->nrm[s], (const T*)c->hi[s], c->k, c->sc,
+    k_sphere<double><<<nbs, RT, 0, c->stream>>>((const double*)c->v, (const double*)c->nrm[s], (const double*)c->hi[s], c->k, c->sc,
                                             c->flags, c->bcnt);
     LAUNCHED();
     k_scan<<<1, 1024, 0, c->stream>>>(c->bcnt, nbs, c->sc);
     LAUNCHED();
-    prof_end(c, e1, BX_PROF_SPHERE, (double)c->k * (3.0 * sizeof(T) + 1.0));
+    prof_end(c, e1, BX_PROF_SPHERE, (double)c->k * 25.0);
   } else {
     CU(cudaMemsetAsync(&c->sc->n_keep, 0, 6 * sizeof(int64_t), c->stream));
   }
@@ -860,17 +863,17 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
 template <typename T>
 int certified(bx_ctx* c, double alpha) {
   const int s = c->cur;
-  k_scatter_x<T><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], (const T*)c->x[s], (T*)c->xfull);
+  k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], (const double*)c->x[s], (double*)c->xfull);
   LAUNCHED();
   int G = 1;
   TRY(run_pass<T>(c, full_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                  (const T*)c->xfull, nullptr, 0, &G));
-  TRY(run_reduce<T>(c, G, (const T*)c->negy, (T*)c->rc, R_CERT, nullptr, 0, 4));
-  TRY(run_pass<T>(c, full_view<T>(c), U_DOT, (const T*)c->rc, nullptr, nullptr, nullptr, nullptr,
-                  (const T*)c->hifull, (T*)c->gfull, (const T*)c->attfull, nullptr, c->bpart + c->Gmax, c->has_inf,
+                  (const double*)c->xfull, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, (const double*)c->negy, (double*)c->rc, R_CERT, nullptr, 0, 4));
+  TRY(run_pass<T>(c, full_view<T>(c), U_DOT, (const double*)c->rc, nullptr, nullptr, nullptr, nullptr,
+                  (const double*)c->hifull, (double*)c->gfull, (const double*)c->attfull, nullptr, c->bpart + c->Gmax, c->has_inf,
                   &G));
-  TRY(dual_point<T>(c, 1, (const T*)c->rc, (const T*)c->y, (T*)c->thetac, (const T*)c->gfull,
-                    (const T*)c->attfull, (const T*)c->lofull, (const T*)c->hifull, (T*)c->vfull, c->n,
+  TRY(dual_point<T>(c, 1, (const double*)c->rc, (const double*)c->y, (double*)c->thetac, (const double*)c->gfull,
+                    (const double*)c->attfull, (const double*)c->lofull, (const double*)c->hifull, (double*)c->vfull, c->n,
                     c->bpart + c->Gmax, G, 0.0, alpha));
   return BX_OK;
 }
@@ -886,11 +889,11 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
       View<T> vw{(const T*)c->A, c->lda, c->scr_idx, 0};
       int G = 1;
       TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                      (const T*)c->scr_val, nullptr, 0, &G));
-      TRY(run_reduce<T>(c, G, (const T*)c->z, (T*)c->z2, R_PLAIN, nullptr, 0, 0));
+                      (const double*)c->scr_val, nullptr, 0, &G));
+      TRY(run_reduce<T>(c, G, (const double*)c->z, (double*)c->z2, R_PLAIN, nullptr, 0, 0));
       std::swap(c->z, c->z2);
-      k_offsets<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const T*)c->y, (const T*)c->z, (T*)c->off,
-                                                            (T*)c->tgt);
+      k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z, (double*)c->off,
+                                                            (double*)c->tgt);
       LAUNCHED();
     }
     TRY(refresh_resid<T>(c));
@@ -898,11 +901,11 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
     c->g_valid = false;
     return BX_OK;
   }
-  ColState<T> src{c->idx[s], (T*)c->x[s], kind == BX_APG ? (T*)c->xprev[s] : nullptr, (T*)c->lo[s], (T*)c->hi[s],
-                  (T*)c->nrm[s], (T*)c->att[s]};
-  ColState<T> dst{c->idx[d], (T*)c->x[d], (T*)c->xprev[d], (T*)c->lo[d], (T*)c->hi[d], (T*)c->nrm[d], (T*)c->att[d]};
-  k_compact<T><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (T*)c->xfull, c->scr_idx,
-                                           (T*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo, c->sat_up + c->n_sat_up,
+  ColState<double> src{c->idx[s], (double*)c->x[s], kind == BX_APG ? (double*)c->xprev[s] : nullptr, (double*)c->lo[s], (double*)c->hi[s],
+                  (double*)c->nrm[s], (double*)c->att[s]};
+  ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->lo[d], (double*)c->hi[d], (double*)c->nrm[d], (double*)c->att[d]};
+  k_compact<double><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (double*)c->xfull, c->scr_idx,
+                                           (double*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo, c->sat_up + c->n_sat_up,
                                            c->col_offset);
   LAUNCHED();
   c->cur = d;
@@ -914,11 +917,11 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
     View<T> vw{(const T*)c->A, c->lda, c->scr_idx, n_lo + n_up};
     int G = 1;
     TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                    (const T*)c->scr_val, nullptr, 0, &G));
-    TRY(run_reduce<T>(c, G, (const T*)c->z, (T*)c->z2, R_PLAIN, nullptr, 0, 0));
+                    (const double*)c->scr_val, nullptr, 0, &G));
+    TRY(run_reduce<T>(c, G, (const double*)c->z, (double*)c->z2, R_PLAIN, nullptr, 0, 0));
     std::swap(c->z, c->z2);
-    k_offsets<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const T*)c->y, (const T*)c->z, (T*)c->off,
-                                                          (T*)c->tgt);
+    k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z, (double*)c->off,
+                                                          (double*)c->tgt);
     LAUNCHED();
   }
   // physical rewrite of the preserved columns (solvers.py:57)
@@ -948,23 +951,28 @@ int reset_state(bx_ctx* c, int kind) {
   c->gram_dirty = true;
   c->g_valid = false;
   c->theta_is_cert = false;
-  k_init_cols<T><<<grid1d(c, c->n), RT, 0, c->stream>>>(c->n, (const T*)c->lofull, (const T*)c->hifull,
-                                                         (T*)c->xfull, c->idx[s], (T*)c->x[s], (T*)c->lo[s],
-                                                         (T*)c->hi[s], (const T*)c->nrmfull, (T*)c->nrm[s],
-                                                         (const T*)c->attfull, (T*)c->att[s]);
+  k_init_cols<double><<<grid1d(c, c->n), RT, 0, c->stream>>>(c->n, (const double*)c->lofull, (const double*)c->hifull,
+                                                         (double*)c->xfull, c->idx[s], (double*)c->x[s], (double*)c->lo[s],
+                                                         (double*)c->hi[s], (const double*)c->nrmfull, (double*)c->nrm[s],
+                                                         (const double*)c->attfull, (double*)c->att[s]);
   LAUNCHED();
-  CU(cudaMemsetAsync(c->z, 0, c->mp * sizeof(T), c->stream));
-  k_offsets<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const T*)c->y, (const T*)c->z, (T*)c->off, (T*)c->tgt);
+  CU(cudaMemsetAsync(c->z, 0, c->mp * sizeof(double), c->stream));
+  k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z, (double*)c->off, (double*)c->tgt);
   LAUNCHED();
   DevScalars h;
   memset(&h, 0, sizeof(h));
   h.mom_t = 1.0;
   h.P = INFINITY;
+  // round-off-sized tolerances: fp64 = the reference / oracle values
+  const bool f32 = sizeof(T) == 4;
+  h.rise_rel = f32 ? 1e-5 : 0.0;
+  h.rs_f = f32 ? 1e-6 : 1e-12;
+  h.rs_g = f32 ? 1e-5 : 1e-12;
   CU(cudaMemcpyAsync(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
   TRY(refresh_resid<T>(c));
   if (kind == BX_APG) {
-    CU(cudaMemcpyAsync(c->xprev[s], c->x[s], c->n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->rprev, c->r, c->mp * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->xprev[s], c->x[s], c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->rprev, c->r, c->mp * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     c->have_apg_state = true;
   }
   return BX_OK;
@@ -973,14 +981,14 @@ int reset_state(bx_ctx* c, int kind) {
 template <typename T>
 int create_typed(bx_ctx* c, const void* y, const void* lower, const void* upper, const void* t) {
   const int64_t m = c->m, n = c->n;
-  CU(cudaMemsetAsync(c->y, 0, c->mp * sizeof(T), c->stream));
-  CU(cudaMemcpyAsync(c->y, y, m * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
-  k_neg<T><<<grid1d(c, m), RT, 0, c->stream>>>(c->mp, (const T*)c->y, (T*)c->negy);
+  CU(cudaMemsetAsync(c->y, 0, c->mp * sizeof(double), c->stream));
+  CU(cudaMemcpyAsync(c->y, y, m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  k_neg<double><<<grid1d(c, m), RT, 0, c->stream>>>(c->mp, (const double*)c->y, (double*)c->negy);
   LAUNCHED();
-  CU(cudaMemcpyAsync(c->lofull, lower, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
-  CU(cudaMemcpyAsync(c->hifull, upper, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->lofull, lower, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->hifull, upper, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CU(cudaMemsetAsync(c->probe, 0, 64, c->stream));
-  k_bounds_probe<T><<<grid1d(c, n), RT, 0, c->stream>>>(n, (const T*)c->lofull, (const T*)c->hifull, c->probe);
+  k_bounds_probe<double><<<grid1d(c, n), RT, 0, c->stream>>>(n, (const double*)c->lofull, (const double*)c->hifull, c->probe);
   LAUNCHED();
   int bits = 0;
   CU(cudaMemcpyAsync(&bits, c->probe, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -991,17 +999,17 @@ int create_typed(bx_ctx* c, const void* y, const void* lower, const void* upper,
   c->bound_bits = bits;
   c->has_inf = (bits & 4) ? 1 : 0;
   // translation vector: neg-ones unless given (duality.py:372-373)
-  CU(cudaMemsetAsync(c->t, 0, c->mp * sizeof(T), c->stream));
+  CU(cudaMemsetAsync(c->t, 0, c->mp * sizeof(double), c->stream));
   if (t) {
-    CU(cudaMemcpyAsync(c->t, t, m * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->t, t, m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   } else {
-    k_fill<T><<<grid1d(c, m), RT, 0, c->stream>>>(m, (T*)c->t, T(-1));
+    k_fill<double><<<grid1d(c, m), RT, 0, c->stream>>>(m, (double*)c->t, T(-1));
     LAUNCHED();
   }
   CU(cudaMemsetAsync(c->probe, 0, 64, c->stream));
   const int nbw = (int)((n * 32 + RT - 1) / RT < 16 * c->nsm ? (n * 32 + RT - 1) / RT : 16 * c->nsm);
-  k_colstats<T><<<nbw, RT, 0, c->stream>>>((const T*)c->A, c->lda, n, m, (const T*)c->t, (T*)c->nrmfull,
-                                            (T*)c->attfull, 1, c->probe);
+  k_colstats<T><<<nbw, RT, 0, c->stream>>>((const T*)c->A, c->lda, n, m, (const double*)c->t, (double*)c->nrmfull,
+                                            (double*)c->attfull, 1, c->probe);
   LAUNCHED();
   int cf = 0;
   CU(cudaMemcpyAsync(&cf, c->probe, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -1072,14 +1080,16 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     const DualOut act = c->hsc->act;
     gap_out = act.gap;
     double cert_gap = NAN;
-    if (act.gap < tol) {
+    const double tol_r = cfg->relative_gap ? tol * fmax(1.0, fabs(act.primal)) : tol;
+    if (act.gap < tol_r) {
       TRY(certified<T>(c, alpha));
       TRY(sync_scalars<T>(c));
       TRY(check_dev_err(c));
       cert_gap = c->hsc->cert.gap;
       gap_out = cert_gap;
       c->theta_is_cert = true;
-      if (cert_gap < tol) converged = true;
+      const double tol_c = cfg->relative_gap ? tol * fmax(1.0, fabs(c->hsc->cert.primal)) : tol;
+      if (cert_gap < tol_c) converged = true;
     }
     int64_t n_lo = 0, n_up = 0;
     if (cfg->screening && kg > 0) {
@@ -1115,7 +1125,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     if (converged) break;
   }
   // x_full <- current preserved iterate (ws.sync, driver.py:492)
-  k_scatter_x<T><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], (const T*)c->x[c->cur], (T*)c->xfull);
+  k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], (const double*)c->x[c->cur], (double*)c->xfull);
   LAUNCHED();
   CU(cudaStreamSynchronize(c->stream));
   if (out) {
@@ -1213,13 +1223,13 @@ int bx_ctx_destroy(bx_ctx* c) {
 const char* bx_last_error(const bx_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int bx_col_norms(bx_ctx* c, void* out) {
-  CU(cudaMemcpyAsync(out, c->nrmfull, c->n * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(out, c->nrmfull, c->n * 8, cudaMemcpyDeviceToDevice, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return BX_OK;
 }
 
 int bx_att(bx_ctx* c, void* out) {
-  CU(cudaMemcpyAsync(out, c->attfull, c->n * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(out, c->attfull, c->n * 8, cudaMemcpyDeviceToDevice, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return BX_OK;
 }
@@ -1306,9 +1316,9 @@ int bx_solve(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* us
 }
 
 int bx_get_state(bx_ctx* c, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper) {
-  if (x) CU(cudaMemcpyAsync(x, c->xfull, c->n * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+  if (x) CU(cudaMemcpyAsync(x, c->xfull, c->n * 8, cudaMemcpyDeviceToDevice, c->stream));
   if (theta)
-    CU(cudaMemcpyAsync(theta, c->theta_is_cert ? c->thetac : c->theta, c->m * c->esz, cudaMemcpyDeviceToDevice,
+    CU(cudaMemcpyAsync(theta, c->theta_is_cert ? c->thetac : c->theta, c->m * 8, cudaMemcpyDeviceToDevice,
                        c->stream));
   if (sat_lower && c->n_sat_lo)
     CU(cudaMemcpyAsync(sat_lower, c->sat_lo, c->n_sat_lo * 8, cudaMemcpyDeviceToDevice, c->stream));

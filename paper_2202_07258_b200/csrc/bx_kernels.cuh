@@ -69,6 +69,10 @@ struct DevScalars {
   double cert_P;    // 0.5 ||A x - y||^2 on the full problem
   DualOut act;      // reduced-problem dual point of this round
   DualOut cert;     // certified (full-problem) dual point
+  double rise_rel;  // StepSizeTooLarge tolerance: 1e-9 + rise_rel * P (0 for fp64, solvers.py:112)
+  double rs_f;      // FISTA restart slacks (1e-12 fp64; fp32 values sized to fp32 round-off)
+  double rs_g;
+  double err_v1, err_v2;  // objective values at a StepSizeTooLarge event
   int64_t n_keep, n_lo, n_up;  // this rank's sphere-test counts
   int64_t g_keep, g_lo, g_up;  // summed over ranks (== local on one GPU)
   int32_t err;
@@ -83,17 +87,20 @@ struct PassArgs {
   const int32_t* colmap;   // column p lives at A + colmap[p]*ld (NULL: p)
   int64_t k;               // columns in this pass
   int64_t m;               // rows
-  const T* vin;            // dot vector (residual / power vector)
-  const T* vin_prev;       // FISTA: previous residual
-  T* x;                    // iterate (updated in place)
-  T* xprev;                // FISTA previous iterate
-  const T* lo;
-  const T* hi;
-  T* g;                    // gradient A'v (written by dot modes, read by U_PG_G)
-  const T* att;            // A't for the epsilon partial
-  const T* nrm;            // ||a_j|| (FISTA restart slack)
-  const T* coef;           // U_AX coefficients (NULL: x)
-  T* part;                 // [gridDim.x][ldp] partial rows of A x'
+  // every vector is fp64; only A (and the per-CTA partial rows) has the
+  // storage type T -- fp32 storage halves the streamed bytes without
+  // lowering the precision of the iterate ("fp32")
+  const double* vin;       // dot vector (residual / power vector)
+  const double* vin_prev;  // FISTA: previous residual
+  double* x;               // iterate (updated in place)
+  double* xprev;           // FISTA previous iterate
+  const double* lo;
+  const double* hi;
+  double* g;               // gradient A'v (written by dot modes, read by U_PG_G)
+  const double* att;       // A't for the epsilon partial
+  const double* nrm;       // ||a_j|| (FISTA restart slack)
+  const double* coef;      // U_AX coefficients (NULL: x)
+  T* part;                 // [gridDim.x][ldp] partial rows of A x' (fp32 accumulation for T = float)
   int64_t ldp;
   double* bpart;           // [gridDim.x] block scalar partial (eps max / sum w^2)
   DevScalars* sc;
@@ -203,6 +210,18 @@ __device__ __forceinline__ float4 pack<float>(const float* o) {
   return make_float4(o[0], o[1], o[2], o[3]);
 }
 
+// V consecutive fp64 values -> registers of type T (16-byte vector loads)
+template <typename T>
+__device__ __forceinline__ void load_rows(const double* p, double* o) {
+  constexpr int V = V16<T>::n;
+#pragma unroll
+  for (int h = 0; h < V / 2; ++h) {
+    const double2 q = *reinterpret_cast<const double2*>(p + 2 * h);
+    o[2 * h] = q.x;
+    o[2 * h + 1] = q.y;
+  }
+}
+
 // columns per slot as a function of R (rows-per-thread chunks)
 __host__ __device__ constexpr int cols_per_slot(int R) { return R >= 6 ? 1 : (R >= 4 ? 2 : (R >= 2 ? 4 : 8)); }
 
@@ -270,17 +289,16 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
 #pragma unroll
       for (int e = 0; e < V; ++e) vr[i][e] = T(0);
       if (row < m) {
-        T cur[V];
-        unpack<T>(*reinterpret_cast<const VT*>(a.vin + row), cur);
+        double cur[V];
+        load_rows<T>(a.vin + row, cur);
         if (beta != 0.0) {
-          T prv[V];
-          unpack<T>(*reinterpret_cast<const VT*>(a.vin_prev + row), prv);
-          const T bt = static_cast<T>(beta);
+          double prv[V];
+          load_rows<T>(a.vin_prev + row, prv);
 #pragma unroll
-          for (int e = 0; e < V; ++e) cur[e] = add_rn(cur[e], mul_rn(bt, sub_rn(cur[e], prv[e])));
+          for (int e = 0; e < V; ++e) cur[e] = add_rn(cur[e], mul_rn(beta, sub_rn(cur[e], prv[e])));
         }
 #pragma unroll
-        for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? cur[e] : T(0);
+        for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? static_cast<T>(cur[e]) : T(0);
       }
     }
   }
@@ -327,41 +345,41 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         double gsum = 0.0;
 #pragma unroll
         for (int w = 0; w < NWARPS; ++w) gsum += red[w * CMAX + tid];
-        const T gj = static_cast<T>(gsum);
+        const double gj = gsum;
         const int64_t p = p0 + (int64_t)gi * C + tid;
         double coef = 0.0;
         switch (a.upd) {
           case U_DOT: {
             a.g[p] = gj;
-            if (a.has_inf && isinf(static_cast<double>(a.hi[p]))) {
-              const double ratio = fmax(-static_cast<double>(gj), 0.0) / fabs(static_cast<double>(a.att[p]));
+            if (a.has_inf && isinf(a.hi[p])) {
+              const double ratio = fmax(-gj, 0.0) / fabs(a.att[p]);
               run = fmax(run, ratio);
             }
           } break;
           case U_PG: {
             a.g[p] = gj;
-            const T xo = a.x[p];
-            const T xn = clip<T>(sub_rn(xo, mul_rn(static_cast<T>(eta), gj)), a.lo[p], a.hi[p]);
+            const double xo = a.x[p];
+            const double xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
             a.x[p] = xn;
-            coef = static_cast<double>(xn);
+            coef = xn;
           } break;
           case U_APG: {
-            const T xo = a.x[p];
-            const T xp = a.xprev[p];
-            T yv = xo;
-            if (beta != 0.0) yv = add_rn(xo, mul_rn(static_cast<T>(beta), sub_rn(xo, xp)));
-            const T xn = clip<T>(sub_rn(yv, mul_rn(static_cast<T>(eta), gj)), a.lo[p], a.hi[p]);
+            const double xo = a.x[p];
+            const double xp = a.xprev[p];
+            double yv = xo;
+            if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
+            const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
             a.xprev[p] = xo;
             a.x[p] = xn;
-            coef = static_cast<double>(xn);
+            coef = xn;
             // gradient restart test g_y'(x+ - x) and its round-off scale
             // sum ||a_j|| |x+ - x| (FISTA)
-            const double dxj = static_cast<double>(xn) - static_cast<double>(xo);
-            run += static_cast<double>(gj) * dxj;
-            run2 += static_cast<double>(a.nrm[p]) * fabs(dxj);
+            const double dxj = xn - xo;
+            run += gj * dxj;
+            run2 += a.nrm[p] * fabs(dxj);
           } break;
           case U_POWER: {
-            coef = static_cast<double>(gj);
+            coef = gj;
             run += coef * coef;
           } break;
           default:
@@ -375,12 +393,12 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         const int64_t p = p0 + (int64_t)gi * C + tid;
         double coef = 0.0;
         if (a.upd == U_PG_G) {
-          const T xo = a.x[p];
-          const T xn = clip<T>(sub_rn(xo, mul_rn(static_cast<T>(eta), a.g[p])), a.lo[p], a.hi[p]);
+          const double xo = a.x[p];
+          const double xn = clip<double>(sub_rn(xo, mul_rn(eta, a.g[p])), a.lo[p], a.hi[p]);
           a.x[p] = xn;
-          coef = static_cast<double>(xn);
+          coef = xn;
         } else {
-          coef = static_cast<double>(a.coef ? a.coef[p] : a.x[p]);
+          coef = a.coef ? a.coef[p] : a.x[p];
         }
         cf[tid] = coef;
       }
@@ -479,8 +497,11 @@ __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, dou
       sc->P = Pn;
       break;
     case R_PG:
-      if (Pn > sc->P + 1e-9) {  // solvers.py:111-114
-        sc->P_prev = sc->P;
+      if (Pn > sc->P + 1e-9 + sc->rise_rel * fabs(sc->P)) {  // solvers.py:111-114
+        if (sc->err == 0) {
+          sc->err_v1 = sc->P;
+          sc->err_v2 = Pn;
+        }
         set_err(sc, DE_STEP_TOO_LARGE);
       }
       sc->P = Pn;
@@ -488,8 +509,8 @@ __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, dou
     case R_APG: {
       const double t = sc->mom_t;
       const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-      const double s_f = 1e-12 * fmax(1.0, fabs(sc->P));
-      const double s_g = 1e-12 * sqrt(2.0 * sc->P) * gscale;
+      const double s_f = sc->rs_f * fmax(1.0, fabs(sc->P));
+      const double s_g = sc->rs_g * sqrt(2.0 * sc->P) * gscale;
       if (Pn > sc->P + s_f || gdot > s_g) {  // function / gradient restart (FISTA)
         sc->mom_t = 1.0;
         sc->restarts += 1;
@@ -513,13 +534,13 @@ __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, dou
 
 template <typename T>
 __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64_t ldp, int G, int64_t m,
-                                               const T* __restrict__ off, T* __restrict__ out,
+                                               const double* __restrict__ off, double* __restrict__ out,
                                                DevScalars* sc, double* bpart, const double* wpart,
                                                int Gw, int mode, int counter) {
   using VT = typename V16<T>::type;
   constexpr int V = V16<T>::n;
   constexpr int RB = 32 * V;
-  __shared__ T sl[RED_SLICES][RB];
+  __shared__ double sl[RED_SLICES][RB];
   __shared__ double sh[RT / 32];
   __shared__ double s_div;
   __shared__ bool last;
@@ -534,9 +555,9 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
   double sq = 0.0;
   for (int64_t r0 = (int64_t)blockIdx.x * RB; r0 < m; r0 += (int64_t)gridDim.x * RB) {
     const int64_t row = r0 + lane * V;
-    T acc[V];
+    double acc[V];  // partial rows summed in fp64 (fixed order)
 #pragma unroll
-    for (int e = 0; e < V; ++e) acc[e] = T(0);
+    for (int e = 0; e < V; ++e) acc[e] = 0.0;
     if (row < m) {
       int bb = warp;
       for (; bb + 3 * RED_SLICES < G; bb += 4 * RED_SLICES) {
@@ -546,13 +567,15 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
         unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)(bb + 2 * RED_SLICES) * ldp + row), q2);
         unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)(bb + 3 * RED_SLICES) * ldp + row), q3);
 #pragma unroll
-        for (int e = 0; e < V; ++e) acc[e] += q0[e] + q1[e] + q2[e] + q3[e];
+        for (int e = 0; e < V; ++e)
+          acc[e] += (static_cast<double>(q0[e]) + static_cast<double>(q1[e])) +
+                    (static_cast<double>(q2[e]) + static_cast<double>(q3[e]));
       }
       for (; bb < G; bb += RED_SLICES) {
         T q[V];
         unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)bb * ldp + row), q);
 #pragma unroll
-        for (int e = 0; e < V; ++e) acc[e] += q[e];
+        for (int e = 0; e < V; ++e) acc[e] += static_cast<double>(q[e]);
       }
     }
 #pragma unroll
@@ -564,13 +587,13 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     for (int q = threadIdx.x; q < RB; q += RT) {
       const int64_t i = r0 + q;
       if (i < m) {
-        T s = sl[0][q];
+        double s = sl[0][q];
 #pragma unroll
         for (int w = 1; w < RED_SLICES; ++w) s += sl[w][q];
         if (off) s = add_rn(s, off[i]);
-        if (mode == R_POWER) s = static_cast<T>(static_cast<double>(s) / s_div);
+        if (mode == R_POWER) s = s / s_div;
         out[i] = s;
-        sq += static_cast<double>(s) * static_cast<double>(s);
+        sq += s * s;
       }
     }
     __syncthreads();
@@ -907,7 +930,8 @@ __global__ void __launch_bounds__(RT) k_gather(const T* __restrict__ A, int64_t 
 // a_j' t (duality.py:350); flags zero columns and non-interior t
 template <typename T>
 __global__ void __launch_bounds__(RT) k_colstats(const T* __restrict__ A, int64_t lda, int64_t n, int64_t m,
-                                                 const T* __restrict__ t, T* __restrict__ nrm, T* __restrict__ att,
+                                                 const double* __restrict__ t, double* __restrict__ nrm,
+                                                 double* __restrict__ att,
                                                  int check_interior, int* __restrict__ flags) {
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * RT + threadIdx.x) >> 5;
@@ -918,17 +942,16 @@ __global__ void __launch_bounds__(RT) k_colstats(const T* __restrict__ A, int64_
     for (int64_t i = lane; i < m; i += 32) {
       const double a = static_cast<double>(col[i]);
       ss += a * a;
-      st += a * static_cast<double>(t[i]);
+      st += a * t[i];
     }
     ss = warp_sum<double>(ss);
     st = warp_sum<double>(st);
     if (lane == 0) {
       const double nj = sqrt(ss);
-      nrm[j] = static_cast<T>(nj);
-      att[j] = static_cast<T>(st);
+      nrm[j] = nj;
+      att[j] = st;
       if (nj == 0.0) atomicOr(&flags[0], 1);
-      if (check_interior && !(static_cast<double>(static_cast<T>(st)) < -1e-10 * static_cast<double>(static_cast<T>(nj))))
-        atomicOr(&flags[0], 2);
+      if (check_interior && !(st < -1e-10 * nj)) atomicOr(&flags[0], 2);
     }
   }
 }

@@ -112,7 +112,7 @@ class _Session:
         self.stream = stream if stream is not None else torch.cuda.current_stream(a.device)
         self.t_dev = None
         if tv is not None:
-            self.t_dev = torch.as_tensor(np.asarray(tv.t), device=a.device).to(self.tdt).contiguous()
+            self.t_dev = torch.as_tensor(np.asarray(tv.t, dtype=np.float64), device=a.device).contiguous()
         self.ctx = ctypes.c_void_p()
         st = L.bx_ctx_create(ctypes.byref(self.ctx), self.m, self.n, self.dtype_code, a.data_ptr(), lda,
                              d["y"].data_ptr(), d["lo"].data_ptr(), d["hi"].data_ptr(),
@@ -165,6 +165,8 @@ class _Session:
         c.screening = 1 if screening else 0
         c.alpha = alpha
         c.slack_scale = slack_scale
+        rel = cfg.relative_gap
+        c.relative_gap = int(self.dtype_code == nat.BX_F32 if rel is None else bool(rel))
         cap = min(cfg.max_rounds or 1_000_000, 250_000)
         trace = np.empty(cap, dtype=TRACE_DTYPE)
         out = nat.SolveOut()
@@ -179,8 +181,8 @@ class _Session:
                             for i, e in enumerate(ents) if e.launches}
         torch = self.torch
         dev = self.dev["a"].device
-        x = torch.empty(self.n, dtype=self.tdt, device=dev)
-        theta = torch.empty(self.m, dtype=self.tdt, device=dev)
+        x = torch.empty(self.n, dtype=torch.float64, device=dev)
+        theta = torch.empty(self.m, dtype=torch.float64, device=dev)
         sl = torch.empty(max(out.n_sat_lower, 1), dtype=torch.int64, device=dev)
         su = torch.empty(max(out.n_sat_upper, 1), dtype=torch.int64, device=dev)
         nat.check(L.bx_get_state(self.ctx, x.data_ptr(), theta.data_ptr(), sl.data_ptr(), su.data_ptr()),
@@ -205,8 +207,9 @@ def _result(p_n, out, tr, x, theta, sl, su, prof, return_device, n_total=None):
 
 
 def _default_slack(p):
-    # driver.py:459 for fp64; fp32 needs a slack scaled to its unit round-off
-    return 1e-12 if p.dtype == np.float64 else 1e-5
+    # driver.py:459 for fp64; fp32 sphere tests need a slack above the fp32
+    # round-off of a_j'theta (~sqrt(m) * 6e-8 ||theta||): 1e-4 ||theta||
+    return 1e-12 if p.dtype == np.float64 else 1e-4
 
 
 def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None, return_device=False,

@@ -103,9 +103,10 @@ class Problem:
         self.dtype = np.dtype(np.float32) if tdt == torch.float32 else np.dtype(np.float64)
         self.m, self.n = int(m), int(n)
         dev = a.device
-        lo = torch.as_tensor(lower, dtype=tdt, device=dev).broadcast_to((n,)).contiguous()
-        hi = torch.as_tensor(upper, dtype=tdt, device=dev).broadcast_to((n,)).contiguous()
-        yv = torch.as_tensor(y, device=dev).to(tdt).reshape(-1).contiguous()
+        f64 = torch.float64  # every vector is fp64; only A has the storage dtype
+        lo = torch.as_tensor(lower, dtype=f64, device=dev).broadcast_to((n,)).contiguous()
+        hi = torch.as_tensor(upper, dtype=f64, device=dev).broadcast_to((n,)).contiguous()
+        yv = torch.as_tensor(y, device=dev).to(f64).reshape(-1).contiguous()
         if yv.shape[0] != m:
             raise DimensionMismatch(f"y has length {yv.shape[0]}, expected {m}")
         self._dev = dict(a=self._device_layout(a.to(tdt)), y=yv, lo=lo, hi=hi, device=dev)
@@ -129,9 +130,10 @@ class Problem:
         p.dtype = np.dtype(np.float32) if tdt == torch.float32 else np.dtype(np.float64)
         p.m, p.n = int(m), int(n)
         dev = storage.device
-        lo = torch.as_tensor(lower, dtype=tdt, device=dev).broadcast_to((n,)).contiguous()
-        hi = torch.as_tensor(upper, dtype=tdt, device=dev).broadcast_to((n,)).contiguous()
-        yv = torch.as_tensor(y, device=dev).to(tdt).reshape(-1).contiguous()
+        f64 = torch.float64
+        lo = torch.as_tensor(lower, dtype=f64, device=dev).broadcast_to((n,)).contiguous()
+        hi = torch.as_tensor(upper, dtype=f64, device=dev).broadcast_to((n,)).contiguous()
+        yv = torch.as_tensor(y, device=dev).to(f64).reshape(-1).contiguous()
         p._dev = dict(a=storage, y=yv, lo=lo, hi=hi, device=dev)
         p.a_matrix = None
         p.y = None
@@ -160,10 +162,10 @@ class Problem:
         """Keep page-locked host copies so uploads run at full PCIe speed."""
         import torch
         if self._pinned is None and self.a_matrix is not None:
-            at = torch.from_numpy(np.ascontiguousarray(self.a_matrix.T))  # (n, m) == column-major A
-            self._pinned = dict(a=at.pin_memory(), y=torch.from_numpy(self.y.astype(self.dtype)).pin_memory(),
-                                lo=torch.from_numpy(self.lower.astype(self.dtype)).pin_memory(),
-                                hi=torch.from_numpy(self.upper.astype(self.dtype)).pin_memory())
+            at = torch.from_numpy(np.array(self.a_matrix.T, order="C"))  # (n, m) == column-major A
+            self._pinned = dict(a=at.pin_memory(), y=torch.from_numpy(self.y.copy()).pin_memory(),
+                                lo=torch.from_numpy(self.lower.copy()).pin_memory(),
+                                hi=torch.from_numpy(self.upper.copy()).pin_memory())
         return self
 
     def device_arrays(self, device=None):
@@ -176,16 +178,15 @@ class Problem:
         if self._pinned is not None:
             src = self._pinned
         else:
-            src = dict(a=torch.from_numpy(np.ascontiguousarray(self.a_matrix.T)),
-                       y=torch.from_numpy(self.y.astype(self.dtype)),
-                       lo=torch.from_numpy(self.lower.astype(self.dtype)),
-                       hi=torch.from_numpy(self.upper.astype(self.dtype)))
+            src = dict(a=torch.from_numpy(np.array(self.a_matrix.T, order="C")),
+                       y=torch.from_numpy(self.y.copy()), lo=torch.from_numpy(self.lower.copy()),
+                       hi=torch.from_numpy(self.upper.copy()))
         nb = self._pinned is not None
         at = src["a"].to(device, non_blocking=nb)
         a_dev = self._device_layout(at.t()) if at.shape[1] % (16 // at.element_size()) else at
-        self._dev = dict(a=a_dev, y=src["y"].to(device, non_blocking=nb).to(tdt),
-                         lo=src["lo"].to(device, non_blocking=nb).to(tdt),
-                         hi=src["hi"].to(device, non_blocking=nb).to(tdt), device=device)
+        self._dev = dict(a=a_dev, y=src["y"].to(device, non_blocking=nb),
+                         lo=src["lo"].to(device, non_blocking=nb),
+                         hi=src["hi"].to(device, non_blocking=nb), device=device)
         return self._dev
 
     def release_device(self):

@@ -24,6 +24,10 @@ class SolverConfig:
     inner_passes: int = 1
     max_rounds: int | None = None
     gap_tol: float = 1e-6
+    # stop on gap <= gap_tol * max(1, P) instead of gap <= gap_tol; None = the
+    # reference's absolute rule for fp64, the relative rule for fp32 storage
+    # (an absolute 1e-6 is below fp32 resolution when P* >> 1)
+    relative_gap: bool | None = None
 
     def __post_init__(self):
         if self.kind not in _SOLVER_KINDS:

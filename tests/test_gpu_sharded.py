@@ -66,3 +66,22 @@ def test_sharded_cd_is_rejected():
     a, y, lo, hi = small_instance(rng, 20, 10, "bvls")
     with pytest.raises(NativeError):
         solve_group(Problem(a, y, lo, hi), SolverConfig(kind="cd"), nranks=2)
+
+
+def test_nccl_plumbing_under_torchrun():
+    """NCCL transport (dlopen'd libnccl, unique-id broadcast, in-place
+    allreduce on the context stream) through torchrun with one GPU: the
+    collective code path runs with one rank and must reproduce solve()."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "scripts", "nccl_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "OK" in out.stdout
