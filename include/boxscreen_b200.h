@@ -204,7 +204,30 @@ int bx_set_profiling(bx_ctx* ctx, int32_t on);
 int bx_get_profile(bx_ctx* ctx, bx_prof_entry* out_host, int32_t n);
 
 /* ---- batched many-RHS APG (BASELINE config 5) ----------------------------- */
+/* K independent NNLS problems sharing one dictionary A (m <= 208), FISTA with
+ * per-problem gap-safe screening, both products on fp64 tensor cores (DMMA);
+ * semantics in oracle/batched_oracle.py.  Not in the reference (it solves one
+ * right-hand side per solve() call, driver.py:371). */
+typedef struct bx_batch bx_batch;
+typedef struct {
+  int64_t rounds, converged, iterations, kernel_launches;
+  double max_gap;
+} bx_batched_out;
 size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs);
+/* A: device, column-major (lda even); Y: device m x K column-major (ldy) */
+int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const double* a, int64_t lda,
+                      const double* y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                      void* cuda_stream);
+/* `rounds` rounds of `passes` FISTA steps + dual point + sphere test; stops
+ * early when every problem's gap < gap_tol.  trace_host (optional, 4 doubles
+ * per round): {converged, max gap, mean gap, mean preserved}. */
+int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
+                   double* trace_host, int64_t trace_cap, bx_batched_out* out_host);
+/* x: n x K (device, column stride ldx_out); stats: 5 x K (device) per-problem
+ * {primal, dual, gap, eps, preserved} of the last round */
+int bx_batched_get(bx_batch* b, double* x, int64_t ldx_out, double* stats);
+const char* bx_batched_last_error(const bx_batch* b);
+int bx_batched_destroy(bx_batch* b);
 
 #ifdef __cplusplus
 }

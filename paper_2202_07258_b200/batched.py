@@ -1,0 +1,79 @@
+"""Batched many-right-hand-side NNLS (BASELINE config 5): K problems sharing
+one dictionary A, solved together by FISTA with per-problem Gap-safe
+screening; both products of every step run on fp64 tensor cores (DMMA) inside
+one persistent kernel per round (csrc/bx_batched.cuh).  Semantics:
+oracle/batched_oracle.py ("Batched FISTA").  Not in the reference,
+which solves one right-hand side per ``solve`` call."""
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import STATUS, NativeError
+from .solvers import auto_step_size
+
+
+@dataclass
+class BatchedResult:
+    x: object                 # (n, K) numpy or CUDA tensor
+    primal: np.ndarray        # per problem, last round
+    dual: np.ndarray
+    gap: np.ndarray
+    eps: np.ndarray
+    preserved: np.ndarray
+    rounds: int
+    converged: int
+    iterations: int
+    eta: float
+    trace: np.ndarray = field(default_factory=lambda: np.zeros((0, 4)))  # per round: converged, max/mean gap, mean preserved
+    kernel_launches: int = 0
+
+
+def _check(st, h, what):
+    if st != 0:
+        msg = nat.lib().bx_batched_last_error(h)
+        raise STATUS.get(st, NativeError)(f"{what}: {msg.decode() if msg else ''}")
+
+
+def solve_batched(a, Y, passes=10, rounds=10, gap_tol=1e-6, screening=True, eta=None, return_device=False):
+    """Run up to ``rounds`` rounds of ``passes`` FISTA steps on every column of
+    Y (m x K); stops early when every problem's gap < gap_tol."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2202_07258_b200 needs a CUDA device (no CPU fallback)")
+    L = nat.lib()
+    dev = torch.device("cuda")
+    a_t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a, dtype=np.float64))
+    y_t = Y if isinstance(Y, torch.Tensor) else torch.from_numpy(np.asarray(Y, dtype=np.float64))
+    m, n = a_t.shape
+    K = y_t.shape[1]
+    lda = m + (m % 2)
+    a_dev = torch.zeros((n, lda), dtype=torch.float64, device=dev)
+    a_dev[:, :m].copy_(a_t.t().to(dev))
+    y_dev = y_t.t().contiguous().to(dev)   # (K, m) == column-major Y, ldy = m
+    if eta is None:
+        eta = auto_step_size(a_dev[:, :m].t(), 1.0)
+    nbytes = L.bx_batched_workspace_bytes(m, n, K)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    h = ctypes.c_void_p()
+    try:
+        _check(L.bx_batched_create(ctypes.byref(h), m, n, K, a_dev.data_ptr(), lda, y_dev.data_ptr(), m,
+                                   ws.data_ptr(), nbytes, stream.cuda_stream), h, "bx_batched_create")
+        trace = np.zeros((rounds, 4))
+        out = nat.BatchedOut()
+        _check(L.bx_batched_run(h, float(eta), passes, rounds, 1 if screening else 0, gap_tol,
+                                trace.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), rounds, ctypes.byref(out)),
+               h, "bx_batched_run")
+        x = torch.empty((K, n), dtype=torch.float64, device=dev)  # column-major n x K
+        stats = torch.empty((5, K), dtype=torch.float64, device=dev)
+        _check(L.bx_batched_get(h, x.data_ptr(), n, stats.data_ptr()), h, "bx_batched_get")
+    finally:
+        L.bx_batched_destroy(h)
+    st = stats.cpu().numpy()
+    xo = x.t() if return_device else x.t().cpu().numpy()
+    return BatchedResult(x=xo, primal=st[0], dual=st[1], gap=st[2], eps=st[3], preserved=st[4].astype(np.int64),
+                         rounds=int(out.rounds), converged=int(out.converged), iterations=int(out.iterations),
+                         eta=float(eta), trace=trace[: int(out.rounds)], kernel_launches=int(out.kernel_launches))

