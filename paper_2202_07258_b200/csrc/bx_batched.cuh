@@ -100,21 +100,45 @@ __device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BatchSmem&
 }
 
 // G tile (coords j0 + 8t + g, problems n0 + 2 tig + e) = A_J' Ry for the warp's
-// 8 problems, 2 coordinate tiles; K = m in steps of 4
+// 8 problems, 2 coordinate tiles; K = m in steps of 4.  Four independent
+// accumulator sets (k-steps interleaved) keep 8 DMMA chains in flight per warp
+// -- a single chain per tile is DMMA-latency bound -- and are summed in a
+// fixed order at the end (deterministic).
 __device__ __forceinline__ void bt_gemm1(const BatchArgs& a, const double* ab, const double* rys, int n0, int g,
                                          int tig, double (&gt)[2][2]) {
+  double acc[4][2][2];
 #pragma unroll
-  for (int t = 0; t < 2; ++t) gt[t][0] = gt[t][1] = 0.0;
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
   const int m4 = (a.m + 3) / 4;
-  for (int kk = 0; kk < m4; ++kk) {
-    const int i = 4 * kk + tig;
-    const double b = rys[(n0 + g) * a.sa + i];
+  const double* rb = rys + (n0 + g) * a.sa + tig;
+  const double* a0 = ab + g * a.sa + tig;
+  const double* a1 = ab + (8 + g) * a.sa + tig;
+  int kk = 0;
+  for (; kk + 4 <= m4; kk += 4) {
+    double b[4], x0[4], x1[4];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const double av = ab[(8 * t + g) * a.sa + i];
-      dmma(gt[t][0], gt[t][1], av, b);
+    for (int u = 0; u < 4; ++u) {
+      b[u] = rb[4 * (kk + u)];
+      x0[u] = a0[4 * (kk + u)];
+      x1[u] = a1[4 * (kk + u)];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dmma(acc[u][0][0], acc[u][0][1], x0[u], b[u]);
+      dmma(acc[u][1][0], acc[u][1][1], x1[u], b[u]);
     }
   }
+  for (; kk < m4; ++kk) {
+    const double b = rb[4 * kk];
+    dmma(acc[0][0][0], acc[0][0][1], a0[4 * kk], b);
+    dmma(acc[0][1][0], acc[0][1][1], a1[4 * kk], b);
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) gt[t][e] = (acc[0][t][e] + acc[1][t][e]) + (acc[2][t][e] + acc[3][t][e]);
 }
 
 // acc (rows 8 mt + g, problems n0 + 2 tig + e) += A_J X_J ; K = 16 coordinates
