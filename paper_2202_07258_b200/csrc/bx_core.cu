@@ -32,6 +32,7 @@
 #include "bx_kernels.cuh"
 #include "bx_cd.cuh"
 #include "bx_batched.cuh"
+#include "bx_small.cuh"
 
 using namespace bx;
 
@@ -215,6 +216,10 @@ struct bx_ctx {
   bool g_valid = false;
   bool theta_is_cert = false;
   bool have_apg_state = false;
+  unsigned* bar = nullptr;  // grid barrier of the cooperative small-round kernel
+  bool dot_done = false;    // the round kernel already produced g and the eps partials
+  int dot_G = 0;
+  bool small_ok = true;     // cooperative small-round path allowed (env BX_NO_SMALL disables)
   int64_t launches = 0;
   std::string err;
 
@@ -381,7 +386,8 @@ void carve(bx_ctx* c, Carver& w) {
   c->sat_up = (int64_t*)w.take(n * 8);
   c->probe = (int*)w.take(64);
   c->ldp = mp;
-  c->part = w.take((size_t)c->Gmax * c->ldp * ea);
+  c->part = w.take((size_t)c->Gmax * c->ldp * 8);  // fp64 sized: also the small-round path's partial rows
+  c->bar = (unsigned*)w.take(64);
   c->bpart = (double*)w.take(c->Gmax * 8 * 4);
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
@@ -773,10 +779,90 @@ int cd_sweeps(bx_ctx* c, int passes) {
   return BX_OK;
 }
 
+// ---- cooperative small-round path (bx_small.cuh) ---------------------------
+template <typename T, int R>
+int launch_small_R(bx_ctx* c, SmallArgs& a, int G, size_t smem) {
+  auto kern = k_round_small<T, R>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&a};
+  const int e0 = prof_begin(c);
+  CU(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(SM_NT), args, smem, c->stream));
+  LAUNCHED();
+  prof_end(c, e0, BX_PROF_PASS_PG, (double)a.passes * (double)a.k * a.m * sizeof(T));
+  return BX_OK;
+}
+
+// Returns 1 when the round ran on the small path, 0 when it does not apply.
+template <typename T>
+int small_round(bx_ctx* c, int kind, int passes, int* ran) {
+  *ran = 0;
+  if (!c->small_ok || c->sharded() || (kind != BX_PG && kind != BX_APG) || c->k == 0) return BX_OK;
+  constexpr int V = 16 / sizeof(T);
+  const int R = (int)((c->m + SM_NT * V - 1) / (SM_NT * V));
+  if (R > 4) return BX_OK;
+  const int G = c->nsm;
+  const int ncmax = (int)((c->k + G - 1) / G);
+  if (ncmax > SM_CMAX) return BX_OK;
+  const int colstride = (int)round_up(c->m, 2 * V);
+  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8) * 8 + 256;
+  const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
+  if (smem > c->smem_cap) return BX_OK;
+  const int s = c->cur;
+  View<T> vw = act_view<T>(c);
+  SmallArgs a;
+  a.A = vw.A;
+  a.ld = vw.ld;
+  a.k = c->k;
+  a.m = (int)c->m;
+  a.x = (double*)c->x[s];
+  a.xprev = (double*)c->xprev[s];
+  a.lo = (const double*)c->lo[s];
+  a.hi = (const double*)c->hi[s];
+  a.nrm = (const double*)c->nrm[s];
+  a.att = (const double*)c->att[s];
+  a.g = (double*)c->g;
+  a.r[0] = (double*)c->r;
+  a.r[1] = (double*)c->rprev;
+  a.off = (const double*)c->off;
+  a.part = (double*)c->part;
+  a.ldp = c->ldp;
+  a.bpart = c->bpart3;
+  a.epart = c->bpart;
+  a.sc = c->sc;
+  a.bar = c->bar;
+  a.passes = passes;
+  a.kind = kind;
+  a.g_valid = c->g_valid ? 1 : 0;
+  a.has_inf = c->has_inf;
+  a.do_dot = 1;
+  a.rc = 0;
+  a.colstride = colstride;
+  a.ncmax = ncmax;
+  int st = BX_OK;
+  switch (R) {
+    case 1: st = launch_small_R<T, 1>(c, a, G, smem); break;
+    case 2: st = launch_small_R<T, 2>(c, a, G, smem); break;
+    case 3: st = launch_small_R<T, 3>(c, a, G, smem); break;
+    default: st = launch_small_R<T, 4>(c, a, G, smem); break;
+  }
+  if (st != BX_OK) return st;
+  if (passes & 1) std::swap(c->r, c->rprev);
+  c->dot_done = true;
+  c->dot_G = G;
+  c->g_valid = true;
+  *ran = 1;
+  return BX_OK;
+}
+
 // one round's primal passes
 template <typename T>
 int primal_passes(bx_ctx* c, int kind, int passes) {
   const int s = c->cur;
+  {
+    int ran = 0;
+    TRY(small_round<T>(c, kind, passes, &ran));
+    if (ran) return BX_OK;
+  }
   for (int p = 0; p < passes; ++p) {
     int G = 1;
     if (kind == BX_PG) {
@@ -837,8 +923,14 @@ template <typename T>
 int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
   const int s = c->cur;
   int G = 1;
-  TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr, (const double*)c->hi[s],
-                  (double*)c->g, (const double*)c->att[s], nullptr, c->bpart, c->has_inf, &G));
+  if (c->dot_done) {
+    G = c->dot_G;  // g and the eps partials came with the round kernel
+    c->dot_done = false;
+  } else {
+    TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr,
+                    (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s], nullptr, c->bpart, c->has_inf,
+                    &G));
+  }
   c->g_valid = true;
   TRY(dual_point<T>(c, 0, (const double*)c->r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g, (const double*)c->att[s],
                     (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->v, c->k, c->bpart, G, slack_scale, alpha));
@@ -1207,7 +1299,9 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   CU(cudaMallocHost((void**)&c->hsc, sizeof(DevScalars)));
   memset(c->hsc, 0, sizeof(DevScalars));
   CU(cudaMemsetAsync(c->sc, 0, sizeof(DevScalars), c->stream));
-  CU(cudaMemsetAsync(c->part, 0, (size_t)c->Gmax * c->ldp * c->esz, c->stream));
+  CU(cudaMemsetAsync(c->part, 0, (size_t)c->Gmax * c->ldp * 8, c->stream));
+  CU(cudaMemsetAsync(c->bar, 0, 64, c->stream));
+  c->small_ok = getenv("BX_NO_SMALL") == nullptr;
   if (dtype == BX_F64) return create_typed<double>(c, y, lower, upper, t);
   return create_typed<float>(c, y, lower, upper, t);
 }

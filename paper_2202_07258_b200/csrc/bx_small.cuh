@@ -1,0 +1,356 @@
+// bx_small.cuh -- one PG / FISTA round of a small problem in ONE cooperative
+// launch (BASELINE config 1: A_act is 16 MB, it fits in the aggregate shared
+// memory of the 148 SMs).
+//
+// The streamed path (k_pass + k_reduce, two launches per step) is latency
+// bound at this size: ~21 us per step for 16 MB.  Here every CTA loads its
+// contiguous block of preserved columns into shared memory ONCE per round and
+// keeps it there; each step is
+//     dots of the local columns with the (register-resident) residual
+//     -> local x update -> local partial A x+ rows  -> grid barrier
+//     -> CTA b reduces rows [b*mb, (b+1)*mb) over all partials in a fixed order
+//        (+ z - y), and its share of ||r||^2 and the restart partials
+//     -> grid barrier -> every CTA folds the per-CTA scalars (same order, same
+//        value everywhere) and takes the same StepSizeTooLarge / restart decision
+// and the round ends with the screening dot pass (g = A'r, epsilon partials)
+// consumed by k_dual.  The arithmetic is the streamed path's: same per-column
+// update, same deterministic reductions (different summation grouping).
+#pragma once
+#include "bx_kernels.cuh"
+
+namespace bx {
+
+constexpr int SM_NT = 512;
+constexpr int SM_CMAX = 48;  // max resident columns per CTA
+
+struct SmallArgs {
+  const void* A;
+  int64_t ld;
+  int64_t k;
+  int m;
+  double* x;
+  double* xprev;
+  const double* lo;
+  const double* hi;
+  const double* nrm;
+  const double* att;
+  double* g;
+  double* r[2];
+  const double* off;
+  double* part;    // [G][ldp] partial rows (fp64)
+  int64_t ldp;
+  double* bpart;   // [G][4] per-CTA scalars
+  double* epart;   // [G] epsilon partials for k_dual
+  DevScalars* sc;
+  unsigned* bar;   // [2] grid barrier: count, generation
+  int passes;
+  int kind;        // 0 PG, 2 APG
+  int g_valid;     // PG: the first step may use the stored gradient
+  int has_inf;
+  int do_dot;      // end the round with the screening dot pass
+  int rc;          // r[rc] holds the current residual
+  int colstride;   // smem elements per column
+  int ncmax;       // resident columns per CTA (smem sized for it)
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g0 = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
+  using VT = typename V16<T>::type;
+  constexpr int V = V16<T>::n;
+  constexpr int NW = SM_NT / 32;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* cols = reinterpret_cast<T*>(smem);
+  double* red = reinterpret_cast<double*>(smem + (((size_t)a.ncmax * a.colstride * sizeof(T) + 127) / 128) * 128);
+  double* gcol = red + NW * SM_CMAX;   // [SM_CMAX] reduced dots
+  double* cf = gcol + SM_CMAX;         // [SM_CMAX] axpy coefficients
+  double* rowscr = cf + SM_CMAX;       // [SM_NT] reduce-phase scratch
+  double* rsx = rowscr + SM_NT;        // [2][SM_NT] restart partials
+  double* sc4 = rsx + 2 * SM_NT;       // [8] block scalars
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = a.m;
+  const int G = gridDim.x, b = blockIdx.x;
+  const int64_t p0 = a.k * b / G, p1 = a.k * (b + 1) / G;
+  const int ncol = (int)(p1 - p0);
+  const int row0 = tid * V;
+
+  // resident columns (read once per round)
+  {
+    const int nv = (m + V - 1) / V;
+    const T* A = static_cast<const T*>(a.A);
+    for (int q = tid; q < ncol * nv; q += SM_NT) {
+      const int c = q / nv, v = q - c * nv;
+      *reinterpret_cast<VT*>(cols + (size_t)c * a.colstride + v * V) =
+          *reinterpret_cast<const VT*>(A + (p0 + c) * a.ld + v * V);
+    }
+  }
+  __syncthreads();
+
+  double eta = a.sc->eta;
+  double t_mom = a.sc->mom_t;
+  double P = a.sc->P;
+  int rc = a.rc;
+  int gv = a.g_valid;
+  // rows of the reduce phase owned by this CTA
+  const int mb = (m + G - 1) / G;
+  const int r_lo = min(m, b * mb), r_hi = min(m, r_lo + mb);
+  const int nrow = r_hi - r_lo;
+
+  auto dots = [&](const double (&vr)[R][V], double* gout) {
+    // all local columns at once: per-thread partial sums -> warp sums ->
+    // per-column fold over warps in order
+    for (int c0 = 0; c0 < ncol; c0 += 8) {
+      double d[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        d[u] = 0.0;
+        if (c0 + u < ncol) {
+          const T* col = cols + (size_t)(c0 + u) * a.colstride;
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            const int row = row0 + i * (SM_NT * V);
+            if (row < m) {
+              T av[V];
+              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+              for (int e = 0; e < V; ++e)
+                if (row + e < m) d[u] += static_cast<double>(av[e]) * vr[i][e];
+            }
+          }
+        }
+        d[u] = warp_sum<double>(d[u]);
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) red[warp * SM_CMAX + c0 + u] = d[u];
+    }
+    __syncthreads();
+    if (tid < ncol) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += red[w * SM_CMAX + tid];
+      gout[tid] = s;
+    }
+    __syncthreads();
+  };
+
+  for (int pass = 0; pass < a.passes; ++pass) {
+    const double* rcur = a.r[rc];
+    const double* rprv = a.r[rc ^ 1];
+    const double tn = (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom)) / 2.0;
+    const double beta = (a.kind == 2) ? (t_mom - 1.0) / tn : 0.0;
+    // residual (or the extrapolated residual) in registers
+    double vr[R][V];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = row0 + i * (SM_NT * V);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        double v = 0.0;
+        if (row + e < m) {
+          // written by other CTAs before the barrier: read through L2
+          v = __ldcg(&rcur[row + e]);
+          if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, __ldcg(&rprv[row + e]))));
+        }
+        vr[i][e] = v;
+      }
+    }
+    const bool use_stored = (a.kind == 0 && gv && pass == 0);
+    if (!use_stored) dots(vr, gcol);
+    // local x update
+    double gd = 0.0, gs = 0.0;
+    if (tid < ncol) {
+      const int64_t p = p0 + tid;
+      const double gj = use_stored ? a.g[p] : gcol[tid];
+      const double xo = a.x[p];
+      double xn;
+      if (a.kind == 2) {
+        const double xp = a.xprev[p];
+        double yv = xo;
+        if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
+        xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
+        a.xprev[p] = xo;
+        const double dx = xn - xo;
+        gd = gj * dx;
+        gs = a.nrm[p] * fabs(dx);
+      } else {
+        a.g[p] = gj;
+        xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
+      }
+      a.x[p] = xn;
+      cf[tid] = xn;
+    }
+    // restart partials of this CTA (fixed order over its columns)
+    if (a.kind == 2) {
+      rsx[tid] = gd;
+      rsx[SM_NT + tid] = gs;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s1 = 0.0, s2 = 0.0;
+      if (a.kind == 2)
+        for (int c = 0; c < ncol; ++c) {
+          s1 += rsx[c];
+          s2 += rsx[SM_NT + c];
+        }
+      sc4[0] = s1;
+      sc4[1] = s2;
+    }
+    // local partial rows of A x+
+    {
+      double acc[R][V];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[i][e] = 0.0;
+      for (int c = 0; c < ncol; ++c) {
+        const double xc = cf[c];
+        const T* col = cols + (size_t)c * a.colstride;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int row = row0 + i * (SM_NT * V);
+          if (row < m) {
+            T av[V];
+            unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[i][e] += static_cast<double>(av[e]) * xc;
+          }
+        }
+      }
+      double* out = a.part + (int64_t)b * a.ldp;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int row = row0 + i * (SM_NT * V);
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (row + e < m) out[row + e] = acc[i][e];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      a.bpart[4 * b + 1] = sc4[0];
+      a.bpart[4 * b + 2] = sc4[1];
+    }
+    grid_barrier(a.bar);
+    // distributed reduce of this CTA's rows: thread (row, slice)
+    double sq = 0.0;
+    if (nrow > 0) {
+      const int slices = SM_NT / nrow;
+      const int rr = tid % nrow, sl = tid / nrow;
+      double s = 0.0;
+      if (sl < slices)
+        for (int q = sl; q < G; q += slices) s += __ldcg(&a.part[(int64_t)q * a.ldp + r_lo + rr]);
+      rowscr[tid] = s;
+      __syncthreads();
+      if (tid < nrow) {
+        double v = 0.0;
+        for (int q = 0; q < slices; ++q) v += rowscr[q * nrow + tid];
+        v = add_rn(v, a.off[r_lo + tid]);
+        a.r[rc ^ 1][r_lo + tid] = v;
+        sq = v * v;
+      }
+    }
+    sq = warp_sum<double>(sq);
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += red[w];
+      a.bpart[4 * b + 0] = s;
+    }
+    grid_barrier(a.bar);
+    // every CTA folds the same values in the same order -> same decision
+    if (warp == 0) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int q = lane; q < G; q += 32) {
+        s0 += __ldcg(&a.bpart[4 * q + 0]);
+        s1 += __ldcg(&a.bpart[4 * q + 1]);
+        s2 += __ldcg(&a.bpart[4 * q + 2]);
+      }
+      s0 = warp_sum<double>(s0);
+      s1 = warp_sum<double>(s1);
+      s2 = warp_sum<double>(s2);
+      if (lane == 0) {
+        sc4[4] = s0;
+        sc4[5] = s1;
+        sc4[6] = s2;
+      }
+    }
+    __syncthreads();
+    const double Pn = 0.5 * sc4[4];
+    if (a.kind == 2) {
+      const double s_f = a.sc->rs_f * fmax(1.0, fabs(P));
+      const double s_g = a.sc->rs_g * sqrt(2.0 * P) * sc4[6];
+      const bool restart = (Pn > P + s_f) || (sc4[5] > s_g);
+      if (b == 0 && tid == 0 && restart) a.sc->restarts += 1;
+      t_mom = restart ? 1.0 : tn;
+    } else {
+      if (Pn > P + 1e-9 + a.sc->rise_rel * fabs(P)) {
+        if (b == 0 && tid == 0) {
+          if (a.sc->err == 0) {
+            a.sc->err_v1 = P;
+            a.sc->err_v2 = Pn;
+          }
+          set_err(a.sc, DE_STEP_TOO_LARGE);
+        }
+      }
+    }
+    P = Pn;
+    rc ^= 1;
+    gv = 0;
+    // next step reads the new residual written by other CTAs: the barrier
+    // above ordered it; keep the block in step before reusing smem scratch
+    __syncthreads();
+  }
+  // screening dot pass at the final x: g = A'r and the epsilon partial
+  if (a.do_dot) {
+    double vr[R][V];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = row0 + i * (SM_NT * V);
+#pragma unroll
+      for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? __ldcg(&a.r[rc][row + e]) : 0.0;
+    }
+    dots(vr, gcol);
+    double ep = 0.0;
+    if (tid < ncol) {
+      const int64_t p = p0 + tid;
+      const double gj = gcol[tid];
+      a.g[p] = gj;
+      if (a.has_inf && isinf(a.hi[p])) ep = fmax(-gj, 0.0) / fabs(a.att[p]);
+    }
+    // max is order independent
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ep = fmax(ep, __shfl_xor_sync(0xffffffffu, ep, o));
+    if (lane == 0) red[warp] = ep;
+    __syncthreads();
+    if (tid == 0) {
+      double e = 0.0;
+      for (int w = 0; w < NW; ++w) e = fmax(e, red[w]);
+      a.epart[b] = e;
+    }
+  }
+  if (b == 0 && tid == 0) {
+    a.sc->P = P;
+    a.sc->mom_t = t_mom;
+  }
+}
+
+}  // namespace bx

@@ -71,12 +71,17 @@ def test_kat_cases_vs_reference():
         assert res.trace[-1].screening_ratio == float(z[name + "_ratio"]), name
 
 
+@pytest.mark.parametrize("streamed", [False, True])
 @pytest.mark.parametrize("cfg_id,fname", [(1, "cfg1_trace.npz"), (2, "cfg2_trace.npz")])
-def test_baseline_config_full_trajectory(cfg_id, fname):
+def test_baseline_config_full_trajectory(cfg_id, fname, streamed, monkeypatch):
     """BASELINE config 1 (PG, 24k rounds) and 2 (CD) at full size: every round's
     primal / dual / gap / preserved count against the reference's own run."""
     from paper_2202_07258_b200 import Problem, SolverConfig, solve
     from paper_2202_07258_b200.generate import make_config
+    if streamed:
+        if cfg_id == 2:
+            pytest.skip("CD has one path")
+        monkeypatch.setenv("BX_NO_SMALL", "1")   # force the streamed k_pass path
     z = _load(fname)
     inst = make_config(cfg_id)
     res = solve(Problem(inst.a, inst.y, inst.lower, inst.upper),

@@ -22,10 +22,21 @@ def _solve_both(a, y, lo, hi, kind, passes=10, tol=1e-8, screening=True, max_rou
     return g, o
 
 
+@pytest.fixture(params=["resident", "streamed"])
+def path(request, monkeypatch):
+    """Run PG / FISTA rounds on the cooperative SM-resident kernel (small
+    problems, bx_small.cuh) or force the streamed k_pass + k_reduce path."""
+    if request.param == "streamed":
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+    else:
+        monkeypatch.delenv("BX_NO_SMALL", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("family", ["nnls", "bvls", "mixed"])
 @pytest.mark.parametrize("kind", ["pg", "apg", "cd"])
 @pytest.mark.parametrize("screening", [True, False])
-def test_small_trajectories(family, kind, screening):
+def test_small_trajectories(family, kind, screening, path):
     rng = np.random.default_rng(zlib.crc32(f"{family}-{kind}-{screening}".encode()))
     for _ in range(4):
         n = int(rng.integers(3, 31))
@@ -76,7 +87,7 @@ def test_zero_column_and_interior():
 
 
 @pytest.mark.parametrize("cfg_id,m,n,rounds", [(1, 1000, 2000, 300), (3, 1000, 5000, 200), (2, 500, 1000, 60)])
-def test_baseline_recipe_prefix(cfg_id, m, n, rounds):
+def test_baseline_recipe_prefix(cfg_id, m, n, rounds, path):
     """BASELINE config recipes at oracle-friendly sizes: first rounds round-by-round."""
     from paper_2202_07258_b200.generate import make_config
     inst = make_config(cfg_id, m=m, n=n)
