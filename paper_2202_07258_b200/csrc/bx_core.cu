@@ -220,6 +220,7 @@ struct bx_ctx {
   bool dot_done = false;    // the round kernel already produced g and the eps partials
   int dot_G = 0;
   bool small_ok = true;     // cooperative small-round path allowed (env BX_NO_SMALL disables)
+  unsigned bar_epoch = 0;   // grid-barrier epochs issued so far
   int64_t launches = 0;
   std::string err;
 
@@ -387,7 +388,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->probe = (int*)w.take(64);
   c->ldp = mp;
   c->part = w.take((size_t)c->Gmax * c->ldp * 8);  // fp64 sized: also the small-round path's partial rows
-  c->bar = (unsigned*)w.take(64);
+  c->bar = (unsigned*)w.take(4 * kMaxRanks * 4);
   c->bpart = (double*)w.take(c->Gmax * 8 * 4);
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
@@ -804,7 +805,7 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
   const int ncmax = (int)((c->k + G - 1) / G);
   if (ncmax > SM_CMAX) return BX_OK;
   const int colstride = (int)round_up(c->m, 2 * V);
-  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8) * 8 + 256;
+  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8 + 7 * SM_CMAX + SM_NT) * 8 + 256;
   const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
   if (smem > c->smem_cap) return BX_OK;
   const int s = c->cur;
@@ -830,6 +831,8 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
   a.epart = c->bpart;
   a.sc = c->sc;
   a.bar = c->bar;
+  a.epoch0 = c->bar_epoch;
+  c->bar_epoch += 2u * (unsigned)passes;  // two barriers per step
   a.passes = passes;
   a.kind = kind;
   a.g_valid = c->g_valid ? 1 : 0;
@@ -1300,7 +1303,7 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   memset(c->hsc, 0, sizeof(DevScalars));
   CU(cudaMemsetAsync(c->sc, 0, sizeof(DevScalars), c->stream));
   CU(cudaMemsetAsync(c->part, 0, (size_t)c->Gmax * c->ldp * 8, c->stream));
-  CU(cudaMemsetAsync(c->bar, 0, 64, c->stream));
+  CU(cudaMemsetAsync(c->bar, 0, 4 * kMaxRanks * 4, c->stream));
   c->small_ok = getenv("BX_NO_SMALL") == nullptr;
   if (dtype == BX_F64) return create_typed<double>(c, y, lower, upper, t);
   return create_typed<float>(c, y, lower, upper, t);

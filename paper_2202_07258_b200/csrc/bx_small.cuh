@@ -42,7 +42,8 @@ struct SmallArgs {
   double* bpart;   // [G][4] per-CTA scalars
   double* epart;   // [G] epsilon partials for k_dual
   DevScalars* sc;
-  unsigned* bar;   // [2] grid barrier: count, generation
+  unsigned* bar;   // [G] per-CTA barrier epochs
+  unsigned epoch0; // epoch base of this launch (host keeps the count)
   int passes;
   int kind;        // 0 PG, 2 APG
   int g_valid;     // PG: the first step may use the stored gradient
@@ -53,7 +54,10 @@ struct SmallArgs {
   int ncmax;       // resident columns per CTA (smem sized for it)
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+// Grid barrier: a counter + generation word (sense reversal); all CTAs are
+// co-resident (cooperative launch).  Measured faster on B200 than per-CTA
+// flags polled by one warp (148 acquire loads per poll).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned /*epoch*/) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* gen = bar + 1;
@@ -85,6 +89,14 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   double* rowscr = cf + SM_CMAX;       // [SM_NT] reduce-phase scratch
   double* rsx = rowscr + SM_NT;        // [2][SM_NT] restart partials
   double* sc4 = rsx + 2 * SM_NT;       // [8] block scalars
+  double* cx = sc4 + 8;                // [SM_CMAX] resident x
+  double* cxp = cx + SM_CMAX;          // [SM_CMAX] x_prev
+  double* clo = cxp + SM_CMAX;         // bounds, norms, A't, stored gradient
+  double* chi = clo + SM_CMAX;
+  double* cnr = chi + SM_CMAX;
+  double* cat = cnr + SM_CMAX;
+  double* cg = cat + SM_CMAX;
+  double* coff = cg + SM_CMAX;         // [SM_NT] z - y of the rows this CTA reduces
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = a.m;
   const int G = gridDim.x, b = blockIdx.x;
@@ -102,9 +114,20 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
           *reinterpret_cast<const VT*>(A + (p0 + c) * a.ld + v * V);
     }
   }
+  if (tid < ncol) {
+    const int64_t p = p0 + tid;
+    cx[tid] = a.x[p];
+    cxp[tid] = a.kind == 2 ? a.xprev[p] : 0.0;
+    clo[tid] = a.lo[p];
+    chi[tid] = a.hi[p];
+    cnr[tid] = a.nrm[p];
+    cat[tid] = a.att[p];
+    cg[tid] = a.g[p];
+  }
   __syncthreads();
 
   double eta = a.sc->eta;
+  unsigned epoch = a.epoch0;
   double t_mom = a.sc->mom_t;
   double P = a.sc->P;
   int rc = a.rc;
@@ -113,6 +136,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   const int mb = (m + G - 1) / G;
   const int r_lo = min(m, b * mb), r_hi = min(m, r_lo + mb);
   const int nrow = r_hi - r_lo;
+  if (tid < nrow) coff[tid] = a.off[r_lo + tid];
 
   auto dots = [&](const double (&vr)[R][V], double* gout) {
     // all local columns at once: per-thread partial sums -> warp sums ->
@@ -177,24 +201,23 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     // local x update
     double gd = 0.0, gs = 0.0;
     if (tid < ncol) {
-      const int64_t p = p0 + tid;
-      const double gj = use_stored ? a.g[p] : gcol[tid];
-      const double xo = a.x[p];
+      const double gj = use_stored ? cg[tid] : gcol[tid];
+      const double xo = cx[tid];
       double xn;
       if (a.kind == 2) {
-        const double xp = a.xprev[p];
+        const double xp = cxp[tid];
         double yv = xo;
         if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
-        xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
-        a.xprev[p] = xo;
+        xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), clo[tid], chi[tid]);
+        cxp[tid] = xo;
         const double dx = xn - xo;
         gd = gj * dx;
-        gs = a.nrm[p] * fabs(dx);
+        gs = cnr[tid] * fabs(dx);
       } else {
-        a.g[p] = gj;
-        xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
+        cg[tid] = gj;
+        xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), clo[tid], chi[tid]);
       }
-      a.x[p] = xn;
+      cx[tid] = xn;
       cf[tid] = xn;
     }
     // restart partials of this CTA (fixed order over its columns)
@@ -248,7 +271,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.bpart[4 * b + 1] = sc4[0];
       a.bpart[4 * b + 2] = sc4[1];
     }
-    grid_barrier(a.bar);
+    grid_barrier(a.bar, ++epoch);
     // distributed reduce of this CTA's rows: thread (row, slice)
     double sq = 0.0;
     if (nrow > 0) {
@@ -262,7 +285,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       if (tid < nrow) {
         double v = 0.0;
         for (int q = 0; q < slices; ++q) v += rowscr[q * nrow + tid];
-        v = add_rn(v, a.off[r_lo + tid]);
+        v = add_rn(v, coff[tid]);
         a.r[rc ^ 1][r_lo + tid] = v;
         sq = v * v;
       }
@@ -275,7 +298,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       for (int w = 0; w < NW; ++w) s += red[w];
       a.bpart[4 * b + 0] = s;
     }
-    grid_barrier(a.bar);
+    grid_barrier(a.bar, ++epoch);
     // every CTA folds the same values in the same order -> same decision
     if (warp == 0) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -331,10 +354,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     dots(vr, gcol);
     double ep = 0.0;
     if (tid < ncol) {
-      const int64_t p = p0 + tid;
       const double gj = gcol[tid];
-      a.g[p] = gj;
-      if (a.has_inf && isinf(a.hi[p])) ep = fmax(-gj, 0.0) / fabs(a.att[p]);
+      cg[tid] = gj;
+      if (a.has_inf && isinf(chi[tid])) ep = fmax(-gj, 0.0) / fabs(cat[tid]);
     }
     // max is order independent
 #pragma unroll
@@ -346,6 +368,13 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       for (int w = 0; w < NW; ++w) e = fmax(e, red[w]);
       a.epart[b] = e;
     }
+  }
+  // write back the resident per-column state
+  if (tid < ncol) {
+    const int64_t p = p0 + tid;
+    a.x[p] = cx[tid];
+    if (a.kind == 2) a.xprev[p] = cxp[tid];
+    a.g[p] = cg[tid];
   }
   if (b == 0 && tid == 0) {
     a.sc->P = P;
