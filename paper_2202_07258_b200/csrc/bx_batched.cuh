@@ -3,15 +3,16 @@
 // oracle/batched_oracle.py).
 //
 // K NNLS problems share one dictionary A (m x n, m <= 208).  A persistent CTA
-// owns a tile of 64 problems and runs whole rounds for it with no grid-wide
+// (16 warps: 8 tiles of 8 problems x 2 coordinate / row halves) owns a tile of
+// 64 problems and runs whole rounds for it with no grid-wide
 // dependency (problems are independent).  Per FISTA step it streams A in
 // chunks J of 16 columns (A is L2 resident: 8 MB at config 5) together with
 // the tile's x / x_prev chunk (HBM), and per chunk
 //     G_J  = A_J' R_y                       (16 x 64, K = m)   DMMA m8n8k4
 //     X+_J = max(Y_J - eta G_J, 0) on the active set  (epilogue, registers)
 //     R+  += A_J X+_J                       (m x 64,  K = 16)  DMMA m8n8k4
-// so the gradient matrix never reaches HBM.  R+ lives in registers (8 warps x
-// 8 problems x m rows); the per-problem restart tests, objective, dual point,
+// so the gradient matrix never reaches HBM.  R+ lives in registers (each warp
+// 8 problems x half the rows); the per-problem restart tests, objective, dual point,
 // gap, radius and the sphere test are all tile-local.
 #pragma once
 #include "bx_kernels.cuh"
@@ -19,10 +20,11 @@
 
 namespace bx {
 
-constexpr int BT_NT = 256;    // threads (8 warps)
-constexpr int BT_TILE = 64;   // problems per tile (8 per warp)
+constexpr int BT_NT = 512;    // threads (16 warps: 8 problem tiles x 2 halves)
+constexpr int BT_TILE = 64;   // problems per tile (8 per warp column)
 constexpr int BT_CH = 16;     // dictionary columns per chunk
 constexpr int BT_MT = 26;     // max m8 row tiles (m <= 208)
+constexpr int BT_MH = 13;     // row tiles per warp half (GEMM2 accumulators)
 constexpr int BT_SX = 20;     // smem stride of x tiles (== 4 mod 16: conflict-free fragments)
 
 struct BatchArgs {
@@ -99,60 +101,47 @@ __device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BatchSmem&
   cp_async_commit();
 }
 
-// G tile (coords j0 + 8t + g, problems n0 + 2 tig + e) = A_J' Ry for the warp's
-// 8 problems, 2 coordinate tiles; K = m in steps of 4.  Four independent
-// accumulator sets (k-steps interleaved) keep 8 DMMA chains in flight per warp
-// -- a single chain per tile is DMMA-latency bound -- and are summed in a
-// fixed order at the end (deterministic).
-__device__ __forceinline__ void bt_gemm1(const BatchArgs& a, const double* ab, const double* rys, int n0, int g,
-                                         int tig, double (&gt)[2][2]) {
-  double acc[4][2][2];
+// G tile (coords 8 mh + g, problems n0 + 2 tig + e) = A_J' Ry: one 8x8 output
+// tile per warp, K = m in steps of 4.  Four independent accumulator sets
+// (k-steps interleaved) keep 4 DMMA chains in flight per warp (a single chain
+// is DMMA-latency bound); they are summed in a fixed order (deterministic).
+__device__ __forceinline__ void bt_gemm1(const BatchArgs& a, const double* ab, const double* rys, int n0, int mh,
+                                         int g, int tig, double (&gt)[2]) {
+  double acc[4][2];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int t = 0; t < 2; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
+  for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = 0.0;
   const int m4 = (a.m + 3) / 4;
   const double* rb = rys + (n0 + g) * a.sa + tig;
-  const double* a0 = ab + g * a.sa + tig;
-  const double* a1 = ab + (8 + g) * a.sa + tig;
+  const double* a0 = ab + (8 * mh + g) * a.sa + tig;
   int kk = 0;
   for (; kk + 4 <= m4; kk += 4) {
-    double b[4], x0[4], x1[4];
+    double b[4], x0[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       b[u] = rb[4 * (kk + u)];
       x0[u] = a0[4 * (kk + u)];
-      x1[u] = a1[4 * (kk + u)];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      dmma(acc[u][0][0], acc[u][0][1], x0[u], b[u]);
-      dmma(acc[u][1][0], acc[u][1][1], x1[u], b[u]);
-    }
+    for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], x0[u], b[u]);
   }
-  for (; kk < m4; ++kk) {
-    const double b = rb[4 * kk];
-    dmma(acc[0][0][0], acc[0][0][1], a0[4 * kk], b);
-    dmma(acc[0][1][0], acc[0][1][1], a1[4 * kk], b);
-  }
+  for (; kk < m4; ++kk) dmma(acc[0][0], acc[0][1], a0[4 * kk], rb[4 * kk]);
 #pragma unroll
-  for (int t = 0; t < 2; ++t)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) gt[t][e] = (acc[0][t][e] + acc[1][t][e]) + (acc[2][t][e] + acc[3][t][e]);
+  for (int e = 0; e < 2; ++e) gt[e] = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
 }
 
-// acc (rows 8 mt + g, problems n0 + 2 tig + e) += A_J X_J ; K = 16 coordinates
+// acc (rows 8 (mlo + q) + g, problems n0 + 2 tig + e) += A_J X_J over this
+// warp's row half [mlo, mhi); K = 16 coordinates
 __device__ __forceinline__ void bt_gemm2(const BatchArgs& a, const double* ab, const double* xns, int n0, int g,
-                                         int tig, double (&acc)[BT_MT][2], int mt_n) {
+                                         int tig, double (&acc)[BT_MH][2], int mlo, int mhi) {
 #pragma unroll
   for (int kk = 0; kk < BT_CH / 4; ++kk) {
     const int j = 4 * kk + tig;
     const double b = xns[(n0 + g) * BT_SX + j];
 #pragma unroll
-    for (int mt = 0; mt < BT_MT; ++mt) {
-      if (mt < mt_n) {
-        const double av = ab[j * a.sa + 8 * mt + g];
-        dmma(acc[mt][0], acc[mt][1], av, b);
+    for (int q = 0; q < BT_MH; ++q) {
+      if (mlo + q < mhi) {
+        const double av = ab[j * a.sa + 8 * (mlo + q) + g];
+        dmma(acc[q][0], acc[q][1], av, b);
       }
     }
   }
@@ -162,7 +151,8 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
-  const int n0 = warp * 8;  // this warp's 8 problems inside the tile
+  const int nt = warp & 7, mh = warp >> 3;  // problem tile of this warp, coordinate / row half
+  const int n0 = nt * 8;
   BatchSmem s;
   {
     double* p = reinterpret_cast<double*>(smem_raw);
@@ -176,13 +166,14 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
     p += 2 * BT_TILE * BT_SX;
     s.xns = p;
     p += BT_TILE * BT_SX;
-    s.red = p;
+    s.red = p;  // [8][64]: per-problem partials of the two warp halves
     p += 8 * BT_TILE;
     s.beta = p;
     p += BT_TILE;
     s.mk = reinterpret_cast<uint32_t*>(p);
   }
   const int mt_n = (a.m + 7) / 8;
+  const int mlo = mh ? BT_MH : 0, mhi = mh ? mt_n : min(BT_MH, mt_n);
   const int nch = (a.n + BT_CH - 1) / BT_CH;
   const int ntiles = a.K / BT_TILE;
   // zero both dictionary buffers once: rows in [m, sa) and columns past n are
@@ -217,9 +208,9 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
         }
         s.rys[q] = v;
       }
-      double acc[BT_MT][2];
+      double acc[BT_MH][2];
 #pragma unroll
-      for (int mt = 0; mt < BT_MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+      for (int q = 0; q < BT_MH; ++q) acc[q][0] = acc[q][1] = 0.0;
       double gdot[2] = {0.0, 0.0}, gsc[2] = {0.0, 0.0};
       const double bt0 = s.beta[n0 + 2 * tig], bt1 = s.beta[n0 + 2 * tig + 1];
       bt_prefetch(a, s, 0, 0, k0, X, Xp, true);
@@ -232,30 +223,29 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
         const double* xs = s.xs + buf * BT_TILE * BT_SX;
         const double* xps = s.xps + buf * BT_TILE * BT_SX;
         const uint32_t* mk = s.mk + buf * BT_TILE;
-        double gt[2][2];
-        bt_gemm1(a, ab, s.rys, n0, g, tig, gt);
-        // epilogue: the FISTA update of this lane's 2 x 2 elements
+        double gt[2];
+        bt_gemm1(a, ab, s.rys, n0, mh, g, tig, gt);
+        // epilogue: the FISTA update of this lane's two elements
         const int j0 = c * BT_CH;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int jj = 8 * t + g;
+        {
+          const int jj = 8 * mh + g;
           const int j = j0 + jj;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int nn = n0 + 2 * tig + e;
-            double xn = 0.0, dx = 0.0;
+            double xn = 0.0;
             if (j < a.n) {
-              const bool act = (mk[nn] >> ((j & 31))) & 1u;
+              const bool act = (mk[nn] >> (j & 31)) & 1u;
               const double x = xs[nn * BT_SX + jj], xp = xps[nn * BT_SX + jj];
               const double bt = e ? bt1 : bt0;
               double yv = x;
               if (bt != 0.0) yv = add_rn(x, mul_rn(bt, sub_rn(x, xp)));
               if (act) {
-                xn = sub_rn(yv, mul_rn(a.eta, gt[t][e]));
+                xn = sub_rn(yv, mul_rn(a.eta, gt[e]));
                 xn = xn < 0.0 ? 0.0 : xn;
               }
-              dx = xn - x;
-              gdot[e] += gt[t][e] * dx;
+              const double dx = xn - x;
+              gdot[e] += gt[e] * dx;
               gsc[e] += a.nrm[j] * fabs(dx);
             }
             s.xns[nn * BT_SX + jj] = xn;
@@ -270,18 +260,18 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
             if (jj < nj) Xp[(int64_t)(k0 + nn) * a.ldx + j0 + jj] = s.xns[nn * BT_SX + jj];
           }
         }
-        bt_gemm2(a, ab, s.xns, n0, g, tig, acc, mt_n);
+        bt_gemm2(a, ab, s.xns, n0, g, tig, acc, mlo, mhi);
       }
       // r+ = A x+ - y  (into the r_prev slot), objective, restart test
       double sq[2] = {0.0, 0.0};
 #pragma unroll
-      for (int mt = 0; mt < BT_MT; ++mt) {
-        const int i = 8 * mt + g;
-        if (mt < mt_n && i < a.m) {
+      for (int q = 0; q < BT_MH; ++q) {
+        const int i = 8 * (mlo + q) + g;
+        if (mlo + q < mhi && i < a.m) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int nn = n0 + 2 * tig + e;
-            const double r = acc[mt][e] - a.Y[(int64_t)(k0 + nn) * a.ldy + i];
+            const double r = acc[q][e] - a.Y[(int64_t)(k0 + nn) * a.ldy + i];
             Rp[(int64_t)(k0 + nn) * a.ldy + i] = r;
             sq[e] += r * r;
           }
@@ -299,16 +289,25 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       if (g == 0) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int k = k0 + n0 + 2 * tig + e;
-          const double Pn = 0.5 * sq[e];
-          const double P = a.P[k];
-          const double t = a.mom[k];
-          const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-          const double s_f = a.rs_f * fmax(1.0, fabs(P));
-          const double s_g = a.rs_g * sqrt(2.0 * P) * gsc[e];
-          a.mom[k] = (Pn > P + s_f || gdot[e] > s_g) ? 1.0 : tn;
-          a.P[k] = Pn;
+          const int nn = n0 + 2 * tig + e;
+          s.red[(0 + mh) * BT_TILE + nn] = sq[e];
+          s.red[(2 + mh) * BT_TILE + nn] = gdot[e];
+          s.red[(4 + mh) * BT_TILE + nn] = gsc[e];
         }
+      }
+      __syncthreads();
+      if (tid < BT_TILE) {
+        const int k = k0 + tid;
+        const double Pn = 0.5 * (s.red[tid] + s.red[BT_TILE + tid]);
+        const double gd = s.red[2 * BT_TILE + tid] + s.red[3 * BT_TILE + tid];
+        const double gs = s.red[4 * BT_TILE + tid] + s.red[5 * BT_TILE + tid];
+        const double P = a.P[k];
+        const double t = a.mom[k];
+        const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+        const double s_f = a.rs_f * fmax(1.0, fabs(P));
+        const double s_g = a.rs_g * sqrt(2.0 * P) * gs;
+        a.mom[k] = (Pn > P + s_f || gd > s_g) ? 1.0 : tn;
+        a.P[k] = Pn;
       }
       par ^= 1;
       __syncthreads();
@@ -331,16 +330,13 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
         cp_async_wait_all();
         __syncthreads();
         if (c + 1 < nch) bt_prefetch(a, s, buf ^ 1, c + 1, k0, X, nullptr, false);
-        double gt[2][2];
-        bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, g, tig, gt);
+        double gt[2];
+        bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, mh, g, tig, gt);
+        const int j = c * BT_CH + 8 * mh + g;
+        if (j < a.n) {
+          const double inv = 1.0 / fabs(a.att[j]);
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int j = c * BT_CH + 8 * t + g;
-          if (j < a.n) {
-            const double inv = 1.0 / fabs(a.att[j]);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) emax[e] = fmax(emax[e], fmax(-gt[t][e], 0.0) * inv);
-          }
+          for (int e = 0; e < 2; ++e) emax[e] = fmax(emax[e], fmax(-gt[e], 0.0) * inv);
         }
       }
 #pragma unroll
@@ -348,9 +344,11 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) emax[e] = fmax(emax[e], __shfl_xor_sync(0xffffffffu, emax[e], o));
       if (g == 0) {
-        s.beta[n0 + 2 * tig] = emax[0];  // reuse: eps per problem
-        s.beta[n0 + 2 * tig + 1] = emax[1];
+        s.red[mh * BT_TILE + n0 + 2 * tig] = emax[0];
+        s.red[mh * BT_TILE + n0 + 2 * tig + 1] = emax[1];
       }
+      __syncthreads();
+      if (tid < BT_TILE) s.beta[tid] = fmax(s.red[tid], s.red[BT_TILE + tid]);  // eps per problem
       __syncthreads();
       // dual objective per problem: theta = -r + eps t (t = -1): theta_i = -r_i - eps
       for (int pb = warp; pb < BT_TILE; pb += BT_NT / 32) {
@@ -374,7 +372,7 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
           st[a.K + k] = D;
           st[2 * a.K + k] = gap;
           st[3 * a.K + k] = eps;
-          s.red[pb] = sqrt(2.0 * gap) + a.slack_scale * fmax(1.0, sqrt(s2));  // radius + slack
+          s.red[6 * BT_TILE + pb] = sqrt(2.0 * gap) + a.slack_scale * fmax(1.0, sqrt(s2));  // radius + slack
         }
       }
       __syncthreads();
@@ -388,25 +386,22 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
           cp_async_wait_all();
           __syncthreads();
           if (c + 1 < nch) bt_prefetch(a, s, buf ^ 1, c + 1, k0, X, nullptr, false);
-          double gt[2][2];
-          bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, g, tig, gt);
+          double gt[2];
+          bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, mh, g, tig, gt);
           const uint32_t* mk = s.mk + buf * BT_TILE;
+          const int j = c * BT_CH + 8 * mh + g;
+          if (j < a.n) {
 #pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const int j = c * BT_CH + 8 * t + g;
-            if (j < a.n) {
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int nn = n0 + 2 * tig + e;
-                const bool act = (mk[nn] >> (j & 31)) & 1u;
-                const double v = add_rn(-gt[t][e], mul_rn(s.beta[nn], a.att[j]));
-                if (act && v < -s.red[nn] * a.nrm[j]) {
-                  const int64_t k = k0 + nn;
-                  atomicAnd(&a.mask[k * a.nw + (j >> 5)], ~(1u << (j & 31)));
-                  const_cast<double*>(X)[k * a.ldx + j] = 0.0;
-                  Xq[k * a.ldx + j] = 0.0;
-                  dirty = 1;
-                }
+            for (int e = 0; e < 2; ++e) {
+              const int nn = n0 + 2 * tig + e;
+              const bool act = (mk[nn] >> (j & 31)) & 1u;
+              const double v = add_rn(-gt[e], mul_rn(s.beta[nn], a.att[j]));
+              if (act && v < -s.red[6 * BT_TILE + nn] * a.nrm[j]) {
+                const int64_t k = k0 + nn;
+                atomicAnd(&a.mask[k * a.nw + (j >> 5)], ~(1u << (j & 31)));
+                const_cast<double*>(X)[k * a.ldx + j] = 0.0;
+                Xq[k * a.ldx + j] = 0.0;
+                dirty = 1;
               }
             }
           }
@@ -418,9 +413,9 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
         for (int which = 0; which < 2; ++which) {
           const double* Xw = which ? Xq : X;
           double* Rw = a.R[which ? 1 - par : par];
-          double acc[BT_MT][2];
+          double acc[BT_MH][2];
 #pragma unroll
-          for (int mt = 0; mt < BT_MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+          for (int q = 0; q < BT_MH; ++q) acc[q][0] = acc[q][1] = 0.0;
           bt_prefetch(a, s, 0, 0, k0, Xw, nullptr, true);
           for (int c = 0; c < nch; ++c) {
             const int buf = c & 1;
@@ -435,32 +430,32 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
               s.xns[nn * BT_SX + jj] = (jj < nj) ? xs[nn * BT_SX + jj] : 0.0;
             }
             __syncthreads();
-            bt_gemm2(a, s.abuf + buf * BT_CH * a.sa, s.xns, n0, g, tig, acc, mt_n);
+            bt_gemm2(a, s.abuf + buf * BT_CH * a.sa, s.xns, n0, g, tig, acc, mlo, mhi);
           }
           double sq[2] = {0.0, 0.0};
 #pragma unroll
-          for (int mt = 0; mt < BT_MT; ++mt) {
-            const int i = 8 * mt + g;
-            if (mt < mt_n && i < a.m) {
+          for (int q = 0; q < BT_MH; ++q) {
+            const int i = 8 * (mlo + q) + g;
+            if (mlo + q < mhi && i < a.m) {
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int nn = n0 + 2 * tig + e;
-                const double r = acc[mt][e] - a.Y[(int64_t)(k0 + nn) * a.ldy + i];
+                const double r = acc[q][e] - a.Y[(int64_t)(k0 + nn) * a.ldy + i];
                 Rw[(int64_t)(k0 + nn) * a.ldy + i] = r;
                 sq[e] += r * r;
               }
             }
           }
-          if (which == 0) {
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
+          for (int e = 0; e < 2; ++e)
 #pragma unroll
-              for (int o = 4; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
-            if (g == 0) {
-              a.P[k0 + n0 + 2 * tig] = 0.5 * sq[0];
-              a.P[k0 + n0 + 2 * tig + 1] = 0.5 * sq[1];
-            }
+            for (int o = 4; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
+          if (g == 0) {
+            s.red[mh * BT_TILE + n0 + 2 * tig] = sq[0];
+            s.red[mh * BT_TILE + n0 + 2 * tig + 1] = sq[1];
           }
+          __syncthreads();
+          if (which == 0 && tid < BT_TILE) a.P[k0 + tid] = 0.5 * (s.red[tid] + s.red[BT_TILE + tid]);
           __syncthreads();
         }
       }
