@@ -60,7 +60,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <typename T>
-__device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, int64_t blk, int64_t row0, int nrows) {
+__device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* gdst, int64_t blk, int64_t row0,
+                                            int nrows) {
+  // the block's 32 x 32 Gram matrix (fp64) rides along
+  for (int q = threadIdx.x; q < CD_B * CD_B / 2; q += CD_NT) cp_async16(gdst + 2 * q, a.gram + blk * CD_B * CD_B + 2 * q);
   // dst[c * rows_pad + i] = A[row0 + i, 32*blk + c]
   const int64_t c0 = blk * CD_B;
   const int nc = (int)min((int64_t)CD_B, a.k - c0);
@@ -84,8 +87,8 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   T* abuf0 = reinterpret_cast<T*>(smem);
   T* abuf1 = abuf0 + CD_B * rows_pad;
   double* part = reinterpret_cast<double*>(abuf1 + CD_B * rows_pad);  // [2][CD_B] partial dots
-  double* gbuf = part + 2 * CD_B;                                       // [CD_B][CD_B] Gram block
-  double* delta = gbuf + CD_B * CD_B;                                   // [CD_B]
+  double* gbuf = part + 2 * CD_B;                                       // [2][CD_B][CD_B] Gram blocks
+  double* delta = gbuf + 2 * CD_B * CD_B;                               // [CD_B]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t row0 = (int64_t)rank * rows_pad;
   const int nrows = (int)max((int64_t)0, min((int64_t)rows_pad, a.m - row0));
@@ -99,17 +102,15 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   }
   const int64_t nblk = (a.k + CD_B - 1) / CD_B;
   int64_t it = 0;  // global block counter (selects buffers)
-  if (nblk > 0 && nrows > 0) cd_prefetch(a, abuf0, 0, row0, nrows);
+  if (nblk > 0) cd_prefetch(a, abuf0, gbuf, 0, row0, nrows);
   for (int pass = 0; pass < a.passes; ++pass) {
     for (int64_t blk = 0; blk < nblk; ++blk, ++it) {
       T* cur = (it & 1) ? abuf1 : abuf0;
       T* nxt = (it & 1) ? abuf0 : abuf1;
       const int64_t c0 = blk * CD_B;
       const int nc = (int)min((int64_t)CD_B, a.k - c0);
-      if (nrows > 0) cp_async_wait_all();
-      // Gram block for the sequential update
-      const double* gsrc = a.gram + blk * CD_B * CD_B;
-      for (int q = tid; q < CD_B * CD_B; q += CD_NT) gbuf[q] = gsrc[q];
+      cp_async_wait_all();
+      const double* gcur = gbuf + (it & 1) * CD_B * CD_B;
       __syncthreads();
       // prefetch the next block while this one is processed
       {
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           nb = 0;
           ++np;
         }
-        if (np < a.passes && nrows > 0) cd_prefetch(a, nxt, nb, row0, nrows);
+        if (np < a.passes) cd_prefetch(a, nxt, gbuf + ((it + 1) & 1) * CD_B * CD_B, nb, row0, nrows);
       }
       // partial dots: every thread multiplies its register rows with the block's
       // columns; a butterfly transpose-reduction leaves column c's warp sum in
@@ -180,23 +181,32 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           const double nj = a.nrm[j];
           sq = nj * nj;  // solvers.py:60 (col_norms ** 2)
         }
+        // Gram row of this lane's coordinate in registers; the chain per
+        // coordinate is then multiply, clip, subtract, one shuffle and one FMA
+        double grow[CD_B];
+#pragma unroll
+        for (int i = 0; i < CD_B; ++i) grow[i] = gcur[lane * CD_B + i];
+        const double isq = 1.0 / sq;
         double dl = 0.0;
-        for (int i = 0; i < nc; ++i) {
-          double di = 0.0;
-          if (lane == i) {
-            const double step = cdot / sq;                             // solvers.py:131
-            double nv = xj - step;                                      // solvers.py:132
-            nv = nv < loj ? loj : nv;
-            nv = nv > hij ? hij : nv;
-            const double dt = nv - xj;                                  // solvers.py:133
-            if (dt != 0.0) {
-              di = dt;
-              xj = nv;
+#pragma unroll
+        for (int i = 0; i < CD_B; ++i) {
+          if (i < nc) {
+            double di = 0.0;
+            if (lane == i) {
+              const double step = cdot * isq;                          // solvers.py:131
+              double nv = xj - step;                                   // solvers.py:132
+              nv = nv < loj ? loj : nv;
+              nv = nv > hij ? hij : nv;
+              const double dt = nv - xj;                               // solvers.py:133
+              if (dt != 0.0) {
+                di = dt;
+                xj = nv;
+              }
+              dl = di;
             }
-            dl = di;
+            di = __shfl_sync(0xffffffffu, di, i);
+            cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
           }
-          di = __shfl_sync(0xffffffffu, di, i);
-          if (di != 0.0 && lane > i && lane < nc) cdot += gbuf[lane * CD_B + i] * di;
         }
         delta[lane] = dl;
         if (lane < nc && rank == 0) xout[j] = xj;
