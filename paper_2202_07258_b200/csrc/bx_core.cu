@@ -482,11 +482,23 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   const uint32_t colstride = (uint32_t)align_up(colbytes, 128);
   const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 3 * CMAX) * 8 + 64;
   const size_t slot = (size_t)C * colstride;
+  const int G = pass_grid(c, vw.k);
   int S = (int)((c->smem_cap - scratch) / slot);
   if (S > SMAX) S = SMAX;
   if (S < 1) return fail(c, BX_ERR_UNSUPPORTED, "column of %u bytes does not fit shared memory", colbytes);
-  const size_t smem = S * slot + scratch;
-  const int G = pass_grid(c, vw.k);
+  // stage the per-column state of each CTA when that costs no ring slot below 2
+  const int64_t per_cta = (vw.k + G - 1) / G;
+  const size_t stage = align_up((size_t)per_cta * 5 * 8, 128);
+  int pre = 0;
+  {
+    int S2 = (int)((c->smem_cap - scratch - stage) / slot);
+    if (S2 > SMAX) S2 = SMAX;
+    if (S2 >= (S < 2 ? S : 2) && S2 >= 1) {
+      S = S2;
+      pre = (int)per_cta;
+    }
+  }
+  const size_t smem = S * slot + scratch + (pre ? stage : 0);
   PassArgs<T> a;
   a.A = vw.A;
   a.ld = vw.ld;
@@ -513,6 +525,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   a.S = S;
   a.colbytes = colbytes;
   a.colstride = colstride;
+  a.pre = pre;
   if (G_out) *G_out = G;
   const int e0 = prof_begin(c);
   int st = BX_OK;

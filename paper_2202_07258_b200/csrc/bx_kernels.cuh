@@ -110,6 +110,7 @@ struct PassArgs {
   int S;                   // ring slots
   uint32_t colbytes;       // bytes moved per column (multiple of 16)
   uint32_t colstride;      // smem bytes per column in a slot
+  int pre;                 // >= columns per CTA: the CTA's per-column state is staged in smem (0: off)
 };
 
 // ----------------------------------------------------------------------------
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   double* red = reinterpret_cast<double*>(bars + SMAX);  // [NWARPS][C]
   double* cf = red + NWARPS * CMAX;                      // [C] axpy coefficients
   double* bscr = cf + CMAX;                              // [2][CMAX] block scalar scratch
+  double* stg = bscr + 2 * CMAX;                         // [5][pre] staged per-column state
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -311,6 +313,31 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   double run = 0.0;   // block-scalar running value (threads tid < C)
   double run2 = 0.0;  // second block scalar (FISTA restart slack)
 
+  // Stage this CTA's per-column state in shared memory once (coalesced), so
+  // the per-column update between the two barriers never waits on HBM.
+  const bool staged = a.pre >= ncol && a.pre > 0;
+  const double *s0 = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr;
+  if (staged) {
+    const double* src[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    switch (a.upd) {
+      case U_DOT: src[0] = a.hi; src[1] = a.att; break;
+      case U_PG_G: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; src[3] = a.g; break;
+      case U_PG: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; break;
+      case U_APG: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; src[3] = a.xprev; src[4] = a.nrm; break;
+      case U_AX: src[0] = a.coef ? a.coef : a.x; break;
+      default: break;
+    }
+    for (int f = 0; f < 5; ++f)
+      if (src[f])
+        for (int q = tid; q < ncol; q += NT) stg[f * a.pre + q] = src[f][p0 + q];
+    s0 = stg;
+    s1 = stg + a.pre;
+    s2 = stg + 2 * a.pre;
+    s3 = stg + 3 * a.pre;
+    s4 = stg + 4 * a.pre;
+    __syncthreads();
+  }
+
   for (int gi = 0; gi < ngroups; ++gi) {
     const int s = gi % S;
     const int cg = min(C, ncol - gi * C);
@@ -346,29 +373,33 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
 #pragma unroll
         for (int w = 0; w < NWARPS; ++w) gsum += red[w * CMAX + tid];
         const double gj = gsum;
-        const int64_t p = p0 + (int64_t)gi * C + tid;
+        const int ql = gi * C + tid;  // local column index
+        const int64_t p = p0 + ql;
         double coef = 0.0;
         switch (a.upd) {
           case U_DOT: {
             a.g[p] = gj;
-            if (a.has_inf && isinf(a.hi[p])) {
-              const double ratio = fmax(-gj, 0.0) / fabs(a.att[p]);
+            const double hj = staged ? s0[ql] : a.hi[p];
+            if (a.has_inf && isinf(hj)) {
+              const double ratio = fmax(-gj, 0.0) / fabs(staged ? s1[ql] : a.att[p]);
               run = fmax(run, ratio);
             }
           } break;
           case U_PG: {
             a.g[p] = gj;
-            const double xo = a.x[p];
-            const double xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
+            const double xo = staged ? s0[ql] : a.x[p];
+            const double xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), staged ? s1[ql] : a.lo[p],
+                                           staged ? s2[ql] : a.hi[p]);
             a.x[p] = xn;
             coef = xn;
           } break;
           case U_APG: {
-            const double xo = a.x[p];
-            const double xp = a.xprev[p];
+            const double xo = staged ? s0[ql] : a.x[p];
+            const double xp = staged ? s3[ql] : a.xprev[p];
             double yv = xo;
             if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
-            const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), a.lo[p], a.hi[p]);
+            const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), staged ? s1[ql] : a.lo[p],
+                                           staged ? s2[ql] : a.hi[p]);
             a.xprev[p] = xo;
             a.x[p] = xn;
             coef = xn;
@@ -376,7 +407,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
             // sum ||a_j|| |x+ - x| (FISTA)
             const double dxj = xn - xo;
             run += gj * dxj;
-            run2 += a.nrm[p] * fabs(dxj);
+            run2 += (staged ? s4[ql] : a.nrm[p]) * fabs(dxj);
           } break;
           case U_POWER: {
             coef = gj;
@@ -390,15 +421,17 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       __syncthreads();
     } else {
       if (tid < cg) {
-        const int64_t p = p0 + (int64_t)gi * C + tid;
+        const int ql = gi * C + tid;
+        const int64_t p = p0 + ql;
         double coef = 0.0;
         if (a.upd == U_PG_G) {
-          const double xo = a.x[p];
-          const double xn = clip<double>(sub_rn(xo, mul_rn(eta, a.g[p])), a.lo[p], a.hi[p]);
+          const double xo = staged ? s0[ql] : a.x[p];
+          const double xn = clip<double>(sub_rn(xo, mul_rn(eta, staged ? s3[ql] : a.g[p])),
+                                         staged ? s1[ql] : a.lo[p], staged ? s2[ql] : a.hi[p]);
           a.x[p] = xn;
           coef = xn;
         } else {
-          coef = a.coef ? a.coef[p] : a.x[p];
+          coef = staged ? s0[ql] : (a.coef ? a.coef[p] : a.x[p]);
         }
         cf[tid] = coef;
       }
