@@ -177,7 +177,11 @@ struct bx_ctx {
   int64_t lda = 0;
   void* Aact = nullptr;  // compacted preserved columns
   int64_t ldact = 0;
-  bool act_is_orig = true;  // before the first compaction the act view is A itself
+  bool act_is_orig = true;  // the preserved columns are read from A itself (through idx when not dense)
+  bool dense = true;        // preserved columns are contiguous in their buffer (no column map)
+  int64_t kphys = 0;        // columns in the physical buffer the act view reads
+  int32_t* pos[2] = {nullptr, nullptr};  // physical column of each preserved position (A_act)
+  void *scr_dx = nullptr, *scr_dxp = nullptr;  // b - x, b - x_prev of newly screened columns
 
   // per-row vectors (mp elements)
   void *y = nullptr, *t = nullptr, *negy = nullptr, *z = nullptr, *z2 = nullptr, *off = nullptr, *tgt = nullptr;
@@ -359,7 +363,10 @@ void carve(bx_ctx* c, Carver& w) {
   void** rows[] = {&c->y, &c->t, &c->negy, &c->z, &c->z2, &c->off, &c->tgt,
                    &c->r, &c->rprev, &c->rc, &c->theta, &c->thetac, &c->u};
   for (void** p : rows) *p = w.take(mp * e);
+  c->scr_dx = w.take(n * 8);
+  c->scr_dxp = w.take(n * 8);
   for (int s = 0; s < 2; ++s) {
+    c->pos[s] = (int32_t*)w.take(n * 4);
     c->idx[s] = (int32_t*)w.take(n * 4);
     c->x[s] = w.take(n * e);
     c->xprev[s] = w.take(n * e);
@@ -453,7 +460,10 @@ struct View {
 
 template <typename T>
 View<T> act_view(bx_ctx* c) {
-  if (c->act_is_orig) return View<T>{(const T*)c->A, c->lda, nullptr, c->k};
+  // lazy compaction: between physical rewrites the preserved columns are read
+  // through a column map (each column is one contiguous bulk copy either way)
+  if (c->act_is_orig) return View<T>{(const T*)c->A, c->lda, c->dense ? nullptr : c->idx[c->cur], c->k};
+  if (!c->dense) return View<T>{(const T*)c->Aact, c->ldact, c->pos[c->cur], c->k};
   return View<T>{(const T*)c->Aact, c->ldact, nullptr, c->k};
 }
 template <typename T>
@@ -826,6 +836,7 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
   SmallArgs a;
   a.A = vw.A;
   a.ld = vw.ld;
+  a.colmap = vw.colmap;
   a.k = c->k;
   a.m = (int)c->m;
   a.x = (double*)c->x[s];
@@ -987,65 +998,79 @@ int certified(bx_ctx* c, double alpha) {
   return BX_OK;
 }
 
+// r += A_S (b_S - x_S) (and r_prev += A_S (b_S - x_prev_S)) over the newly
+// screened columns: the residual of the snapped iterate without a pass over the
+// preserved set.  The reference recomputes it (solvers.py:64); the next step's
+// pass recomputes r = A x + z - y from scratch anyway, so only the one dot of
+// that step sees the (rounding-level) difference.  Collective in sharded mode
+// (every rank contributes its own screened columns, possibly none).
+template <typename T>
+int refresh_incremental(bx_ctx* c, int64_t nscr, int kind) {
+  View<T> vw{(const T*)c->A, c->lda, c->scr_idx, nscr};
+  int G = 1;
+  TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                  (const double*)c->scr_dx, nullptr, 0, &G));
+  TRY(run_reduce<T>(c, G, (const double*)c->r, (double*)c->r, R_SET, nullptr, 0, 0));
+  if (kind == BX_APG) {
+    TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    (const double*)c->scr_dxp, nullptr, 0, &G));
+    TRY(run_reduce<T>(c, G, (const double*)c->rprev, (double*)c->rprev, R_PLAIN, nullptr, 0, 0));
+  }
+  return BX_OK;
+}
+
 // apply_screening + Workspace.refresh (screening.py:72-94, solvers.py:54-65)
 template <typename T>
 int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, bool z_update) {
   const int s = c->cur, d = 1 - c->cur;
   const int nbs = (int)((c->k + RT - 1) / RT);
-  if (n_lo + n_up == 0) {
-    // nothing screened on this rank: keep its columns, join the collectives
-    if (z_update) {
-      View<T> vw{(const T*)c->A, c->lda, c->scr_idx, 0};
-      int G = 1;
-      TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                      (const double*)c->scr_val, nullptr, 0, &G));
-      TRY(run_reduce<T>(c, G, (const double*)c->z, (double*)c->z2, R_PLAIN, nullptr, 0, 0));
-      std::swap(c->z, c->z2);
-      k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z, (double*)c->off,
-                                                            (double*)c->tgt);
-      LAUNCHED();
-    }
-    TRY(refresh_resid<T>(c));
-    if (kind == BX_APG) TRY(refresh_rprev<T>(c));
-    c->g_valid = false;
-    return BX_OK;
+  const int64_t nscr = n_lo + n_up;
+  if (nscr > 0) {
+    ColState<double> src{c->idx[s], (double*)c->x[s], kind == BX_APG ? (double*)c->xprev[s] : nullptr,
+                         (double*)c->lo[s], (double*)c->hi[s], (double*)c->nrm[s], (double*)c->att[s],
+                         c->dense ? nullptr : c->pos[s]};
+    ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->lo[d], (double*)c->hi[d],
+                         (double*)c->nrm[d], (double*)c->att[d], c->act_is_orig ? nullptr : c->pos[d]};
+    k_compact<double><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (double*)c->xfull, c->scr_idx,
+                                                 (double*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo,
+                                                 c->sat_up + c->n_sat_up, c->col_offset, (double*)c->scr_dx,
+                                                 (double*)c->scr_dxp);
+    LAUNCHED();
+    c->cur = d;
+    c->k = n_keep;
+    c->n_sat_lo += n_lo;
+    c->n_sat_up += n_up;
+    c->dense = false;
   }
-  ColState<double> src{c->idx[s], (double*)c->x[s], kind == BX_APG ? (double*)c->xprev[s] : nullptr, (double*)c->lo[s], (double*)c->hi[s],
-                  (double*)c->nrm[s], (double*)c->att[s]};
-  ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->lo[d], (double*)c->hi[d], (double*)c->nrm[d], (double*)c->att[d]};
-  k_compact<double><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (double*)c->xfull, c->scr_idx,
-                                           (double*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo, c->sat_up + c->n_sat_up,
-                                           c->col_offset);
-  LAUNCHED();
-  c->cur = d;
-  c->k = n_keep;
-  c->n_sat_lo += n_lo;
-  c->n_sat_up += n_up;
-  // z += A_S bound_S  (only when some screened bound is nonzero)
+  // z += A_S bound_S  (only when some screened bound is nonzero; collective)
   if (z_update) {
-    View<T> vw{(const T*)c->A, c->lda, c->scr_idx, n_lo + n_up};
+    View<T> vw{(const T*)c->A, c->lda, c->scr_idx, nscr};
     int G = 1;
     TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                     (const double*)c->scr_val, nullptr, 0, &G));
     TRY(run_reduce<T>(c, G, (const double*)c->z, (double*)c->z2, R_PLAIN, nullptr, 0, 0));
     std::swap(c->z, c->z2);
-    k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z, (double*)c->off,
-                                                          (double*)c->tgt);
+    k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z,
+                                                             (double*)c->off, (double*)c->tgt);
     LAUNCHED();
   }
-  // physical rewrite of the preserved columns (solvers.py:57)
-  if (c->k > 0) {
-    int nb = (int)(c->k < 8 * c->nsm ? c->k : 8 * c->nsm);
-    const int e0 = prof_begin(c);
-    k_gather<T><<<nb, RT, 0, c->stream>>>((const T*)c->A, c->lda, c->idx[c->cur], c->k, c->m, (T*)c->Aact,
-                                           c->ldact);
-    LAUNCHED();
-    prof_end(c, e0, BX_PROF_GATHER, 2.0 * (double)c->k * c->m * sizeof(T));
+  TRY(refresh_incremental<T>(c, nscr, kind));
+  // physical rewrite of the preserved columns (solvers.py:57) once half the
+  // physical buffer is dead -- or always for CD, whose kernels read A_act densely
+  if (nscr > 0 && (kind == BX_CD || c->k < c->kphys / 2)) {
+    if (c->k > 0) {
+      int nb = (int)(c->k < 8 * c->nsm ? c->k : 8 * c->nsm);
+      const int e0 = prof_begin(c);
+      k_gather<T><<<nb, RT, 0, c->stream>>>((const T*)c->A, c->lda, c->idx[c->cur], c->k, c->m, (T*)c->Aact,
+                                             c->ldact);
+      LAUNCHED();
+      prof_end(c, e0, BX_PROF_GATHER, 2.0 * (double)c->k * c->m * sizeof(T));
+    }
+    c->act_is_orig = false;
+    c->dense = true;
+    c->kphys = c->k;
   }
-  c->act_is_orig = false;
   c->gram_dirty = true;
-  TRY(refresh_resid<T>(c));
-  if (kind == BX_APG) TRY(refresh_rprev<T>(c));
   c->g_valid = false;
   return BX_OK;
 }
@@ -1057,6 +1082,8 @@ int reset_state(bx_ctx* c, int kind) {
   c->k = c->n;
   c->n_sat_lo = c->n_sat_up = 0;
   c->act_is_orig = true;
+  c->dense = true;
+  c->kphys = c->n;
   c->gram_dirty = true;
   c->g_valid = false;
   c->theta_is_cert = false;

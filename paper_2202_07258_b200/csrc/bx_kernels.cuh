@@ -889,6 +889,7 @@ struct ColState {
   T* hi;
   T* nrm;
   T* att;
+  int32_t* pos;  // physical column in the compacted buffer (src NULL: identity)
 };
 
 template <typename T>
@@ -896,7 +897,7 @@ __global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flag
                                                 int64_t k, ColState<T> src, ColState<T> dst, T* __restrict__ x_full,
                                                 int32_t* __restrict__ scr_idx, T* __restrict__ scr_val, int64_t n_lo_total,
                                                 int64_t* __restrict__ sat_lo, int64_t* __restrict__ sat_up,
-                                                int64_t col_offset) {
+                                                int64_t col_offset, T* __restrict__ scr_dx, T* __restrict__ scr_dxp) {
   __shared__ int32_t woff[RT / 32][3];
   const int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x;
   const int f = (j < k) ? flags[j] : 3;
@@ -924,24 +925,27 @@ __global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flag
   const int32_t id = src.idx[j];
   if (f == 0) {
     dst.idx[pos] = id;
+    if (dst.pos) dst.pos[pos] = src.pos ? src.pos[j] : static_cast<int32_t>(j);
     dst.x[pos] = src.x[j];
     if (src.xprev) dst.xprev[pos] = src.xprev[j];
     dst.lo[pos] = src.lo[j];
     dst.hi[pos] = src.hi[j];
     dst.nrm[pos] = src.nrm[j];
     dst.att[pos] = src.att[j];
-  } else if (f == 1) {
-    const T b = src.lo[j];
-    x_full[id] = b;
-    scr_idx[pos] = id;
-    scr_val[pos] = b;
-    sat_lo[pos] = col_offset + id;
   } else {
-    const T b = src.hi[j];
+    // screened: x snapped to its bound; (b - x) and (b - x_prev) drive the
+    // incremental residual refresh r += A_S (b - x_S)
+    const T b = (f == 1) ? src.lo[j] : src.hi[j];
+    const int64_t q = (f == 1) ? pos : n_lo_total + pos;
     x_full[id] = b;
-    scr_idx[n_lo_total + pos] = id;
-    scr_val[n_lo_total + pos] = b;
-    sat_up[pos] = col_offset + id;
+    scr_idx[q] = id;
+    scr_val[q] = b;
+    scr_dx[q] = sub_rn(b, src.x[j]);
+    scr_dxp[q] = src.xprev ? sub_rn(b, src.xprev[j]) : T(0);
+    if (f == 1)
+      sat_lo[pos] = col_offset + id;
+    else
+      sat_up[pos] = col_offset + id;
   }
 }
 

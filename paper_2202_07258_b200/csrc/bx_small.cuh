@@ -26,6 +26,7 @@ constexpr int SM_CMAX = 48;  // max resident columns per CTA
 struct SmallArgs {
   const void* A;
   int64_t ld;
+  const int32_t* colmap;  // column p at A + colmap[p] * ld (NULL: p)
   int64_t k;
   int m;
   double* x;
@@ -110,8 +111,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     const T* A = static_cast<const T*>(a.A);
     for (int q = tid; q < ncol * nv; q += SM_NT) {
       const int c = q / nv, v = q - c * nv;
+      const int64_t col = a.colmap ? (int64_t)a.colmap[p0 + c] : (p0 + c);
       *reinterpret_cast<VT*>(cols + (size_t)c * a.colstride + v * V) =
-          *reinterpret_cast<const VT*>(A + (p0 + c) * a.ld + v * V);
+          *reinterpret_cast<const VT*>(A + col * a.ld + v * V);
     }
   }
   if (tid < ncol) {
