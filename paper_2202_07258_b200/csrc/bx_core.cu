@@ -40,6 +40,7 @@ namespace {
 
 constexpr size_t kAlign = 256;
 constexpr int kMaxRanks = 256;
+constexpr int kSmallRounds = 1024;  // rounds per device-resident small-round launch
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
@@ -221,6 +222,8 @@ struct bx_ctx {
   bool theta_is_cert = false;
   bool have_apg_state = false;
   unsigned* bar = nullptr;  // grid barrier of the cooperative small-round kernel
+  int* done = nullptr;      // small-round kernel: completed rounds, event flag, residual parity
+  double* dtrace = nullptr; // small-round kernel: per-round trace records [kSmallRounds][8]
   bool dot_done = false;    // the round kernel already produced g and the eps partials
   int dot_G = 0;
   bool small_ok = true;     // cooperative small-round path allowed (env BX_NO_SMALL disables)
@@ -396,6 +399,8 @@ void carve(bx_ctx* c, Carver& w) {
   c->ldp = mp;
   c->part = w.take((size_t)c->Gmax * c->ldp * 8);  // fp64 sized: also the small-round path's partial rows
   c->bar = (unsigned*)w.take(4 * kMaxRanks * 4);
+  c->done = (int*)w.take(64);
+  c->dtrace = (double*)w.take(kSmallRounds * 8 * 8);
   c->bpart = (double*)w.take(c->Gmax * 8 * 4);
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
@@ -816,10 +821,25 @@ int launch_small_R(bx_ctx* c, SmallArgs& a, int G, size_t smem) {
   return BX_OK;
 }
 
-// Returns 1 when the round ran on the small path, 0 when it does not apply.
+struct SmallLoop {
+  int max_rounds = 1;
+  double tol = 0.0;
+  int relative_gap = 0;
+  int screening = 0;
+  double slack_scale = 1e-12;
+  double alpha = 1.0;
+};
+
+// Runs up to lp.max_rounds rounds on the small path.  *ran = 0 when the path
+// does not apply.  With max_rounds > 1 the kernel stops at the first event
+// round; *done = event-free rounds completed (trace records in c->dtrace) and
+// *event = 1 when the following round's passes + dot pass also ran and its
+// dual / screening step is left to the host.
 template <typename T>
-int small_round(bx_ctx* c, int kind, int passes, int* ran) {
+int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran, int* done, int* event) {
   *ran = 0;
+  *done = 0;
+  *event = 0;
   if (!c->small_ok || c->sharded() || (kind != BX_PG && kind != BX_APG) || c->k == 0) return BX_OK;
   constexpr int V = 16 / sizeof(T);
   const int R = (int)((c->m + SM_NT * V - 1) / (SM_NT * V));
@@ -827,6 +847,7 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
   const int G = c->nsm;
   const int ncmax = (int)((c->k + G - 1) / G);
   if (ncmax > SM_CMAX) return BX_OK;
+  if (lp.max_rounds > 1 && (c->m + G - 1) / G > SM_NT) return BX_OK;
   const int colstride = (int)round_up(c->m, 2 * V);
   const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8 + 7 * SM_CMAX + SM_NT) * 8 + 256;
   const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
@@ -855,8 +876,7 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
   a.epart = c->bpart;
   a.sc = c->sc;
   a.bar = c->bar;
-  a.epoch0 = c->bar_epoch;
-  c->bar_epoch += 2u * (unsigned)passes;  // two barriers per step
+  a.epoch0 = 0;
   a.passes = passes;
   a.kind = kind;
   a.g_valid = c->g_valid ? 1 : 0;
@@ -865,6 +885,18 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
   a.rc = 0;
   a.colstride = colstride;
   a.ncmax = ncmax;
+  a.max_rounds = lp.max_rounds < kSmallRounds ? lp.max_rounds : kSmallRounds;
+  a.t = (const double*)c->t;
+  a.tgt = (const double*)c->tgt;
+  a.theta = (double*)c->theta;
+  a.dpart = c->bpart3 + 8 * c->Gmax;
+  a.trace = c->dtrace;
+  a.done = c->done;
+  a.tol = lp.tol;
+  a.relative_gap = lp.relative_gap;
+  a.screening = lp.screening;
+  a.slack_scale = lp.slack_scale;
+  a.alpha = lp.alpha;
   int st = BX_OK;
   switch (R) {
     case 1: st = launch_small_R<T, 1>(c, a, G, smem); break;
@@ -873,11 +905,21 @@ int small_round(bx_ctx* c, int kind, int passes, int* ran) {
     default: st = launch_small_R<T, 4>(c, a, G, smem); break;
   }
   if (st != BX_OK) return st;
-  if (passes & 1) std::swap(c->r, c->rprev);
-  c->dot_done = true;
+  int hd[3] = {0, 0, 0};
+  CU(cudaMemcpyAsync(hd, c->done, sizeof(hd), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (a.max_rounds <= 1) {
+    hd[0] = 0;
+    hd[1] = 1;  // the single round's dual / screening step is the host's
+    hd[2] = passes & 1;
+  }
+  if (hd[2] & 1) std::swap(c->r, c->rprev);
+  c->dot_done = hd[1] != 0;
   c->dot_G = G;
   c->g_valid = true;
   *ran = 1;
+  *done = hd[0];
+  *event = hd[1];
   return BX_OK;
 }
 
@@ -886,8 +928,9 @@ template <typename T>
 int primal_passes(bx_ctx* c, int kind, int passes) {
   const int s = c->cur;
   {
-    int ran = 0;
-    TRY(small_round<T>(c, kind, passes, &ran));
+    int ran = 0, done = 0, ev = 0;
+    SmallLoop lp;
+    TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
     if (ran) return BX_OK;
   }
   for (int p = 0; p < passes; ++p) {
@@ -1206,10 +1249,60 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   bool converged = false;
   double gap_out = INFINITY;
   int64_t ntrace = 0;
+  SmallLoop lp;
+  lp.tol = tol;
+  lp.relative_gap = cfg->relative_gap;
+  lp.screening = cfg->screening;
+  lp.slack_scale = slack_scale;
+  lp.alpha = alpha;
   for (int64_t rnd = 1; rnd <= max_rounds; ++rnd) {
     rounds = rnd;
-    TRY(primal_passes<T>(c, kind, passes));
-    iters += passes;
+    // small problems: device-resident rounds until the next event
+    if (!c->prof) {
+      lp.max_rounds = (int)std::min<int64_t>(max_rounds - rnd + 1, kSmallRounds);
+      int ran = 0, done = 0, ev = 0;
+      if (lp.max_rounds > 1) TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
+      if (ran) {
+        if (done > 0) {
+          std::vector<double> tr(8 * (size_t)done);
+          CU(cudaMemcpyAsync(tr.data(), c->dtrace, tr.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+          CU(cudaStreamSynchronize(c->stream));
+          const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          for (int q = 0; q < done && trace && ntrace < cap; ++q) {
+            bx_trace_rec& t = trace[ntrace++];
+            t.round = rnd + q;
+            t.elapsed = el;
+            t.primal = tr[8 * q + 0];
+            t.dual = tr[8 * q + 1];
+            t.gap = tr[8 * q + 2];
+            t.preserved_count = kg;
+            t.newly_screened_lower = t.newly_screened_upper = 0;
+            t.eps = tr[8 * q + 3];
+            t.radius = tr[8 * q + 4];
+            t.step = eta;
+            t.certified_gap = NAN;
+            t.momentum = tr[8 * q + 5];
+            t.restarts = (int64_t)tr[8 * q + 6];
+          }
+          gap_out = tr[8 * (done - 1) + 2];
+          iters += (int64_t)done * passes;
+          rnd += done;
+          rounds = rnd - 1;
+        }
+        if (!ev) {
+          --rnd;  // the for loop's ++rnd resumes at the next undone round
+          continue;
+        }
+        rounds = rnd;
+        iters += passes;  // the event round's passes + dot pass ran on the device
+      } else {
+        TRY(primal_passes<T>(c, kind, passes));
+        iters += passes;
+      }
+    } else {
+      TRY(primal_passes<T>(c, kind, passes));
+      iters += passes;
+    }
     TRY(dual_screen<T>(c, cfg->screening, slack_scale, alpha));
     TRY(sync_scalars<T>(c));
     TRY(check_dev_err(c));

@@ -53,6 +53,22 @@ struct SmallArgs {
   int rc;          // r[rc] holds the current residual
   int colstride;   // smem elements per column
   int ncmax;       // resident columns per CTA (smem sized for it)
+  // device-resident round loop (max_rounds > 1): after each round the kernel
+  // evaluates the dual point, the gap, the stop test and the sphere test
+  // itself, and returns to the host only at an event (something screened, a
+  // convergence candidate, an error) or after max_rounds.
+  int max_rounds;
+  const double* t;    // translation vector (rows)
+  const double* tgt;  // y - z (rows)
+  double* theta;      // dual point (rows)
+  double* dpart;      // [G][8] dual / count partials
+  double* trace;      // [max_rounds][8] per completed round
+  int* done;          // [2]: completed event-free rounds, event flag
+  double tol;
+  int relative_gap;
+  int screening;
+  double slack_scale;
+  double alpha;
 };
 
 // Grid barrier: a counter + generation word (sense reversal); all CTAs are
@@ -177,6 +193,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     __syncthreads();
   };
 
+  int done_rounds = 0, event = 0;
+  bool perr = false;
+  for (int rnd = 0; rnd < a.max_rounds; ++rnd) {
   for (int pass = 0; pass < a.passes; ++pass) {
     const double* rcur = a.r[rc];
     const double* rprv = a.r[rc ^ 1];
@@ -328,6 +347,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       t_mom = restart ? 1.0 : tn;
     } else {
       if (Pn > P + 1e-9 + a.sc->rise_rel * fabs(P)) {
+        perr = true;
         if (b == 0 && tid == 0) {
           if (a.sc->err == 0) {
             a.sc->err_v1 = P;
@@ -345,6 +365,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     __syncthreads();
   }
   // screening dot pass at the final x: g = A'r and the epsilon partial
+  double ep = 0.0;
   if (a.do_dot) {
     double vr[R][V];
 #pragma unroll
@@ -354,7 +375,6 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? __ldcg(&a.r[rc][row + e]) : 0.0;
     }
     dots(vr, gcol);
-    double ep = 0.0;
     if (tid < ncol) {
       const double gj = gcol[tid];
       cg[tid] = gj;
@@ -371,6 +391,121 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.epart[b] = e;
     }
   }
+  if (a.max_rounds <= 1) break;
+  if (perr) {
+    event = 1;
+    break;
+  }
+  // ---- device dual point (driver.py:423-441), gap, stop and sphere tests ----
+  grid_barrier(a.bar, 0);
+  if (warp == 0) {
+    double e = 0.0;
+    for (int q = lane; q < G; q += 32) e = fmax(e, __ldcg(&a.epart[q]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) sc4[2] = e;
+  }
+  __syncthreads();
+  const double eps = a.has_inf ? sc4[2] : 0.0;
+  {
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+    for (int i = r_lo + tid; i < r_hi; i += SM_NT) {
+      double th = -__ldcg(&a.r[rc][i]);
+      if (eps > 0.0) th = add_rn(th, mul_rn(eps, a.t[i]));
+      a.theta[i] = th;
+      s1 += th * a.tgt[i];
+      s2 += th * th;
+    }
+    if (tid < ncol) {
+      double vj = -cg[tid];
+      if (a.has_inf) vj = add_rn(vj, mul_rn(eps, cat[tid]));
+      gcol[tid] = vj;  // v for the sphere test
+      s3 = clo[tid] * fmin(vj, 0.0);
+      if (!isinf(chi[tid])) s4 = chi[tid] * fmax(vj, 0.0);
+    }
+    s1 = warp_sum<double>(s1);
+    s2 = warp_sum<double>(s2);
+    s3 = warp_sum<double>(s3);
+    s4 = warp_sum<double>(s4);
+    if (lane == 0) {
+      rsx[4 * warp + 0] = s1;
+      rsx[4 * warp + 1] = s2;
+      rsx[4 * warp + 2] = s3;
+      rsx[4 * warp + 3] = s4;
+    }
+    __syncthreads();
+    if (tid < 4) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w) acc += rsx[4 * w + tid];
+      a.dpart[8 * b + tid] = acc;
+    }
+  }
+  grid_barrier(a.bar, 0);
+  if (warp == 0) {
+    double t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0;
+    for (int q = lane; q < G; q += 32) {
+      t1 += __ldcg(&a.dpart[8 * q + 0]);
+      t2 += __ldcg(&a.dpart[8 * q + 1]);
+      t3 += __ldcg(&a.dpart[8 * q + 2]);
+      t4 += __ldcg(&a.dpart[8 * q + 3]);
+    }
+    t1 = warp_sum<double>(t1);
+    t2 = warp_sum<double>(t2);
+    t3 = warp_sum<double>(t3);
+    t4 = warp_sum<double>(t4);
+    if (lane == 0) {
+      double dual = t1 - 0.5 * t2;
+      dual -= t3;
+      dual -= t4;
+      sc4[3] = dual;
+      sc4[4] = t2;
+    }
+  }
+  __syncthreads();
+  const double dual = sc4[3];
+  const double raw = P - dual;
+  const double gap = fmax(raw, 0.0);
+  const double radius = sqrt(2.0 * gap / a.alpha);
+  const double thr = radius + a.slack_scale * fmax(1.0, sqrt(sc4[4]));
+  const double tol_r = a.relative_gap ? a.tol * fmax(1.0, fabs(P)) : a.tol;
+  // events the host must handle: weak-duality violation, a convergence
+  // candidate (certified gap), anything screened
+  bool ev = (raw < -1e-9) || (gap < tol_r);
+  int nscr = 0;
+  if (a.screening && tid < ncol) {
+    const double vj = gcol[tid];
+    const double tj = thr * cnr[tid];
+    nscr = (vj < -tj) || (vj > tj && !isinf(chi[tid]));
+  }
+  nscr = __syncthreads_count(nscr);
+  if (tid == 0) a.dpart[8 * b + 4] = (double)nscr;
+  grid_barrier(a.bar, 0);
+  if (warp == 0) {
+    double c = 0.0;
+    for (int q = lane; q < G; q += 32) c += __ldcg(&a.dpart[8 * q + 4]);
+    c = warp_sum<double>(c);
+    if (lane == 0) sc4[5] = c;
+  }
+  __syncthreads();
+  ev = ev || (sc4[5] > 0.0);
+  if (ev) {
+    event = 1;
+    break;
+  }
+  if (b == 0 && tid == 0) {
+    double* tr = a.trace + 8 * rnd;
+    tr[0] = P;
+    tr[1] = dual;
+    tr[2] = gap;
+    tr[3] = eps;
+    tr[4] = radius;
+    tr[5] = t_mom;
+    tr[6] = (double)a.sc->restarts;
+  }
+  ++done_rounds;
+  gv = (a.kind == 0) ? 1 : 0;  // PG: the next round starts from this round's gradient
+  __syncthreads();
+  }  // rounds
   // write back the resident per-column state
   if (tid < ncol) {
     const int64_t p = p0 + tid;
@@ -381,6 +516,11 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   if (b == 0 && tid == 0) {
     a.sc->P = P;
     a.sc->mom_t = t_mom;
+    if (a.done) {
+      a.done[0] = done_rounds;
+      a.done[1] = event;
+      a.done[2] = rc;
+    }
   }
 }
 
