@@ -229,6 +229,7 @@ struct bx_ctx {
   bool small_ok = true;     // cooperative small-round path allowed (env BX_NO_SMALL disables)
   unsigned bar_epoch = 0;   // grid-barrier epochs issued so far
   int64_t launches = 0;
+  int last_Gw = 0;  // block count of the last pass's scalar partials (bpart)
   std::string err;
 
   // live per-kernel timing (CUDA events on the context stream)
@@ -454,6 +455,13 @@ int launch_pass_R(bx_ctx* c, const PassArgs<T>& a, bool dot, bool axpy, int G, s
   return launch_pass_RDX<T, R, false, true>(c, a, G, smem);
 }
 
+int grid1d(bx_ctx* c, int64_t n) {
+  int64_t b = (n + RT - 1) / RT;
+  if (b > 4 * c->nsm) b = 4 * c->nsm;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
 // A "view" of columns the pass streams
 template <typename T>
 struct View {
@@ -485,15 +493,28 @@ int pass_grid(bx_ctx* c, int64_t k) {
 
 // Launch one streamed pass.  Returns the grid used through *G_out.
 template <typename T>
+int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
+                     double* xprev, const double* lo, const double* hi, double* g, const double* att,
+                     const double* coef, double* bpart, int has_inf, int* G_out, const double* nrm);
+
+// One streamed pass over the columns of `vw`, rows [row0, row0 + mrows) (the
+// whole column by default).  accumulate >= 0 turns a U_DOT pass into a
+// row-block partial dot (0: first block, 1: add).
+template <typename T>
 int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
              double* xprev, const double* lo, const double* hi, double* g, const double* att, const double* coef,
-             double* bpart, int has_inf, int* G_out, const double* nrm = nullptr) {
-  const int R = pick_R(c->m, sizeof(T));
-  if (R < 0) return fail(c, BX_ERR_UNSUPPORTED, "m=%lld exceeds the fused-pass envelope", (long long)c->m);
+             double* bpart, int has_inf, int* G_out, const double* nrm = nullptr, int64_t row0 = 0,
+             int64_t mrows = -1, int accumulate = -1) {
+  const int64_t mm = mrows < 0 ? c->m : mrows;
+  const int R = pick_R(mm, sizeof(T));
+  if (R < 0 && mrows < 0)
+    return run_pass_blocked<T>(c, vw, upd, vin, vin_prev, x, xprev, lo, hi, g, att, coef, bpart, has_inf, G_out,
+                               nrm);
+  if (R < 0) return fail(c, BX_ERR_UNSUPPORTED, "row block of %lld rows", (long long)mm);
   const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
   const bool axpy = (upd != U_DOT);
   const int C = cols_per_slot(R);
-  const uint32_t colbytes = (uint32_t)align_up((size_t)c->m * sizeof(T), 16);
+  const uint32_t colbytes = (uint32_t)align_up((size_t)mm * sizeof(T), 16);
   const uint32_t colstride = (uint32_t)align_up(colbytes, 128);
   const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 3 * CMAX) * 8 + 64;
   const size_t slot = (size_t)C * colstride;
@@ -515,13 +536,15 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   }
   const size_t smem = S * slot + scratch + (pre ? stage : 0);
   PassArgs<T> a;
-  a.A = vw.A;
+  a.A = vw.A + row0;
   a.ld = vw.ld;
   a.colmap = vw.colmap;
   a.k = vw.k;
-  a.m = c->m;
-  a.vin = vin;
-  a.vin_prev = vin_prev;
+  a.m = mm;
+  a.vin = vin ? vin + row0 : nullptr;
+  a.vin_prev = vin_prev ? vin_prev + row0 : nullptr;
+  a.accumulate = accumulate;
+  a.extrap = (upd == U_DOT && accumulate >= 0 && vin_prev != nullptr) ? 1 : 0;
   a.x = x;
   a.xprev = xprev;
   a.lo = lo;
@@ -530,7 +553,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   a.att = att;
   a.nrm = nrm;
   a.coef = coef;
-  a.part = (T*)c->part;
+  a.part = (T*)c->part + row0;
   a.ldp = c->ldp;
   a.bpart = bpart;
   a.sc = c->sc;
@@ -542,6 +565,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   a.colstride = colstride;
   a.pre = pre;
   if (G_out) *G_out = G;
+  c->last_Gw = G;
   const int e0 = prof_begin(c);
   int st = BX_OK;
   switch (R) {
@@ -565,6 +589,52 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
     prof_end(c, e0, BX_PROF_PASS_DOT + upd, bytes);
   }
   return st;
+}
+
+// Row-blocked step for m beyond the register-resident envelope: the dot is
+// accumulated over row blocks, the per-column update runs once the full dot is
+// known (k_colupdate), then A x' is formed block by block into the same
+// partial-row buffer.  Two reads of A per step instead of one.
+template <typename T>
+int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
+                     double* xprev, const double* lo, const double* hi, double* g, const double* att,
+                     const double* coef, double* bpart, int has_inf, int* G_out, const double* nrm) {
+  constexpr int64_t BR = (int64_t)NT * (16 / sizeof(T)) * 8;  // rows per block (R = 8)
+  const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
+  const bool axpy = (upd != U_DOT);
+  double* gg = g ? g : (double*)c->g;
+  int G = 1;
+  if (dot) {
+    for (int64_t r0 = 0, q = 0; r0 < c->m; r0 += BR, ++q) {
+      const int64_t mr = std::min(BR, c->m - r0);
+      TRY(run_pass<T>(c, vw, U_DOT, vin, (upd == U_APG) ? vin_prev : nullptr, nullptr, nullptr, nullptr, hi, gg,
+                      att, nullptr, nullptr, 0, &G, nullptr, r0, mr, q ? 1 : 0));
+    }
+  }
+  const double* cf = coef ? coef : x;  // U_AX without coefficients multiplies by x
+  int gw = G;
+  if (upd != U_AX) {
+    const int nb = grid1d(c, vw.k);
+    k_colupdate<<<nb, RT, 0, c->stream>>>(upd, vw.k, x, xprev, lo, hi, gg, att, nrm, (double*)c->coef, bpart,
+                                          has_inf, c->sc);
+    LAUNCHED();
+    if (upd == U_DOT) {
+      if (G_out) *G_out = nb;
+      return BX_OK;
+    }
+    cf = (const double*)c->coef;
+    gw = nb;
+  }
+  if (axpy) {
+    for (int64_t r0 = 0; r0 < c->m; r0 += BR) {
+      const int64_t mr = std::min(BR, c->m - r0);
+      TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, cf,
+                      nullptr, 0, &G, nullptr, r0, mr, -1));
+    }
+  }
+  if (G_out) *G_out = G;
+  c->last_Gw = gw;  // the reduce reads the k_colupdate block partials
+  return BX_OK;
 }
 
 template <typename T>
@@ -601,12 +671,6 @@ int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const
   return BX_OK;
 }
 
-int grid1d(bx_ctx* c, int64_t n) {
-  int64_t b = (n + RT - 1) / RT;
-  if (b > 4 * c->nsm) b = 4 * c->nsm;
-  if (b < 1) b = 1;
-  return (int)b;
-}
 
 // ---------------------------------------------------------------------------
 // building blocks of a round
@@ -672,7 +736,7 @@ int power_iter(bx_ctx* c, int iters, const double* v0_host, double* sigma, int64
   for (int it = 0; it < iters; ++it) {
     TRY(run_pass<T>(c, act_view<T>(c), U_POWER, (const double*)c->u, nullptr, nullptr, nullptr, nullptr, nullptr,
                     (double*)c->g, nullptr, nullptr, c->bpart, 0, &G));
-    TRY(run_reduce<T>(c, G, nullptr, (double*)c->u, R_POWER, c->bpart, G, 1));
+    TRY(run_reduce<T>(c, G, nullptr, (double*)c->u, R_POWER, c->bpart, c->last_Gw, 1));
   }
   TRY(sync_scalars<T>(c));
   if (c->hsc->err == DE_POWER_ZERO) {
@@ -950,7 +1014,7 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
                       (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, c->bpart, 0, &G,
                       (const double*)c->nrm[s]));
       // r_prev <- r, r <- new residual: write into the r_prev buffer, swap
-      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->rprev, R_APG, c->bpart, G, 2));
+      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->rprev, R_APG, c->bpart, c->last_Gw, 2));
       std::swap(c->r, c->rprev);
     } else {
       return cd_sweeps<T>(c, passes);  // all sweeps in one launch
@@ -1413,8 +1477,6 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   if (lda < m) return fail(c, BX_ERR_DIMENSION, "lda < m");
   if (((uintptr_t)a % 16) || ((lda * (int64_t)c->esz) % 16))
     return fail(c, BX_ERR_INVALID_ARGUMENT, "A base and column stride must be 16-byte aligned");
-  if (pick_R(m, c->esz) < 0)
-    return fail(c, BX_ERR_UNSUPPORTED, "m=%lld rows exceeds the fused-pass envelope", (long long)m);
   c->A = a;
   c->lda = lda;
   c->stream = (cudaStream_t)cuda_stream;
@@ -1648,6 +1710,7 @@ struct bx_batch {
   double* red = nullptr;   // [4] round summary
   double* hred = nullptr;  // pinned mirror
   int64_t launches = 0;
+  int blocked_Gw = 0;  // row-blocked path: block count of the last k_colupdate partials
   std::string err;
   int nsm = 148;
   size_t smem = 0;

@@ -111,6 +111,8 @@ struct PassArgs {
   uint32_t colbytes;       // bytes moved per column (multiple of 16)
   uint32_t colstride;      // smem bytes per column in a slot
   int pre;                 // >= columns per CTA: the CTA's per-column state is staged in smem (0: off)
+  int accumulate;          // U_DOT over a row block: g[p] = (accumulate ? g[p] : 0) + block dot, no epsilon
+  int extrap;              // dot with the FISTA extrapolated residual r + beta (r - r_prev)
 };
 
 // ----------------------------------------------------------------------------
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   double beta = 0.0;
   const double eta = a.sc->eta;
   if (DOT) {
-    if (a.upd == U_APG) {
+    if (a.upd == U_APG || a.extrap) {
       const double t = a.sc->mom_t;
       const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
       beta = (t - 1.0) / tn;
@@ -378,6 +380,10 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         double coef = 0.0;
         switch (a.upd) {
           case U_DOT: {
+            if (a.accumulate >= 0) {  // row-blocked path: partial dot of this row block
+              a.g[p] = a.accumulate ? add_rn(a.g[p], gj) : gj;
+              break;
+            }
             a.g[p] = gj;
             const double hj = staged ? s0[ql] : a.hi[p];
             if (a.has_inf && isinf(hj)) {
@@ -1050,6 +1056,84 @@ __global__ void k_bounds_probe(int64_t n, const T* __restrict__ lo, const T* __r
     if (isnan(l) || isnan(u)) f |= 32;
   }
   if (f) atomicOr(out, f);
+}
+
+// Row-blocked path (m beyond the register-resident envelope): after the dot
+// has been accumulated over all row blocks, the per-column update of the mode
+// (the same arithmetic as k_pass's epilogue) and its block scalar partials.
+// Writes coef (the axpy coefficients of the following A x blocks).
+__global__ void __launch_bounds__(RT) k_colupdate(int upd, int64_t k, double* __restrict__ x, double* __restrict__ xprev,
+                                                  const double* __restrict__ lo, const double* __restrict__ hi,
+                                                  const double* __restrict__ g, const double* __restrict__ att,
+                                                  const double* __restrict__ nrm, double* __restrict__ coef,
+                                                  double* __restrict__ bpart, int has_inf, const DevScalars* sc) {
+  __shared__ double sh[RT / 32][2];
+  const double eta = sc->eta;
+  double beta = 0.0;
+  if (upd == U_APG) {
+    const double t = sc->mom_t;
+    const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    beta = (t - 1.0) / tn;
+  }
+  double r1 = 0.0, r2 = 0.0;
+  for (int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x; p < k; p += (int64_t)gridDim.x * RT) {
+    const double gj = g[p];
+    switch (upd) {
+      case U_DOT:
+        if (has_inf && isinf(hi[p])) r1 = fmax(r1, fmax(-gj, 0.0) / fabs(att[p]));
+        break;
+      case U_PG:
+      case U_PG_G: {
+        const double xn = clip<double>(sub_rn(x[p], mul_rn(eta, gj)), lo[p], hi[p]);
+        x[p] = xn;
+        coef[p] = xn;
+      } break;
+      case U_APG: {
+        const double xo = x[p], xp = xprev[p];
+        double yv = xo;
+        if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
+        const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), lo[p], hi[p]);
+        xprev[p] = xo;
+        x[p] = xn;
+        coef[p] = xn;
+        const double dx = xn - xo;
+        r1 += gj * dx;
+        r2 += nrm[p] * fabs(dx);
+      } break;
+      case U_POWER:
+        coef[p] = gj;
+        r1 += gj * gj;
+        break;
+      default:
+        break;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (upd == U_DOT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r1 = fmax(r1, __shfl_xor_sync(0xffffffffu, r1, o));
+  } else {
+    r1 = warp_sum<double>(r1);
+    r2 = warp_sum<double>(r2);
+  }
+  if (lane == 0) {
+    sh[warp][0] = r1;
+    sh[warp][1] = r2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bpart) {
+    double v1 = sh[0][0], v2 = sh[0][1];
+    for (int w = 1; w < RT / 32; ++w) {
+      v1 = (upd == U_DOT) ? fmax(v1, sh[w][0]) : v1 + sh[w][0];
+      v2 += sh[w][1];
+    }
+    if (upd == U_APG) {
+      bpart[2 * blockIdx.x] = v1;
+      bpart[2 * blockIdx.x + 1] = v2;
+    } else {
+      bpart[blockIdx.x] = v1;
+    }
+  }
 }
 
 // column-sharded helpers -----------------------------------------------------

@@ -95,3 +95,15 @@ def test_baseline_recipe_prefix(cfg_id, m, n, rounds, path):
                        tol=inst.gap_tol, max_rounds=rounds)
     probs = compare_traces(g, o)
     assert not probs, probs[:3]
+
+
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+def test_tall_matrix_row_blocked_path(kind):
+    """m = 13000 fp64 rows is beyond the register-resident fused pass: the
+    row-blocked path (dot over row blocks, column update, A x blocks) must
+    follow the oracle round by round."""
+    from paper_2202_07258_b200.generate import make_config
+    inst = make_config(3, m=13000, n=600)
+    g, o = _solve_both(inst.a, inst.y, inst.lower, inst.upper, kind, passes=10, tol=1e-6, max_rounds=40)
+    probs = compare_traces(g, o)
+    assert not probs, probs[:3]
