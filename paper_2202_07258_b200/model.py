@@ -41,6 +41,18 @@ class QuadraticLoss:
     conjugate = staticmethod(conj_loss)
 
 
+def _readonly_view(arr):
+    """Zero-copy torch view of a (read-only, like the reference's Problem
+    arrays, model.py:85-87) C-contiguous numpy array; it is only ever read."""
+    import warnings
+
+    import torch
+    arr = np.ascontiguousarray(arr)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(arr)
+
+
 def _is_torch(x):
     try:
         import torch
@@ -162,7 +174,7 @@ class Problem:
         """Keep page-locked host copies so uploads run at full PCIe speed."""
         import torch
         if self._pinned is None and self.a_matrix is not None:
-            at = torch.from_numpy(np.array(self.a_matrix.T, order="C"))  # (n, m) == column-major A
+            at = _readonly_view(self.a_matrix.T)  # (n, m) == column-major A
             self._pinned = dict(a=at.pin_memory(), y=torch.from_numpy(self.y.copy()).pin_memory(),
                                 lo=torch.from_numpy(self.lower.copy()).pin_memory(),
                                 hi=torch.from_numpy(self.upper.copy()).pin_memory())
@@ -178,9 +190,8 @@ class Problem:
         if self._pinned is not None:
             src = self._pinned
         else:
-            src = dict(a=torch.from_numpy(np.array(self.a_matrix.T, order="C")),
-                       y=torch.from_numpy(self.y.copy()), lo=torch.from_numpy(self.lower.copy()),
-                       hi=torch.from_numpy(self.upper.copy()))
+            src = dict(a=_readonly_view(self.a_matrix.T), y=torch.from_numpy(self.y.copy()),
+                       lo=torch.from_numpy(self.lower.copy()), hi=torch.from_numpy(self.upper.copy()))
         nb = self._pinned is not None
         at = src["a"].to(device, non_blocking=nb)
         a_dev = self._device_layout(at.t()) if at.shape[1] % (16 // at.element_size()) else at
