@@ -16,6 +16,10 @@ the hot path named by ``BASELINE.json:north_star``:
 * power-iteration step rule      -- solvers.py:72-98
 * dual translation / scaling, reduced dual, gap clamp, certified gap
                                  -- driver.py:183-209, 112-128; duality.py:103-209
+* bounded-variable active set (Lawson-Hanson) ``active-set``
+                                 -- solvers.py:140-204 (+ ActiveSetState, :38-45;
+                                    x0 = l and 10 n rounds, driver.py:144-147;
+                                    KKT-optimal exit, driver.py:246-252)
 * gap-safe sphere test + slack   -- screening.py:11-15, 46-69; driver.py:214-221
 * screening application / compaction / step re-estimate
                                  -- screening.py:72-94; driver.py:222-235
@@ -40,6 +44,7 @@ test_solvers.py:205, screened coordinates saturated in that optimum).
 import math
 
 import numpy as np
+import scipy.linalg as sla
 
 GAP_ROUNDOFF = 1e-9          # duality.py:322 (weak-duality round-off slack)
 SLACK_SCALE = 1e-12          # driver.py:219
@@ -236,6 +241,61 @@ def apg_passes(w, eta, passes, mom):
     w.g = w.mat.T @ w.r
 
 
+def _passive_lstsq(mat, rhs, cols):
+    """Least squares on the passive columns through the Cholesky factor of
+    their Gram matrix (solvers.py:140-148; the same LAPACK calls, so the
+    restatement reproduces the reference bit for bit)."""
+    sub = mat[:, cols]
+    try:
+        fac = sla.cho_factor(sub.T @ sub)
+    except sla.LinAlgError:
+        raise OracleError("SingularSubproblem", "passive-column least-squares system is singular")
+    return sla.cho_solve(fac, sub.T @ rhs)
+
+
+def active_set_pass(w, passive):
+    """One outer bounded-variable Lawson-Hanson iteration (solvers.py:151-204).
+
+    ``passive`` (bool over the view's columns) is updated in place.  Returns
+    True when no bound coordinate violates the optimality conditions.
+    """
+    x, lo, hi = w.x, w.lo, w.hi
+    neg_g = -w.g
+    tol = 1e-10 * w.nrm * max(float(np.linalg.norm(w.r)), 1.0)
+    bound = ~passive
+    pull_up = bound & (x <= lo) & (neg_g > tol)
+    pull_dn = bound & ~np.isinf(hi) & (x >= hi) & (neg_g < -tol)
+    score = np.maximum(np.where(pull_up, neg_g, 0.0), np.where(pull_dn, -neg_g, 0.0))
+    if not score.any():
+        return True
+    passive[int(np.argmax(score))] = True
+    for _ in range(2 * x.size + 2):
+        free = np.flatnonzero(passive)
+        fixed = ~passive
+        rhs = w.tgt - w.mat[:, fixed] @ x[fixed] if fixed.any() else w.tgt
+        s = _passive_lstsq(w.mat, rhs, free)
+        lo_f, hi_f = lo[free], hi[free]
+        low, high = s < lo_f, s > hi_f
+        if not (low.any() or high.any()):
+            x[free] = s
+            break
+        cur = x[free]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            frac = np.where(low, (lo_f - cur) / (s - cur),
+                            np.where(high, (hi_f - cur) / (s - cur), np.inf))
+        step = min(max(float(np.min(frac)), 0.0), 1.0)
+        x[free] = cur + step * (s - cur)
+        hit = frac <= step + 1e-12
+        x[free[hit & low]] = lo_f[hit & low]
+        x[free[hit & high]] = hi_f[hit & high]
+        passive[free[hit]] = False
+    else:
+        raise OracleError("SingularSubproblem", "active-set inner loop failed to make progress")
+    w.r = w.mat @ x + w.off
+    w.g = w.mat.T @ w.r
+    return False
+
+
 # --------------------------------------------------------------------------
 # Algorithm 1 (driver.py:131-256)
 # --------------------------------------------------------------------------
@@ -266,10 +326,16 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
         att_full = translation_att(a, t, norms)
     if np.any(norms == 0.0):
         raise OracleError("ZeroColumn", f"zero column at {int(np.argmin(norms))}")
-    if kind not in ("pg", "cd", "apg"):
+    if kind not in ("pg", "cd", "apg", "active-set"):
         raise ValueError(kind)
-    x_full = np.clip(np.zeros(n), lo, hi)
-    limit = max_rounds or 10 ** 6
+    if kind == "active-set":
+        # coordinates start on a bound (driver.py:144-147)
+        x_full = lo.copy()
+        limit = max_rounds or 10 * n
+        passive_full = np.zeros(n, dtype=bool)
+    else:
+        x_full = np.clip(np.zeros(n), lo, hi)
+        limit = max_rounds or 10 ** 6
     keep = np.arange(n)
     sat_lo = np.empty(0, dtype=int)
     sat_up = np.empty(0, dtype=int)
@@ -287,12 +353,17 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
     rounds = 0
     for rnd in range(1, limit + 1):
         rounds = rnd
+        optimal = False
         if kind == "pg":
             pg_passes(w, eta, inner_passes)
         elif kind == "apg":
             apg_passes(w, eta, inner_passes, mom)
-        else:
+        elif kind == "cd":
             cd_passes(w, inner_passes)
+        else:
+            passive = passive_full[w.idx]
+            optimal = active_set_pass(w, passive)
+            passive_full[w.idx] = passive
 
         # dual point on the reduced problem (driver.py:183-201)
         theta = -w.r
@@ -344,6 +415,8 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
                 sat_up = np.concatenate([sat_up, new_up])
                 gone = np.concatenate([new_lo, new_up])
                 keep = keep[~np.isin(keep, gone)]
+                if kind == "active-set":
+                    passive_full[gone] = False   # ActiveSetState.drop_screened
                 old = w
                 w = ActiveView(a, y, lo, hi, norms, z, x_full, keep)
                 if kind == "apg" and old.x_prev is not None:
@@ -364,6 +437,14 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
         if round_hook is not None:
             round_hook(rnd, w, rec)
         if converged:
+            break
+        if optimal:
+            # KKT-optimal active set: decided by the certified gap alone
+            # (driver.py:246-252)
+            w.write_back(x_full)
+            cert, th_c, _, _ = certified_gap(a, y, lo, hi, inf_mask, x_full, t, att_full)
+            theta_out, gap_out = th_c, cert
+            converged = cert < gap_tol
             break
     w.write_back(x_full)
     return dict(x=x_full.copy(), theta=np.asarray(theta_out).copy(), gap=gap_out,

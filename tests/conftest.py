@@ -39,6 +39,18 @@ def small_instance(rng, m, n, family):
     return np.asfortranarray(a), y, lo, hi
 
 
+def medium_nnls(seed=4242, m=300, n=600, nnz=30):
+    """Seeded screened-NNLS instance with a few hundred passive columns at the
+    active-set optimum (regenerated instead of stored in the fixtures)."""
+    rng = np.random.default_rng(seed)
+    a = rng.random((m, n))
+    a /= np.linalg.norm(a, axis=0)
+    x0 = np.zeros(n)
+    x0[rng.permutation(n)[:nnz]] = np.abs(rng.standard_normal(nnz))
+    y = a @ x0 + 0.01 * rng.standard_normal(m)
+    return np.asfortranarray(a), y, np.zeros(n), np.full(n, np.inf)
+
+
 def gpu_available():
     try:
         import torch

@@ -16,6 +16,12 @@ Fixtures
   kat_cases.npz       known-answer cases from the reference test-suite shapes
   optimum_cases.npz   high-accuracy optima (active set, certified gap 1e-12)
                       for solution-level pinning of the FISTA extension
+  active_cases.npz    the active-set (bounded Lawson-Hanson) solver: 18 small
+                      instances (nnls/bvls/mixed x 3 seeds x screening on/off),
+                      the reference suite's two KATs (test_solvers.py:144-159)
+                      and a 300 x 600 screened NNLS instance
+  cfg1_as_trace.npz   BASELINE config 1's instance solved by the active-set
+                      kind (gap 1e-6): the reference's whole trajectory
   cfg1_trace.npz      BASELINE config 1 at full size (1000 x 2000, PG, 10
                       passes/round, gap 1e-6): the reference's whole trajectory
   cfg2_trace.npz      BASELINE config 2 at full size (2000 x 4000, CD, gap 1e-7)
@@ -37,7 +43,7 @@ sys.path.insert(0, REF)
 
 import boxscreen as bs  # noqa: E402  (the reference)
 
-from conftest import small_instance  # noqa: E402
+from conftest import medium_nnls, small_instance  # noqa: E402
 from paper_2202_07258_b200.generate import make_config  # noqa: E402
 
 
@@ -148,12 +154,61 @@ def optimum_cases():
     print("optimum_cases:", len(names))
 
 
-def full_config(cfg_id, fname):
+def _store_case(out, key, meta, a, y, lo, hi, res):
+    out[key + "_meta"] = np.array(meta)
+    out[key + "_a"] = np.asarray(a, float)
+    out[key + "_y"] = np.asarray(y, float)
+    out[key + "_lo"] = lo
+    out[key + "_hi"] = hi
+    for k, v in trace_arrays(res).items():
+        out[f"{key}_tr_{k}"] = v
+    out[key + "_x"] = res.x
+    out[key + "_theta"] = res.theta
+    out[key + "_final"] = np.array([res.gap, res.rounds, float(res.converged)])
+    out[key + "_sat_lower"] = np.asarray(res.sat_lower, np.int64)
+    out[key + "_sat_upper"] = np.asarray(res.sat_upper, np.int64)
+
+
+def active_cases():
+    out = {}
+    i = 0
+    for family in ("nnls", "bvls", "mixed"):
+        for seed in range(3):
+            rng = np.random.default_rng(3000 + 31 * seed + len(family))
+            n = int(rng.integers(3, 41))
+            m = int(rng.integers(n, 81))
+            a, y, lo, hi = small_instance(rng, m, n, family)
+            for screening in (True, False):
+                res = bs.solve(bs.Problem(a, y, lo, hi), bs.SolverConfig(kind="active-set", gap_tol=1e-8),
+                               screening=screening)
+                _store_case(out, f"c{i:03d}", [family, "active-set", str(int(screening))], a, y, lo, hi, res)
+                i += 1
+    # test_solvers.py:144-159 shapes
+    for a, y in ((np.eye(2), [1.0, -1.0]), (np.eye(2), [-1.0, -2.0])):
+        lo, hi = np.zeros(2), np.full(2, np.inf)
+        res = bs.solve(bs.Problem(a, y, 0.0, np.inf), bs.SolverConfig(kind="active-set"), screening=False)
+        _store_case(out, f"c{i:03d}", ["kat", "active-set", "0"], a, y, lo, hi, res)
+        i += 1
+    # a screened NNLS instance with a few hundred passive columns
+    # (the matrix is regenerated from its seed by tests/conftest.py:medium_nnls)
+    a, y, lo, hi = medium_nnls()
+    res = bs.solve(bs.Problem(a, y, lo, hi), bs.SolverConfig(kind="active-set", gap_tol=1e-8), screening=True)
+    key = f"c{i:03d}"
+    _store_case(out, key, ["medium", "active-set", "1"], a, y, lo, hi, res)
+    out[key + "_a"] = np.zeros((0, 0))
+    out[key + "_digest"] = np.array(digest(a, y))
+    i += 1
+    out["count"] = np.array(i)
+    np.savez_compressed(os.path.join(HERE, "active_cases.npz"), **out)
+    print("active_cases:", i)
+
+
+def full_config(cfg_id, fname, kind=None, gap_tol=None):
     inst = make_config(cfg_id)
     p = bs.Problem(inst.a, inst.y, inst.lower, inst.upper)
     t0 = time.time()
-    res = bs.solve(p, bs.SolverConfig(kind=inst.kind, inner_passes=inst.inner_passes, gap_tol=inst.gap_tol),
-                   screening=True)
+    res = bs.solve(p, bs.SolverConfig(kind=kind or inst.kind, inner_passes=inst.inner_passes,
+                                      gap_tol=gap_tol or inst.gap_tol), screening=True)
     el = time.time() - t0
     out = {f"tr_{k}": v for k, v in trace_arrays(res).items()}
     out.update(x=res.x, theta=res.theta, final=np.array([res.gap, res.rounds, float(res.converged)]),
@@ -165,13 +220,17 @@ def full_config(cfg_id, fname):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "kat", "optimum", "cfg2", "cfg1"]
+    which = sys.argv[1:] or ["small", "kat", "optimum", "active", "cfg1as", "cfg2", "cfg1"]
     if "small" in which:
         small_cases()
     if "kat" in which:
         kat_cases()
     if "optimum" in which:
         optimum_cases()
+    if "active" in which:
+        active_cases()
+    if "cfg1as" in which:
+        full_config(1, "cfg1_as_trace.npz", kind="active-set", gap_tol=1e-6)
     if "cfg2" in which:
         full_config(2, "cfg2_trace.npz")
     if "cfg1" in which:

@@ -85,6 +85,55 @@ def test_cfg2_prefix_bitwise():
         np.testing.assert_array_equal(got, z["tr_" + f][:15], err_msg=f)
 
 
+def _active_inputs(z, key):
+    if str(z[key + "_meta"][0]) == "medium":
+        import hashlib
+        from conftest import medium_nnls
+        a, y, lo, hi = medium_nnls()
+        h = hashlib.sha256()
+        for arr in (a, y):
+            h.update(np.ascontiguousarray(arr).tobytes())
+        assert h.hexdigest() == str(z[key + "_digest"])
+        return a, y, lo, hi
+    return z[key + "_a"], z[key + "_y"], z[key + "_lo"], z[key + "_hi"]
+
+
+def test_active_set_cases_bitwise():
+    """The active-set kind (bounded Lawson-Hanson, solvers.py:140-204):
+    every trace value, the final state and the saturated sets equal."""
+    z = _load("active_cases.npz")
+    n_checked = 0
+    for key, fam, kind, scr in _cases(z):
+        a, y, lo, hi = _active_inputs(z, key)
+        tol = 1e-6 if fam == "kat" else 1e-8
+        o = oracle_solve(a, y, lo, hi, kind="active-set", gap_tol=tol, screening=scr)
+        gap, rounds, conv = z[key + "_final"]
+        assert (o["rounds"], o["converged"], o["gap"]) == (int(rounds), bool(conv), gap), key
+        for f in ("primal", "dual", "gap", "preserved"):
+            got = np.array([r[f] for r in o["trace"]])
+            np.testing.assert_array_equal(got, z[f"{key}_tr_{f}"], err_msg=f"{key} {f}")
+        np.testing.assert_array_equal(o["x"], z[key + "_x"], err_msg=key)
+        np.testing.assert_array_equal(o["theta"], z[key + "_theta"], err_msg=key)
+        np.testing.assert_array_equal(o["sat_lower"], z[key + "_sat_lower"])
+        np.testing.assert_array_equal(o["sat_upper"], z[key + "_sat_upper"])
+        n_checked += 1
+    assert n_checked == 21
+    # test_solvers.py:144-147: the two-iteration example lands on [1, 0]
+    np.testing.assert_allclose(z["c018_x"], [1.0, 0.0], atol=1e-12)
+
+
+def test_cfg1_active_set_prefix_bitwise():
+    """BASELINE config 1's instance through the active-set kind: the first 60
+    outer iterations exactly (the full 287 take ~5 s more)."""
+    from paper_2202_07258_b200.generate import make_config
+    z = _load("cfg1_as_trace.npz")
+    inst = make_config(1)
+    o = oracle_solve(inst.a, inst.y, inst.lower, inst.upper, kind="active-set", gap_tol=1e-6, max_rounds=60)
+    for f in ("primal", "dual", "gap", "preserved"):
+        got = np.array([r[f] for r in o["trace"]])
+        np.testing.assert_array_equal(got, z["tr_" + f][:60], err_msg=f)
+
+
 def test_apg_solution_level_pin():
     """The FISTA extension is not in the reference: pinned at solution level
     against the reference's active-set optimum (certified gap 1e-12): objective
