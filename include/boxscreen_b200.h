@@ -52,14 +52,17 @@ typedef enum {
   BX_ERR_CUDA = 8,                 /* CUDA runtime failure (no reference analogue) */
   BX_ERR_UNSUPPORTED = 9,          /* shape outside the compiled kernel envelope   */
   BX_ERR_WORKSPACE = 10,           /* caller workspace too small / misaligned      */
-  BX_ERR_NOT_INTERIOR = 11         /* errors.py:25  NotInterior                */
+  BX_ERR_NOT_INTERIOR = 11,        /* errors.py:25  NotInterior                */
+  BX_ERR_SINGULAR = 12             /* errors.py:56  SingularSubproblem (active set) */
 } bx_status;
 
 typedef enum { BX_F64 = 0, BX_F32 = 1 } bx_dtype;
 
-/* solver kinds: solvers.py:17 ("pg", "cd"); "apg" is the FISTA extension of
- * BASELINE.json configs 3 and 5 (not in the reference). */
-typedef enum { BX_PG = 0, BX_CD = 1, BX_APG = 2 } bx_kind;
+/* solver kinds: solvers.py:17 ("pg", "cd", "active-set"); "apg" is the FISTA
+ * extension of BASELINE.json configs 3 and 5 (not in the reference).
+ * BX_ACTIVE_SET (bounded Lawson-Hanson, solvers.py:140-204) needs the extra
+ * workspace of bx_ctx_set_active_set_workspace. */
+typedef enum { BX_PG = 0, BX_CD = 1, BX_APG = 2, BX_ACTIVE_SET = 3 } bx_kind;
 
 typedef struct bx_ctx bx_ctx;
 
@@ -67,7 +70,8 @@ typedef struct bx_ctx bx_ctx;
 typedef struct {
   int32_t kind;          /* bx_kind                                              */
   int32_t inner_passes;  /* >= 1                                                 */
-  int64_t max_rounds;    /* <= 0: reference default (10**6, driver.py:390)       */
+  int64_t max_rounds;    /* <= 0: reference default (10**6; 10 n for the active
+                            set, driver.py:144-150)                              */
   double gap_tol;        /* > 0                                                  */
   double step_size;      /* <= 0 or NaN: auto (power iteration, solvers.py:89)   */
   int32_t power_iters;   /* default 50                                           */
@@ -162,6 +166,15 @@ int bx_solve(bx_ctx* ctx, const bx_solve_cfg* cfg, bx_start_vector_fn start_fn,
  * pointer may be NULL.  Device pointers. */
 int bx_get_state(bx_ctx* ctx, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper);
 
+/* ---- active-set solver (solvers.py:140-204) ------------------------------ */
+/* bytes of the active-set scratch: the passive Cholesky factor R
+ * (min(m, n)^2 fp64, updated by column appends and Givens deletions instead
+ * of the reference's per-iteration refactorisation) plus O(m + n) vectors */
+size_t bx_active_set_workspace_bytes(int64_t m, int64_t n);
+/* hand that scratch to a context (required before bx_solve with
+ * BX_ACTIVE_SET; the caller owns the memory, as with bx_ctx_create's) */
+int bx_ctx_set_active_set_workspace(bx_ctx* ctx, void* workspace, size_t workspace_bytes);
+
 /* ---- multi-GPU column sharding ---------------------------- */
 /* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller */
 int bx_nccl_unique_id(unsigned char* id_out_host);
@@ -193,6 +206,7 @@ enum {
   BX_PROF_SPHERE = 8,
   BX_PROF_GATHER = 9,
   BX_PROF_CD = 10,
+  BX_PROF_ACTIVE = 11,     /* active-set selection / factor update / solve  */
   BX_PROF_SLOTS = 12
 };
 typedef struct {

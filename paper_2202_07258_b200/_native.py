@@ -14,8 +14,8 @@ from .errors import STATUS, NativeError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libboxscreen_b200.so")
 
 BX_F64, BX_F32 = 0, 1
-BX_PG, BX_CD, BX_APG = 0, 1, 2
-KINDS = {"pg": BX_PG, "cd": BX_CD, "apg": BX_APG}
+BX_PG, BX_CD, BX_APG, BX_ACTIVE_SET = 0, 1, 2, 3
+KINDS = {"pg": BX_PG, "cd": BX_CD, "apg": BX_APG, "active-set": BX_ACTIVE_SET}
 
 
 class SolveCfg(ctypes.Structure):
@@ -48,7 +48,7 @@ class ProfEntry(ctypes.Structure):
 
 PROF_SLOTS = 12
 PROF_NAMES = ["pass_dot", "pass_pg_g", "pass_pg", "pass_apg", "pass_power", "pass_ax", "reduce", "dual",
-              "sphere", "gather", "cd", "other"]
+              "sphere", "gather", "cd", "active"]
 
 class BatchedOut(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("converged", ctypes.c_int64), ("iterations", ctypes.c_int64),
@@ -79,6 +79,8 @@ SIGNATURES = {
     "bx_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveCfg), START_FN, _vp, ctypes.POINTER(TraceRec), _i64,
                                 ctypes.POINTER(SolveOut)]),
     "bx_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "bx_active_set_workspace_bytes": (_sz, [_i64, _i64]),
+    "bx_ctx_set_active_set_workspace": (ctypes.c_int, [_vp, _vp, _sz]),
     "bx_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "bx_ctx_set_comm": (ctypes.c_int, [_vp, ctypes.c_char_p, _i32, _i32, _i64, _i64]),
     "bx_group_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i32]),

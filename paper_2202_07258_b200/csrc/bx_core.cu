@@ -13,10 +13,12 @@
 //   compact()         apply_screening (screening.py:72-94) + refresh + step
 //                     re-estimate (driver.py:462-475)
 //   certified()       _certified_gap (driver.py:352-357)
+//   as_step()         active_set_step (solvers.py:151-204), bx_active.cuh
 //   bx_solve          solve (driver.py:371-496)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <mutex>
@@ -33,6 +35,7 @@
 #include "bx_cd.cuh"
 #include "bx_batched.cuh"
 #include "bx_small.cuh"
+#include "bx_active.cuh"
 
 using namespace bx;
 
@@ -242,6 +245,18 @@ struct bx_ctx {
   };
   std::vector<Pending> pending;
   bx_prof_entry pstat[BX_PROF_SLOTS];
+
+  // active-set solver: caller scratch (bx_ctx_set_active_set_workspace); the
+  // passive mask rides in xprev[] (unused by this kind) through compaction
+  int pcap = 0;                 // factor capacity min(m, n)
+  double* asR = nullptr;        // [pcap][pcap] Cholesky factor, logical column j in slot as_cslot[j]
+  int32_t *as_cslot = nullptr, *as_plist = nullptr, *as_hitf = nullptr;
+  double *as_avec = nullptr, *as_rhs = nullptr, *as_c = nullptr, *as_b = nullptr, *as_s = nullptr,
+         *as_frac = nullptr;
+  AsState* as = nullptr;
+  AsState* has = nullptr;       // pinned mirror
+  bool as_dirty = true;         // the factor no longer matches the passive mask (compaction)
+  int as_p = 0;                 // host copy of the factor size
 
   // multi-GPU column sharding
   Comm* comm = nullptr;
@@ -1023,6 +1038,113 @@ int primal_passes(bx_ctx* c, int kind, int passes) {
   return BX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// active set (solvers.py:140-204; kernels in bx_active.cuh)
+// ---------------------------------------------------------------------------
+int as_sync(bx_ctx* c) {
+  CU(cudaMemcpyAsync(c->has, c->as, sizeof(AsState), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  TRY(prof_drain(c));
+  c->as_p = c->has->p;
+  if (c->has->status == AS_SINGULAR)
+    return fail(c, BX_ERR_SINGULAR, "passive-column least-squares system is singular (pivot %.3e, %d columns)",
+                c->has->d2, c->has->p);
+  return BX_OK;
+}
+
+// append preserved column j (j < 0: the one k_as_select chose) to the factor
+template <typename T>
+int as_append(bx_ctx* c, int32_t j) {
+  View<T> vw = act_view<T>(c);
+  k_as_colcopy<T><<<grid1d(c, c->m), RT, 0, c->stream>>>(vw.A, vw.ld, vw.colmap, c->m, c->as_avec, c->as_plist, c->as,
+                                                          j);
+  LAUNCHED();
+  const int npl = c->as_p + 1;
+  k_as_dots<T><<<(npl + 7) / 8, 256, 0, c->stream>>>(vw.A, vw.ld, vw.colmap, c->as_plist, npl, c->as_avec, c->m,
+                                                      c->as_c);
+  LAUNCHED();
+  k_as_append<<<1, AS_NT, 0, c->stream>>>(c->asR, c->pcap, c->pcap, c->as_cslot, c->as, c->as_c);
+  LAUNCHED();
+  ++c->as_p;  // provisional; as_sync reads the device count
+  return BX_OK;
+}
+
+// refactor after a compaction: append the passive columns in preserved order
+// (the order the reference's flatnonzero gives its Gram matrix)
+template <typename T>
+int as_rebuild(bx_ctx* c) {
+  const int s = c->cur;
+  k_as_reset<<<grid1d(c, c->pcap), RT, 0, c->stream>>>(c->pcap, c->as_cslot, c->as);
+  LAUNCHED();
+  c->as_p = 0;
+  std::vector<double> mask(c->k > 0 ? c->k : 1);
+  if (c->k > 0) CU(cudaMemcpyAsync(mask.data(), c->xprev[s], c->k * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (int64_t j = 0; j < c->k; ++j)
+    if (mask[j] != 0.0) TRY(as_append<T>(c, (int32_t)j));
+  TRY(as_sync(c));
+  c->as_dirty = false;
+  return BX_OK;
+}
+
+// One outer iteration; *optimal = true when no bound coordinate violates the
+// optimality conditions (the residual and gradient are then unchanged).
+template <typename T>
+int as_step(bx_ctx* c, bool* optimal) {
+  const int s = c->cur;
+  *optimal = false;
+  if (c->as_dirty) TRY(as_rebuild<T>(c));
+  double* pmask = (double*)c->xprev[s];
+  if (!c->g_valid) {
+    int G = 1;
+    TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr,
+                    (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, c->bpart, 0, &G));
+  }
+  const int e0 = prof_begin(c);
+  k_as_select<<<1, AS_NT, 0, c->stream>>>(c->k, c->m, (const double*)c->x[s], (const double*)c->lo[s],
+                                          (const double*)c->hi[s], (const double*)c->g, (const double*)c->nrm[s],
+                                          pmask, (const double*)c->r, c->as_plist, c->as);
+  LAUNCHED();
+  prof_end(c, e0, BX_PROF_ACTIVE, 8.0 * (6.0 * c->k + c->m));
+  TRY(as_sync(c));
+  if (c->has->jstar < 0) {
+    *optimal = true;
+    return BX_OK;
+  }
+  TRY(as_append<T>(c, -1));
+  const int64_t limit = 2 * c->k + 2;  // solvers.py:180
+  const int nbk = grid1d(c, c->k);
+  for (int64_t it = 0; it < limit; ++it) {
+    // rhs = (y - z) - A_F x_F over the fixed (non-passive) columns
+    k_as_coef<<<nbk, RT, 0, c->stream>>>(c->k, (const double*)c->x[s], pmask, (double*)c->coef);
+    LAUNCHED();
+    int G = 1;
+    TRY(run_pass<T>(c, act_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, (const double*)c->coef, nullptr, 0, &G));
+    TRY(run_reduce<T>(c, G, (const double*)c->tgt, c->as_rhs, R_PLAIN, nullptr, 0, 0));
+    View<T> vw = act_view<T>(c);
+    const int p = c->as_p;
+    if (p > 0) {
+      k_as_dots<T><<<(p + 7) / 8, 256, 0, c->stream>>>(vw.A, vw.ld, vw.colmap, c->as_plist, p, c->as_rhs, c->m,
+                                                        c->as_b);
+      LAUNCHED();
+    }
+    const int e1 = prof_begin(c);
+    k_as_solve<<<1, AS_NT, 0, c->stream>>>(c->asR, c->pcap, c->as_cslot, c->as_plist, c->as, c->as_b, c->as_s,
+                                           c->as_frac, c->as_hitf, (double*)c->x[s], (const double*)c->lo[s],
+                                           (const double*)c->hi[s], pmask);
+    LAUNCHED();
+    prof_end(c, e1, BX_PROF_ACTIVE, 8.0 * ((double)p * p + 8.0 * p));
+    TRY(as_sync(c));
+    if (c->has->status == AS_DONE) {
+      TRY(refresh_resid<T>(c));  // solvers.py:202-203 (g by the next dot pass)
+      c->g_valid = false;
+      return BX_OK;
+    }
+  }
+  return fail(c, BX_ERR_SINGULAR, "active-set inner loop failed to make progress");
+}
+
 // epsilon (max over ranks), theta, reduced dual, gap, radius (k_dual [+ fin])
 template <typename T>
 int dual_point(bx_ctx* c, int which, const double* r, const double* tgt, double* theta, const double* g,
@@ -1133,7 +1255,8 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
   const int nbs = (int)((c->k + RT - 1) / RT);
   const int64_t nscr = n_lo + n_up;
   if (nscr > 0) {
-    ColState<double> src{c->idx[s], (double*)c->x[s], kind == BX_APG ? (double*)c->xprev[s] : nullptr,
+    const bool carry2 = kind == BX_APG || kind == BX_ACTIVE_SET;  // momentum state / passive mask
+    ColState<double> src{c->idx[s], (double*)c->x[s], carry2 ? (double*)c->xprev[s] : nullptr,
                          (double*)c->lo[s], (double*)c->hi[s], (double*)c->nrm[s], (double*)c->att[s],
                          c->dense ? nullptr : c->pos[s]};
     ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->lo[d], (double*)c->hi[d],
@@ -1148,6 +1271,7 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
     c->n_sat_lo += n_lo;
     c->n_sat_up += n_up;
     c->dense = false;
+    if (kind == BX_ACTIVE_SET) c->as_dirty = true;  // preserved positions moved
   }
   // z += A_S bound_S  (only when some screened bound is nonzero; collective)
   if (z_update) {
@@ -1199,6 +1323,16 @@ int reset_state(bx_ctx* c, int kind) {
                                                          (double*)c->hi[s], (const double*)c->nrmfull, (double*)c->nrm[s],
                                                          (const double*)c->attfull, (double*)c->att[s]);
   LAUNCHED();
+  if (kind == BX_ACTIVE_SET) {
+    // coordinates start on a bound (driver.py:144-147); empty passive set
+    CU(cudaMemcpyAsync(c->x[s], c->lo[s], c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->xfull, c->lo[s], c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemsetAsync(c->xprev[s], 0, c->n * sizeof(double), c->stream));
+    k_as_reset<<<grid1d(c, c->pcap), RT, 0, c->stream>>>(c->pcap, c->as_cslot, c->as);
+    LAUNCHED();
+    c->as_p = 0;
+    c->as_dirty = false;
+  }
   CU(cudaMemsetAsync(c->z, 0, c->mp * sizeof(double), c->stream));
   k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z, (double*)c->off, (double*)c->tgt);
   LAUNCHED();
@@ -1289,13 +1423,19 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   const auto t0 = std::chrono::steady_clock::now();
   const int kind = cfg->kind;
   const int passes = cfg->inner_passes;
-  const int64_t max_rounds = cfg->max_rounds > 0 ? cfg->max_rounds : 1000000;
+  const int64_t n_all = c->sharded() ? c->n_global : c->n;
+  const int64_t max_rounds =
+      cfg->max_rounds > 0 ? cfg->max_rounds : (kind == BX_ACTIVE_SET ? 10 * n_all : 1000000);  // driver.py:144-150
   const double tol = cfg->gap_tol;
   const double alpha = cfg->alpha > 0 ? cfg->alpha : 1.0;
   const double slack_scale = cfg->slack_scale >= 0 ? cfg->slack_scale : 1e-12;
   const bool auto_eta = !(cfg->step_size > 0);  // NaN or <= 0
   if (kind == BX_CD && c->sharded())
     return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent is sequential: replicas only, no column sharding");
+  if (kind == BX_ACTIVE_SET && c->sharded())
+    return fail(c, BX_ERR_UNSUPPORTED, "the active set is sequential: replicas only, no column sharding");
+  if (kind == BX_ACTIVE_SET && !c->as)
+    return fail(c, BX_ERR_WORKSPACE, "active-set scratch not attached (bx_ctx_set_active_set_workspace)");
   TRY(validate(c));
   TRY(reset_state<T>(c, kind));
   double eta = cfg->step_size;
@@ -1321,8 +1461,12 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   lp.alpha = alpha;
   for (int64_t rnd = 1; rnd <= max_rounds; ++rnd) {
     rounds = rnd;
-    // small problems: device-resident rounds until the next event
-    if (!c->prof) {
+    bool optimal = false;
+    if (kind == BX_ACTIVE_SET) {
+      TRY(as_step<T>(c, &optimal));
+      iters += 1;
+    } else if (!c->prof) {
+      // small problems: device-resident rounds until the next event
       lp.max_rounds = (int)std::min<int64_t>(max_rounds - rnd + 1, kSmallRounds);
       int ran = 0, done = 0, ev = 0;
       if (lp.max_rounds > 1) TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
@@ -1416,6 +1560,17 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       tr.momentum = c->hsc->mom_t;
     }
     if (converged) break;
+    if (optimal) {
+      // KKT-optimal active set: the certified gap alone decides (driver.py:246-252)
+      TRY(certified<T>(c, alpha));
+      TRY(sync_scalars<T>(c));
+      TRY(check_dev_err(c));
+      gap_out = c->hsc->cert.gap;
+      c->theta_is_cert = true;
+      const double tol_c = cfg->relative_gap ? tol * fmax(1.0, fabs(c->hsc->cert.primal)) : tol;
+      converged = gap_out < tol_c;
+      break;
+    }
   }
   // x_full <- current preserved iterate (ws.sync, driver.py:492)
   k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], (const double*)c->x[c->cur], (double*)c->xfull);
@@ -1508,6 +1663,7 @@ int bx_ctx_destroy(bx_ctx* c) {
   if (!c) return BX_OK;
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->hsc) cudaFreeHost(c->hsc);
+  if (c->has) cudaFreeHost(c->has);
   delete c->comm;
   delete c;
   return BX_OK;
@@ -1599,7 +1755,7 @@ int64_t bx_preserved_count(const bx_ctx* c) { return c ? c->k : -1; }
 int bx_solve(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* user, bx_trace_rec* trace,
              int64_t cap, bx_solve_out* out) {
   if (!c || !cfg) return BX_ERR_INVALID_ARGUMENT;
-  if (cfg->kind != BX_PG && cfg->kind != BX_CD && cfg->kind != BX_APG)
+  if (cfg->kind != BX_PG && cfg->kind != BX_CD && cfg->kind != BX_APG && cfg->kind != BX_ACTIVE_SET)
     return fail(c, BX_ERR_INVALID_ARGUMENT, "unknown solver kind %d", cfg->kind);
   if (!(cfg->gap_tol > 0)) return fail(c, BX_ERR_INVALID_ARGUMENT, "gap_tol must be positive");
   if (cfg->inner_passes < 1) return fail(c, BX_ERR_INVALID_ARGUMENT, "inner_passes must be >= 1");
@@ -1618,6 +1774,43 @@ int bx_get_state(bx_ctx* c, void* x, void* theta, int64_t* sat_lower, int64_t* s
   if (sat_upper && c->n_sat_up)
     CU(cudaMemcpyAsync(sat_upper, c->sat_up, c->n_sat_up * 8, cudaMemcpyDeviceToDevice, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+size_t bx_active_set_workspace_bytes(int64_t m, int64_t n) {
+  const int64_t pcap = std::max<int64_t>(1, std::min(m, n));
+  const int64_t mp = round_up(m, 32);
+  Carver w{nullptr, 0, 0, true};
+  w.take((size_t)pcap * pcap * 8);
+  for (int i = 0; i < 3; ++i) w.take((size_t)(pcap + 1) * 4);
+  for (int i = 0; i < 2; ++i) w.take((size_t)mp * 8);
+  for (int i = 0; i < 4; ++i) w.take((size_t)(pcap + 1) * 8);
+  w.take(sizeof(AsState));
+  return w.off + kAlign;
+}
+
+int bx_ctx_set_active_set_workspace(bx_ctx* c, void* workspace, size_t bytes) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  const size_t need = bx_active_set_workspace_bytes(c->m, c->n);
+  if (!workspace || bytes < need)
+    return fail(c, BX_ERR_WORKSPACE, "active-set workspace of %zu bytes, need %zu", bytes, need);
+  c->pcap = (int)std::max<int64_t>(1, std::min(c->m, c->n));
+  const int64_t pcap = c->pcap;
+  Carver w{(char*)align_up((uintptr_t)workspace, kAlign), 0, bytes, false};
+  c->asR = (double*)w.take((size_t)pcap * pcap * 8);
+  c->as_cslot = (int32_t*)w.take((size_t)(pcap + 1) * 4);
+  c->as_plist = (int32_t*)w.take((size_t)(pcap + 1) * 4);
+  c->as_hitf = (int32_t*)w.take((size_t)(pcap + 1) * 4);
+  c->as_avec = (double*)w.take((size_t)c->mp * 8);
+  c->as_rhs = (double*)w.take((size_t)c->mp * 8);
+  c->as_c = (double*)w.take((size_t)(pcap + 1) * 8);
+  c->as_b = (double*)w.take((size_t)(pcap + 1) * 8);
+  c->as_s = (double*)w.take((size_t)(pcap + 1) * 8);
+  c->as_frac = (double*)w.take((size_t)(pcap + 1) * 8);
+  c->as = (AsState*)w.take(sizeof(AsState));
+  if (!c->has) CU(cudaMallocHost((void**)&c->has, sizeof(AsState)));
+  memset(c->has, 0, sizeof(AsState));
+  c->as_dirty = true;
   return BX_OK;
 }
 

@@ -152,8 +152,19 @@ class _Session:
                                           ctypes.byref(sig)), self.ctx, "bx_power_iter")
         return sig.value
 
+    def attach_active_set(self):
+        """Scratch of the active-set kind: the passive Cholesky factor
+        (min(m, n)^2 fp64) and its vectors, owned here like the workspace."""
+        L = nat.lib()
+        nbytes = L.bx_active_set_workspace_bytes(self.m, self.n)
+        self.as_ws = self.torch.empty(nbytes, dtype=self.torch.uint8, device=self.ws.device)
+        nat.check(L.bx_ctx_set_active_set_workspace(self.ctx, self.as_ws.data_ptr(), nbytes), self.ctx,
+                  "bx_ctx_set_active_set_workspace")
+
     def run(self, cfg, screening, alpha, slack_scale, profile=False):
         L = nat.lib()
+        if cfg.kind == "active-set" and getattr(self, "as_ws", None) is None:
+            self.attach_active_set()
         nat.check(L.bx_set_profiling(self.ctx, 1 if profile else 0), self.ctx, "bx_set_profiling")
         c = nat.SolveCfg()
         c.kind = nat.KINDS[cfg.kind]
@@ -221,8 +232,6 @@ def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=
     ``profile`` times every kernel launch with CUDA events (info["profile"]).
     """
     cfg = cfg or SolverConfig()
-    if cfg.kind == "active-set":
-        raise NotImplementedError("the active-set solver is outside the GPU hot path (SURVEY.md 8f)")
     if not isinstance(p, Problem):
         raise TypeError("p must be a Problem")
     if slack_scale is None:

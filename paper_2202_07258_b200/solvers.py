@@ -12,7 +12,7 @@ import numpy as np
 
 # "apg" = accelerated projected gradient (FISTA + function-value restart),
 # BASELINE.json configs 3 and 5; "active-set" is the reference's third kind
-# (SURVEY.md section 8f "next"), not built on the GPU path yet.
+# (bounded Lawson-Hanson, solvers.py:140-204; csrc/bx_active.cuh).
 _SOLVER_KINDS = ("pg", "cd", "apg", "active-set")
 
 
