@@ -1417,6 +1417,20 @@ int validate(bx_ctx* c) {
   return BX_OK;
 }
 
+// two CUDA events, destroyed with the scope
+struct EventPair {
+  cudaEvent_t e[2] = {nullptr, nullptr};
+  int create(bx_ctx* c) {
+    for (auto& x : e) CU(cudaEventCreate(&x));
+    return BX_OK;
+  }
+  cudaEvent_t operator[](int i) const { return e[i]; }
+  ~EventPair() {
+    for (auto x : e)
+      if (x) cudaEventDestroy(x);
+  }
+};
+
 template <typename T>
 int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* user, bx_trace_rec* trace,
                 int64_t cap, bx_solve_out* out) {
@@ -1453,6 +1467,9 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   bool converged = false;
   double gap_out = INFINITY;
   int64_t ntrace = 0;
+  double excluded = 0.0;  // seconds of gap evaluation left out of the trace (screening off)
+  EventPair gap_ev;
+  if (!cfg->screening) TRY(gap_ev.create(c));
   SmallLoop lp;
   lp.tol = tol;
   lp.relative_gap = cfg->relative_gap;
@@ -1475,7 +1492,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
           std::vector<double> tr(8 * (size_t)done);
           CU(cudaMemcpyAsync(tr.data(), c->dtrace, tr.size() * 8, cudaMemcpyDeviceToHost, c->stream));
           CU(cudaStreamSynchronize(c->stream));
-          const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() - excluded;
           for (int q = 0; q < done && trace && ntrace < cap; ++q) {
             bx_trace_rec& t = trace[ntrace++];
             t.round = rnd + q;
@@ -1511,16 +1528,33 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       TRY(primal_passes<T>(c, kind, passes));
       iters += passes;
     }
+    // offline-gap convention (driver.py:180-181, 237-238): without screening
+    // the gap evaluation is excluded from the trace's elapsed time -- here the
+    // device time of the dual / certificate kernels, bracketed by events
+    if (!cfg->screening) CU(cudaEventRecord(gap_ev[0], c->stream));
     TRY(dual_screen<T>(c, cfg->screening, slack_scale, alpha));
+    if (!cfg->screening) CU(cudaEventRecord(gap_ev[1], c->stream));
     TRY(sync_scalars<T>(c));
     TRY(check_dev_err(c));
+    if (!cfg->screening) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, gap_ev[0], gap_ev[1]));
+      excluded += 1e-3 * ms;
+    }
     const DualOut act = c->hsc->act;
     gap_out = act.gap;
     double cert_gap = NAN;
     const double tol_r = cfg->relative_gap ? tol * fmax(1.0, fabs(act.primal)) : tol;
     if (act.gap < tol_r) {
+      if (!cfg->screening) CU(cudaEventRecord(gap_ev[0], c->stream));
       TRY(certified<T>(c, alpha));
+      if (!cfg->screening) CU(cudaEventRecord(gap_ev[1], c->stream));
       TRY(sync_scalars<T>(c));
+      if (!cfg->screening) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, gap_ev[0], gap_ev[1]));
+        excluded += 1e-3 * ms;
+      }
       TRY(check_dev_err(c));
       cert_gap = c->hsc->cert.gap;
       gap_out = cert_gap;
@@ -1545,7 +1579,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     if (trace && ntrace < cap) {
       bx_trace_rec& tr = trace[ntrace++];
       tr.round = rnd;
-      tr.elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      tr.elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() - excluded;
       tr.primal = act.primal;
       tr.dual = act.dual;
       tr.gap = act.gap;

@@ -201,6 +201,24 @@ class _Session:
         return out, trace[: min(out.rounds, cap)], x, theta, sl[: out.n_sat_lower], su[: out.n_sat_upper]
 
 
+def column_stats(p, t=None):
+    """(||a_j||, A't) computed on the GPU (k_colstats, the setup pass of
+    bx_ctx_create) as host fp64 arrays; A't is None without ``t``."""
+    import types
+    tv = None if t is None else types.SimpleNamespace(t=np.asarray(t, dtype=np.float64).ravel())
+    with _Session(p, tv=tv) as s:
+        torch = s.torch
+        dev = s.dev["a"].device
+        nrm = torch.empty(p.n, dtype=torch.float64, device=dev)
+        nat.check(nat.lib().bx_col_norms(s.ctx, nrm.data_ptr()), s.ctx, "bx_col_norms")
+        att = None
+        if tv is not None:
+            att_d = torch.empty(p.n, dtype=torch.float64, device=dev)
+            nat.check(nat.lib().bx_att(s.ctx, att_d.data_ptr()), s.ctx, "bx_att")
+            att = att_d.cpu().numpy()
+        return nrm.cpu().numpy(), att
+
+
 def _result(p_n, out, tr, x, theta, sl, su, prof, return_device, n_total=None):
     n = n_total or p_n
     trace = [TraceRecord(int(r["round"]), float(r["elapsed"]), float(r["primal"]), float(r["dual"]),

@@ -167,3 +167,71 @@ def make_config(cfg_id, seed=0, m=None, n=None):
     else:
         raise ValueError("config 5 is batched: use bump_dictionary + batched_rhs")
     return Instance(c["name"], a, y, lo, hi, x0, c["kind"], c["inner_passes"], c["gap_tol"])
+
+
+# ---------------------------------------------------------------------------
+# The reference's own benchmark families (generate.py:15-77): GenSpec /
+# generate, used by the CLI `gen` command, the estimator tests and compare_t.
+# Same streams (one spawned child per drawn object), same draws, so the same
+# spec gives the same arrays as the reference (tests/test_frontends.py pins
+# digests made from the reference).
+# ---------------------------------------------------------------------------
+
+@dataclass
+class GenSpec:
+    family: str  # "bvls" or "nnls"
+    m: int
+    n: int
+    box_halfwidth: float = 1.0  # bvls only
+    sparsity: float = 0.05      # nnls: density of the planted solution
+    noise_std: float = 1.0
+    seed: int = 0
+
+    def __post_init__(self):
+        from .errors import BadSpec
+        if self.family not in ("bvls", "nnls"):
+            raise BadSpec(f"unknown family {self.family!r}")
+        if self.m < 1 or self.n < 1:
+            raise BadSpec("m and n must be >= 1")
+        if self.family == "bvls" and not self.box_halfwidth > 0:
+            raise BadSpec("box_halfwidth must be positive")
+        if self.family == "nnls":
+            if not 0 < self.sparsity <= 1:
+                raise BadSpec("sparsity must be in (0, 1]")
+            if round(self.sparsity * self.n) < 1:
+                raise BadSpec("sparsity * n must round to at least 1")
+
+
+def gen_bvls(spec):
+    """Gaussian box instance: A, y ~ N(0, 1) entrywise, box [-b, b]."""
+    from .errors import BadSpec
+    from .model import Problem
+    if spec.family != "bvls":
+        raise BadSpec("gen_bvls needs a bvls spec")
+    s_a, s_y = _streams(spec.seed, 2)
+    a = s_a.standard_normal((spec.m, spec.n))
+    y = s_y.standard_normal(spec.m)
+    half = spec.box_halfwidth
+    return Problem(a, y, np.full(spec.n, -half), np.full(spec.n, half))
+
+
+def gen_nnls(spec):
+    """Half-normal matrix, planted sparse half-normal x, Gaussian noise."""
+    from .errors import BadSpec, ZeroColumn
+    from .model import Problem
+    if spec.family != "nnls":
+        raise BadSpec("gen_nnls needs an nnls spec")
+    s_a, s_x, s_e = _streams(spec.seed, 3)
+    a = np.abs(s_a.standard_normal((spec.m, spec.n)))
+    if not np.all(np.linalg.norm(a, axis=0) > 0.0):
+        raise ZeroColumn("generated matrix has a zero column")
+    nnz = int(round(spec.sparsity * spec.n))
+    x_true = np.zeros(spec.n)
+    where = s_x.choice(spec.n, size=nnz, replace=False)
+    x_true[where] = np.abs(s_x.standard_normal(nnz))
+    y = a @ x_true + spec.noise_std * s_e.standard_normal(spec.m)
+    return Problem(a, y, np.zeros(spec.n), np.full(spec.n, np.inf))
+
+
+def generate(spec):
+    return gen_nnls(spec) if spec.family == "nnls" else gen_bvls(spec)

@@ -22,6 +22,9 @@ Fixtures
                       and a 300 x 600 screened NNLS instance
   cfg1_as_trace.npz   BASELINE config 1's instance solved by the active-set
                       kind (gap 1e-6): the reference's whole trajectory
+  frontends.npz       the thin wrappers around the solver: GenSpec draws
+                      (digests), estimator fits, compare_t curves,
+                      solve-linear translation vectors, a CLI solve result
   cfg1_trace.npz      BASELINE config 1 at full size (1000 x 2000, PG, 10
                       passes/round, gap 1e-6): the reference's whole trajectory
   cfg2_trace.npz      BASELINE config 2 at full size (2000 x 4000, CD, gap 1e-7)
@@ -42,6 +45,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, REF)
 
 import boxscreen as bs  # noqa: E402  (the reference)
+import boxscreen.bench  # noqa: E402,F401
 
 from conftest import medium_nnls, small_instance  # noqa: E402
 from paper_2202_07258_b200.generate import make_config  # noqa: E402
@@ -203,6 +207,62 @@ def active_cases():
     print("active_cases:", i)
 
 
+def frontends():
+    import json
+    import subprocess
+    import tempfile
+    out = {}
+    specs = [dict(family="nnls", m=30, n=20, seed=0), dict(family="bvls", m=25, n=10, box_halfwidth=0.4, seed=1),
+             dict(family="nnls", m=30, n=20, seed=2), dict(family="nnls", m=20, n=20, seed=3),
+             dict(family="nnls", m=30, n=40, seed=2), dict(family="nnls", m=50, n=80, sparsity=0.1,
+                                                            noise_std=0.5, seed=7)]
+    out["gen_specs"] = np.array([json.dumps(sp) for sp in specs])
+    out["gen_digest"] = np.array([digest(*(lambda p: (p.a_matrix, p.y, p.lower, p.upper))(
+        bs.generate(bs.GenSpec(**sp)))) for sp in specs])
+    out["gen_instance_hash"] = np.array([bs.bench.instance_hash(bs.generate(bs.GenSpec(**sp))) for sp in specs])
+    # estimator fits (test_estimator.py shapes)
+    fits = [("nnls0", specs[0], {}), ("bvls1", specs[1], dict(lower=-0.4, upper=0.4, solver="pg")),
+            ("nnls2_tight", specs[2], dict(tol=1e-8)), ("nnls2_off", specs[2], dict(tol=1e-8, screening=False)),
+            ("nnls3_as", specs[3], dict(solver="active-set"))]
+    out["fit_names"] = np.array([f[0] for f in fits])
+    for name, sp, kw in fits:
+        p = bs.generate(bs.GenSpec(**sp))
+        est = bs.BoxConstrainedRegression(**kw).fit(p.a_matrix, p.y)
+        out[f"fit_{name}_kw"] = np.array(json.dumps(kw))
+        out[f"fit_{name}_spec"] = np.array(json.dumps(sp))
+        out[f"fit_{name}_coef"] = est.coef_
+        out[f"fit_{name}_stats"] = np.array([est.gap_, est.n_iter_, float(est.converged_)])
+    # compare_t (test_harness.py:221-229 shape)
+    p = bs.generate(bs.GenSpec(**specs[4]))
+    rounds, curves = bs.bench.compare_t(p, ["neg-ones", "neg-mean-column", ("neg-column", {"column": 0})])
+    out["ct_labels"] = np.array(list(curves))
+    out["ct_curves"] = np.array([curves[k] for k in curves])
+    # solve-linear t on full-rank Gaussian columns
+    rng = np.random.default_rng(77)
+    a = rng.standard_normal((40, 10))
+    pl = bs.Problem(a, rng.standard_normal(40), np.zeros(10), np.full(10, np.inf))
+    out["sl_a"] = a
+    out["sl_y"] = pl.y
+    out["sl_t"] = bs.select_translation_vector(pl, "solve-linear").t
+    # CLI solve on a generated instance
+    with tempfile.TemporaryDirectory() as d:
+        env = dict(os.environ, PYTHONPATH=REF)
+        subprocess.run([sys.executable, "-m", "boxscreen.cli", "gen", "--family", "nnls", "--m", "40", "--n", "60",
+                        "--seed", "5", "--out-prefix", os.path.join(d, "p")], check=True, env=env)
+        subprocess.run([sys.executable, "-m", "boxscreen.cli", "solve", "--a", os.path.join(d, "p_A.mtx"), "--y",
+                        os.path.join(d, "p_y.csv"), "--solver", "pg", "--inner-passes", "5", "--tol", "1e-8",
+                        "--result-out", os.path.join(d, "r.json"), "--trace-out", os.path.join(d, "t.csv")],
+                       check=True, env=env)
+        with open(os.path.join(d, "r.json")) as fh:
+            r = json.load(fh)
+        out["cli_x"] = np.array(r["x"])
+        out["cli_stats"] = np.array([r["gap"], r["rounds"], float(r["converged"])])
+        with open(os.path.join(d, "t.csv")) as fh:
+            out["cli_trace_header"] = np.array(fh.readline().strip())
+    np.savez_compressed(os.path.join(HERE, "frontends.npz"), **out)
+    print("frontends: ok")
+
+
 def full_config(cfg_id, fname, kind=None, gap_tol=None):
     inst = make_config(cfg_id)
     p = bs.Problem(inst.a, inst.y, inst.lower, inst.upper)
@@ -220,7 +280,7 @@ def full_config(cfg_id, fname, kind=None, gap_tol=None):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "kat", "optimum", "active", "cfg1as", "cfg2", "cfg1"]
+    which = sys.argv[1:] or ["small", "kat", "optimum", "active", "frontends", "cfg1as", "cfg2", "cfg1"]
     if "small" in which:
         small_cases()
     if "kat" in which:
@@ -229,6 +289,8 @@ if __name__ == "__main__":
         optimum_cases()
     if "active" in which:
         active_cases()
+    if "frontends" in which:
+        frontends()
     if "cfg1as" in which:
         full_config(1, "cfg1_as_trace.npz", kind="active-set", gap_tol=1e-6)
     if "cfg2" in which:
