@@ -33,7 +33,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAJ_PATH = os.path.join(ROOT, "profiles", "cfg3_trajectory.json")
+def traj_path(cfg_id):
+    """Preserved-count trajectory of the GPU solve of a config (the CPU arm's
+    iteration weights), written with --write-trajectory."""
+    return os.path.join(ROOT, "profiles", f"cfg{cfg_id}_trajectory.json")
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -127,7 +130,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # the CPU side: oracle port timed on the host cores (cpu_baseline / reference arm)
 # ---------------------------------------------------------------------------
-def cpu_rate(inst, k_bins, budget_s, passes=None):
+def cpu_rate(inst, k_bins, budget_s, passes=None, kmax=8000):
     """Oracle FISTA iterations/s over the solve's preserved-set trajectory.
 
     ``k_bins`` = [(k, iterations)] -- how many iterations the screened solve
@@ -135,7 +138,10 @@ def cpu_rate(inst, k_bins, budget_s, passes=None):
     (oracle/boxscreen_oracle.py:apg_passes, the reference's two-GEMV
     Workspace arithmetic) are timed on a k-column working set; the rate is
     total iterations / sum(iterations_b * seconds_per_iteration(k_b)).
-    Returns (rate, details).
+    Bins wider than ``kmax`` columns are timed on ``kmax`` of them and scaled
+    by k / kmax (the passes are GEMVs, linear in k), so the fp64 working set
+    stays bounded (config 4's shard is 10 GB in fp64).  The oracle always runs
+    in fp64 (the reference's arithmetic).  Returns (rate, details).
     """
     from oracle.boxscreen_oracle import ActiveView, apg_passes, cd_passes, pg_passes
     a, y, lo, hi = inst.a, inst.y, inst.lower, inst.upper
@@ -155,9 +161,11 @@ def cpu_rate(inst, k_bins, budget_s, passes=None):
     tsum = 0.0
     x_full = np.zeros(n)
     for k, it in k_bins:
-        keep = np.sort(perm[:k])
-        w = ActiveView(a, y, lo, hi, norms, np.zeros(a.shape[0]), x_full, keep)
-        eta = 0.5 / (0.75 * k + 10.0)  # timing only: cost does not depend on the step
+        kt = min(k, kmax)
+        keep = np.sort(perm[:kt])
+        sub = np.asarray(a[:, keep], dtype=np.float64, order="F")
+        w = ActiveView(sub, y, lo[keep], hi[keep], norms[keep], np.zeros(a.shape[0]), x_full[keep], np.arange(kt))
+        eta = 0.5 / (0.75 * kt + 10.0)  # timing only: cost does not depend on the step
         mom = [1.0]
         t0 = time.perf_counter()
         done = 0
@@ -167,8 +175,8 @@ def cpu_rate(inst, k_bins, budget_s, passes=None):
             el = time.perf_counter() - t0
             if el > per_bin or done >= it:
                 break
-        sec_per_it = el / done
-        details.append(dict(k=int(k), iterations_in_solve=int(it), timed_iterations=done,
+        sec_per_it = el / done * (k / kt)
+        details.append(dict(k=int(k), timed_columns=int(kt), iterations_in_solve=int(it), timed_iterations=done,
                             sec_per_iteration=sec_per_it))
         tsum += it * sec_per_it
         del w
@@ -224,15 +232,27 @@ def blas_threads():
 
 
 # ---------------------------------------------------------------------------
+CFG4_COLS_PER_GPU = 62500  # BASELINE config 4: 500,000 columns over 8 GPUs (weak scaling unit)
+
+
 def make_instance(cfg_id):
-    from paper_2202_07258_b200.generate import make_config
-    return make_config(cfg_id)
+    """The single-GPU workload of a config.  Config 4 is the weak-scaling
+    unit: 20000 x 62,500 fp32 (its columns of the 8-GPU 500,000-column run)."""
+    from paper_2202_07258_b200.generate import CONFIGS, Instance, make_config, sparse_nnls_block
+    if cfg_id != 4:
+        return make_config(cfg_id)
+    c = CONFIGS[4]
+    n = CFG4_COLS_PER_GPU
+    a, y, lo, hi, x0 = sparse_nnls_block(c["m"], n, c["density"], c["snr"], 0, n, lambda v: v, dtype=np.float32)
+    return Instance(c["name"], a, y, lo, hi, x0, c["kind"], c["inner_passes"], c["gap_tol"])
 
 
 def config_block(cfg_id, inst):
     from paper_2202_07258_b200.generate import CONFIGS
     c = CONFIGS[cfg_id]
-    return {"workload": c["name"], "m": int(inst.a.shape[0]), "n": int(inst.a.shape[1]), "solver": inst.kind,
+    extra = {"n_per_gpu": CFG4_COLS_PER_GPU, "parallelism": "1 GPU = one 62,500-column shard of the 8-GPU run"} \
+        if cfg_id == 4 else {}
+    return {"workload": c["name"], **extra, "m": int(inst.a.shape[0]), "n": int(inst.a.shape[1]), "solver": inst.kind,
             "inner_passes": inst.inner_passes, "gap_tol": inst.gap_tol, "screening": True,
             "problem": "NNLS" if np.isinf(inst.upper).all() else "BVLS", "seed": 0,
             "l2_policy": "inputs larger than L2 (A = %.1f GB > 126 MB L2)" % (inst.a.nbytes / 1e9)
@@ -246,10 +266,12 @@ def run_reference(args):
         return 0
     inst = make_instance(args.config)
     try:
-        with open(TRAJ_PATH) as fh:
+        with open(traj_path(args.config)) as fh:
             traj = json.load(fh)
+        if traj.get("config") != args.config:
+            raise ValueError("trajectory of another config")
         bins = [tuple(b) for b in traj["k_bins"]]
-        src = "preserved-count trajectory of the GPU solve (profiles/cfg3_trajectory.json)"
+        src = f"preserved-count trajectory of the GPU solve (profiles/cfg{args.config}_trajectory.json)"
     except Exception:
         bins = [(inst.a.shape[1], 100)]
         src = "unscreened working set (no trajectory file)"
@@ -581,15 +603,15 @@ def run_ours(args):
     # trajectory for the CPU arm (preserved-count bins of this solve)
     bins = k_bins_from_trace(prof_res.info["trace_arrays"], inst.inner_passes)
     if args.write_trajectory and rank == 0:
-        os.makedirs(os.path.dirname(TRAJ_PATH), exist_ok=True)
-        with open(TRAJ_PATH, "w") as fh:
+        os.makedirs(os.path.dirname(traj_path(args.config)), exist_ok=True)
+        with open(traj_path(args.config), "w") as fh:
             json.dump({"config": args.config, "k_bins": bins, "rounds": prof_res.rounds,
                        "iterations": prof_res.info["iterations"]}, fh, indent=1)
 
     # end to end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        p_host = Problem(inst.a, inst.y, inst.lower, inst.upper, pin=True)
+        p_host = Problem(inst.a, inst.y, inst.lower, inst.upper, dtype=inst.a.dtype, pin=True)
         h2d = p_host.a_matrix.nbytes + 8 * (m + 2 * n)
         e_it, e_t, d2h = 0, 0.0, 0
         for s in range(args.steps + 1):
