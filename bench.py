@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--write-trajectory", action="store_true")
+    ap.add_argument("--cfg4-rounds", type=int, default=100,
+                    help="config 4: rounds (x10 PG passes + screening) per step; BASELINE gives it no gap target")
     return ap.parse_args()
 
 
@@ -233,6 +235,10 @@ def blas_threads():
 
 # ---------------------------------------------------------------------------
 CFG4_COLS_PER_GPU = 62500  # BASELINE config 4: 500,000 columns over 8 GPUs (weak scaling unit)
+# BASELINE config 4 states no gap target (its check is the 1e-4 objective
+# agreement with fp64) and plain PG needs millions of steps to a 1e-6 gap on
+# this coherent matrix, so a step is a fixed budget of screened rounds
+CFG4_STEP = "fixed budget: --cfg4-rounds rounds of 10 PG passes + the screening pass (no gap target in config 4)"
 
 
 def make_instance(cfg_id):
@@ -257,7 +263,7 @@ def config_block(cfg_id, inst):
             "problem": "NNLS" if np.isinf(inst.upper).all() else "BVLS", "seed": 0,
             "l2_policy": "inputs larger than L2 (A = %.1f GB > 126 MB L2)" % (inst.a.nbytes / 1e9)
             if inst.a.nbytes > 126e6 else "working set L2-resident (reported, not flushed)",
-            "step": "one full solve to certified gap <= gap_tol"}
+            "step": CFG4_STEP if cfg_id == 4 else "one full solve to certified gap <= gap_tol"}
 
 
 def run_reference(args):
@@ -348,7 +354,8 @@ def run_sharded(args, rank, world, dev):
     a_dev = torch.from_numpy(np.ascontiguousarray(a_blk.T)).to(dev)
     tdt = a_dev.dtype
     p = Problem.from_device_storage(a_dev, m, torch.from_numpy(y).to(dev).to(tdt), lo, hi)
-    cfg = SolverConfig(kind=c["kind"], inner_passes=c["inner_passes"], gap_tol=c["gap_tol"])
+    cfg = SolverConfig(kind=c["kind"], inner_passes=c["inner_passes"], gap_tol=c["gap_tol"],
+                       max_rounds=args.cfg4_rounds if args.config == 4 else None)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         solve_distributed(p, c0, n, cfg)
@@ -402,7 +409,8 @@ def run_sharded(args, rank, world, dev):
             "data": "synthetic (seeded numpy, BASELINE config recipe; per-rank column blocks of the same draw)",
             "config": {"workload": c["name"], "m": m, "n": n, "solver": c["kind"], "inner_passes": c["inner_passes"],
                        "gap_tol": c["gap_tol"], "screening": True, "parallelism": f"column-sharded x{world} (NCCL)",
-                       "l2_policy": "inputs larger than L2", "step": "one full solve to certified gap <= gap_tol"},
+                       "l2_policy": "inputs larger than L2",
+                       "step": CFG4_STEP if args.config == 4 else "one full solve to certified gap <= gap_tol"},
             "time_to_gap_s": elapsed / args.steps, "converged": all(r.converged for r in results),
             "rounds": r0.rounds, "iterations_per_solve": r0.info["iterations"],
             "final_preserved": r0.trace[-1].preserved_count, "certified_gap": r0.gap, "gpu_launches": launches,
@@ -558,7 +566,8 @@ def run_ours(args):
 
     inst = make_instance(args.config)
     m, n = inst.a.shape
-    cfg = SolverConfig(kind=inst.kind, inner_passes=inst.inner_passes, gap_tol=inst.gap_tol)
+    cfg = SolverConfig(kind=inst.kind, inner_passes=inst.inner_passes, gap_tol=inst.gap_tol,
+                       max_rounds=args.cfg4_rounds if args.config == 4 else None)
     tdt = torch.float32 if inst.a.dtype == np.float32 else torch.float64
     a_dev = torch.from_numpy(np.ascontiguousarray(inst.a.T)).to(dev)  # (n, m) == column-major A
     p_dev = Problem(a_dev.t(), torch.from_numpy(inst.y).to(dev), inst.lower, inst.upper)
