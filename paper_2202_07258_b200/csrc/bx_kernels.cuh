@@ -340,10 +340,24 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     __syncthreads();
   }
 
+  // ring slot / mbarrier phase of group gi: a running counter on the fp32
+  // pass, gi % S on the fp64 pass (A/B on the B200: the counter is ~5%
+  // faster for fp32 and ~14% slower for fp64, scheduling of the 128-register
+  // fp64 kernel)
+  int s_run = 0;
+  uint32_t ph_run = 0;
   for (int gi = 0; gi < ngroups; ++gi) {
-    const int s = gi % S;
+    int s;
+    uint32_t ph;
+    if constexpr (sizeof(T) == 4) {
+      s = s_run;
+      ph = ph_run;
+    } else {
+      s = gi % S;
+      ph = (uint32_t)((gi / S) & 1);
+    }
     const int cg = min(C, ncol - gi * C);
-    mbar_wait(&bars[s], (uint32_t)((gi / S) & 1));
+    mbar_wait(&bars[s], ph);
     const unsigned char* slot = smem + s * slot_bytes;
     if (DOT) {
       T d[C];
@@ -352,15 +366,44 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         d[c] = T(0);
         if (c < cg) {
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
+          if constexpr (sizeof(T) == 8) {
+            // fp64: one chain per thread (measured faster than split sums here)
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              const int row = row0 + i * (NT * V);
+              if (row < m) {
+                T av[V];
+                unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+                for (int e = 0; e < V; ++e) d[c] += ((row + e < m) ? av[e] : T(0)) * vr[i][e];
+              }
+            }
+          } else {
+          // fp32 (twice the elements per byte): V independent partial sums
+          // (short dependency chains) combined in a fixed order; only the
+          // vector holding row m-1 needs a guard
+          T dd[V];
+#pragma unroll
+          for (int e = 0; e < V; ++e) dd[e] = T(0);
 #pragma unroll
           for (int i = 0; i < R; ++i) {
             const int row = row0 + i * (NT * V);
-            if (row < m) {
+            if (row + V <= m) {
               T av[V];
               unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
 #pragma unroll
-              for (int e = 0; e < V; ++e) d[c] += ((row + e < m) ? av[e] : T(0)) * vr[i][e];
+              for (int e = 0; e < V; ++e) dd[e] += av[e] * vr[i][e];
+            } else if (row < m) {
+              T av[V];
+              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+              for (int e = 0; e < V; ++e)
+                if (row + e < m) dd[e] += av[e] * vr[i][e];
             }
+          }
+          d[c] = dd[0];
+#pragma unroll
+          for (int e = 1; e < V; ++e) d[c] += dd[e];
           }
         }
         d[c] = warp_sum<T>(d[c]);
@@ -455,14 +498,27 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
             if (row < m) {
               T av[V];
               unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+              if constexpr (sizeof(T) == 8) {
 #pragma unroll
-              for (int e = 0; e < V; ++e) acc[i][e] += ((row + e < m) ? av[e] : T(0)) * cc;
+                for (int e = 0; e < V; ++e) acc[i][e] += ((row + e < m) ? av[e] : T(0)) * cc;
+              } else {
+                // rows >= m of the last vector only reach the padding of the
+                // partial row, which k_reduce never reads: no per-element guard
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc[i][e] += av[e] * cc;
+              }
             }
           }
         }
       }
     }
     __syncthreads();  // every thread is done with slot s
+    if constexpr (sizeof(T) == 4) {
+      if (++s_run == S) {
+        s_run = 0;
+        ph_run ^= 1u;
+      }
+    }
     if (tid == 0 && gi + S < ngroups) {
       const int gn = gi + S;
       const int cgn = min(C, ncol - gn * C);

@@ -169,7 +169,12 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
 #pragma unroll
           for (int i = 0; i < R; ++i) {
             const int row = row0 + i * (SM_NT * V);
-            if (row < m) {
+            if (row + V <= m) {  // full vector: no per-element guard
+              T av[V];
+              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+              for (int e = 0; e < V; ++e) d[u] += static_cast<double>(av[e]) * vr[i][e];
+            } else if (row < m) {
               T av[V];
               unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
 #pragma unroll
