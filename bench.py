@@ -408,7 +408,10 @@ def run_sharded(args, rank, world, dev):
             "dtype": "f32" if dt == np.float32 else "f64",
             "data": "synthetic (seeded numpy, BASELINE config recipe; per-rank column blocks of the same draw)",
             "config": {"workload": c["name"], "m": m, "n": n, "solver": c["kind"], "inner_passes": c["inner_passes"],
-                       "gap_tol": c["gap_tol"], "screening": True, "parallelism": f"column-sharded x{world} (NCCL)",
+                       "gap_tol": c["gap_tol"], "screening": True, "parallelism": f"column-sharded x{world}",
+                       "exchange": ("per-step reduction: fused reduce + peer-memory exchange kernel (CUDA IPC, "
+                                    "NVLink); per-round scalars: NCCL")
+                       if os.environ.get("BX_EXCHANGE", "fused") == "fused" else "NCCL allreduces",
                        "l2_policy": "inputs larger than L2",
                        "step": CFG4_STEP if args.config == 4 else "one full solve to certified gap <= gap_tol"},
             "time_to_gap_s": elapsed / args.steps, "converged": all(r.converged for r in results),

@@ -183,6 +183,17 @@ int bx_nccl_unique_id(unsigned char* id_out_host);
 int bx_ctx_set_comm(bx_ctx* ctx, const unsigned char* id_host, int32_t rank,
                     int32_t nranks, int64_t col_offset, int64_t n_global);
 
+/* fused reduce + peer exchange for the per-step reduction of the sharded
+ * PG / FISTA pass (replaces its NCCL allreduces with ONE kernel that stores
+ * each row block straight into every peer's buffer over NVLink and sums the
+ * peers' blocks in rank order; csrc/bx_exchange.cuh).  After attaching a
+ * communicator: bx_peer_alloc allocates this rank's receive buffer and
+ * exports its 64-byte CUDA IPC handle (handle_out may be NULL for the
+ * in-process group); bx_peer_open maps every rank's buffer from the
+ * nranks x 64 gathered handles (NULL: in-process group).  At most 8 ranks. */
+int bx_peer_alloc(bx_ctx* ctx, unsigned char* ipc_handle_out);
+int bx_peer_open(bx_ctx* ctx, const unsigned char* ipc_handles);
+
 /* in-process rank group: ranks are threads of one process sharing a GPU or
  * several; the allreduce is host-barrier + device sum (test transport of the
  * column-sharded path; production uses NCCL through bx_ctx_set_comm) */

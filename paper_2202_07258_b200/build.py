@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libboxscreen_b200.so")
 SOURCES = ["bx_core.cu"]
-HEADERS = ["bx_kernels.cuh", "bx_cd.cuh", "bx_batched.cuh", "bx_small.cuh", "bx_active.cuh"]
+HEADERS = ["bx_kernels.cuh", "bx_cd.cuh", "bx_batched.cuh", "bx_small.cuh", "bx_active.cuh", "bx_exchange.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 

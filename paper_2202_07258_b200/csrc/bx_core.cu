@@ -36,6 +36,7 @@
 #include "bx_batched.cuh"
 #include "bx_small.cuh"
 #include "bx_active.cuh"
+#include "bx_exchange.cuh"
 
 using namespace bx;
 
@@ -102,6 +103,13 @@ struct bx_group {
   int arrived = 0;
   long gen = 0;
   std::vector<const void*> ptrs;
+  // fused reduce + exchange emulated over all ranks in one cooperative launch
+  std::vector<void*> xbufs;    // each rank's exchange buffer (registered by bx_peer_open)
+  std::vector<XArgs> xargs;    // each rank's arguments of the current call
+  XArgs* xargs_dev = nullptr;  // device copy (rank 0 launches)
+  ~bx_group() {
+    if (xargs_dev) cudaFree(xargs_dev);
+  }
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const long my = gen;
@@ -120,6 +128,13 @@ struct Comm {
   // in-place allreduce of count elements on `stream`; returns 0 on success
   virtual int allreduce(void* buf, size_t count, int dtype, int op, cudaStream_t stream, std::string& err) = 0;
 };
+
+// receive buffer of the fused exchange: [2 parities][kXPeers][mp + kXExtra]
+// fp64, then the flags [kXPeers][nb_max] u32
+inline size_t xrecv_doubles(int64_t mp) { return (size_t)2 * kXPeers * (mp + kXExtra); }
+inline size_t xbuf_bytes(int64_t mp, int nb_max) {
+  return xrecv_doubles(mp) * 8 + (size_t)kXPeers * nb_max * 4;
+}
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
@@ -162,6 +177,42 @@ struct LocalComm : Comm {
     g->barrier();  // every rank has read every buffer
     cudaMemcpyAsync(buf, tmp, count * es, cudaMemcpyDeviceToDevice, stream);
     return 0;
+  }
+  // fused reduce + exchange of every rank in ONE cooperative launch over all
+  // ranks' buffers (ranks are threads on one GPU; no kernel waits on another)
+  int xreduce(XArgs mine, int nb_max, bool f32, cudaStream_t stream, std::string& err) {
+    if (cudaStreamSynchronize(stream) != cudaSuccess) {
+      err = "LocalComm: stream sync";
+      return 1;
+    }
+    g->xargs[rank] = mine;
+    g->barrier();
+    int rc = 0;
+    if (rank == 0) {
+      const int n = g->n;
+      for (int q = 0; q < n; ++q) {
+        XArgs& a = g->xargs[q];
+        for (int p = 0; p < n; ++p) {
+          char* base = static_cast<char*>(g->xbufs[p]);
+          a.recv[p] = reinterpret_cast<double*>(base);
+          a.flag[p] = reinterpret_cast<unsigned*>(base + xrecv_doubles(a.mp) * 8);
+        }
+        a.my_recv = a.recv[q];
+        a.my_flag = a.flag[q];
+      }
+      if (!g->xargs_dev && cudaMalloc(&g->xargs_dev, kXPeers * sizeof(XArgs)) != cudaSuccess) rc = 1;
+      if (!rc) cudaMemcpyAsync(g->xargs_dev, g->xargs.data(), n * sizeof(XArgs), cudaMemcpyHostToDevice, stream);
+      const XArgs* dev = g->xargs_dev;
+      int nb = mine.nb;
+      void* kargs[] = {(void*)&dev, (void*)&nb};
+      const void* fn = f32 ? (const void*)k_xreduce_group<float> : (const void*)k_xreduce_group<double>;
+      if (!rc && cudaLaunchCooperativeKernel(fn, dim3(n * nb), dim3(XT), kargs, 0, stream) != cudaSuccess) rc = 1;
+      if (!rc && cudaStreamSynchronize(stream) != cudaSuccess) rc = 1;
+      if (rc) err = "LocalComm: fused exchange launch";
+      (void)nb_max;
+    }
+    g->barrier();  // the results are in every rank's buffers
+    return rc;
   }
 };
 
@@ -257,6 +308,15 @@ struct bx_ctx {
   AsState* has = nullptr;       // pinned mirror
   bool as_dirty = true;         // the factor no longer matches the passive mask (compaction)
   int as_p = 0;                 // host copy of the factor size
+
+  // fused reduce + peer exchange (bx_peer_alloc / bx_peer_open)
+  int xmode = 0;                  // 0: collectives only, 1: IPC peers (GPUs), 2: in-process group
+  void* xbuf = nullptr;           // this rank's receive buffer + flags (cudaMalloc: IPC-exportable)
+  double* xpeer_recv[kXPeers] = {};
+  unsigned* xpeer_flag[kXPeers] = {};
+  std::vector<void*> xopened;     // IPC mappings to close
+  unsigned xepoch = 0;
+  int xnb = 1;
 
   // multi-GPU column sharding
   Comm* comm = nullptr;
@@ -653,7 +713,53 @@ int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, c
 }
 
 template <typename T>
+int run_xreduce(bx_ctx* c, int G, const double* off, double* out, int mode, const double* wpart, int Gw,
+                int counter) {
+  XArgs a;
+  memset(&a, 0, sizeof(a));
+  a.part = c->part;
+  a.ldp = c->ldp;
+  a.G = G;
+  a.m = c->m;
+  a.mp = c->mp;
+  a.off = off;
+  a.out = out;
+  a.sc = c->sc;
+  a.bpart = c->bpart2;
+  a.wpart = (wpart && Gw > 0) ? wpart : nullptr;
+  a.Gw = Gw;
+  a.stride = a.wpart ? (mode == R_APG ? 2 : 1) : 0;
+  a.mode = mode;
+  a.counter = counter;
+  a.rank = c->rank;
+  a.nranks = c->nranks;
+  a.nb = c->xnb;
+  a.epoch = ++c->xepoch;
+  const int e0 = prof_begin(c);
+  if (c->xmode == 2) {
+    std::string e;
+    if (static_cast<LocalComm*>(c->comm)->xreduce(a, c->nsm, sizeof(T) == 4, c->stream, e) != 0)
+      return fail(c, BX_ERR_CUDA, "%s", e.c_str());
+    ++c->launches;
+  } else {
+    for (int q = 0; q < c->nranks; ++q) {
+      a.recv[q] = c->xpeer_recv[q];
+      a.flag[q] = c->xpeer_flag[q];
+    }
+    a.my_recv = c->xpeer_recv[c->rank];
+    a.my_flag = c->xpeer_flag[c->rank];
+    void* kargs[] = {(void*)&a};
+    CU(cudaLaunchCooperativeKernel((const void*)k_xreduce<T>, dim3(c->xnb), dim3(XT), kargs, 0, c->stream));
+    LAUNCHED();
+  }
+  prof_end(c, e0, BX_PROF_REDUCE, (double)c->m * sizeof(T) * G + 8.0 * c->m * (2.0 * c->nranks + 1));
+  return BX_OK;
+}
+
+template <typename T>
 int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const double* wpart, int Gw, int counter) {
+  // column-sharded with the peer exchange attached: one fused kernel
+  if (c->sharded() && c->xmode) return run_xreduce<T>(c, G, off, out, mode, wpart, Gw, counter);
   const int64_t rb = 32 * (16 / (int64_t)sizeof(T));
   int nb = (int)((c->m + rb - 1) / rb);
   if (nb > 4 * c->nsm) nb = 4 * c->nsm;
@@ -1698,6 +1804,8 @@ int bx_ctx_destroy(bx_ctx* c) {
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->hsc) cudaFreeHost(c->hsc);
   if (c->has) cudaFreeHost(c->has);
+  for (void* p : c->xopened) cudaIpcCloseMemHandle(p);
+  if (c->xbuf) cudaFree(c->xbuf);
   delete c->comm;
   delete c;
   return BX_OK;
@@ -1845,6 +1953,60 @@ int bx_ctx_set_active_set_workspace(bx_ctx* c, void* workspace, size_t bytes) {
   if (!c->has) CU(cudaMallocHost((void**)&c->has, sizeof(AsState)));
   memset(c->has, 0, sizeof(AsState));
   c->as_dirty = true;
+  return BX_OK;
+}
+
+int bx_peer_alloc(bx_ctx* c, unsigned char* handle_out) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (!c->sharded()) return fail(c, BX_ERR_INVALID_ARGUMENT, "attach a communicator before bx_peer_alloc");
+  if (c->nranks > kXPeers) return fail(c, BX_ERR_UNSUPPORTED, "fused exchange: at most %d ranks", kXPeers);
+  if (!c->xbuf) {
+    const size_t bytes = xbuf_bytes(c->mp, c->nsm);
+    CU(cudaMalloc(&c->xbuf, bytes));
+    CU(cudaMemset(c->xbuf, 0, bytes));
+    CU(cudaDeviceSynchronize());
+  }
+  if (handle_out) {
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, c->xbuf));
+    memcpy(handle_out, &h, sizeof(h));
+  }
+  return BX_OK;
+}
+
+int bx_peer_open(bx_ctx* c, const unsigned char* handles) {
+  if (!c || !c->xbuf) return c ? fail(c, BX_ERR_INVALID_ARGUMENT, "bx_peer_alloc first") : BX_ERR_INVALID_ARGUMENT;
+  // CTAs of the fused reduction: row blocks of a multiple of XCH rows
+  auto fit_nb = [&](int64_t cap) {
+    const int64_t per = xrows_per_cta(c->m, (int)std::max<int64_t>(1, cap));
+    return (int)std::max<int64_t>(1, (c->m + per - 1) / per);
+  };
+  if (!handles) {
+    LocalComm* lc = dynamic_cast<LocalComm*>(c->comm);
+    if (!lc) return fail(c, BX_ERR_INVALID_ARGUMENT, "NULL handles need the in-process group");
+    lc->g->xbufs.resize(lc->g->n, nullptr);
+    lc->g->xargs.resize(lc->g->n);
+    lc->g->xbufs[c->rank] = c->xbuf;
+    // every emulated rank's CTAs must be co-resident in one cooperative grid
+    c->xnb = fit_nb(c->nsm / c->nranks);
+    c->xmode = 2;
+    return BX_OK;
+  }
+  for (int q = 0; q < c->nranks; ++q) {
+    void* p = nullptr;
+    if (q == c->rank) {
+      p = c->xbuf;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles + 64 * q, sizeof(h));
+      CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->xopened.push_back(p);
+    }
+    c->xpeer_recv[q] = static_cast<double*>(p);
+    c->xpeer_flag[q] = reinterpret_cast<unsigned*>(static_cast<char*>(p) + xrecv_doubles(c->mp) * 8);
+  }
+  c->xnb = fit_nb(c->nsm);
+  c->xmode = 1;
   return BX_OK;
 }
 

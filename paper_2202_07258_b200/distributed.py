@@ -14,10 +14,18 @@ dual_point / global_k).  Two transports behind one C++ interface:
   their own streams, synchronised by host barriers only -- the test transport
   that runs the exact sharded code path on a single GPU.
 
+The per-step reduction (the hot collective: once per PG / FISTA step) runs
+by default as ONE fused kernel per rank that reduces the pass's partial rows
+and exchanges them over peer memory (CUDA IPC mappings, NVLink / NVSwitch),
+``csrc/bx_exchange.cuh``; ``exchange="nccl"`` (or BX_EXCHANGE=nccl) keeps it
+on NCCL allreduces.  On the in-process group the fused exchange of all ranks
+runs as one cooperative launch over their buffers.
+
 Coordinate descent is sequential and is not sharded (replicas only).
 """
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -41,8 +49,15 @@ def shard(p, c0, c1):
     return Problem.from_device_storage(d["a"][c0:c1], p.m, d["y"], d["lo"][c0:c1], d["hi"][c0:c1])
 
 
+def _exchange(exchange):
+    ex = exchange or os.environ.get("BX_EXCHANGE", "fused")
+    if ex not in ("fused", "nccl"):
+        raise ValueError(f"exchange must be 'fused' or 'nccl', not {ex!r}")
+    return ex
+
+
 def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None,
-                return_shards=False):
+                return_shards=False, exchange=None):
     """Column-sharded solve with ``nranks`` ranks as threads on the current GPU."""
     import torch
     cfg = cfg or SolverConfig()
@@ -57,6 +72,8 @@ def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLo
             s = _Session(shard(p, c0, c1), tv=tv, stream=torch.cuda.Stream())
             s.attach_group(group, r, c0, p.n)
             sessions.append(s)
+            if _exchange(exchange) == "fused":
+                s.attach_peers()
 
         def work(r):
             try:
@@ -86,7 +103,7 @@ def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLo
 
 
 def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, tv=None, loss=QuadraticLoss,
-                      slack_scale=None, return_device=True, pg=None, profile=False):
+                      slack_scale=None, return_device=True, pg=None, profile=False, exchange=None):
     """This rank's part of an NCCL column-sharded solve (call on every rank of
     the torch.distributed group ``pg``).  Returns the rank-local result: x is
     the shard's block, trace / gap / theta are global."""
@@ -101,6 +118,12 @@ def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, t
     dist.broadcast_object_list(box, src=0, group=pg)
     with _Session(p_shard, tv=tv) as s:
         s.attach_nccl(box[0], rank, world, col_offset, n_global)
+        if _exchange(exchange) == "fused":
+            def gather(h):
+                hs = [None] * world
+                dist.all_gather_object(hs, h, group=pg)
+                return hs
+            s.attach_peers(gather)
         out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
         prof = s.profile
     return _result(n_global, out, tr, x, theta, sl, su, prof, return_device, n_total=n_global)

@@ -133,6 +133,21 @@ class _Session:
         nat.check(nat.lib().bx_ctx_set_comm(self.ctx, uid, rank, nranks, col_offset, n_global), self.ctx,
                   "bx_ctx_set_comm")
 
+    def attach_peers(self, gather=None):
+        """Fused reduce + peer exchange for the per-step reduction
+        (csrc/bx_exchange.cuh).  ``gather(handle_bytes) -> list of every
+        rank's handle`` for NCCL ranks (one GPU each); None for the
+        in-process group."""
+        L = nat.lib()
+        if gather is None:
+            nat.check(L.bx_peer_alloc(self.ctx, None), self.ctx, "bx_peer_alloc")
+            nat.check(L.bx_peer_open(self.ctx, None), self.ctx, "bx_peer_open")
+            return
+        h = ctypes.create_string_buffer(64)
+        nat.check(L.bx_peer_alloc(self.ctx, h), self.ctx, "bx_peer_alloc")
+        handles = b"".join(gather(h.raw))
+        nat.check(L.bx_peer_open(self.ctx, handles), self.ctx, "bx_peer_open")
+
     def __enter__(self):
         return self
 

@@ -20,12 +20,17 @@ p = Problem(inst.a, inst.y, inst.lower, inst.upper)
 cfg = SolverConfig(kind="apg", inner_passes=10, gap_tol=1e-6, max_rounds=300)
 ref = solve(p, cfg)
 c0, c1 = column_blocks(p.n, world)[rank]
-res = solve_distributed(shard(p, c0, c1), c0, p.n, cfg, return_device=False)
 orc = dict(trace=[dict(primal=t.primal, dual=t.dual, gap=t.gap, preserved=t.preserved_count) for t in ref.trace])
-probs = compare_traces(res, orc)
-dx = float(np.max(np.abs(res.x - ref.x[c0:c1]))) if c1 > c0 else 0.0
-ok = not probs and dx <= 1e-8 * max(1.0, float(np.max(np.abs(ref.x))))
-print(f"rank {rank}/{world}: rounds {res.rounds} vs {ref.rounds}, max|dx| {dx:.2e}, "
-      f"launches {res.info['kernel_launches']}, {'OK' if ok else 'MISMATCH ' + str(probs[:2])}", flush=True)
+ok = True
+# both transports of the per-step reduction: the fused reduce + peer
+# exchange kernel (CUDA IPC buffers) and the NCCL allreduce schedule
+for exchange in ("fused", "nccl"):
+    res = solve_distributed(shard(p, c0, c1), c0, p.n, cfg, return_device=False, exchange=exchange)
+    probs = compare_traces(res, orc)
+    dx = float(np.max(np.abs(res.x - ref.x[c0:c1]))) if c1 > c0 else 0.0
+    good = not probs and dx <= 1e-8 * max(1.0, float(np.max(np.abs(ref.x))))
+    ok = ok and good
+    print(f"rank {rank}/{world} [{exchange}]: rounds {res.rounds} vs {ref.rounds}, max|dx| {dx:.2e}, "
+          f"launches {res.info['kernel_launches']}, {'OK' if good else 'MISMATCH ' + str(probs[:2])}", flush=True)
 dist.destroy_process_group()
 sys.exit(0 if ok else 1)
