@@ -313,15 +313,36 @@ def metric_name(cfg_id):
             f"[config {cfg_id}]")
 
 
-def roofline_block(prof):
+NCU_TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def ncu_traffic(cfg_id):
+    """DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    dominant kernel from the committed `ncu --set full` capture of this
+    config (profiles/ncu_traffic.json, one launch), with that launch's
+    algorithmic bytes, so traffic / algorithmic shows any re-reads."""
+    try:
+        with open(NCU_TRAFFIC_PATH) as fh:
+            ent = json.load(fh)[str(cfg_id)]
+    except Exception:
+        return None, None
+    t = float(ent["dram_read_bytes"]) + float(ent["dram_write_bytes"])
+    info = {"traffic_source": ent["source"], "traffic_kernel": ent["kernel"],
+            "traffic_launch_algorithmic": ent.get("algorithmic"),
+            "traffic_over_algorithmic": (t / ent["algorithmic"]) if ent.get("algorithmic") else None}
+    return t, info
+
+
+def roofline_block(prof, cfg_id=None):
     hbm, peak_src, _ = peaks()
     prof = prof or {}
     tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
     dom_name = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
     dom = prof.get(dom_name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
     achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["ms"] > 0 else 0.0
-    return {"bound": "hbm", "kernel": f"k_pass[{dom_name}]", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+    traffic, tinfo = ncu_traffic(cfg_id)
+    out = {"bound": "hbm", "kernel": f"k_pass[{dom_name}]", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
             "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / max(1, dom["launches"]),
             "share_of_kernel_time": dom["ms"] / tot_ms,
             "bytes_per_launch_avg": dom["bytes"] / max(1, dom["launches"]),
@@ -330,6 +351,9 @@ def roofline_block(prof):
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                             "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
                         for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+    if tinfo:
+        out.update(tinfo)
+    return out
 
 
 def run_sharded(args, rank, world, dev):
@@ -377,7 +401,7 @@ def run_sharded(args, rank, world, dev):
     iters = sum(r.info["iterations"] for r in results)
     launches = sum(r.info["kernel_launches"] for r in results)
     prof_res = solve_distributed(p, c0, n, cfg, profile=True)
-    roof = roofline_block(prof_res.info["profile"])
+    roof = roofline_block(prof_res.info["profile"], args.config)
     e2e = None
     if not args.no_e2e:
         p_host = Problem(a_blk, y, lo, hi, dtype=dt, pin=True)
@@ -501,9 +525,10 @@ def run_batched(args, rank, world, dev):
     peak = dgemm_peak(dev)
     achieved = flops / el / 1e12
     roof = {"bound": "tensor", "kernel": "k_batched_round (DMMA.8x8x4)", "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": ncu_traffic(5)[0],
             "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (fp64 tensor cores)",
             "algorithmic_flops_per_round": (10 * 4.0 + 2 * 2.0) * m * n * kl}
+    roof.update(ncu_traffic(5)[1] or {})
     e2e = None
     if not args.no_e2e:
         a_pin = torch.from_numpy(a).pin_memory()
@@ -610,7 +635,7 @@ def run_ours(args):
 
     # live roofline of the dominant kernel (one extra, instrumented solve)
     prof_res = solve(p_dev, cfg, return_device=True, profile=True)
-    roof = roofline_block(prof_res.info["profile"])
+    roof = roofline_block(prof_res.info["profile"], args.config)
 
     # trajectory for the CPU arm (preserved-count bins of this solve)
     bins = k_bins_from_trace(prof_res.info["trace_arrays"], inst.inner_passes)

@@ -213,6 +213,30 @@ __device__ __forceinline__ float4 pack<float>(const float* o) {
   return make_float4(o[0], o[1], o[2], o[3]);
 }
 
+// packed fp32 FMA, SASS FFMA2 (sm_100a): d = a * b + c on two lanes, each
+// lane rounded exactly like a scalar fma.rn.f32
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+// acc[e] += a[e] * v[e], e < 4
+__device__ __forceinline__ void fma2_acc(float* acc, const float* a, const float* v) {
+  const float2 lo = ffma2(make_float2(a[0], a[1]), make_float2(v[0], v[1]), make_float2(acc[0], acc[1]));
+  const float2 hi = ffma2(make_float2(a[2], a[3]), make_float2(v[2], v[3]), make_float2(acc[2], acc[3]));
+  acc[0] = lo.x; acc[1] = lo.y; acc[2] = hi.x; acc[3] = hi.y;
+}
+// acc[e] += a[e] * c, e < 4
+__device__ __forceinline__ void fma2_axpy(float* acc, const float* a, float c) {
+  const float2 cc = make_float2(c, c);
+  const float2 lo = ffma2(make_float2(a[0], a[1]), cc, make_float2(acc[0], acc[1]));
+  const float2 hi = ffma2(make_float2(a[2], a[3]), cc, make_float2(acc[2], acc[3]));
+  acc[0] = lo.x; acc[1] = lo.y; acc[2] = hi.x; acc[3] = hi.y;
+}
+
 // V consecutive fp64 values -> registers of type T (16-byte vector loads)
 template <typename T>
 __device__ __forceinline__ void load_rows(const double* p, double* o) {
@@ -391,8 +415,9 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
             if (row + V <= m) {
               T av[V];
               unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
-#pragma unroll
-              for (int e = 0; e < V; ++e) dd[e] += av[e] * vr[i][e];
+              // packed fp32 FMA (FFMA2): same per-element fma.rn as the
+              // scalar chains, half the issue slots
+              fma2_acc(dd, av, vr[i]);
             } else if (row < m) {
               T av[V];
               unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
@@ -504,8 +529,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
               } else {
                 // rows >= m of the last vector only reach the padding of the
                 // partial row, which k_reduce never reads: no per-element guard
-#pragma unroll
-                for (int e = 0; e < V; ++e) acc[i][e] += av[e] * cc;
+                fma2_axpy(acc[i], av, cc);
               }
             }
           }
