@@ -51,8 +51,10 @@ struct BatchArgs {
   double rs_f, rs_g, slack_scale;
 };
 
+// not volatile: a pure function of its operands, so the compiler may
+// schedule it freely
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -68,19 +70,43 @@ struct BatchSmem {
   double* beta;  // [64]
 };
 
-__device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BatchSmem& s, int buf, int c, int k0,
-                                            const double* X, const double* Xp, bool with_x) {
+// This thread's 16-byte pieces of a dictionary chunk (16 columns x m rows),
+// decomposed once per kernel: the (column, row) split of a piece index is the
+// same for every chunk, so the per-chunk copy loop has no integer division.
+constexpr int BT_PMAX = (BT_CH * (BT_MT * 8 / 2) + BT_NT - 1) / BT_NT;
+struct BtPlan {
+  int jj[BT_PMAX];    // column within the chunk (BT_CH: no piece)
+  int soff[BT_PMAX];  // smem offset (doubles)
+  int goff[BT_PMAX];  // global offset from the chunk's first column (doubles)
+};
+__device__ __forceinline__ BtPlan bt_plan(const BatchArgs& a) {
+  BtPlan pl;
+  const int mv = (a.m + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < BT_PMAX; ++i) {
+    const int q = threadIdx.x + i * BT_NT;
+    const int jj = q < BT_CH * mv ? q / mv : BT_CH;
+    const int v = q - jj * mv;
+    pl.jj[i] = jj;
+    pl.soff[i] = jj * a.sa + 2 * v;
+    pl.goff[i] = (int)(jj * a.lda) + 2 * v;
+  }
+  return pl;
+}
+
+__device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BtPlan& pl, const BatchSmem& s, int buf, int c,
+                                            int k0, const double* X, const double* Xp, bool with_x) {
   const int j0 = c * BT_CH;
   const int nj = min(BT_CH, a.n - j0);
   // A chunk: 16 columns x m rows (16-byte pieces)
-  const int mv = (a.m + 1) / 2;
   double* ab = s.abuf + buf * BT_CH * a.sa;
-  for (int q = threadIdx.x; q < BT_CH * mv; q += BT_NT) {
-    const int jj = q / mv, v = q - jj * mv;
-    if (jj < nj)
-      cp_async16(ab + jj * a.sa + 2 * v, a.A + (int64_t)(j0 + jj) * a.lda + 2 * v);
-    else
-      *reinterpret_cast<double2*>(ab + jj * a.sa + 2 * v) = make_double2(0.0, 0.0);
+  const double* ag = a.A + (int64_t)j0 * a.lda;
+#pragma unroll
+  for (int i = 0; i < BT_PMAX; ++i) {
+    if (pl.jj[i] < nj)
+      cp_async16(ab + pl.soff[i], ag + pl.goff[i]);
+    else if (pl.jj[i] < BT_CH)
+      *reinterpret_cast<double2*>(ab + pl.soff[i]) = make_double2(0.0, 0.0);
   }
   if (with_x) {
     // x / x_prev chunks: 64 problems x 16 coordinates
@@ -124,26 +150,54 @@ __device__ __forceinline__ void bt_gemm1(const BatchArgs& a, const double* ab, c
 #pragma unroll
     for (int u = 0; u < 4; ++u) dmma(acc[u][0], acc[u][1], x0[u], b[u]);
   }
-  for (; kk < m4; ++kk) dmma(acc[0][0], acc[0][1], a0[4 * kk], rb[4 * kk]);
+  // remainder (m4 % 4 k-steps): warp-uniform, unrolled per count so no
+  // DMMA sits in a data-dependent loop
+  switch (m4 - kk) {
+    case 3: dmma(acc[2][0], acc[2][1], a0[4 * (kk + 2)], rb[4 * (kk + 2)]);  // fallthrough
+    case 2: dmma(acc[1][0], acc[1][1], a0[4 * (kk + 1)], rb[4 * (kk + 1)]);  // fallthrough
+    case 1: dmma(acc[0][0], acc[0][1], a0[4 * kk], rb[4 * kk]); break;
+    default: break;
+  }
 #pragma unroll
   for (int e = 0; e < 2; ++e) gt[e] = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
 }
 
 // acc (rows 8 (mlo + q) + g, problems n0 + 2 tig + e) += A_J X_J over this
-// warp's row half [mlo, mhi); K = 16 coordinates
-__device__ __forceinline__ void bt_gemm2(const BatchArgs& a, const double* ab, const double* xns, int n0, int g,
-                                         int tig, double (&acc)[BT_MH][2], int mlo, int mhi) {
+// warp's row half [mlo, mlo + NQ); K = 16 coordinates.  NQ is a compile-time
+// tile count: an unguarded, fully unrolled DMMA sequence (a per-tile guard
+// makes every DMMA predicated, and the compiler then brackets each one with
+// WARPSYNC + NOP)
+template <int NQ>
+__device__ __forceinline__ void bt_gemm2_n(const BatchArgs& a, const double* ab, const double* xns, int n0, int g,
+                                           int tig, double (&acc)[BT_MH][2], int mlo) {
+  const double* ag = ab + 8 * mlo + g;
 #pragma unroll
   for (int kk = 0; kk < BT_CH / 4; ++kk) {
     const int j = 4 * kk + tig;
     const double b = xns[(n0 + g) * BT_SX + j];
+    const double* aj = ag + j * a.sa;
 #pragma unroll
-    for (int q = 0; q < BT_MH; ++q) {
-      if (mlo + q < mhi) {
-        const double av = ab[j * a.sa + 8 * (mlo + q) + g];
-        dmma(acc[q][0], acc[q][1], av, b);
-      }
-    }
+    for (int q = 0; q < NQ; ++q) dmma(acc[q][0], acc[q][1], aj[8 * q], b);
+  }
+}
+__device__ __forceinline__ void bt_gemm2(const BatchArgs& a, const double* ab, const double* xns, int n0, int g,
+                                         int tig, double (&acc)[BT_MH][2], int mlo, int mhi) {
+  // warp-uniform dispatch on the tile count of this row half
+  switch (mhi - mlo) {
+    case 13: bt_gemm2_n<13>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 12: bt_gemm2_n<12>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 11: bt_gemm2_n<11>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 10: bt_gemm2_n<10>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 9: bt_gemm2_n<9>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 8: bt_gemm2_n<8>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 7: bt_gemm2_n<7>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 6: bt_gemm2_n<6>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 5: bt_gemm2_n<5>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 4: bt_gemm2_n<4>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 3: bt_gemm2_n<3>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 2: bt_gemm2_n<2>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    case 1: bt_gemm2_n<1>(a, ab, xns, n0, g, tig, acc, mlo); break;
+    default: break;
   }
 }
 
@@ -172,6 +226,7 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
     p += BT_TILE;
     s.mk = reinterpret_cast<uint32_t*>(p);
   }
+  const BtPlan pl = bt_plan(a);
   const int mt_n = (a.m + 7) / 8;
   const int mlo = mh ? BT_MH : 0, mhi = mh ? mt_n : min(BT_MH, mt_n);
   const int nch = (a.n + BT_CH - 1) / BT_CH;
@@ -213,12 +268,12 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       for (int q = 0; q < BT_MH; ++q) acc[q][0] = acc[q][1] = 0.0;
       double gdot[2] = {0.0, 0.0}, gsc[2] = {0.0, 0.0};
       const double bt0 = s.beta[n0 + 2 * tig], bt1 = s.beta[n0 + 2 * tig + 1];
-      bt_prefetch(a, s, 0, 0, k0, X, Xp, true);
+      bt_prefetch(a, pl, s, 0, 0, k0, X, Xp, true);
       for (int c = 0; c < nch; ++c) {
         const int buf = c & 1;
         cp_async_wait_all();
         __syncthreads();
-        if (c + 1 < nch) bt_prefetch(a, s, buf ^ 1, c + 1, k0, X, Xp, true);
+        if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, X, Xp, true);
         const double* ab = s.abuf + buf * BT_CH * a.sa;
         const double* xs = s.xs + buf * BT_TILE * BT_SX;
         const double* xps = s.xps + buf * BT_TILE * BT_SX;
@@ -324,12 +379,12 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       }
       // sweep 1: epsilon_k = max_j (v_jk)+ / |a_j't|, v = -A'r
       double emax[2] = {0.0, 0.0};
-      bt_prefetch(a, s, 0, 0, k0, X, nullptr, false);
+      bt_prefetch(a, pl, s, 0, 0, k0, X, nullptr, false);
       for (int c = 0; c < nch; ++c) {
         const int buf = c & 1;
         cp_async_wait_all();
         __syncthreads();
-        if (c + 1 < nch) bt_prefetch(a, s, buf ^ 1, c + 1, k0, X, nullptr, false);
+        if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, X, nullptr, false);
         double gt[2];
         bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, mh, g, tig, gt);
         const int j = c * BT_CH + 8 * mh + g;
@@ -380,12 +435,12 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       __shared__ int dirty;
       if (tid == 0) dirty = 0;
       if (a.screening) {
-        bt_prefetch(a, s, 0, 0, k0, X, nullptr, false);
+        bt_prefetch(a, pl, s, 0, 0, k0, X, nullptr, false);
         for (int c = 0; c < nch; ++c) {
           const int buf = c & 1;
           cp_async_wait_all();
           __syncthreads();
-          if (c + 1 < nch) bt_prefetch(a, s, buf ^ 1, c + 1, k0, X, nullptr, false);
+          if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, X, nullptr, false);
           double gt[2];
           bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, mh, g, tig, gt);
           const uint32_t* mk = s.mk + buf * BT_TILE;
@@ -416,12 +471,12 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
           double acc[BT_MH][2];
 #pragma unroll
           for (int q = 0; q < BT_MH; ++q) acc[q][0] = acc[q][1] = 0.0;
-          bt_prefetch(a, s, 0, 0, k0, Xw, nullptr, true);
+          bt_prefetch(a, pl, s, 0, 0, k0, Xw, nullptr, true);
           for (int c = 0; c < nch; ++c) {
             const int buf = c & 1;
             cp_async_wait_all();
             __syncthreads();
-            if (c + 1 < nch) bt_prefetch(a, s, buf ^ 1, c + 1, k0, Xw, nullptr, true);
+            if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, Xw, nullptr, true);
             // stage the chunk in the conflict-free layout of xns
             const double* xs = s.xs + buf * BT_TILE * BT_SX;
             const int nj = min(BT_CH, a.n - c * BT_CH);
