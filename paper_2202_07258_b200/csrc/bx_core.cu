@@ -1034,7 +1034,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   if (ncmax > SM_CMAX) return BX_OK;
   if (lp.max_rounds > 1 && (c->m + G - 1) / G > SM_NT) return BX_OK;
   const int colstride = (int)round_up(c->m, 2 * V);
-  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8 + 7 * SM_CMAX + SM_NT) * 8 + 256;
+  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8 + 7 * SM_CMAX + SM_NT + round_up(c->m, 8)) * 8 + 256;
   const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
   if (smem > c->smem_cap) return BX_OK;
   const int s = c->cur;

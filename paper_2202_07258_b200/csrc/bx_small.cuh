@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   double* cat = cnr + SM_CMAX;
   double* cg = cat + SM_CMAX;
   double* coff = cg + SM_CMAX;         // [SM_NT] z - y of the rows this CTA reduces
+  double* rv = coff + SM_NT;           // [m, padded] the dot vector of this step
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = a.m;
   const int G = gridDim.x, b = blockIdx.x;
@@ -156,44 +157,40 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   const int nrow = r_hi - r_lo;
   if (tid < nrow) coff[tid] = a.off[r_lo + tid];
 
-  auto dots = [&](const double (&vr)[R][V], double* gout) {
-    // all local columns at once: per-thread partial sums -> warp sums ->
-    // per-column fold over warps in order
-    for (int c0 = 0; c0 < ncol; c0 += 8) {
-      double d[8];
+  // dots of the local columns with rv (shared memory): one warp per column,
+  // lanes over 16-byte row vectors with two independent chains, then one
+  // butterfly -- no cross-warp fold
+  auto dots = [&](double* gout) {
+    const int nv = m / V;  // full vectors; the m % V tail goes to lane 0
+    for (int c = warp; c < ncol; c += NW) {
+      const T* col = cols + (size_t)c * a.colstride;
+      double s0 = 0.0, s1 = 0.0;
+      int vi = lane;
+      for (; vi + 32 < nv; vi += 64) {
+        T av[V], aw[V];
+        double rr[V], rw[V];
+        unpack<T>(*reinterpret_cast<const VT*>(col + vi * V), av);
+        unpack<T>(*reinterpret_cast<const VT*>(col + (vi + 32) * V), aw);
+        load_rows<T>(rv + vi * V, rr);
+        load_rows<T>(rv + (vi + 32) * V, rw);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        d[u] = 0.0;
-        if (c0 + u < ncol) {
-          const T* col = cols + (size_t)(c0 + u) * a.colstride;
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            const int row = row0 + i * (SM_NT * V);
-            if (row + V <= m) {  // full vector: no per-element guard
-              T av[V];
-              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
-#pragma unroll
-              for (int e = 0; e < V; ++e) d[u] += static_cast<double>(av[e]) * vr[i][e];
-            } else if (row < m) {
-              T av[V];
-              unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
-#pragma unroll
-              for (int e = 0; e < V; ++e)
-                if (row + e < m) d[u] += static_cast<double>(av[e]) * vr[i][e];
-            }
-          }
+        for (int e = 0; e < V; ++e) {
+          s0 += static_cast<double>(av[e]) * rr[e];
+          s1 += static_cast<double>(aw[e]) * rw[e];
         }
-        d[u] = warp_sum<double>(d[u]);
+      }
+      if (vi < nv) {
+        T av[V];
+        double rr[V];
+        unpack<T>(*reinterpret_cast<const VT*>(col + vi * V), av);
+        load_rows<T>(rv + vi * V, rr);
+#pragma unroll
+        for (int e = 0; e < V; ++e) s0 += static_cast<double>(av[e]) * rr[e];
       }
       if (lane == 0)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) red[warp * SM_CMAX + c0 + u] = d[u];
-    }
-    __syncthreads();
-    if (tid < ncol) {
-      double s = 0.0;
-      for (int w = 0; w < NW; ++w) s += red[w * SM_CMAX + tid];
-      gout[tid] = s;
+        for (int row = nv * V; row < m; ++row) s1 += static_cast<double>(col[row]) * rv[row];
+      const double sum = warp_sum<double>(s0 + s1);
+      if (lane == 0) gout[c] = sum;
     }
     __syncthreads();
   };
@@ -206,24 +203,18 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     const double* rprv = a.r[rc ^ 1];
     const double tn = (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom)) / 2.0;
     const double beta = (a.kind == 2) ? (t_mom - 1.0) / tn : 0.0;
-    // residual (or the extrapolated residual) in registers
-    double vr[R][V];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = row0 + i * (SM_NT * V);
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        double v = 0.0;
-        if (row + e < m) {
-          // written by other CTAs before the barrier: read through L2
-          v = __ldcg(&rcur[row + e]);
-          if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, __ldcg(&rprv[row + e]))));
-        }
-        vr[i][e] = v;
-      }
-    }
     const bool use_stored = (a.kind == 0 && gv && pass == 0);
-    if (!use_stored) dots(vr, gcol);
+    if (!use_stored) {
+      // residual (or the extrapolated residual) -> shared memory; written by
+      // other CTAs before the barrier: read through L2
+      for (int row = tid; row < m; row += SM_NT) {
+        double v = __ldcg(&rcur[row]);
+        if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, __ldcg(&rprv[row]))));
+        rv[row] = v;
+      }
+      __syncthreads();
+      dots(gcol);
+    }
     // local x update
     double gd = 0.0, gs = 0.0;
     if (tid < ncol) {
@@ -246,21 +237,26 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       cx[tid] = xn;
       cf[tid] = xn;
     }
-    // restart partials of this CTA (fixed order over its columns)
+    // restart partials of this CTA (fixed order: lane-strided, then one
+    // butterfly in warp 0)
     if (a.kind == 2) {
       rsx[tid] = gd;
       rsx[SM_NT + tid] = gs;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
       double s1 = 0.0, s2 = 0.0;
       if (a.kind == 2)
-        for (int c = 0; c < ncol; ++c) {
+        for (int c = lane; c < ncol; c += 32) {
           s1 += rsx[c];
           s2 += rsx[SM_NT + c];
         }
-      sc4[0] = s1;
-      sc4[1] = s2;
+      s1 = warp_sum<double>(s1);
+      s2 = warp_sum<double>(s2);
+      if (lane == 0) {
+        sc4[0] = s1;
+        sc4[1] = s2;
+      }
     }
     // local partial rows of A x+
     {
@@ -298,25 +294,17 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.bpart[4 * b + 2] = sc4[1];
     }
     grid_barrier(a.bar, ++epoch);
-    // distributed reduce of this CTA's rows: thread (row, slice)
+    // distributed reduce of this CTA's rows: one warp per row, lanes over
+    // the G partials (independent L2 loads), one butterfly
     double sq = 0.0;
-    if (nrow > 0) {
-      const int slices = SM_NT / nrow;
-      const int rr = tid % nrow, sl = tid / nrow;
+    for (int rr = warp; rr < nrow; rr += NW) {
       double s = 0.0;
-      if (sl < slices)
-        for (int q = sl; q < G; q += slices) s += __ldcg(&a.part[(int64_t)q * a.ldp + r_lo + rr]);
-      rowscr[tid] = s;
-      __syncthreads();
-      if (tid < nrow) {
-        double v = 0.0;
-        for (int q = 0; q < slices; ++q) v += rowscr[q * nrow + tid];
-        v = add_rn(v, coff[tid]);
-        a.r[rc ^ 1][r_lo + tid] = v;
-        sq = v * v;
-      }
+      for (int q = lane; q < G; q += 32) s += __ldcg(&a.part[(int64_t)q * a.ldp + r_lo + rr]);
+      s = warp_sum<double>(s);
+      const double v = add_rn(s, coff[rr]);
+      if (lane == 0) a.r[rc ^ 1][r_lo + rr] = v;
+      sq += v * v;
     }
-    sq = warp_sum<double>(sq);
     if (lane == 0) red[warp] = sq;
     __syncthreads();
     if (tid == 0) {
@@ -372,14 +360,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   // screening dot pass at the final x: g = A'r and the epsilon partial
   double ep = 0.0;
   if (a.do_dot) {
-    double vr[R][V];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = row0 + i * (SM_NT * V);
-#pragma unroll
-      for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? __ldcg(&a.r[rc][row + e]) : 0.0;
-    }
-    dots(vr, gcol);
+    for (int row = tid; row < m; row += SM_NT) rv[row] = __ldcg(&a.r[rc][row]);
+    __syncthreads();
+    dots(gcol);
     if (tid < ncol) {
       const double gj = gcol[tid];
       cg[tid] = gj;
