@@ -59,20 +59,46 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// per-column state of a block (x of the pass, lo, hi, ||a_j||): thread
+// f * CD_B + c loads field f of column c through L2 when the block is
+// prefetched and parks it in shared memory after the current block's axpy,
+// so the sequential update never waits on global memory.  x of pass p was
+// written by rank 0 in pass p - 1, several cluster barriers earlier.
+constexpr int CD_ST = 4;
+template <typename T>
+__device__ __forceinline__ double cd_state_load(const CdArgs<T>& a, int64_t blk, int pass) {
+  const int f = threadIdx.x / CD_B, c = threadIdx.x % CD_B;
+  const int64_t j = blk * CD_B + c;
+  if (f >= CD_ST || j >= a.k) return 0.0;
+  const double* src = f == 0 ? ((pass & 1) ? a.x2 : a.x) : (f == 1 ? a.lo : (f == 2 ? a.hi : a.nrm));
+  return __ldcg(src + j);
+}
+
 template <typename T>
 __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* gdst, int64_t blk, int64_t row0,
                                             int nrows) {
   // the block's 32 x 32 Gram matrix (fp64) rides along
   for (int q = threadIdx.x; q < CD_B * CD_B / 2; q += CD_NT) cp_async16(gdst + 2 * q, a.gram + blk * CD_B * CD_B + 2 * q);
-  // dst[c * rows_pad + i] = A[row0 + i, 32*blk + c]
   const int64_t c0 = blk * CD_B;
   const int nc = (int)min((int64_t)CD_B, a.k - c0);
+  // dst[c * rows_pad + i] = A[row0 + i, 32*blk + c]; (column, vector) of
+  // piece q advanced incrementally (no integer division per piece)
   constexpr int V = 16 / sizeof(T);
   const int nvec = (nrows + V - 1) / V;  // rows_per_cta is a multiple of V
-  const int rows_pad = a.rows_per_cta;
-  for (int q = threadIdx.x; q < nc * nvec; q += CD_NT) {
-    const int c = q / nvec, v = q - c * nvec;
-    cp_async16(dst + (int64_t)c * rows_pad + v * V, a.A + (c0 + c) * a.ld + row0 + v * V);
+  if (nvec > 0) {
+    const int rows_pad = a.rows_per_cta;
+    const int dc = CD_NT / nvec, dv = CD_NT - dc * nvec;
+    int c = threadIdx.x / nvec, v = threadIdx.x - c * nvec;
+    const T* src = a.A + c0 * a.ld + row0;
+    while (c < nc) {
+      cp_async16(dst + (int64_t)c * rows_pad + v * V, src + c * a.ld + v * V);
+      c += dc;
+      v += dv;
+      if (v >= nvec) {
+        v -= nvec;
+        ++c;
+      }
+    }
   }
   cp_async_commit();
 }
@@ -89,6 +115,8 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   double* part = reinterpret_cast<double*>(abuf1 + CD_B * rows_pad);  // [2][CD_B] partial dots
   double* gbuf = part + 2 * CD_B;                                       // [2][CD_B][CD_B] Gram blocks
   double* delta = gbuf + 2 * CD_B * CD_B;                               // [CD_B]
+  double* allpart = delta + CD_B;                                        // [2][NC][CD_B] pushed partial dots
+  double* cst = allpart + 2 * 16 * CD_B;                                 // [2][CD_ST][CD_B] column state
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t row0 = (int64_t)rank * rows_pad;
   const int nrows = (int)max((int64_t)0, min((int64_t)rows_pad, a.m - row0));
@@ -102,7 +130,11 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   }
   const int64_t nblk = (a.k + CD_B - 1) / CD_B;
   int64_t it = 0;  // global block counter (selects buffers)
-  if (nblk > 0) cd_prefetch(a, abuf0, gbuf, 0, row0, nrows);
+  double pfv = 0.0;  // per-column state of the prefetched block (threads < CD_ST * CD_B)
+  if (nblk > 0) {
+    cd_prefetch(a, abuf0, gbuf, 0, row0, nrows);
+    if (tid < CD_ST * CD_B) cst[tid] = cd_state_load(a, 0, 0);
+  }
   for (int pass = 0; pass < a.passes; ++pass) {
     for (int64_t blk = 0; blk < nblk; ++blk, ++it) {
       T* cur = (it & 1) ? abuf1 : abuf0;
@@ -119,7 +151,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           nb = 0;
           ++np;
         }
-        if (np < a.passes) cd_prefetch(a, nxt, gbuf + ((it + 1) & 1) * CD_B * CD_B, nb, row0, nrows);
+        if (np < a.passes) {
+          cd_prefetch(a, nxt, gbuf + ((it + 1) & 1) * CD_B * CD_B, nb, row0, nrows);
+          pfv = cd_state_load(a, nb, (int)np);
+        }
       }
       // partial dots: every thread multiplies its register rows with the block's
       // columns; a butterfly transpose-reduction leaves column c's warp sum in
@@ -152,10 +187,15 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         __shared__ double wpart[CD_NT / 32][CD_B];
         wpart[warp][lane] = pd[0];
         __syncthreads();
+        // push this CTA's partials into every CTA's slot [rank] (remote
+        // stores, made visible by the cluster barrier): the combine below
+        // then reads local shared memory only
+        double* slot = allpart + (it & 1) * 16 * CD_B + rank * CD_B;
         if (tid < CD_B) {
           double s = 0.0;
           for (int w = 0; w < CD_NT / 32; ++w) s += wpart[w][tid];
           mypart[tid] = s;
+          for (int q = 0; q < NC; ++q) cluster.map_shared_rank(slot, q)[tid] = s;
         }
       }
       cluster.sync();  // every CTA's partial dots are visible
@@ -164,21 +204,19 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       if (warp == 0) {
         double cdot = 0.0;
         if (lane < nc) {
-          for (int q = 0; q < NC; ++q) {
-            const double* rp = cluster.map_shared_rank(part + (it & 1) * CD_B, q);
-            cdot += rp[lane];
-          }
+          const double* ap = allpart + (it & 1) * 16 * CD_B + lane;
+          for (int q = 0; q < NC; ++q) cdot += ap[q * CD_B];
         }
         const int64_t j = c0 + lane;
-        const double* xin = (pass & 1) ? a.x2 : a.x;
         double* xout = (pass & 1) ? a.x : a.x2;
+        const double* cs = cst + (it & 1) * CD_ST * CD_B;
         double xj = 0.0, loj = 0.0, hij = 0.0;
         double sq = 1.0;
         if (lane < nc) {
-          xj = xin[j];
-          loj = a.lo[j];
-          hij = a.hi[j];
-          const double nj = a.nrm[j];
+          xj = cs[lane];
+          loj = cs[CD_B + lane];
+          hij = cs[2 * CD_B + lane];
+          const double nj = cs[3 * CD_B + lane];
           sq = nj * nj;  // solvers.py:60 (col_norms ** 2)
         }
         // Gram row of this lane's coordinate in registers; the chain per
@@ -210,6 +248,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         }
         delta[lane] = dl;
         if (lane < nc && rank == 0) xout[j] = xj;
+        // one block per pass: the next block's x is this block's output,
+        // which every CTA has just computed redundantly
+        if (nblk == 1) cst[((it + 1) & 1) * CD_ST * CD_B + lane] = xj;
       }
       __syncthreads();
       // r += A_J delta_J on this CTA's rows
@@ -225,6 +266,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           rr[q] = acc;
         }
       }
+      // the next block's column state (its buffer was last read by warp 0
+      // two blocks ago)
+      if (tid < CD_ST * CD_B && (nblk > 1 || tid >= CD_B)) cst[((it + 1) & 1) * CD_ST * CD_B + tid] = pfv;
       __syncthreads();
     }
   }

@@ -938,7 +938,7 @@ int cd_sweeps(bx_ctx* c, int passes) {
   constexpr int V = 16 / sizeof(T);
   int NC = 8;
   int64_t rows = round_up((c->m + NC - 1) / NC, V);
-  const size_t fixed = (2 * CD_B + 2 * CD_B * CD_B + CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
+  const size_t fixed = (2 * CD_B + 2 * CD_B * CD_B + CD_B + 2 * 16 * CD_B + 2 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
   auto smem_for = [&](int64_t r) { return 2 * CD_B * (size_t)r * sizeof(T) + fixed; };
   if (rows > CD_NT * CD_RMAX || smem_for(rows) > c->smem_cap) {
     NC = 16;
