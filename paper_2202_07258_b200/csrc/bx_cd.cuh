@@ -229,20 +229,18 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
 #pragma unroll
         for (int i = 0; i < CD_B; ++i) {
           if (i < nc) {
-            double di = 0.0;
-            if (lane == i) {
-              const double step = cdot * isq;                          // solvers.py:131
-              double nv = xj - step;                                   // solvers.py:132
-              nv = nv < loj ? loj : nv;
-              nv = nv > hij ? hij : nv;
-              const double dt = nv - xj;                               // solvers.py:133
-              if (dt != 0.0) {
-                di = dt;
-                xj = nv;
-              }
-              dl = di;
-            }
-            di = __shfl_sync(0xffffffffu, di, i);
+            // every lane evaluates its tentative coordinate step (no
+            // divergence); only lane i's -- whose dot now carries the
+            // corrections of all earlier coordinates -- is broadcast and kept
+            const double step = cdot * isq;                            // solvers.py:131
+            double nv = xj - step;                                     // solvers.py:132
+            nv = nv < loj ? loj : nv;
+            nv = nv > hij ? hij : nv;
+            const double dt = nv - xj;                                 // solvers.py:133
+            const double di = __shfl_sync(0xffffffffu, dt, i);
+            const bool me = lane == i;
+            xj = (me && dt != 0.0) ? nv : xj;
+            dl = me ? dt : dl;
             cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
           }
         }
