@@ -999,6 +999,7 @@ int launch_small_R(bx_ctx* c, SmallArgs& a, int G, size_t smem) {
   auto kern = k_round_small<T, R>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&a};
+  CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), c->stream));  // the launch's barrier counter
   const int e0 = prof_begin(c);
   CU(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(SM_NT), args, smem, c->stream));
   LAUNCHED();

@@ -71,24 +71,27 @@ struct SmallArgs {
   double alpha;
 };
 
-// Grid barrier: a counter + generation word (sense reversal); all CTAs are
-// co-resident (cooperative launch).  Measured faster on B200 than per-CTA
-// flags polled by one warp (148 acquire loads per poll).
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned /*epoch*/) {
+// Grid barrier: one monotonic arrival counter per launch (zeroed by the host
+// before the launch); the n-th barrier of the launch completes when the
+// counter reaches n * gridDim.x.  Arrival is a fire-and-forget reduction
+// after the release fence and the wait polls with acquire loads -- no
+// generation word to read first and no reset inside the kernel (one L2 round
+// trip less per barrier than a sense-reversal barrier).  All CTAs are
+// co-resident (cooperative launch).
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& nbar) {
   __syncthreads();
+  ++nbar;
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g0 = *gen;
     __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g0) {
-      }
+    atomicAdd(bar, 1u);
+    const unsigned target = nbar * gridDim.x;
+    while (ld_acquire_gpu(bar) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   __syncthreads();
 
   double eta = a.sc->eta;
-  unsigned epoch = a.epoch0;
+  unsigned nbar = 0;  // grid barriers passed in this launch
   double t_mom = a.sc->mom_t;
   double P = a.sc->P;
   int rc = a.rc;
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.bpart[4 * b + 1] = sc4[0];
       a.bpart[4 * b + 2] = sc4[1];
     }
-    grid_barrier(a.bar, ++epoch);
+    grid_barrier(a.bar, nbar);
     // distributed reduce of this CTA's rows: one warp per row, lanes over
     // the G partials (independent L2 loads), one butterfly
     double sq = 0.0;
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       for (int w = 0; w < NW; ++w) s += red[w];
       a.bpart[4 * b + 0] = s;
     }
-    grid_barrier(a.bar, ++epoch);
+    grid_barrier(a.bar, nbar);
     // every CTA folds the same values in the same order -> same decision
     if (warp == 0) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     break;
   }
   // ---- device dual point (driver.py:423-441), gap, stop and sphere tests ----
-  grid_barrier(a.bar, 0);
+  grid_barrier(a.bar, nbar);
   if (warp == 0) {
     double e = 0.0;
     for (int q = lane; q < G; q += 32) e = fmax(e, __ldcg(&a.epart[q]));
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.dpart[8 * b + tid] = acc;
     }
   }
-  grid_barrier(a.bar, 0);
+  grid_barrier(a.bar, nbar);
   if (warp == 0) {
     double t1 = 0.0, t2 = 0.0, t3 = 0.0, t4 = 0.0;
     for (int q = lane; q < G; q += 32) {
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   }
   nscr = __syncthreads_count(nscr);
   if (tid == 0) a.dpart[8 * b + 4] = (double)nscr;
-  grid_barrier(a.bar, 0);
+  grid_barrier(a.bar, nbar);
   if (warp == 0) {
     double c = 0.0;
     for (int q = lane; q < G; q += 32) c += __ldcg(&a.dpart[8 * q + 4]);
