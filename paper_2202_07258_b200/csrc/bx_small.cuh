@@ -73,8 +73,8 @@ struct SmallArgs {
 
 // Grid barrier: one monotonic arrival counter per launch (zeroed by the host
 // before the launch); the n-th barrier of the launch completes when the
-// counter reaches n * gridDim.x.  Arrival is a fire-and-forget reduction
-// after the release fence and the wait polls with acquire loads -- no
+// counter reaches n * gridDim.x.  Arrival is a fire-and-forget release
+// reduction and the wait polls with acquire loads -- no
 // generation word to read first and no reset inside the kernel (one L2 round
 // trip less per barrier than a sense-reversal barrier).  All CTAs are
 // co-resident (cooperative launch).
@@ -87,8 +87,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& nbar) {
   __syncthreads();
   ++nbar;
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    // release-reduction: orders this CTA's prior writes (made visible to
+    // thread 0 by the CTA barrier) before the arrival, without a full fence
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     const unsigned target = nbar * gridDim.x;
     while (ld_acquire_gpu(bar) < target) {
     }
@@ -200,6 +201,12 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
 
   int done_rounds = 0, event = 0;
   bool perr = false;
+  // this thread's rows (tid + q * SM_NT) of the current and the previous
+  // residual, loaded right after the barrier that completes them -- in the
+  // same L2 round trip as the objective fold instead of one after it
+  constexpr int PR = R * V;
+  double pr[PR], pp[PR];
+  bool have_pre = false;
   for (int rnd = 0; rnd < a.max_rounds; ++rnd) {
   for (int pass = 0; pass < a.passes; ++pass) {
     const double* rcur = a.r[rc];
@@ -210,10 +217,22 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     if (!use_stored) {
       // residual (or the extrapolated residual) -> shared memory; written by
       // other CTAs before the barrier: read through L2
-      for (int row = tid; row < m; row += SM_NT) {
-        double v = __ldcg(&rcur[row]);
-        if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, __ldcg(&rprv[row]))));
-        rv[row] = v;
+      if (have_pre) {
+#pragma unroll
+        for (int q = 0; q < PR; ++q) {
+          const int row = tid + q * SM_NT;
+          if (row < m) {
+            double v = pr[q];
+            if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, pp[q])));
+            rv[row] = v;
+          }
+        }
+      } else {
+        for (int row = tid; row < m; row += SM_NT) {
+          double v = __ldcg(&rcur[row]);
+          if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, __ldcg(&rprv[row]))));
+          rv[row] = v;
+        }
       }
       __syncthreads();
       dots(gcol);
@@ -316,6 +335,17 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.bpart[4 * b + 0] = s;
     }
     grid_barrier(a.bar, nbar);
+    // the next step's residual rows: r just completed (r[rc ^ 1]) and the
+    // previous one (r[rc]), issued before the fold below
+#pragma unroll
+    for (int q = 0; q < PR; ++q) {
+      const int row = tid + q * SM_NT;
+      if (row < m) {
+        pr[q] = __ldcg(&a.r[rc ^ 1][row]);
+        pp[q] = (a.kind == 2) ? __ldcg(&a.r[rc][row]) : 0.0;
+      }
+    }
+    have_pre = true;
     // every CTA folds the same values in the same order -> same decision
     if (warp == 0) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -363,7 +393,13 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   // screening dot pass at the final x: g = A'r and the epsilon partial
   double ep = 0.0;
   if (a.do_dot) {
-    for (int row = tid; row < m; row += SM_NT) rv[row] = __ldcg(&a.r[rc][row]);
+    if (have_pre) {
+#pragma unroll
+      for (int q = 0; q < PR; ++q)
+        if (tid + q * SM_NT < m) rv[tid + q * SM_NT] = pr[q];
+    } else {
+      for (int row = tid; row < m; row += SM_NT) rv[row] = __ldcg(&a.r[rc][row]);
+    }
     __syncthreads();
     dots(gcol);
     if (tid < ncol) {
