@@ -333,6 +333,14 @@ def ncu_traffic(cfg_id):
     return t, info
 
 
+KERNEL_NAMES = {"cd": "k_cd (block-exact cyclic CD on an 8-CTA cluster)",
+                "small_round": "k_round_small (cooperative SM-resident PG/FISTA round)"}
+
+
+def kernel_name(key):
+    return KERNEL_NAMES.get(key, f"k_pass[{key}]")
+
+
 def roofline_block(prof, cfg_id=None):
     hbm, peak_src, _ = peaks()
     prof = prof or {}
@@ -341,7 +349,7 @@ def roofline_block(prof, cfg_id=None):
     dom = prof.get(dom_name, {"ms": 0.0, "bytes": 0.0, "launches": 0})
     achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["ms"] > 0 else 0.0
     traffic, tinfo = ncu_traffic(cfg_id)
-    out = {"bound": "hbm", "kernel": f"k_pass[{dom_name}]", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+    out = {"bound": "hbm", "kernel": kernel_name(dom_name), "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
             "launches": dom["launches"], "avg_launch_us": 1e3 * dom["ms"] / max(1, dom["launches"]),
             "share_of_kernel_time": dom["ms"] / tot_ms,

@@ -218,7 +218,8 @@ enum {
   BX_PROF_GATHER = 9,
   BX_PROF_CD = 10,
   BX_PROF_ACTIVE = 11,     /* active-set selection / factor update / solve  */
-  BX_PROF_SLOTS = 12
+  BX_PROF_SMALL = 12,      /* cooperative SM-resident round kernel (small problems) */
+  BX_PROF_SLOTS = 13
 };
 typedef struct {
   int64_t launches;

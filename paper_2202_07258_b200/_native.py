@@ -46,9 +46,9 @@ class ProfEntry(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
-PROF_SLOTS = 12
+PROF_SLOTS = 13
 PROF_NAMES = ["pass_dot", "pass_pg_g", "pass_pg", "pass_apg", "pass_power", "pass_ax", "reduce", "dual",
-              "sphere", "gather", "cd", "active"]
+              "sphere", "gather", "cd", "active", "small_round"]
 
 class BatchedOut(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("converged", ctypes.c_int64), ("iterations", ctypes.c_int64),

@@ -1003,7 +1003,7 @@ int launch_small_R(bx_ctx* c, SmallArgs& a, int G, size_t smem) {
   const int e0 = prof_begin(c);
   CU(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(SM_NT), args, smem, c->stream));
   LAUNCHED();
-  prof_end(c, e0, BX_PROF_PASS_PG, (double)a.passes * (double)a.k * a.m * sizeof(T));
+  prof_end(c, e0, BX_PROF_SMALL, (double)a.passes * (double)a.k * a.m * sizeof(T));
   return BX_OK;
 }
 
