@@ -4,7 +4,7 @@
  * `boxscreen` package, arXiv 2202.07258).
  *
  * The reference has no FFI: its solver dispatch is the string if/elif at
- * /root/reference/pkg/src/boxscreen/driver.py:411-418 over the kinds listed at
+ * /root/reference/pkg/src/boxscreen/driver.py:171-178 over the kinds listed at
  * solvers.py:17, operating on the Workspace state contract of
  * solvers.py:48-69.  Every entry point below replaces one reference symbol;
  * the symbol is cited beside it.  A Python binding of exactly these entry
@@ -66,7 +66,7 @@ typedef enum { BX_PG = 0, BX_CD = 1, BX_APG = 2, BX_ACTIVE_SET = 3 } bx_kind;
 
 typedef struct bx_ctx bx_ctx;
 
-/* SolverConfig (solvers.py:20-35) + the solve() flags (driver.py:371). */
+/* SolverConfig (solvers.py:20-35) + the solve() flags (driver.py:131). */
 typedef struct {
   int32_t kind;          /* bx_kind                                              */
   int32_t inner_passes;  /* >= 1                                                 */
@@ -82,7 +82,7 @@ typedef struct {
                             DESIGN.md); 0: absolute gap (reference rule)        */
 } bx_solve_cfg;
 
-/* TraceRecord (driver.py:268-278) plus the dual-point internals. */
+/* TraceRecord (driver.py:28-38) plus the dual-point internals. */
 typedef struct {
   int64_t round;
   double elapsed;
@@ -117,9 +117,9 @@ typedef void (*bx_start_vector_fn)(int64_t k, int64_t seed, double* out_host, vo
 /* bytes of device scratch a context of this shape needs */
 size_t bx_workspace_bytes(int64_t m, int64_t n, int32_t dtype);
 
-/* Problem (model.py:47-99) + ScreeningState (screening.py:221-230) +
- * TranslationVector (duality.py:339-357).  `t` may be NULL: neg-ones
- * (duality.py:372-373).  Validates zero columns (ZeroColumn) and, when some
+/* Problem (model.py:47-99) + ScreeningState (screening.py:27-36) +
+ * TranslationVector (duality.py:41-59).  `t` may be NULL: neg-ones
+ * (duality.py:74-75).  Validates zero columns (ZeroColumn) and, when some
  * upper bound is infinite, strict interiority (NoInteriorPoint). */
 int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype,
                   const void* a, int64_t lda, const void* y,
@@ -132,36 +132,36 @@ const char* bx_last_error(const bx_ctx* ctx);
 
 /* column norms ||a_j|| (model.py:89-92), length n, fp64 */
 int bx_col_norms(bx_ctx* ctx, void* out);
-/* A't (duality.py:350), length n, fp64 */
+/* A't (duality.py:52), length n, fp64 */
 int bx_att(bx_ctx* ctx, void* out);
 /* spectral_norm_estimate on the preserved columns (solvers.py:72-86) */
 int bx_power_iter(bx_ctx* ctx, int32_t iters, const double* v0_host, double* sigma_out);
 /* reset the primal point to clip(0, l, u) and rebuild the workspace
- * (driver.py:389, solvers.py:54-65) */
+ * (driver.py:149, solvers.py:54-65) */
 int bx_reset(bx_ctx* ctx);
 /* `passes` primal passes of the given kind on the preserved set:
  * pg_step (solvers.py:101-116), cd_sweep (:119-137), FISTA */
 int bx_primal_passes(bx_ctx* ctx, int32_t kind, double eta, int32_t passes);
 /* dual point + reduced gap + (optionally) the sphere test for the current
- * iterate: driver.py:423-441 and 453-461.  out_scalars_host receives
+ * iterate: driver.py:183-201 and 453-461.  out_scalars_host receives
  * {primal, dual, gap, eps, radius, slack, n_new_lower, n_new_upper}. */
 int bx_dual_screen(bx_ctx* ctx, int32_t screening, double slack_scale, double* out_scalars_host);
 /* apply_screening (screening.py:72-94) + Workspace.refresh (solvers.py:54-65):
  * snaps screened x to bounds, updates z, compacts A and the per-column state
  * (ballot/prefix-sum), recomputes the residual. */
 int bx_compact(bx_ctx* ctx);
-/* _certified_gap on the full problem (driver.py:352-357 ->
- * duality.py:457-507); out_host = {gap, primal, dual, eps} */
+/* _certified_gap on the full problem (driver.py:112-117 ->
+ * duality.py:159-209); out_host = {gap, primal, dual, eps} */
 int bx_certified_gap(bx_ctx* ctx, double* out_host);
 /* preserved count, and the preserved original indices (int32, device) */
 int64_t bx_preserved_count(const bx_ctx* ctx);
 
-/* ---- the Algorithm-1 loop (driver.py:371-496) ---------------------------- */
+/* ---- the Algorithm-1 loop (driver.py:131-256) ---------------------------- */
 int bx_solve(bx_ctx* ctx, const bx_solve_cfg* cfg, bx_start_vector_fn start_fn,
              void* start_user, bx_trace_rec* trace_host, int64_t trace_cap,
              bx_solve_out* out_host);
 
-/* final state (SolveResult, driver.py:281-290): x (n, fp64), theta
+/* final state (SolveResult, driver.py:41-50): x (n, fp64), theta
  * (m, fp64), sat_lower / sat_upper (int64, in screening order).  Any
  * pointer may be NULL.  Device pointers. */
 int bx_get_state(bx_ctx* ctx, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper);
@@ -233,7 +233,7 @@ int bx_get_profile(bx_ctx* ctx, bx_prof_entry* out_host, int32_t n);
 /* K independent NNLS problems sharing one dictionary A (m <= 208), FISTA with
  * per-problem gap-safe screening, both products on fp64 tensor cores (DMMA);
  * semantics in oracle/batched_oracle.py.  Not in the reference (it solves one
- * right-hand side per solve() call, driver.py:371). */
+ * right-hand side per solve() call, driver.py:131). */
 typedef struct bx_batch bx_batch;
 typedef struct {
   int64_t rounds, converged, iterations, kernel_launches;

@@ -15,7 +15,7 @@ Gap-safe screening, with two batched simplifications:
   (a smaller preserved set only makes it more conservative);
 * screening masks instead of compaction: a screened coordinate of problem k
   is fixed at its bound (0) and frozen; the dual point and the gap are those
-  of the FULL problem (epsilon over all columns, duality.py:485-507), so each
+  of the FULL problem (epsilon over all columns, duality.py:187-209), so each
   round's gap is already the certified one.
 
 Per round (inner_passes FISTA steps, then the dual point at x):

@@ -46,9 +46,9 @@ import math
 import numpy as np
 import scipy.linalg as sla
 
-GAP_ROUNDOFF = 1e-9          # duality.py:322 (weak-duality round-off slack)
+GAP_ROUNDOFF = 1e-9          # duality.py:24 (weak-duality round-off slack)
 SLACK_SCALE = 1e-12          # driver.py:219
-INTERIOR_TOL = 1e-10         # duality.py:346 (strict_tol)
+INTERIOR_TOL = 1e-10         # duality.py:48 (strict_tol)
 RESTART_SLACK = 1e-12        # FISTA restart threshold (extension)
 
 
@@ -93,7 +93,7 @@ def safe_step(a, alpha=1.0, iters=50):
 
 
 def translation_att(a, t, norms):
-    """A't with the strict-interiority check (duality.py:346-357)."""
+    """A't with the strict-interiority check (duality.py:48-59)."""
     att = a.T @ t
     if np.any(att >= -INTERIOR_TOL * norms):
         raise OracleError("NoInteriorPoint", f"max a_j't = {att.max():.3e}")
@@ -101,14 +101,14 @@ def translation_att(a, t, norms):
 
 
 def clamp(gap):
-    """duality.py:450-454."""
+    """duality.py:152-156."""
     if gap < -GAP_ROUNDOFF:
         raise OracleError("InternalConsistency", f"duality gap {gap:.3e}")
     return max(gap, 0.0)
 
 
 # --------------------------------------------------------------------------
-# the full-problem certificate (driver.py:112-117 -> duality.py:457-507)
+# the full-problem certificate (driver.py:112-117 -> duality.py:159-209)
 # --------------------------------------------------------------------------
 
 def certified_gap(a, y, lo, hi, inf_mask, x, t=None, att=None):
@@ -122,7 +122,7 @@ def certified_gap(a, y, lo, hi, inf_mask, x, t=None, att=None):
     else:
         theta = zg
         atth = atz
-    # dual objective (duality.py:401-422) with the quadratic conjugate
+    # dual objective (duality.py:103-124) with the quadratic conjugate
     u = -theta
     d = -float(np.sum(u * y + 0.5 * u * u))
     d -= float(lo @ np.minimum(atth, 0.0))
@@ -321,7 +321,7 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
     att_full = None
     if inf_mask.any():
         # the translation vector is built before the screening state
-        # (driver.py:381-392), so NoInteriorPoint precedes ZeroColumn
+        # (driver.py:141-152), so NoInteriorPoint precedes ZeroColumn
         t = -np.ones(m) if t is None else np.asarray(t, dtype=float).ravel()
         att_full = translation_att(a, t, norms)
     if np.any(norms == 0.0):

@@ -3,18 +3,18 @@
 // the kernels of bx_kernels.cuh launched on the context's stream.
 //
 // Reference mapping (file:line in /root/reference/pkg/src/boxscreen):
-//   bx_ctx_create     Problem (model.py:55-87), ScreeningState (screening.py:221-230),
-//                     TranslationVector (duality.py:346-357)
+//   bx_ctx_create     Problem (model.py:55-87), ScreeningState (screening.py:27-36),
+//                     TranslationVector (duality.py:48-59)
 //   refresh()         Workspace.refresh (solvers.py:54-65)
 //   primal_passes()   pg_step (solvers.py:101-116), cd_sweep (solvers.py:119-137),
 //                     FISTA extension
-//   dual_screen()     driver.py:423-441 (dual point, reduced dual, clamp_gap) and
-//                     driver.py:453-461 (radius, slack, safe_screen_test)
+//   dual_screen()     driver.py:183-201 (dual point, reduced dual, clamp_gap) and
+//                     driver.py:213-221 (radius, slack, safe_screen_test)
 //   compact()         apply_screening (screening.py:72-94) + refresh + step
-//                     re-estimate (driver.py:462-475)
-//   certified()       _certified_gap (driver.py:352-357)
+//                     re-estimate (driver.py:222-235)
+//   certified()       _certified_gap (driver.py:112-117)
 //   as_step()         active_set_step (solvers.py:151-204), bx_active.cuh
-//   bx_solve          solve (driver.py:371-496)
+//   bx_solve          solve (driver.py:131-256)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -1314,7 +1314,7 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
   return BX_OK;
 }
 
-// _certified_gap (driver.py:352-357): full-problem A x, A'(y - A x), epsilon
+// _certified_gap (driver.py:112-117): full-problem A x, A'(y - A x), epsilon
 // over all infinite-upper columns, dual objective
 template <typename T>
 int certified(bx_ctx* c, double alpha) {
@@ -1482,7 +1482,7 @@ int create_typed(bx_ctx* c, const void* y, const void* lower, const void* upper,
   if (bits & 16) return fail(c, BX_ERR_INVALID_ARGUMENT, "need lower_j < upper_j for every coordinate");
   c->bound_bits = bits;
   c->has_inf = (bits & 4) ? 1 : 0;
-  // translation vector: neg-ones unless given (duality.py:372-373)
+  // translation vector: neg-ones unless given (duality.py:74-75)
   CU(cudaMemsetAsync(c->t, 0, c->mp * sizeof(double), c->stream));
   if (t) {
     CU(cudaMemcpyAsync(c->t, t, m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -1499,7 +1499,7 @@ int create_typed(bx_ctx* c, const void* y, const void* lower, const void* upper,
   CU(cudaMemcpyAsync(&cf, c->probe, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   // reported by bx_solve (after agreeing across ranks): the reference raises
-  // these from solve(), driver.py:381-392
+  // these from solve(), driver.py:141-152
   c->col_bits = cf;
   return BX_OK;
 }
@@ -1518,7 +1518,7 @@ int validate(bx_ctx* c) {
   c->has_inf = f[0] ? 1 : 0;
   c->bound_bits = (c->bound_bits & ~3) | (f[1] ? 1 : 0) | (f[2] ? 2 : 0);
   // the translation vector is built before the screening state
-  // (driver.py:381-392), so NoInteriorPoint takes precedence over ZeroColumn
+  // (driver.py:141-152), so NoInteriorPoint takes precedence over ZeroColumn
   if (c->has_inf && f[4]) return fail(c, BX_ERR_NO_INTERIOR, "strategy did not yield a strictly interior t");
   if (f[3]) return fail(c, BX_ERR_ZERO_COLUMN, "zero column in A");
   return BX_OK;
@@ -1713,7 +1713,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       break;
     }
   }
-  // x_full <- current preserved iterate (ws.sync, driver.py:492)
+  // x_full <- current preserved iterate (ws.sync, driver.py:252)
   k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], (const double*)c->x[c->cur], (double*)c->xfull);
   LAUNCHED();
   CU(cudaStreamSynchronize(c->stream));

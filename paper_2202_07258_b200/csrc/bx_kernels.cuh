@@ -17,9 +17,9 @@
 //              objective, the StepSizeTooLarge guard (solvers.py:111-114) or
 //              the FISTA restart test.
 //   k_dual     dual translation/scaling + reduced dual + gap clamp + radius +
-//              slack (driver.py:423-441, 453-459; duality.py:452-454).
+//              slack (driver.py:183-201, 453-459; duality.py:154-156).
 //   k_sphere / k_scan / k_compact / k_gather
-//              gap-safe sphere test (screening.py:254-263) with warp-ballot /
+//              gap-safe sphere test (screening.py:60-69) with warp-ballot /
 //              block prefix-sum compaction of the preserved set and the
 //              physical rewrite of A_act (solvers.py:57).
 #pragma once
@@ -747,8 +747,8 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
 // ----------------------------------------------------------------------------
 // k_dual: dual point, reduced dual objective, clamped gap, radius, slack
 // ----------------------------------------------------------------------------
-// _reduced_dual (driver.py:360-368) / eval_dual (duality.py:401-422), clamp_gap
-// (duality.py:452), radius (screening.py:11-15), slack (driver.py:459)
+// _reduced_dual (driver.py:120-128) / eval_dual (duality.py:103-124), clamp_gap
+// (duality.py:154), radius (screening.py:11-15), slack (driver.py:219)
 __device__ __forceinline__ void dual_finalize(DevScalars* sc, int which, double t1, double t2, double t3, double t4,
                                               double eps, double slack_scale, double alpha) {
   DualOut* out = which ? &sc->cert : &sc->act;
@@ -796,15 +796,15 @@ __global__ void __launch_bounds__(RT) k_dual(const T* __restrict__ r, const T* _
   double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
   const int64_t stride = (int64_t)gridDim.x * RT;
   for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < m; i += stride) {
-    T th = -r[i];  // driver.py:424
-    if (eps > 0.0) th = add_rn(th, mul_rn(te, t[i]));  // driver.py:434-435
+    T th = -r[i];  // driver.py:184
+    if (eps > 0.0) th = add_rn(th, mul_rn(te, t[i]));  // driver.py:194-195
     theta[i] = th;
     s1 += static_cast<double>(th) * static_cast<double>(tgt[i]);
     s2 += static_cast<double>(th) * static_cast<double>(th);
   }
   for (int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x; j < k; j += stride) {
-    T vj = -g[j];  // driver.py:425
-    if (has_inf) vj = add_rn(vj, mul_rn(te, att[j]));  // driver.py:436
+    T vj = -g[j];  // driver.py:185
+    if (has_inf) vj = add_rn(vj, mul_rn(te, att[j]));  // driver.py:196
     v[j] = vj;
     const double vd = static_cast<double>(vj);
     s3 += static_cast<double>(lo[j]) * fmin(vd, 0.0);
@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(1024) k_scan(int32_t* bcnt, int nb, DevScalars
 
 // scatter by flag: kept columns -> compacted per-column state (order kept);
 // screened -> x_full snapped to its bound, the (column, bound) list for the
-// z update, and the global sat_lower / sat_upper lists (screening.py:278-288)
+// z update, and the global sat_lower / sat_upper lists (screening.py:84-94)
 template <typename T>
 struct ColState {
   int32_t* idx;
@@ -1050,7 +1050,7 @@ __global__ void __launch_bounds__(RT) k_gather(const T* __restrict__ A, int64_t 
 }
 
 // per-column statistics of the original matrix: ||a_j|| (model.py:89-92) and
-// a_j' t (duality.py:350); flags zero columns and non-interior t
+// a_j' t (duality.py:52); flags zero columns and non-interior t
 template <typename T>
 __global__ void __launch_bounds__(RT) k_colstats(const T* __restrict__ A, int64_t lda, int64_t n, int64_t m,
                                                  const double* __restrict__ t, double* __restrict__ nrm,
@@ -1085,7 +1085,7 @@ __global__ void k_init_cols(int64_t n, const T* __restrict__ lo, const T* __rest
                             const T* __restrict__ nrm, T* __restrict__ nrm2, const T* __restrict__ att,
                             T* __restrict__ att2) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const T x0 = clip<T>(T(0), lo[j], hi[j]);  // driver.py:389
+    const T x0 = clip<T>(T(0), lo[j], hi[j]);  // driver.py:149
     x_full[j] = x0;
     x[j] = x0;
     idx[j] = static_cast<int32_t>(j);

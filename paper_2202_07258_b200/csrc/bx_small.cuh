@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     event = 1;
     break;
   }
-  // ---- device dual point (driver.py:423-441), gap, stop and sphere tests ----
+  // ---- device dual point (driver.py:183-201), gap, stop and sphere tests ----
   grid_barrier(a.bar, nbar);
   if (warp == 0) {
     double e = 0.0;

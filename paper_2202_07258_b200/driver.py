@@ -68,7 +68,7 @@ TRACE_CSV_COLUMNS = ("round", "elapsed_s", "primal", "dual", "gap", "preserved",
 
 
 def trace_to_csv(trace, path):
-    """Byte-compatible with driver.py:312-320."""
+    """Byte-compatible with driver.py:72-80."""
     with open(path, "w", newline="") as fh:
         writer = csv.writer(fh)
         writer.writerow(TRACE_CSV_COLUMNS)
@@ -251,7 +251,7 @@ def _result(p_n, out, tr, x, theta, sl, su, prof, return_device, n_total=None):
 
 
 def _default_slack(p):
-    # driver.py:459 for fp64; fp32 sphere tests need a slack above the fp32
+    # driver.py:219 for fp64; fp32 sphere tests need a slack above the fp32
     # round-off of a_j'theta (~sqrt(m) * 6e-8 ||theta||): 1e-4 ||theta||
     return 1e-12 if p.dtype == np.float64 else 1e-4
 
@@ -260,7 +260,7 @@ def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=
           profile=False):
     """Run the chosen primal solver with (or without) dynamic safe screening.
 
-    Same contract as the reference's ``solve`` (driver.py:371-496).  With
+    Same contract as the reference's ``solve`` (driver.py:131-256).  With
     ``return_device`` the result's x / theta stay CUDA tensors (no host copy);
     ``profile`` times every kernel launch with CUDA events (info["profile"]).
     """

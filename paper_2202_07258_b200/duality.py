@@ -21,7 +21,7 @@ STRATEGIES = ("neg-ones", "neg-column", "neg-mean-column", "solve-linear", "cust
 
 
 def clamp_gap(gap):
-    """duality.py:450-454."""
+    """duality.py:152-156."""
     from .errors import InternalConsistency
     if gap < -GAP_ROUNDOFF:
         raise InternalConsistency(f"duality gap {gap:.3e} below round-off slack")
