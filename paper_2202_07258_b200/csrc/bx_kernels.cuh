@@ -17,7 +17,7 @@
 //              objective, the StepSizeTooLarge guard (solvers.py:111-114) or
 //              the FISTA restart test.
 //   k_dual     dual translation/scaling + reduced dual + gap clamp + radius +
-//              slack (driver.py:183-201, 453-459; duality.py:154-156).
+//              slack (driver.py:183-201, 213-219; duality.py:154-156).
 //   k_sphere / k_scan / k_compact / k_gather
 //              gap-safe sphere test (screening.py:60-69) with warp-ballot /
 //              block prefix-sum compaction of the preserved set and the
