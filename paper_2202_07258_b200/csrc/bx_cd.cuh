@@ -65,6 +65,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // so the sequential update never waits on global memory.  x of pass p was
 // written by rank 0 in pass p - 1, several cluster barriers earlier.
 constexpr int CD_ST = 4;
+// field 3 is stashed as 1 / ||a_j||^2 (col_norms ** 2, solvers.py:60), so the
+// division is off the sequential update's critical path; zero-padded
+// columns past k stash 1 (never used)
+__device__ __forceinline__ double cd_isq(double nj) { return nj == 0.0 ? 1.0 : 1.0 / (nj * nj); }
 template <typename T>
 __device__ __forceinline__ double cd_state_load(const CdArgs<T>& a, int64_t blk, int pass) {
   const int f = threadIdx.x / CD_B, c = threadIdx.x % CD_B;
@@ -133,7 +137,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   double pfv = 0.0;  // per-column state of the prefetched block (threads < CD_ST * CD_B)
   if (nblk > 0) {
     cd_prefetch(a, abuf0, gbuf, 0, row0, nrows);
-    if (tid < CD_ST * CD_B) cst[tid] = cd_state_load(a, 0, 0);
+    if (tid < CD_ST * CD_B) {
+      const double v = cd_state_load(a, 0, 0);
+      cst[tid] = tid >= 3 * CD_B ? cd_isq(v) : v;
+    }
   }
   for (int pass = 0; pass < a.passes; ++pass) {
     for (int64_t blk = 0; blk < nblk; ++blk, ++it) {
@@ -216,15 +223,14 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           xj = cs[lane];
           loj = cs[CD_B + lane];
           hij = cs[2 * CD_B + lane];
-          const double nj = cs[3 * CD_B + lane];
-          sq = nj * nj;  // solvers.py:60 (col_norms ** 2)
+          sq = cs[3 * CD_B + lane];  // 1 / ||a_j||^2, stashed with the column state
         }
         // Gram row of this lane's coordinate in registers; the chain per
         // coordinate is then multiply, clip, subtract, one shuffle and one FMA
         double grow[CD_B];
 #pragma unroll
         for (int i = 0; i < CD_B; ++i) grow[i] = gcur[lane * CD_B + i];
-        const double isq = 1.0 / sq;
+        const double isq = sq;
         double dl = 0.0;
 #pragma unroll
         for (int i = 0; i < CD_B; ++i) {
@@ -232,8 +238,8 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
             // every lane evaluates its tentative coordinate step (no
             // divergence); only lane i's -- whose dot now carries the
             // corrections of all earlier coordinates -- is broadcast and kept
-            const double step = cdot * isq;                            // solvers.py:131
-            double nv = xj - step;                                     // solvers.py:132
+            // x - (a.r)/||a||^2 as one fused multiply-add (solvers.py:131-132)
+            double nv = fma(-cdot, isq, xj);
             nv = nv < loj ? loj : nv;
             nv = nv > hij ? hij : nv;
             const double dt = nv - xj;                                 // solvers.py:133
@@ -266,7 +272,8 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       }
       // the next block's column state (its buffer was last read by warp 0
       // two blocks ago)
-      if (tid < CD_ST * CD_B && (nblk > 1 || tid >= CD_B)) cst[((it + 1) & 1) * CD_ST * CD_B + tid] = pfv;
+      if (tid < CD_ST * CD_B && (nblk > 1 || tid >= CD_B))
+        cst[((it + 1) & 1) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
       __syncthreads();
     }
   }
