@@ -45,7 +45,7 @@ struct CdArgs {
   const double* lo;
   const double* hi;
   const double* nrm; // ||a_j||  (sq = nrm^2, as solvers.py:60)
-  const double* gram;  // [nblocks][B][B] Gram blocks (fp64)
+  const double* gram;  // [nblocks][2][B][B]: G_JJ = A_J'A_J and X_J = A_next(J)'A_J (fp64)
   double* r;         // residual (in/out, m)
   DevScalars* sc;
   int passes;
@@ -58,12 +58,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // per-column state of a block (x of the pass, lo, hi, ||a_j||): thread
-// f * CD_B + c loads field f of column c through L2 when the block is
-// prefetched and parks it in shared memory after the current block's axpy,
-// so the sequential update never waits on global memory.  x of pass p was
-// written by rank 0 in pass p - 1, several cluster barriers earlier.
+// f * CD_B + c loads field f of column c through L2 one block ahead and parks
+// it in shared memory at the end of the current block, so the sequential
+// update never waits on global memory.  x of pass p was written by rank 0 in
+// pass p - 1, several cluster barriers earlier.
 constexpr int CD_ST = 4;
 // field 3 is stashed as 1 / ||a_j||^2 (col_norms ** 2, solvers.py:60), so the
 // division is off the sequential update's critical path; zero-padded
@@ -78,11 +79,16 @@ __device__ __forceinline__ double cd_state_load(const CdArgs<T>& a, int64_t blk,
   return __ldcg(src + j);
 }
 
+// rows of a CTA are owned by warps 1..7 (warp 0 runs the sequential update):
+// thread t >= 32 owns rows (t - 32) + q * CD_RT
+constexpr int CD_RT = CD_NT - 32;
+
 template <typename T>
 __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* gdst, int64_t blk, int64_t row0,
                                             int nrows) {
-  // the block's 32 x 32 Gram matrix (fp64) rides along
-  for (int q = threadIdx.x; q < CD_B * CD_B / 2; q += CD_NT) cp_async16(gdst + 2 * q, a.gram + blk * CD_B * CD_B + 2 * q);
+  // the block's Gram matrix and its cross-Gram with the next block ride along
+  for (int q = threadIdx.x; q < 2 * CD_B * CD_B / 2; q += CD_NT)
+    cp_async16(gdst + 2 * q, a.gram + blk * 2 * CD_B * CD_B + 2 * q);
   const int64_t c0 = blk * CD_B;
   const int nc = (int)min((int64_t)CD_B, a.k - c0);
   // dst[c * rows_pad + i] = A[row0 + i, 32*blk + c]; (column, vector) of
@@ -107,6 +113,21 @@ __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* 
   cp_async_commit();
 }
 
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// Software-pipelined block-exact CD: while warp 0 runs block J's sequential
+// update, warps 1..7 compute block J+1's partial dots against the residual
+// that still lacks block J's move, and push them to every CTA of the
+// cluster; warp 0 then adds the missing term with the cross-Gram block
+//     d_{J+1} = A_{J+1}'(r + A_J delta_J) = A_{J+1}'r + X_J delta_J,
+// (exact arithmetic identity) before r += A_J delta_J.  Three shared-memory
+// slots: block J (axpy), J+1 (dots), J+2 (in flight).
 template <typename T>
 __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -114,175 +135,210 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   const int NC = (int)cluster.num_blocks();
   extern __shared__ __align__(1024) unsigned char smem[];
   const int rows_pad = a.rows_per_cta;
-  T* abuf0 = reinterpret_cast<T*>(smem);
-  T* abuf1 = abuf0 + CD_B * rows_pad;
-  double* part = reinterpret_cast<double*>(abuf1 + CD_B * rows_pad);  // [2][CD_B] partial dots
-  double* gbuf = part + 2 * CD_B;                                       // [2][CD_B][CD_B] Gram blocks
-  double* delta = gbuf + 2 * CD_B * CD_B;                               // [CD_B]
-  double* allpart = delta + CD_B;                                        // [2][NC][CD_B] pushed partial dots
-  double* cst = allpart + 2 * 16 * CD_B;                                 // [2][CD_ST][CD_B] column state
+  T* abuf = reinterpret_cast<T*>(smem);                                      // [3][CD_B][rows_pad]
+  double* gbuf = reinterpret_cast<double*>(abuf + 3 * CD_B * rows_pad);     // [3][2][CD_B][CD_B]
+  double* part = gbuf + 3 * 2 * CD_B * CD_B;                                // [2] scratch
+  double* delta = part + 2;                                                 // [CD_B]
+  double* allpart = delta + CD_B;                                           // [2][16][CD_B] pushed partial dots
+  double* cst = allpart + 2 * 16 * CD_B;                                    // [3][CD_ST][CD_B] column state
+  __shared__ double wpart[CD_NT / 32][CD_B];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t row0 = (int64_t)rank * rows_pad;
   const int nrows = (int)max((int64_t)0, min((int64_t)rows_pad, a.m - row0));
+  const int rt = tid - 32;  // row thread index (warps 1..7)
 
-  // residual rows in registers: thread owns rows tid + q*CD_NT
+  // residual rows in registers (warps 1..7)
   double rr[CD_RMAX];
 #pragma unroll
   for (int q = 0; q < CD_RMAX; ++q) {
-    const int i = tid + q * CD_NT;
-    rr[q] = (i < nrows) ? a.r[row0 + i] : 0.0;
+    const int i = rt + q * CD_RT;
+    rr[q] = (rt >= 0 && i < nrows) ? a.r[row0 + i] : 0.0;
   }
   const int64_t nblk = (a.k + CD_B - 1) / CD_B;
-  int64_t it = 0;  // global block counter (selects buffers)
-  double pfv = 0.0;  // per-column state of the prefetched block (threads < CD_ST * CD_B)
-  if (nblk > 0) {
-    cd_prefetch(a, abuf0, gbuf, 0, row0, nrows);
-    if (tid < CD_ST * CD_B) {
-      const double v = cd_state_load(a, 0, 0);
-      cst[tid] = tid >= 3 * CD_B ? cd_isq(v) : v;
+  const int64_t total = nblk * a.passes;  // blocks over all passes, in order
+  auto slot_a = [&](int64_t it) { return abuf + ((int)it % 3) * CD_B * rows_pad; };
+  auto slot_g = [&](int64_t it) { return gbuf + ((int)it % 3) * 2 * CD_B * CD_B; };
+  // 32-bit block / pass of a global block index (nblk <= 2^26 columns / 32)
+  const int nb32 = (int)nblk;
+  auto blk_of = [&](int64_t it) { return (int64_t)((int)it % nb32); };
+  auto pass_of = [&](int64_t it) { return (int)it / nb32; };
+
+  // partial dots of block `it` over this CTA's rows -> pushed into slot
+  // parity(it) of every CTA (warps 1..7; named barrier 1 among them)
+  auto dots_push = [&](int64_t it) {
+    const T* cur = slot_a(it);
+    const int nc = (int)min((int64_t)CD_B, a.k - blk_of(it) * CD_B);
+    double pd[CD_B];
+#pragma unroll
+    for (int c = 0; c < CD_B; ++c) pd[c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < CD_RMAX; ++q) {
+      const int i = rt + q * CD_RT;
+      if (i < nrows) {
+        const double rv = rr[q];
+#pragma unroll
+        for (int c = 0; c < CD_B; ++c)
+          if (c < nc) pd[c] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * rv;
+      }
     }
+    // butterfly transpose-reduction: column c's warp sum lands in lane c
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int q = 0; q < o; ++q) {
+        const double send = upper ? pd[q] : pd[q + o];
+        const double keep = upper ? pd[q + o] : pd[q];
+        pd[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    wpart[warp][lane] = pd[0];
+    asm volatile("bar.sync 1, %0;" ::"r"(CD_RT) : "memory");
+    if (warp == 1) {
+      double s = 0.0;
+      for (int w = 1; w < CD_NT / 32; ++w) s += wpart[w][lane];
+      double* slot = allpart + (it & 1) * 16 * CD_B + rank * CD_B;
+      for (int q = 0; q < NC; ++q) cluster.map_shared_rank(slot, q)[lane] = s;
+    }
+  };
+  // warp 0: combine the pushed partials of block `it` in rank order
+  auto combine = [&](int64_t it) {
+    const double* ap = allpart + (it & 1) * 16 * CD_B + lane;
+    double d = 0.0;
+    for (int q = 0; q < NC; ++q) d += ap[q * CD_B];
+    return d;
+  };
+
+  double pfv = 0.0;   // column state of the block after next (threads < CD_ST * CD_B)
+  double cdot = 0.0;  // warp 0: the current block's dot, lane = column
+  if (total > 0) {
+    // prologue: blocks 0 and 1 in flight, block 0's column state, block 0's dots
+    cd_prefetch(a, slot_a(0), slot_g(0), blk_of(0), row0, nrows);
+    if (total > 1) cd_prefetch(a, slot_a(1), slot_g(1), blk_of(1), row0, nrows);
+    if (tid < CD_ST * CD_B) {
+      const double v = cd_state_load(a, blk_of(0), pass_of(0));
+      cst[tid] = tid >= 3 * CD_B ? cd_isq(v) : v;
+      if (total > 1) {
+        const double w = cd_state_load(a, blk_of(1), pass_of(1));
+        cst[CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(w) : w;
+      }
+    }
+    if (total > 1) cp_async_wait_1(); else cp_async_wait_all();
+    __syncthreads();
+    if (warp == 0) {
+      cluster_arrive_relaxed();
+    } else {
+      dots_push(0);
+      cluster_arrive_release();
+    }
+    cluster_wait();
+    if (warp == 0) cdot = combine(0);
   }
-  for (int pass = 0; pass < a.passes; ++pass) {
-    for (int64_t blk = 0; blk < nblk; ++blk, ++it) {
-      T* cur = (it & 1) ? abuf1 : abuf0;
-      T* nxt = (it & 1) ? abuf0 : abuf1;
-      const int64_t c0 = blk * CD_B;
-      const int nc = (int)min((int64_t)CD_B, a.k - c0);
-      cp_async_wait_all();
-      const double* gcur = gbuf + (it & 1) * CD_B * CD_B;
-      __syncthreads();
-      // prefetch the next block while this one is processed
-      {
-        int64_t nb = blk + 1, np = pass;
-        if (nb == nblk) {
-          nb = 0;
-          ++np;
-        }
-        if (np < a.passes) {
-          cd_prefetch(a, nxt, gbuf + ((it + 1) & 1) * CD_B * CD_B, nb, row0, nrows);
-          pfv = cd_state_load(a, nb, (int)np);
+  for (int64_t it = 0; it < total; ++it) {
+    const int64_t blk = blk_of(it);
+    const int pass = pass_of(it);
+    const int64_t c0 = blk * CD_B;
+    const int nc = (int)min((int64_t)CD_B, a.k - c0);
+    const bool has_next = it + 1 < total;
+    // block it+1's data (issued one iteration ago) must have landed
+    cp_async_wait_all();
+    __syncthreads();
+    if (it + 2 < total) {
+      cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows);
+      pfv = cd_state_load(a, blk_of(it + 2), pass_of(it + 2));
+    }
+    if (warp == 0) {
+      cluster_arrive_relaxed();  // warp 0 publishes nothing this phase
+      // ---- sequential block update (lane = column), redundantly per CTA ----
+      const int64_t j = c0 + lane;
+      double* xout = (pass & 1) ? a.x : a.x2;
+      const double* cs = cst + (it % 3) * CD_ST * CD_B;
+      double xj = 0.0, loj = 0.0, hij = 0.0, isq = 1.0;
+      if (lane < nc) {
+        xj = cs[lane];
+        loj = cs[CD_B + lane];
+        hij = cs[2 * CD_B + lane];
+        isq = cs[3 * CD_B + lane];  // 1 / ||a_j||^2
+      }
+      const double* gcur = slot_g(it);
+      double grow[CD_B];
+#pragma unroll
+      for (int i = 0; i < CD_B; ++i) grow[i] = gcur[lane * CD_B + i];
+      double dl = 0.0;
+#pragma unroll
+      for (int i = 0; i < CD_B; ++i) {
+        if (i < nc) {
+          // every lane evaluates its tentative coordinate step (no
+          // divergence); only lane i's -- whose dot now carries the
+          // corrections of all earlier coordinates -- is broadcast and kept
+          double nv = fma(-cdot, isq, xj);  // x - (a.r)/||a||^2 (solvers.py:131-132)
+          nv = nv < loj ? loj : nv;
+          nv = nv > hij ? hij : nv;
+          const double dt = nv - xj;  // solvers.py:133
+          const double di = __shfl_sync(0xffffffffu, dt, i);
+          const bool me = lane == i;
+          xj = (me && dt != 0.0) ? nv : xj;
+          dl = me ? dt : dl;
+          cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
         }
       }
-      // partial dots: every thread multiplies its register rows with the block's
-      // columns; a butterfly transpose-reduction leaves column c's warp sum in
-      // lane c (31 shuffles instead of 32 x 5)
-      double* mypart = part + (it & 1) * CD_B;
-      {
-        double pd[CD_B];
+      delta[lane] = dl;
+      if (lane < nc && rank == 0) xout[j] = xj;
+      // short passes (<= 3 blocks): the x this block produces is read again
+      // within the state look-ahead; every CTA computed it redundantly, so
+      // it goes straight into the slot of block it + nblk
+      if (nblk <= 3 && it + nblk < total) cst[((it + nblk) % 3) * CD_ST * CD_B + lane] = xj;
+    } else {
+      // ---- block it+1's partial dots against r without delta_it ----
+      if (has_next) dots_push(it + 1);
+      cluster_arrive_release();
+    }
+    cluster_wait();
+    if (warp == 0 && has_next) {
+      // d_{it+1} = pushed partial dots + X_it delta_it (rank order, then the
+      // cross-Gram term in column order)
+      __syncwarp();  // delta[] of every lane
+      double d = combine(it + 1);
+      const double* xg = slot_g(it) + CD_B * CD_B + lane * CD_B;
+      double corr = 0.0;
 #pragma unroll
-        for (int c = 0; c < CD_B; ++c) pd[c] = 0.0;
-#pragma unroll
-        for (int q = 0; q < CD_RMAX; ++q) {
-          const int i = tid + q * CD_NT;
-          if (i < nrows) {
-            const double rv = rr[q];
-#pragma unroll
-            for (int c = 0; c < CD_B; ++c)
-              if (c < nc) pd[c] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * rv;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const bool upper = (lane & o) != 0;
-#pragma unroll
-          for (int q = 0; q < o; ++q) {
-            const double send = upper ? pd[q] : pd[q + o];
-            const double keep = upper ? pd[q + o] : pd[q];
-            pd[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-          }
-        }
-        __shared__ double wpart[CD_NT / 32][CD_B];
-        wpart[warp][lane] = pd[0];
-        __syncthreads();
-        // push this CTA's partials into every CTA's slot [rank] (remote
-        // stores, made visible by the cluster barrier): the combine below
-        // then reads local shared memory only
-        double* slot = allpart + (it & 1) * 16 * CD_B + rank * CD_B;
-        if (tid < CD_B) {
-          double s = 0.0;
-          for (int w = 0; w < CD_NT / 32; ++w) s += wpart[w][tid];
-          mypart[tid] = s;
-          for (int q = 0; q < NC; ++q) cluster.map_shared_rank(slot, q)[tid] = s;
-        }
-      }
-      cluster.sync();  // every CTA's partial dots are visible
-      // combine partial dots of all CTAs in rank order, then the sequential
-      // block update on warp 0 (lane = column), redundantly in every CTA
-      if (warp == 0) {
-        double cdot = 0.0;
-        if (lane < nc) {
-          const double* ap = allpart + (it & 1) * 16 * CD_B + lane;
-          for (int q = 0; q < NC; ++q) cdot += ap[q * CD_B];
-        }
-        const int64_t j = c0 + lane;
-        double* xout = (pass & 1) ? a.x : a.x2;
-        const double* cs = cst + (it & 1) * CD_ST * CD_B;
-        double xj = 0.0, loj = 0.0, hij = 0.0;
-        double sq = 1.0;
-        if (lane < nc) {
-          xj = cs[lane];
-          loj = cs[CD_B + lane];
-          hij = cs[2 * CD_B + lane];
-          sq = cs[3 * CD_B + lane];  // 1 / ||a_j||^2, stashed with the column state
-        }
-        // Gram row of this lane's coordinate in registers; the chain per
-        // coordinate is then multiply, clip, subtract, one shuffle and one FMA
-        double grow[CD_B];
-#pragma unroll
-        for (int i = 0; i < CD_B; ++i) grow[i] = gcur[lane * CD_B + i];
-        const double isq = sq;
-        double dl = 0.0;
-#pragma unroll
-        for (int i = 0; i < CD_B; ++i) {
-          if (i < nc) {
-            // every lane evaluates its tentative coordinate step (no
-            // divergence); only lane i's -- whose dot now carries the
-            // corrections of all earlier coordinates -- is broadcast and kept
-            // x - (a.r)/||a||^2 as one fused multiply-add (solvers.py:131-132)
-            double nv = fma(-cdot, isq, xj);
-            nv = nv < loj ? loj : nv;
-            nv = nv > hij ? hij : nv;
-            const double dt = nv - xj;                                 // solvers.py:133
-            const double di = __shfl_sync(0xffffffffu, dt, i);
-            const bool me = lane == i;
-            xj = (me && dt != 0.0) ? nv : xj;
-            dl = me ? dt : dl;
-            cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
-          }
-        }
-        delta[lane] = dl;
-        if (lane < nc && rank == 0) xout[j] = xj;
-        // one block per pass: the next block's x is this block's output,
-        // which every CTA has just computed redundantly
-        if (nblk == 1) cst[((it + 1) & 1) * CD_ST * CD_B + lane] = xj;
-      }
-      __syncthreads();
-      // r += A_J delta_J on this CTA's rows
+      for (int l = 0; l < CD_B; ++l) corr = fma(xg[l], delta[l], corr);
+      cdot = d + corr;
+    }
+    __syncthreads();  // delta visible to the row warps
+    // r += A_J delta_J on this CTA's rows
+    if (warp > 0) {
+      const T* cur = slot_a(it);
 #pragma unroll
       for (int q = 0; q < CD_RMAX; ++q) {
-        const int i = tid + q * CD_NT;
+        const int i = rt + q * CD_RT;
         if (i < nrows) {
-          double acc = rr[q];
-          for (int c = 0; c < nc; ++c) {
+          // four independent chains over the block's columns (c mod 4),
+          // combined in a fixed order
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int c = 0; c < CD_B; ++c) {
             const double dc = delta[c];
-            if (dc != 0.0) acc += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * dc;
+            if (c < nc && dc != 0.0) acc[c & 3] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * dc;
           }
-          rr[q] = acc;
+          rr[q] += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
       }
-      // the next block's column state (its buffer was last read by warp 0
-      // two blocks ago)
-      if (tid < CD_ST * CD_B && (nblk > 1 || tid >= CD_B))
-        cst[((it + 1) & 1) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
-      __syncthreads();
     }
+    // park block it+2's column state (its slot last held block it-1).  x of
+    // a later pass comes from global memory only when rank 0 wrote it at
+    // least two iterations ago (ordered by the cluster barriers since);
+    // otherwise warp 0 has written it above
+    if (it + 2 < total && tid < CD_ST * CD_B && (tid >= CD_B || nblk >= 4 || pass_of(it + 2) == 0))
+      cst[((it + 2) % 3) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
+    __syncthreads();
   }
   // write back the residual rows and the objective 0.5 ||r||^2
   double sq = 0.0;
 #pragma unroll
   for (int q = 0; q < CD_RMAX; ++q) {
-    const int i = tid + q * CD_NT;
-    if (i < nrows) {
+    const int i = rt + q * CD_RT;
+    if (rt >= 0 && i < nrows) {
       a.r[row0 + i] = rr[q];
       sq += rr[q] * rr[q];
     }
@@ -305,37 +361,49 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   cluster.sync();  // keep smem alive until rank 0 has read it
 }
 
-// Gram blocks G_JJ = A_J' A_J for consecutive blocks of CD_B preserved columns
+// Gram blocks for consecutive blocks of CD_B preserved columns:
+// [blk][0] = G_JJ = A_J'A_J and [blk][1] = X_J = A_next'A_J with next = J+1
+// (block 0 after the last: the next pass starts over)
 template <typename T>
 __global__ void __launch_bounds__(256) k_gram(const T* __restrict__ A, int64_t ld, int64_t m, int64_t k,
                                               double* __restrict__ gram) {
-  __shared__ T tile[CD_B][129];  // 128-row chunk of the block's columns (+1 pad)
+  __shared__ T tile[2][CD_B][65];  // 64-row chunk of the block's / next block's columns (+1 pad)
+  const int64_t nblk = (k + CD_B - 1) / CD_B;
   const int64_t blk = blockIdx.x;
-  const int64_t c0 = blk * CD_B;
+  const int64_t nb = (blk + 1) % nblk;
+  const int64_t c0 = blk * CD_B, c1 = nb * CD_B;
   const int nc = (int)min((int64_t)CD_B, k - c0);
-  // thread -> 4 (i, l) pairs of the 32x32 block
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t r0 = 0; r0 < m; r0 += 128) {
-    const int nr = (int)min((int64_t)128, m - r0);
+  const int nc1 = (int)min((int64_t)CD_B, k - c1);
+  // thread -> 4 (i, l) pairs of each 32x32 block
+  double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  for (int64_t r0 = 0; r0 < m; r0 += 64) {
+    const int nr = (int)min((int64_t)64, m - r0);
     __syncthreads();
-    for (int q = threadIdx.x; q < CD_B * 128; q += 256) {
-      const int c = q / 128, i = q % 128;
-      tile[c][i] = (c < nc && i < nr) ? A[(c0 + c) * ld + r0 + i] : T(0);
+    for (int q = threadIdx.x; q < CD_B * 64; q += 256) {
+      const int c = q / 64, i = q % 64;
+      tile[0][c][i] = (c < nc && i < nr) ? A[(c0 + c) * ld + r0 + i] : T(0);
+      tile[1][c][i] = (c < nc1 && i < nr) ? A[(c1 + c) * ld + r0 + i] : T(0);
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int p = threadIdx.x * 4 + u;
       const int i = p / CD_B, l = p % CD_B;
-      double s = 0.0;
-      for (int rr = 0; rr < nr; ++rr) s += static_cast<double>(tile[i][rr]) * static_cast<double>(tile[l][rr]);
-      acc[u] += s;
+      double s = 0.0, sx = 0.0;
+      for (int rr = 0; rr < nr; ++rr) {
+        const double al = static_cast<double>(tile[0][l][rr]);
+        s += static_cast<double>(tile[0][i][rr]) * al;
+        sx += static_cast<double>(tile[1][i][rr]) * al;
+      }
+      acc[0][u] += s;
+      acc[1][u] += sx;
     }
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int p = threadIdx.x * 4 + u;
-    gram[blk * CD_B * CD_B + p] = acc[u];
+    gram[blk * 2 * CD_B * CD_B + p] = acc[0][u];
+    gram[blk * 2 * CD_B * CD_B + CD_B * CD_B + p] = acc[1][u];
   }
 }
 

@@ -457,7 +457,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->g = w.take(n * e);
   c->v = w.take(n * e);
   c->coef = w.take(n * e);
-  c->gram = w.take((size_t)((n + CD_B - 1) / CD_B) * CD_B * CD_B * 8);
+  c->gram = w.take((size_t)((n + CD_B - 1) / CD_B) * 2 * CD_B * CD_B * 8);  // G_JJ and the cross block X_J
   c->xfull = w.take(n * e);
   c->lofull = w.take(n * e);
   c->hifull = w.take(n * e);
@@ -938,13 +938,13 @@ int cd_sweeps(bx_ctx* c, int passes) {
   constexpr int V = 16 / sizeof(T);
   int NC = 8;
   int64_t rows = round_up((c->m + NC - 1) / NC, V);
-  const size_t fixed = (2 * CD_B + 2 * CD_B * CD_B + CD_B + 2 * 16 * CD_B + 2 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
-  auto smem_for = [&](int64_t r) { return 2 * CD_B * (size_t)r * sizeof(T) + fixed; };
-  if (rows > CD_NT * CD_RMAX || smem_for(rows) > c->smem_cap) {
+  const size_t fixed = (3 * 2 * CD_B * CD_B + 2 + CD_B + 2 * 16 * CD_B + 3 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
+  auto smem_for = [&](int64_t r) { return 3 * CD_B * (size_t)r * sizeof(T) + fixed; };
+  if (rows > CD_RT * CD_RMAX || smem_for(rows) > c->smem_cap) {
     NC = 16;
     rows = round_up((c->m + NC - 1) / NC, V);
   }
-  if (rows > CD_NT * CD_RMAX || smem_for(rows) > c->smem_cap)
+  if (rows > CD_RT * CD_RMAX || smem_for(rows) > c->smem_cap)
     return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent: m=%lld exceeds the cluster envelope", (long long)c->m);
   if (c->gram_dirty) {
     const int nblk = (int)((c->k + CD_B - 1) / CD_B);
