@@ -82,6 +82,9 @@ class ClockSampler:
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
+        # sampling period (BX_SMI_MS overrides; A/B on config 2 showed no
+        # measurable interference at 200 ms)
+        self.period_ms = int(os.environ.get("BX_SMI_MS", "200"))
         self.proc = None
         self.lines = []
         self.t = None
@@ -89,7 +92,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
