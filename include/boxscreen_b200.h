@@ -193,6 +193,10 @@ int bx_ctx_set_comm(bx_ctx* ctx, const unsigned char* id_host, int32_t rank,
  * nranks x 64 gathered handles (NULL: in-process group).  At most 8 ranks. */
 int bx_peer_alloc(bx_ctx* ctx, unsigned char* ipc_handle_out);
 int bx_peer_open(bx_ctx* ctx, const unsigned char* ipc_handles);
+/* Fall back to the NCCL schedule for the per-step reduction (unmaps the
+ * peers): every rank calls it when any rank failed to map its peers, so all
+ * ranks run the same schedule. */
+int bx_peer_disable(bx_ctx* ctx);
 
 /* in-process rank group: ranks are threads of one process sharing a GPU or
  * several; the allreduce is host-barrier + device sum (test transport of the

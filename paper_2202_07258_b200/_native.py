@@ -83,6 +83,7 @@ SIGNATURES = {
     "bx_ctx_set_active_set_workspace": (ctypes.c_int, [_vp, _vp, _sz]),
     "bx_peer_alloc": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "bx_peer_open": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "bx_peer_disable": (ctypes.c_int, [_vp]),
     "bx_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "bx_ctx_set_comm": (ctypes.c_int, [_vp, ctypes.c_char_p, _i32, _i32, _i64, _i64]),
     "bx_group_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i32]),

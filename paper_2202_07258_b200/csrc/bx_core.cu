@@ -2011,6 +2011,14 @@ int bx_peer_open(bx_ctx* c, const unsigned char* handles) {
   return BX_OK;
 }
 
+int bx_peer_disable(bx_ctx* c) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  for (void* p : c->xopened) cudaIpcCloseMemHandle(p);
+  c->xopened.clear();
+  c->xmode = 0;
+  return BX_OK;
+}
+
 int bx_nccl_unique_id(unsigned char* id_out) {
   if (!g_nccl.load()) return BX_ERR_UNSUPPORTED;
   ncclUniqueId id;

@@ -43,6 +43,17 @@ def column_blocks(n, world):
     return [(n * r // world, n * (r + 1) // world) for r in range(world)]
 
 
+def agree_all(ok, pg=None):
+    """True iff ``ok`` holds on every rank of ``pg`` (MIN all-reduce; the
+    tensor lives where the group's backend wants it)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(pg) == "nccl" else torch.device("cpu")
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=pg)
+    return bool(t.item())
+
+
 def shard(p, c0, c1):
     """Problem over columns [c0, c1) of p, sharing p's device storage."""
     d = p.device_arrays()
@@ -123,7 +134,8 @@ def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, t
                 hs = [None] * world
                 dist.all_gather_object(hs, h, group=pg)
                 return hs
-            s.attach_peers(gather)
+
+            s.attach_peers(gather, lambda ok: agree_all(ok, pg))
         out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
         prof = s.profile
     return _result(n_global, out, tr, x, theta, sl, su, prof, return_device, n_total=n_global)

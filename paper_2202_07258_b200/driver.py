@@ -133,20 +133,30 @@ class _Session:
         nat.check(nat.lib().bx_ctx_set_comm(self.ctx, uid, rank, nranks, col_offset, n_global), self.ctx,
                   "bx_ctx_set_comm")
 
-    def attach_peers(self, gather=None):
+    def attach_peers(self, gather=None, agree=None):
         """Fused reduce + peer exchange for the per-step reduction
         (csrc/bx_exchange.cuh).  ``gather(handle_bytes) -> list of every
         rank's handle`` for NCCL ranks (one GPU each); None for the
-        in-process group."""
+        in-process group.  ``agree(ok) -> bool`` is True when every rank
+        mapped its peers (an all-reduce over the ranks)."""
         L = nat.lib()
         if gather is None:
             nat.check(L.bx_peer_alloc(self.ctx, None), self.ctx, "bx_peer_alloc")
             nat.check(L.bx_peer_open(self.ctx, None), self.ctx, "bx_peer_open")
             return
+        # every rank takes part in the gather and the agreement even when its
+        # own step failed, so no rank is left waiting in a collective; if
+        # any rank cannot map its peers, all fall back to the NCCL schedule
         h = ctypes.create_string_buffer(64)
-        nat.check(L.bx_peer_alloc(self.ctx, h), self.ctx, "bx_peer_alloc")
+        ok = L.bx_peer_alloc(self.ctx, h) == 0
         handles = b"".join(gather(h.raw))
-        nat.check(L.bx_peer_open(self.ctx, handles), self.ctx, "bx_peer_open")
+        ok = ok and L.bx_peer_open(self.ctx, handles) == 0
+        if agree is not None and not agree(ok):
+            nat.check(L.bx_peer_disable(self.ctx), self.ctx, "bx_peer_disable")
+            import warnings
+            warnings.warn("fused peer exchange unavailable on some rank; using the NCCL schedule")
+        elif not ok:
+            nat.check(L.bx_peer_open(self.ctx, handles), self.ctx, "bx_peer_open")  # raise with the message
 
     def __enter__(self):
         return self

@@ -95,3 +95,37 @@ def test_column_blocks():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
             assert max(c1 - c0 for c0, c1 in b) - min(c1 - c0 for c0, c1 in b) <= 1
+
+
+def _agree_worker(rank, world, port, oks, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        here = os.path.dirname(os.path.abspath(__file__))
+        sys.path.insert(0, os.path.dirname(here))
+        from paper_2202_07258_b200.distributed import agree_all
+        q.put((rank, [agree_all(ok) for ok in oks[rank]]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_fallback_agreement():
+    """The fused peer exchange is used only when every rank mapped its peers
+    (distributed.agree_all): one failing rank turns it off on all ranks, so
+    every rank runs the same per-step schedule."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    oks = [[True, True, False], [True, False, True]]
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, oks, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0] == got[1] == [True, False, False]
