@@ -544,13 +544,14 @@ def run_batched(args, rank, world, dev):
     if not args.no_e2e:
         a_pin = torch.from_numpy(a).pin_memory()
         y_pin = torch.from_numpy(np.ascontiguousarray(Y)).pin_memory()
+        x_pin = torch.empty((kl, n), dtype=torch.float64, pin_memory=True)  # the result's host buffer, reused
         e_t, e_it = 0.0, 0
         for s_ in range(args.steps + 1):
             torch.cuda.synchronize()
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record(stream)
             r = solve_batched(a_pin.to(dev, non_blocking=True), y_pin.to(dev, non_blocking=True), passes=10,
-                              rounds=rounds, gap_tol=c["gap_tol"], eta=eta, return_device=False)
+                              rounds=rounds, gap_tol=c["gap_tol"], eta=eta, return_device=False, x_out=x_pin)
             t1.record(stream)
             torch.cuda.synchronize()
             if s_:
