@@ -299,16 +299,21 @@ def run_reference(args):
     sample = (f"oracle FISTA passes (numpy/OpenBLAS, reference Workspace arithmetic) timed at {len(bins)} "
               f"preserved-count bins weighted by {src}; {sum(d['timed_iterations'] for d in details)} "
               f"iterations per step")
-    line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": "iters/s",
+    line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": unit_name(args.config),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config recipe)",
             "config": config_block(args.config, inst),
-            "cpu_baseline": {"value": rate, "unit": "iters/s", "cores": thr, "kind": "port", "sample": sample,
+            "cpu_baseline": {"value": rate, "unit": unit_name(args.config), "cores": thr, "kind": "port", "sample": sample,
                              "cpu_model": model, "nproc": cores, "bins": details},
-            "e2e": {"value": rate, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": rate, "unit": unit_name(args.config), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def unit_name(cfg_id):
+    """Config 4's unit is one 62,500-column shard iteration (weak scaling)."""
+    return "shard-iters/s" if cfg_id == 4 else "iters/s"
 
 
 def metric_name(cfg_id):
@@ -433,11 +438,17 @@ def run_sharded(args, rank, world, dev):
                 continue
             e_t += float(tt.item())
             e_it += r.info["iterations"]
-        e2e = {"value": e_it / e_t, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": (world if args.config == 4 else 1) * e_it / e_t,
+               "unit": unit_name(args.config), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(8 * (c1 - c0) + 8 * m), "ms_per_step": 1000.0 * e_t / args.steps,
                "note": "per-rank bytes; every rank uploads its own column block"}
     r0 = results[0]
-    line = {"metric": metric_name(args.config), "value": iters / elapsed, "unit": "iters/s", "n_gpus": world,
+    # config 4 is weak scaling (62,500 columns per GPU): the whole-job value is
+    # shard-iterations/s (world x iterations/s of the global solve), the N=1
+    # unit; config 3 is strong scaling of one fixed problem: iterations/s
+    agg = world if args.config == 4 else 1
+    line = {"metric": metric_name(args.config), "value": agg * iters / elapsed,
+            "unit": unit_name(args.config), "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / args.steps,
             "higher_is_better": True, "scaling": "strong" if args.config == 3 else "weak", "vs_baseline": None,
             "dtype": "f32" if dt == np.float32 else "f64",
@@ -678,20 +689,20 @@ def run_ours(args):
             e_it += r.info["iterations"]
             d2h = r.x.nbytes + r.theta.nbytes + 8 * (r.sat_lower.size + r.sat_upper.size)
         p_host.release_device()
-        e2e = {"value": world * e_it / e_t, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": world * e_it / e_t, "unit": unit_name(args.config), "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000.0 * e_t / args.steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, det = cpu_rate(inst, bins, args.cpu_budget)
         cores, model = cpu_info()
-        cpu = {"value": rate, "unit": "iters/s", "cores": blas_threads(), "kind": "port",
+        cpu = {"value": rate, "unit": unit_name(args.config), "cores": blas_threads(), "kind": "port",
                "sample": (f"oracle FISTA passes at {len(bins)} preserved-count bins of this solve, "
                           f"{sum(d['timed_iterations'] for d in det)} iterations, ~{args.cpu_budget:.0f}s"),
                "cpu_model": model, "nproc": cores}
 
     r0 = results[0]
-    line = {"metric": metric_name(args.config), "value": value, "unit": "iters/s", "n_gpus": world,
+    line = {"metric": metric_name(args.config), "value": value, "unit": unit_name(args.config), "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if world == 1 else "replicas", "vs_baseline": None,
             "dtype": "f32" if inst.a.dtype == np.float32 else "f64",
