@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--write-trajectory", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="configs 3/4: take the NCCL column-sharded path even at N=1 (exercises the N>1 code)")
     ap.add_argument("--cfg4-rounds", type=int, default=100,
                     help="config 4: rounds (x10 PG passes + screening) per step; BASELINE gives it no gap target")
     return ap.parse_args()
@@ -466,6 +468,8 @@ def run_sharded(args, rank, world, dev):
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    from paper_2202_07258_b200.distributed import release_comms
+    release_comms()
     dist.destroy_process_group()
     return 0
 
@@ -606,9 +610,13 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            if world == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         if args.config in (3, 4):
             return run_sharded(args, rank, world, dev)
     if args.config == 5:

@@ -183,6 +183,22 @@ int bx_nccl_unique_id(unsigned char* id_out_host);
 int bx_ctx_set_comm(bx_ctx* ctx, const unsigned char* id_host, int32_t rank,
                     int32_t nranks, int64_t col_offset, int64_t n_global);
 
+/* Persistent communicator for repeated sharded solves: the NCCL
+ * communicator and the fused exchange's IPC-mapped buffers (sized for up to
+ * m rows) are set up once per process group and borrowed by every context
+ * (bx_ctx_use_comm), instead of bx_ctx_set_comm + bx_peer_* per solve.
+ * Setup is collective: every rank calls bx_comm_create with the same unique
+ * id, bx_comm_peer_alloc, exchanges the 64-byte handles, bx_comm_peer_open
+ * (or, when any rank failed, bx_comm_peer_disable on all ranks).  The
+ * communicator must outlive the contexts that use it. */
+typedef struct bx_comm bx_comm;
+int bx_comm_create(bx_comm** out, const unsigned char* id_host, int32_t rank, int32_t nranks);
+int bx_comm_destroy(bx_comm* comm);
+int bx_comm_peer_alloc(bx_comm* comm, int64_t m, unsigned char* ipc_handle_out);
+int bx_comm_peer_open(bx_comm* comm, const unsigned char* ipc_handles);
+int bx_comm_peer_disable(bx_comm* comm);
+int bx_ctx_use_comm(bx_ctx* ctx, bx_comm* comm, int64_t col_offset, int64_t n_global);
+
 /* fused reduce + peer exchange for the per-step reduction of the sharded
  * PG / FISTA pass (replaces its NCCL allreduces with ONE kernel that stores
  * each row block straight into every peer's buffer over NVLink and sums the

@@ -84,6 +84,12 @@ SIGNATURES = {
     "bx_peer_alloc": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "bx_peer_open": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "bx_peer_disable": (ctypes.c_int, [_vp]),
+    "bx_comm_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_char_p, _i32, _i32]),
+    "bx_comm_destroy": (ctypes.c_int, [_vp]),
+    "bx_comm_peer_alloc": (ctypes.c_int, [_vp, _i64, ctypes.c_char_p]),
+    "bx_comm_peer_open": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "bx_comm_peer_disable": (ctypes.c_int, [_vp]),
+    "bx_ctx_use_comm": (ctypes.c_int, [_vp, _vp, _i64, _i64]),
     "bx_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "bx_ctx_set_comm": (ctypes.c_int, [_vp, ctypes.c_char_p, _i32, _i32, _i64, _i64]),
     "bx_group_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i32]),

@@ -219,6 +219,29 @@ struct LocalComm : Comm {
 // ---------------------------------------------------------------------------
 // the context
 // ---------------------------------------------------------------------------
+// A communicator that outlives contexts (bx_comm_create): the NCCL
+// communicator plus the fused exchange's IPC-mapped receive buffers and
+// their epoch counter, set up once per process group and borrowed by every
+// sharded solve (a new ncclCommInitRank and IPC mapping per solve costs more
+// than a config-4 solve step).
+struct bx_comm {
+  NcclComm* nc = nullptr;
+  int rank = 0, nranks = 1;
+  int xmode = 0;                  // 1 once every peer is mapped
+  void* xbuf = nullptr;
+  int64_t xmp = 0;                // rows the buffer was sized for
+  int xnsm = 0;
+  double* xpeer_recv[kXPeers] = {};
+  unsigned* xpeer_flag[kXPeers] = {};
+  std::vector<void*> xopened;
+  unsigned xepoch = 0;            // shared by every context: flags only grow
+  ~bx_comm() {
+    for (void* p : xopened) cudaIpcCloseMemHandle(p);
+    if (xbuf) cudaFree(xbuf);
+    delete nc;
+  }
+};
+
 struct bx_ctx {
   int64_t m = 0, n = 0, mp = 0;  // rows, columns, padded rows
   int dtype = BX_F64;
@@ -316,7 +339,9 @@ struct bx_ctx {
   unsigned* xpeer_flag[kXPeers] = {};
   std::vector<void*> xopened;     // IPC mappings to close
   unsigned xepoch = 0;
+  unsigned* xepoch_p = nullptr;   // the epoch counter in use (own, or the borrowed bx_comm's)
   int xnb = 1;
+  bool comm_owned = true;         // false: `comm` belongs to a bx_comm
 
   // multi-GPU column sharding
   Comm* comm = nullptr;
@@ -350,6 +375,12 @@ int fail(bx_ctx* c, int code, const char* fmt, ...) {
   do {                                                                                             \
     cudaError_t e_ = (call);                                                                       \
     if (e_ != cudaSuccess) return fail(c, BX_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+// context-free variant (communicator calls): status only
+#define CUR(call)                          \
+  do {                                     \
+    if ((call) != cudaSuccess) return BX_ERR_CUDA; \
   } while (0)
 
 #define LAUNCHED()                                                                                   \
@@ -734,7 +765,7 @@ int run_xreduce(bx_ctx* c, int G, const double* off, double* out, int mode, cons
   a.rank = c->rank;
   a.nranks = c->nranks;
   a.nb = c->xnb;
-  a.epoch = ++c->xepoch;
+  a.epoch = ++*(c->xepoch_p ? c->xepoch_p : &c->xepoch);
   const int e0 = prof_begin(c);
   if (c->xmode == 2) {
     std::string e;
@@ -1807,7 +1838,7 @@ int bx_ctx_destroy(bx_ctx* c) {
   if (c->has) cudaFreeHost(c->has);
   for (void* p : c->xopened) cudaIpcCloseMemHandle(p);
   if (c->xbuf) cudaFree(c->xbuf);
-  delete c->comm;
+  if (c->comm_owned) delete c->comm;
   delete c;
   return BX_OK;
 }
@@ -1975,13 +2006,15 @@ int bx_peer_alloc(bx_ctx* c, unsigned char* handle_out) {
   return BX_OK;
 }
 
+// CTAs of the fused reduction: row blocks of a multiple of XCH rows
+static int x_fit_nb(const bx_ctx* c, int64_t cap) {
+  const int64_t per = xrows_per_cta(c->m, (int)std::max<int64_t>(1, cap));
+  return (int)std::max<int64_t>(1, (c->m + per - 1) / per);
+}
+
 int bx_peer_open(bx_ctx* c, const unsigned char* handles) {
   if (!c || !c->xbuf) return c ? fail(c, BX_ERR_INVALID_ARGUMENT, "bx_peer_alloc first") : BX_ERR_INVALID_ARGUMENT;
-  // CTAs of the fused reduction: row blocks of a multiple of XCH rows
-  auto fit_nb = [&](int64_t cap) {
-    const int64_t per = xrows_per_cta(c->m, (int)std::max<int64_t>(1, cap));
-    return (int)std::max<int64_t>(1, (c->m + per - 1) / per);
-  };
+  auto fit_nb = [&](int64_t cap) { return x_fit_nb(c, cap); };
   if (!handles) {
     LocalComm* lc = dynamic_cast<LocalComm*>(c->comm);
     if (!lc) return fail(c, BX_ERR_INVALID_ARGUMENT, "NULL handles need the in-process group");
@@ -2040,12 +2073,105 @@ int bx_ctx_set_comm(bx_ctx* c, const unsigned char* id_host, int32_t rank, int32
     delete nc;
     return fail(c, BX_ERR_CUDA, "ncclCommInitRank: %d", r);
   }
-  delete c->comm;
+  if (c->comm_owned) delete c->comm;
   c->comm = nc;
+  c->comm_owned = true;
   c->rank = rank;
   c->nranks = nranks;
   c->col_offset = col_offset;
   c->n_global = n_global;
+  return BX_OK;
+}
+
+int bx_comm_create(bx_comm** out, const unsigned char* id_host, int32_t rank, int32_t nranks) {
+  if (!out || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return BX_ERR_INVALID_ARGUMENT;
+  if (!g_nccl.load()) return BX_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  memcpy(id.internal, id_host, 128);
+  bx_comm* cm = new bx_comm();
+  cm->nc = new NcclComm();
+  if (g_nccl.init_rank(&cm->nc->comm, nranks, id, rank) != 0) {
+    delete cm;
+    return BX_ERR_CUDA;
+  }
+  cm->rank = rank;
+  cm->nranks = nranks;
+  *out = cm;
+  return BX_OK;
+}
+
+int bx_comm_destroy(bx_comm* cm) {
+  delete cm;
+  return BX_OK;
+}
+
+int bx_comm_peer_alloc(bx_comm* cm, int64_t m, unsigned char* handle_out) {
+  if (!cm || m < 1 || !handle_out) return BX_ERR_INVALID_ARGUMENT;
+  if (cm->nranks > kXPeers) return BX_ERR_UNSUPPORTED;
+  if (!cm->xbuf) {
+    int dev = 0, nsm = 0;
+    CUR(cudaGetDevice(&dev));
+    CUR(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    cm->xmp = round_up(m, 32);
+    cm->xnsm = nsm;
+    const size_t bytes = xbuf_bytes(cm->xmp, nsm);
+    CUR(cudaMalloc(&cm->xbuf, bytes));
+    CUR(cudaMemset(cm->xbuf, 0, bytes));
+    CUR(cudaDeviceSynchronize());
+  }
+  cudaIpcMemHandle_t h;
+  CUR(cudaIpcGetMemHandle(&h, cm->xbuf));
+  memcpy(handle_out, &h, sizeof(h));
+  return BX_OK;
+}
+
+int bx_comm_peer_open(bx_comm* cm, const unsigned char* handles) {
+  if (!cm || !cm->xbuf || !handles) return BX_ERR_INVALID_ARGUMENT;
+  for (int q = 0; q < cm->nranks; ++q) {
+    void* p = nullptr;
+    if (q == cm->rank) {
+      p = cm->xbuf;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles + 64 * q, sizeof(h));
+      CUR(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      cm->xopened.push_back(p);
+    }
+    cm->xpeer_recv[q] = static_cast<double*>(p);
+    cm->xpeer_flag[q] = reinterpret_cast<unsigned*>(static_cast<char*>(p) + xrecv_doubles(cm->xmp) * 8);
+  }
+  cm->xmode = 1;
+  return BX_OK;
+}
+
+int bx_comm_peer_disable(bx_comm* cm) {
+  if (!cm) return BX_ERR_INVALID_ARGUMENT;
+  for (void* p : cm->xopened) cudaIpcCloseMemHandle(p);
+  cm->xopened.clear();
+  cm->xmode = 0;
+  return BX_OK;
+}
+
+int bx_ctx_use_comm(bx_ctx* c, bx_comm* cm, int64_t col_offset, int64_t n_global) {
+  if (!c || !cm || !cm->nc) return c ? fail(c, BX_ERR_INVALID_ARGUMENT, "null communicator") : BX_ERR_INVALID_ARGUMENT;
+  if (cm->xmode == 1 && (c->mp > cm->xmp || c->nsm > cm->xnsm))
+    return fail(c, BX_ERR_UNSUPPORTED, "communicator exchange buffer sized for m <= %lld", (long long)cm->xmp);
+  if (c->comm_owned) delete c->comm;
+  c->comm = cm->nc;
+  c->comm_owned = false;
+  c->rank = cm->rank;
+  c->nranks = cm->nranks;
+  c->col_offset = col_offset;
+  c->n_global = n_global;
+  c->xmode = cm->xmode;
+  if (cm->xmode == 1) {
+    for (int q = 0; q < cm->nranks; ++q) {
+      c->xpeer_recv[q] = cm->xpeer_recv[q];
+      c->xpeer_flag[q] = cm->xpeer_flag[q];
+    }
+    c->xnb = x_fit_nb(c, c->nsm);
+    c->xepoch_p = &cm->xepoch;
+  }
   return BX_OK;
 }
 
@@ -2070,8 +2196,9 @@ int bx_ctx_set_group(bx_ctx* c, bx_group* g, int32_t rank, int64_t col_offset, i
   lc->rank = rank;
   lc->tmp = c->grp_tmp;
   lc->dptrs = c->grp_ptrs;
-  delete c->comm;
+  if (c->comm_owned) delete c->comm;
   c->comm = lc;
+  c->comm_owned = true;
   c->rank = rank;
   c->nranks = g->n;
   c->col_offset = col_offset;

@@ -113,29 +113,84 @@ def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLo
     return _result(p.n, out, tr, x, theta, sl, su, None, False)
 
 
+class ShardComm:
+    """The NCCL communicator and the fused exchange's IPC-mapped receive
+    buffers of one process group, set up once (collectively) and borrowed by
+    every sharded solve on it (bx_comm_create / bx_ctx_use_comm): a fresh
+    ncclCommInitRank + IPC mapping per solve would cost more than a solve
+    step at config 4."""
+
+    def __init__(self, pg, m, exchange):
+        import torch.distributed as dist
+        L = nat.lib()
+        self.m = m
+        self.exchange = exchange
+        rank, world = dist.get_rank(pg), dist.get_world_size(pg)
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            nat.check(L.bx_nccl_unique_id(uid), None, "bx_nccl_unique_id")
+        box = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=pg)
+        h = ctypes.c_void_p()
+        st = L.bx_comm_create(ctypes.byref(h), box[0], rank, world)
+        if st != 0:
+            nat.check(st, None, "bx_comm_create")
+        self.handle = h
+        self.fused = False
+        if exchange == "fused":
+            # every rank takes part in the gather and the agreement even when
+            # its own step failed; any failure puts all ranks on NCCL
+            hb = ctypes.create_string_buffer(64)
+            ok = L.bx_comm_peer_alloc(h, m, hb) == 0
+            hs = [None] * world
+            dist.all_gather_object(hs, hb.raw, group=pg)
+            ok = ok and L.bx_comm_peer_open(h, b"".join(hs)) == 0
+            if agree_all(ok, pg):
+                self.fused = True
+            else:
+                L.bx_comm_peer_disable(h)
+                import warnings
+                warnings.warn("fused peer exchange unavailable on some rank; using the NCCL schedule")
+
+    def close(self):
+        if self.handle:
+            nat.lib().bx_comm_destroy(self.handle)
+            self.handle = None
+
+
+_COMMS = {}
+
+
+def shard_comm(pg, m, exchange):
+    """The cached ShardComm of ``pg`` (created on first use, collectively)."""
+    import torch.distributed as dist
+    key = (id(pg), dist.get_rank(pg), dist.get_world_size(pg), exchange)
+    cm = _COMMS.get(key)
+    if cm is None or cm.m < m:
+        if cm is not None:
+            cm.close()
+        cm = _COMMS[key] = ShardComm(pg, m, exchange)
+    return cm
+
+
+def release_comms():
+    """Destroy the cached communicators (call before destroy_process_group)."""
+    for cm in _COMMS.values():
+        cm.close()
+    _COMMS.clear()
+
+
 def solve_distributed(p_shard, col_offset, n_global, cfg=None, screening=True, tv=None, loss=QuadraticLoss,
                       slack_scale=None, return_device=True, pg=None, profile=False, exchange=None):
     """This rank's part of an NCCL column-sharded solve (call on every rank of
     the torch.distributed group ``pg``).  Returns the rank-local result: x is
-    the shard's block, trace / gap / theta are global."""
-    import torch.distributed as dist
+    the shard's block, trace / gap / theta are global.  The communicator is
+    created on the first call for ``pg`` and reused (shard_comm)."""
     cfg = cfg or SolverConfig()
     slack_scale = _default_slack(p_shard) if slack_scale is None else slack_scale
-    rank, world = dist.get_rank(pg), dist.get_world_size(pg)
-    uid = ctypes.create_string_buffer(128)
-    if rank == 0:
-        nat.check(nat.lib().bx_nccl_unique_id(uid), None, "bx_nccl_unique_id")
-    box = [uid.raw if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0, group=pg)
+    cm = shard_comm(pg, p_shard.m, _exchange(exchange))
     with _Session(p_shard, tv=tv) as s:
-        s.attach_nccl(box[0], rank, world, col_offset, n_global)
-        if _exchange(exchange) == "fused":
-            def gather(h):
-                hs = [None] * world
-                dist.all_gather_object(hs, h, group=pg)
-                return hs
-
-            s.attach_peers(gather, lambda ok: agree_all(ok, pg))
+        s.use_comm(cm, col_offset, n_global)
         out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
         prof = s.profile
     return _result(n_global, out, tr, x, theta, sl, su, prof, return_device, n_total=n_global)

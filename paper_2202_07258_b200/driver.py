@@ -133,6 +133,11 @@ class _Session:
         nat.check(nat.lib().bx_ctx_set_comm(self.ctx, uid, rank, nranks, col_offset, n_global), self.ctx,
                   "bx_ctx_set_comm")
 
+    def use_comm(self, comm, col_offset, n_global):
+        """Borrow a persistent communicator (distributed.ShardComm)."""
+        nat.check(nat.lib().bx_ctx_use_comm(self.ctx, comm.handle, col_offset, n_global), self.ctx,
+                  "bx_ctx_use_comm")
+
     def attach_peers(self, gather=None, agree=None):
         """Fused reduce + peer exchange for the per-step reduction
         (csrc/bx_exchange.cuh).  ``gather(handle_bytes) -> list of every

@@ -32,5 +32,7 @@ for exchange in ("fused", "nccl"):
     ok = ok and good
     print(f"rank {rank}/{world} [{exchange}]: rounds {res.rounds} vs {ref.rounds}, max|dx| {dx:.2e}, "
           f"launches {res.info['kernel_launches']}, {'OK' if good else 'MISMATCH ' + str(probs[:2])}", flush=True)
+from paper_2202_07258_b200.distributed import release_comms  # noqa: E402
+release_comms()
 dist.destroy_process_group()
 sys.exit(0 if ok else 1)
