@@ -343,7 +343,7 @@ def ncu_traffic(cfg_id):
     return t, info
 
 
-KERNEL_NAMES = {"cd": "k_cd (block-exact cyclic CD on an 8-CTA cluster)",
+KERNEL_NAMES = {"cd": "k_cd (software-pipelined block-exact cyclic CD on a thread-block cluster)",
                 "small_round": "k_round_small (cooperative SM-resident PG/FISTA round)"}
 
 
