@@ -164,36 +164,43 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   // dots of the local columns with rv (shared memory): one warp per column,
   // lanes over 16-byte row vectors with two independent chains, then one
   // butterfly -- no cross-warp fold
+  // warp-level dot of local column c with rv (shared memory): lanes over
+  // 16-byte row vectors with two independent chains, one butterfly (every
+  // lane ends with the sum)
+  const int nv = m / V;  // full vectors; the m % V tail goes to lane 0
+  auto col_dot = [&](int c) {
+    const T* col = cols + (size_t)c * a.colstride;
+    double s0 = 0.0, s1 = 0.0;
+    int vi = lane;
+    for (; vi + 32 < nv; vi += 64) {
+      T av[V], aw[V];
+      double rr[V], rw[V];
+      unpack<T>(*reinterpret_cast<const VT*>(col + vi * V), av);
+      unpack<T>(*reinterpret_cast<const VT*>(col + (vi + 32) * V), aw);
+      load_rows<T>(rv + vi * V, rr);
+      load_rows<T>(rv + (vi + 32) * V, rw);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        s0 += static_cast<double>(av[e]) * rr[e];
+        s1 += static_cast<double>(aw[e]) * rw[e];
+      }
+    }
+    if (vi < nv) {
+      T av[V];
+      double rr[V];
+      unpack<T>(*reinterpret_cast<const VT*>(col + vi * V), av);
+      load_rows<T>(rv + vi * V, rr);
+#pragma unroll
+      for (int e = 0; e < V; ++e) s0 += static_cast<double>(av[e]) * rr[e];
+    }
+    if (lane == 0)
+      for (int row = nv * V; row < m; ++row) s1 += static_cast<double>(col[row]) * rv[row];
+    return warp_sum<double>(s0 + s1);
+  };
+  // dots of all local columns into gout (one warp per column)
   auto dots = [&](double* gout) {
-    const int nv = m / V;  // full vectors; the m % V tail goes to lane 0
     for (int c = warp; c < ncol; c += NW) {
-      const T* col = cols + (size_t)c * a.colstride;
-      double s0 = 0.0, s1 = 0.0;
-      int vi = lane;
-      for (; vi + 32 < nv; vi += 64) {
-        T av[V], aw[V];
-        double rr[V], rw[V];
-        unpack<T>(*reinterpret_cast<const VT*>(col + vi * V), av);
-        unpack<T>(*reinterpret_cast<const VT*>(col + (vi + 32) * V), aw);
-        load_rows<T>(rv + vi * V, rr);
-        load_rows<T>(rv + (vi + 32) * V, rw);
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          s0 += static_cast<double>(av[e]) * rr[e];
-          s1 += static_cast<double>(aw[e]) * rw[e];
-        }
-      }
-      if (vi < nv) {
-        T av[V];
-        double rr[V];
-        unpack<T>(*reinterpret_cast<const VT*>(col + vi * V), av);
-        load_rows<T>(rv + vi * V, rr);
-#pragma unroll
-        for (int e = 0; e < V; ++e) s0 += static_cast<double>(av[e]) * rr[e];
-      }
-      if (lane == 0)
-        for (int row = nv * V; row < m; ++row) s1 += static_cast<double>(col[row]) * rv[row];
-      const double sum = warp_sum<double>(s0 + s1);
+      const double sum = col_dot(c);
       if (lane == 0) gout[c] = sum;
     }
     __syncthreads();
@@ -214,6 +221,27 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     const double tn = (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom)) / 2.0;
     const double beta = (a.kind == 2) ? (t_mom - 1.0) / tn : 0.0;
     const bool use_stored = (a.kind == 0 && gv && pass == 0);
+    // column update (PG / FISTA), done by the lane that holds the column's
+    // dot -- no CTA barrier between the dots and the updates
+    auto update_col = [&](int c, double gj) {
+      const double xo = cx[c];
+      double xn;
+      if (a.kind == 2) {
+        const double xp = cxp[c];
+        double yv = xo;
+        if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
+        xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), clo[c], chi[c]);
+        cxp[c] = xo;
+        const double dx = xn - xo;
+        rsx[c] = gj * dx;                  // restart partials of this CTA
+        rsx[SM_NT + c] = cnr[c] * fabs(dx);
+      } else {
+        cg[c] = gj;
+        xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), clo[c], chi[c]);
+      }
+      cx[c] = xn;
+      cf[c] = xn;
+    };
     if (!use_stored) {
       // residual (or the extrapolated residual) -> shared memory; written by
       // other CTAs before the barrier: read through L2
@@ -235,37 +263,17 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
         }
       }
       __syncthreads();
-      dots(gcol);
-    }
-    // local x update
-    double gd = 0.0, gs = 0.0;
-    if (tid < ncol) {
-      const double gj = use_stored ? cg[tid] : gcol[tid];
-      const double xo = cx[tid];
-      double xn;
-      if (a.kind == 2) {
-        const double xp = cxp[tid];
-        double yv = xo;
-        if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
-        xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), clo[tid], chi[tid]);
-        cxp[tid] = xo;
-        const double dx = xn - xo;
-        gd = gj * dx;
-        gs = cnr[tid] * fabs(dx);
-      } else {
-        cg[tid] = gj;
-        xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), clo[tid], chi[tid]);
+      for (int c = warp; c < ncol; c += NW) {
+        const double gj = col_dot(c);
+        if (lane == 0) update_col(c, gj);
       }
-      cx[tid] = xn;
-      cf[tid] = xn;
-    }
-    // restart partials of this CTA (fixed order: lane-strided, then one
-    // butterfly in warp 0)
-    if (a.kind == 2) {
-      rsx[tid] = gd;
-      rsx[SM_NT + tid] = gs;
+    } else {
+      for (int c = warp; c < ncol; c += NW)
+        if (lane == 0) update_col(c, cg[c]);
     }
     __syncthreads();
+    // restart partials of this CTA (fixed order: lane-strided, then one
+    // butterfly in warp 0; lane 0 = thread 0 also publishes them below)
     if (warp == 0) {
       double s1 = 0.0, s2 = 0.0;
       if (a.kind == 2)
@@ -310,7 +318,8 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
           if (row + e < m) out[row + e] = acc[i][e];
       }
     }
-    __syncthreads();
+    // thread 0 wrote sc4 itself (warp 0's fold); the grid barrier's entry
+    // CTA barrier orders every thread's partial rows before the arrival
     if (tid == 0) {
       a.bpart[4 * b + 1] = sc4[0];
       a.bpart[4 * b + 2] = sc4[1];
