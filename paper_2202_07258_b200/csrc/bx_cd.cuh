@@ -50,6 +50,7 @@ struct CdArgs {
   DevScalars* sc;
   int passes;
   int rows_per_cta;  // multiple of 2
+  int slots;         // shared-memory block slots (the kernel's NS): 3, or 2 for large m
 };
 
 // cp.async 16-byte global->shared copy (LDGSTS)
@@ -128,7 +129,7 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 //     d_{J+1} = A_{J+1}'(r + A_J delta_J) = A_{J+1}'r + X_J delta_J,
 // (exact arithmetic identity) before r += A_J delta_J.  Three shared-memory
 // slots: block J (axpy), J+1 (dots), J+2 (in flight).
-template <typename T>
+template <typename T, int NS>
 __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -136,8 +137,8 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int rows_pad = a.rows_per_cta;
   T* abuf = reinterpret_cast<T*>(smem);                                      // [3][CD_B][rows_pad]
-  double* gbuf = reinterpret_cast<double*>(abuf + 3 * CD_B * rows_pad);     // [3][2][CD_B][CD_B]
-  double* part = gbuf + 3 * 2 * CD_B * CD_B;                                // [2] scratch
+  double* gbuf = reinterpret_cast<double*>(abuf + NS * CD_B * rows_pad);    // [NS][2][CD_B][CD_B]
+  double* part = gbuf + NS * 2 * CD_B * CD_B;                               // [2] scratch
   double* delta = part + 2;                                                 // [CD_B]
   double* allpart = delta + CD_B;                                           // [2][16][CD_B] pushed partial dots
   double* cst = allpart + 2 * 16 * CD_B;                                    // [3][CD_ST][CD_B] column state
@@ -156,8 +157,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   }
   const int64_t nblk = (a.k + CD_B - 1) / CD_B;
   const int64_t total = nblk * a.passes;  // blocks over all passes, in order
-  auto slot_a = [&](int64_t it) { return abuf + ((int)it % 3) * CD_B * rows_pad; };
-  auto slot_g = [&](int64_t it) { return gbuf + ((int)it % 3) * 2 * CD_B * CD_B; };
+  // slot of a block (constant divisors: no integer division sequence)
+  auto sidx = [&](int64_t it) { return (int)it % NS; };
+  auto slot_a = [&](int64_t it) { return abuf + sidx(it) * CD_B * rows_pad; };
+  auto slot_g = [&](int64_t it) { return gbuf + sidx(it) * 2 * CD_B * CD_B; };
   // 32-bit block / pass of a global block index (nblk <= 2^26 columns / 32)
   const int nb32 = (int)nblk;
   auto blk_of = [&](int64_t it) { return (int64_t)((int)it % nb32); };
@@ -244,7 +247,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     cp_async_wait_all();
     __syncthreads();
     if (it + 2 < total) {
-      cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows);
+      // three slots: block it+2 goes into the slot block it-1 freed; two
+      // slots: it must wait for block it's axpy (end of this iteration)
+      if constexpr (NS == 3) cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows);
       pfv = cd_state_load(a, blk_of(it + 2), pass_of(it + 2));
     }
     if (warp == 0) {
@@ -331,6 +336,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     // otherwise warp 0 has written it above
     if (it + 2 < total && tid < CD_ST * CD_B && (tid >= CD_B || nblk >= 4 || pass_of(it + 2) == 0))
       cst[((it + 2) % 3) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
+    if (NS == 2 && it + 2 < total) {  // (compile-time NS)
+      __syncthreads();  // block it's slot is free
+      cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows);
+    }
     __syncthreads();
   }
   // write back the residual rows and the objective 0.5 ||r||^2

@@ -969,13 +969,20 @@ int cd_sweeps(bx_ctx* c, int passes) {
   constexpr int V = 16 / sizeof(T);
   int NC = 8;
   int64_t rows = round_up((c->m + NC - 1) / NC, V);
-  const size_t fixed = (3 * 2 * CD_B * CD_B + 2 + CD_B + 2 * 16 * CD_B + 3 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
-  auto smem_for = [&](int64_t r) { return 3 * CD_B * (size_t)r * sizeof(T) + fixed; };
-  if (rows > CD_RT * CD_RMAX || smem_for(rows) > c->smem_cap) {
+  const size_t fixed = (2 + CD_B + 2 * 16 * CD_B + 3 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
+  // three block slots (blocks J, J+1 and J+2 in flight) when they fit,
+  // else two (the next block's copy then waits for this block's axpy)
+  int slots = 3;
+  auto smem_for = [&](int64_t r) {
+    return (size_t)slots * (CD_B * (size_t)r * sizeof(T) + 2 * CD_B * CD_B * 8) + fixed;
+  };
+  auto fits = [&]() { return rows <= CD_RT * CD_RMAX && smem_for(rows) <= c->smem_cap; };
+  if (!fits()) {
     NC = 16;
     rows = round_up((c->m + NC - 1) / NC, V);
   }
-  if (rows > CD_RT * CD_RMAX || smem_for(rows) > c->smem_cap)
+  if (!fits()) slots = 2;
+  if (!fits())
     return fail(c, BX_ERR_UNSUPPORTED, "coordinate descent: m=%lld exceeds the cluster envelope", (long long)c->m);
   if (c->gram_dirty) {
     const int nblk = (int)((c->k + CD_B - 1) / CD_B);
@@ -1000,9 +1007,11 @@ int cd_sweeps(bx_ctx* c, int passes) {
   a.sc = c->sc;
   a.passes = passes;
   a.rows_per_cta = (int)rows;
+  a.slots = slots;
   const size_t smem = smem_for(rows);
-  CU(cudaFuncSetAttribute(k_cd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CU(cudaFuncSetAttribute(k_cd<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  auto kern = slots == 3 ? k_cd<T, 3> : k_cd<T, 2>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(NC, 1, 1);
   lc.blockDim = dim3(CD_NT, 1, 1);
@@ -1016,7 +1025,7 @@ int cd_sweeps(bx_ctx* c, int passes) {
   lc.attrs = at;
   lc.numAttrs = 1;
   const int e0 = prof_begin(c);
-  CU(cudaLaunchKernelEx(&lc, k_cd<T>, a));
+  CU(cudaLaunchKernelEx(&lc, kern, a));
   LAUNCHED();
   prof_end(c, e0, BX_PROF_CD, 2.0 * (double)passes * c->k * c->m * sizeof(T));
   if (passes & 1) CU(cudaMemcpyAsync(c->x[s], c->coef, c->k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));

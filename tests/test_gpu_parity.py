@@ -107,3 +107,17 @@ def test_tall_matrix_row_blocked_path(kind):
     g, o = _solve_both(inst.a, inst.y, inst.lower, inst.upper, kind, passes=10, tol=1e-6, max_rounds=40)
     probs = compare_traces(g, o)
     assert not probs, probs[:3]
+
+
+@pytest.mark.parametrize("m,n", [(4500, 300), (2000, 70), (2000, 40)])
+def test_cd_block_pipeline_shapes(m, n):
+    """Coordinate descent shapes off the config-2 path: m = 4500 leaves room
+    for only two shared-memory block slots (the next block's copy waits for
+    the axpy), and n = 70 / 40 give passes of three / two blocks, where the
+    column-state look-ahead takes x from the redundant update instead of
+    global memory; 10 sweeps per round exercise the cross-pass hand-off."""
+    from paper_2202_07258_b200.generate import make_config
+    inst = make_config(2, m=m, n=n)
+    g, o = _solve_both(inst.a, inst.y, inst.lower, inst.upper, "cd", passes=10, tol=1e-9, max_rounds=15)
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, probs[:3]
