@@ -45,6 +45,7 @@ namespace {
 constexpr size_t kAlign = 256;
 constexpr int kMaxRanks = 256;
 constexpr int kSmallRounds = 1024;  // rounds per device-resident small-round launch
+constexpr int kF32CertEvery = 50;   // fp32 storage: rounds between fp64 certificate attempts
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
@@ -540,10 +541,10 @@ int pick_R(int64_t m, size_t esz) {
   return -1;
 }
 
-template <typename T, int R, bool D, bool X>
+template <typename T, int R, bool D, bool X, typename AT = T>
 int launch_pass_RDX(bx_ctx* c, const PassArgs<T>& a, int G, size_t smem) {
   static bool attr_set = false;
-  auto kern = k_pass<T, R, D, X>;
+  auto kern = k_pass<T, R, D, X, AT>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_cap);
     if (e != cudaSuccess) return fail(c, BX_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -555,7 +556,12 @@ int launch_pass_RDX(bx_ctx* c, const PassArgs<T>& a, int G, size_t smem) {
 }
 
 template <typename T, int R>
-int launch_pass_R(bx_ctx* c, const PassArgs<T>& a, bool dot, bool axpy, int G, size_t smem) {
+int launch_pass_R(bx_ctx* c, const PassArgs<T>& a, bool dot, bool axpy, int G, size_t smem, bool acc64) {
+  if constexpr (sizeof(T) == 4) {
+    // certificate passes over fp32 storage: fp64 accumulation
+    if (acc64 && dot && !axpy) return launch_pass_RDX<T, R, true, false, double>(c, a, G, smem);
+    if (acc64 && !dot && axpy) return launch_pass_RDX<T, R, false, true, double>(c, a, G, smem);
+  }
   if (dot && axpy) return launch_pass_RDX<T, R, true, true>(c, a, G, smem);
   if (dot) return launch_pass_RDX<T, R, true, false>(c, a, G, smem);
   return launch_pass_RDX<T, R, false, true>(c, a, G, smem);
@@ -610,7 +616,7 @@ template <typename T>
 int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
              double* xprev, const double* lo, const double* hi, double* g, const double* att, const double* coef,
              double* bpart, int has_inf, int* G_out, const double* nrm = nullptr, int64_t row0 = 0,
-             int64_t mrows = -1, int accumulate = -1) {
+             int64_t mrows = -1, int accumulate = -1, bool acc64 = false) {
   const int64_t mm = mrows < 0 ? c->m : mrows;
   const int R = pick_R(mm, sizeof(T));
   if (R < 0 && mrows < 0)
@@ -675,13 +681,13 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   const int e0 = prof_begin(c);
   int st = BX_OK;
   switch (R) {
-    case 1: st = launch_pass_R<T, 1>(c, a, dot, axpy, G, smem); break;
-    case 2: st = launch_pass_R<T, 2>(c, a, dot, axpy, G, smem); break;
-    case 4: st = launch_pass_R<T, 4>(c, a, dot, axpy, G, smem); break;
-    case 6: st = launch_pass_R<T, 6>(c, a, dot, axpy, G, smem); break;
-    case 8: st = launch_pass_R<T, 8>(c, a, dot, axpy, G, smem); break;
-    case 10: st = launch_pass_R<T, 10>(c, a, dot, axpy, G, smem); break;
-    case 12: st = launch_pass_R<T, 12>(c, a, dot, axpy, G, smem); break;
+    case 1: st = launch_pass_R<T, 1>(c, a, dot, axpy, G, smem, acc64); break;
+    case 2: st = launch_pass_R<T, 2>(c, a, dot, axpy, G, smem, acc64); break;
+    case 4: st = launch_pass_R<T, 4>(c, a, dot, axpy, G, smem, acc64); break;
+    case 6: st = launch_pass_R<T, 6>(c, a, dot, axpy, G, smem, acc64); break;
+    case 8: st = launch_pass_R<T, 8>(c, a, dot, axpy, G, smem, acc64); break;
+    case 10: st = launch_pass_R<T, 10>(c, a, dot, axpy, G, smem, acc64); break;
+    case 12: st = launch_pass_R<T, 12>(c, a, dot, axpy, G, smem, acc64); break;
     default: st = fail(c, BX_ERR_UNSUPPORTED, "R=%d", R);
   }
   if (e0 >= 0) {
@@ -1362,12 +1368,19 @@ int certified(bx_ctx* c, double alpha) {
   k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], (const double*)c->x[s], (double*)c->xfull);
   LAUNCHED();
   int G = 1;
+  // fp32 storage: the certificate's A x and A'r accumulate in fp64 (a fp32
+  // sum of A x carries ~1e-7 |Ax| of noise, which puts a floor of ~1e-7
+  // |Ax|^2 under the computed gap however optimal x is)
+  const bool acc64 = sizeof(T) == 4 && c->m <= (int64_t)NT * 4 * 12;
   TRY(run_pass<T>(c, full_view<T>(c), U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                  (const double*)c->xfull, nullptr, 0, &G));
-  TRY(run_reduce<T>(c, G, (const double*)c->negy, (double*)c->rc, R_CERT, nullptr, 0, 4));
+                  (const double*)c->xfull, nullptr, 0, &G, nullptr, 0, -1, -1, acc64));
+  if (acc64)
+    TRY(run_reduce<double>(c, G, (const double*)c->negy, (double*)c->rc, R_CERT, nullptr, 0, 4));
+  else
+    TRY(run_reduce<T>(c, G, (const double*)c->negy, (double*)c->rc, R_CERT, nullptr, 0, 4));
   TRY(run_pass<T>(c, full_view<T>(c), U_DOT, (const double*)c->rc, nullptr, nullptr, nullptr, nullptr,
                   (const double*)c->hifull, (double*)c->gfull, (const double*)c->attfull, nullptr, c->bpart + c->Gmax, c->has_inf,
-                  &G));
+                  &G, nullptr, 0, -1, -1, acc64));
   TRY(dual_point<T>(c, 1, (const double*)c->rc, (const double*)c->y, (double*)c->thetac, (const double*)c->gfull,
                     (const double*)c->attfull, (const double*)c->lofull, (const double*)c->hifull, (double*)c->vfull, c->n,
                     c->bpart + c->Gmax, G, 0.0, alpha));
@@ -1617,6 +1630,8 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   double excluded = 0.0;  // seconds of gap evaluation left out of the trace (screening off)
   EventPair gap_ev;
   if (!cfg->screening) TRY(gap_ev.create(c));
+  const bool f32cert = c->esz == 4 && kind != BX_ACTIVE_SET;
+  int64_t last_cert = 0;
   SmallLoop lp;
   lp.tol = tol;
   lp.relative_gap = cfg->relative_gap;
@@ -1632,6 +1647,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     } else if (!c->prof) {
       // small problems: device-resident rounds until the next event
       lp.max_rounds = (int)std::min<int64_t>(max_rounds - rnd + 1, kSmallRounds);
+      if (f32cert) lp.max_rounds = (int)std::min<int64_t>(lp.max_rounds, last_cert + kF32CertEvery - rnd);
       int ran = 0, done = 0, ev = 0;
       if (lp.max_rounds > 1) TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
       if (ran) {
@@ -1692,7 +1708,11 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     gap_out = act.gap;
     double cert_gap = NAN;
     const double tol_r = cfg->relative_gap ? tol * fmax(1.0, fabs(act.primal)) : tol;
-    if (act.gap < tol_r) {
+    // fp32 storage: the reduced gap of the fp32-accumulated residual has a
+    // floor of ~1e-7 |Ax|^2, so the fp64-accumulated certificate is also
+    // tried every kF32CertEvery rounds (it alone decides convergence)
+    if (act.gap < tol_r || (f32cert && rnd >= last_cert + kF32CertEvery)) {
+      last_cert = rnd;
       if (!cfg->screening) CU(cudaEventRecord(gap_ev[0], c->stream));
       TRY(certified<T>(c, alpha));
       if (!cfg->screening) CU(cudaEventRecord(gap_ev[1], c->stream));

@@ -255,7 +255,10 @@ __host__ __device__ constexpr int cols_per_slot(int R) { return R >= 6 ? 1 : (R 
 // ----------------------------------------------------------------------------
 // k_pass: one streamed pass over k columns (see header comment)
 // ----------------------------------------------------------------------------
-template <typename T, int R, bool DOT, bool AXPY>
+// AT: accumulation type of the dot vector, the dots and the partial rows --
+// T for the hot passes; double for fp32 storage in the rare certificate
+// passes (then a.part holds fp64 partial rows)
+template <typename T, int R, bool DOT, bool AXPY, typename AT = T>
 __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   using VT = typename V16<T>::type;
   constexpr int V = V16<T>::n;
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   }
 
   // the dot vector, register resident: thread owns rows (i*NT + tid)*V + e
-  T vr[DOT ? R : 1][V];
+  AT vr[DOT ? R : 1][V];
   double beta = 0.0;
   const double eta = a.sc->eta;
   if (DOT) {
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     for (int i = 0; i < R; ++i) {
       const int row = row0 + i * (NT * V);
 #pragma unroll
-      for (int e = 0; e < V; ++e) vr[i][e] = T(0);
+      for (int e = 0; e < V; ++e) vr[i][e] = AT(0);
       if (row < m) {
         double cur[V];
         load_rows<T>(a.vin + row, cur);
@@ -326,16 +329,16 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
           for (int e = 0; e < V; ++e) cur[e] = add_rn(cur[e], mul_rn(beta, sub_rn(cur[e], prv[e])));
         }
 #pragma unroll
-        for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? static_cast<T>(cur[e]) : T(0);
+        for (int e = 0; e < V; ++e) vr[i][e] = (row + e < m) ? static_cast<AT>(cur[e]) : AT(0);
       }
     }
   }
 
-  T acc[AXPY ? R : 1][V];
+  AT acc[AXPY ? R : 1][V];
 #pragma unroll
   for (int i = 0; i < (AXPY ? R : 1); ++i)
 #pragma unroll
-    for (int e = 0; e < V; ++e) acc[i][e] = T(0);
+    for (int e = 0; e < V; ++e) acc[i][e] = AT(0);
   double run = 0.0;   // block-scalar running value (threads tid < C)
   double run2 = 0.0;  // second block scalar (FISTA restart slack)
 
@@ -384,10 +387,10 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     mbar_wait(&bars[s], ph);
     const unsigned char* slot = smem + s * slot_bytes;
     if (DOT) {
-      T d[C];
+      AT d[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        d[c] = T(0);
+        d[c] = AT(0);
         if (c < cg) {
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
           if constexpr (sizeof(T) == 8) {
@@ -402,6 +405,25 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
                 for (int e = 0; e < V; ++e) d[c] += ((row + e < m) ? av[e] : T(0)) * vr[i][e];
               }
             }
+          } else if constexpr (sizeof(AT) == 8) {
+            // fp32 storage, fp64 accumulation (certificate passes)
+            double dd[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) dd[e] = 0.0;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              const int row = row0 + i * (NT * V);
+              if (row < m) {
+                T av[V];
+                unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                  if (row + e < m) dd[e] += static_cast<double>(av[e]) * vr[i][e];
+              }
+            }
+            d[c] = dd[0];
+#pragma unroll
+            for (int e = 1; e < V; ++e) d[c] += dd[e];
           } else {
           // fp32 (twice the elements per byte): V independent partial sums
           // (short dependency chains) combined in a fixed order; only the
@@ -431,7 +453,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
           for (int e = 1; e < V; ++e) d[c] += dd[e];
           }
         }
-        d[c] = warp_sum<T>(d[c]);
+        d[c] = warp_sum<AT>(d[c]);
       }
       if (lane == 0) {
 #pragma unroll
@@ -515,7 +537,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (c < cg) {
-          const T cc = static_cast<T>(cf[c]);
+          const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll
           for (int i = 0; i < R; ++i) {
@@ -526,6 +548,9 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
               if constexpr (sizeof(T) == 8) {
 #pragma unroll
                 for (int e = 0; e < V; ++e) acc[i][e] += ((row + e < m) ? av[e] : T(0)) * cc;
+              } else if constexpr (sizeof(AT) == 8) {
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc[i][e] += static_cast<double>(av[e]) * cc;
               } else {
                 // rows >= m of the last vector only reach the padding of the
                 // partial row, which k_reduce never reads: no per-element guard
@@ -557,11 +582,22 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   }
 
   if (AXPY) {
-    T* out = a.part + b * a.ldp;
+    if constexpr (sizeof(AT) == sizeof(T)) {
+      T* out = a.part + b * a.ldp;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int row = row0 + i * (NT * V);
-      if (row < m) *reinterpret_cast<VT*>(out + row) = pack<T>(acc[i]);
+      for (int i = 0; i < R; ++i) {
+        const int row = row0 + i * (NT * V);
+        if (row < m) *reinterpret_cast<VT*>(out + row) = pack<T>(acc[i]);
+      }
+    } else {
+      AT* out = reinterpret_cast<AT*>(a.part) + b * a.ldp;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int row = row0 + i * (NT * V);
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          if (row + e < m) out[row + e] = acc[i][e];
+      }
     }
   }
   if (a.bpart) {

@@ -1,0 +1,67 @@
+"""Edge shapes of every device path vs the oracle, round by round: ragged row
+counts (odd m, m % 4 != 0 for the fp32 16-byte vectors), single rows and
+columns, the small-path / streamed-path / register-envelope boundaries, and
+a problem whose whole preserved set is screened away (k = 0 afterwards)."""
+
+import numpy as np
+import pytest
+
+from oracle.boxscreen_oracle import objective, oracle_solve
+from parity import compare_final, compare_traces
+from test_gpu_parity import _solve_both
+
+pytestmark = pytest.mark.gpu
+
+
+def _nnls(m, n, seed):
+    rng = np.random.default_rng(seed)
+    a = np.abs(rng.standard_normal((m, n))) + 0.05
+    y = a @ (np.maximum(rng.standard_normal(n), 0.0) * (rng.random(n) < 0.3)) + 0.05 * rng.standard_normal(m)
+    return np.asfortranarray(a), y, np.zeros(n), np.full(n, np.inf)
+
+
+@pytest.mark.parametrize("m,n", [(1, 5), (3, 1), (7, 40), (1001, 300), (4096, 300), (4097, 300)])
+@pytest.mark.parametrize("kind", ["pg", "apg", "cd"])
+@pytest.mark.parametrize("streamed", [False, True])
+def test_ragged_and_boundary_shapes(m, n, kind, streamed, monkeypatch):
+    if streamed:
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+    else:
+        monkeypatch.delenv("BX_NO_SMALL", raising=False)
+    a, y, lo, hi = _nnls(m, n, seed=m * 31 + n)
+    g, o = _solve_both(a, y, lo, hi, kind, passes=10 if kind != "cd" else 1, tol=1e-9, max_rounds=30)
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, probs[:3]
+
+
+@pytest.mark.parametrize("kind", ["pg", "apg", "cd"])
+def test_everything_screened(kind):
+    """A >= 0 and y < 0: x* = 0 and every column is screened within a few
+    rounds; the rounds after that run on an empty preserved set."""
+    rng = np.random.default_rng(11)
+    a = np.asfortranarray(np.abs(rng.standard_normal((50, 80))) + 0.1)
+    y = -np.abs(rng.standard_normal(50)) - 0.5
+    g, o = _solve_both(a, y, np.zeros(80), np.full(80, np.inf), kind, passes=10, tol=1e-10, max_rounds=50)
+    assert g.converged and o["converged"]
+    assert g.trace[-1].preserved_count == 0 and len(g.sat_lower) == 80
+    np.testing.assert_array_equal(g.x, 0.0)
+    assert not compare_traces(g, o)
+
+
+@pytest.mark.parametrize("m", [5, 1023, 4099])
+def test_fp32_ragged_rows(m):
+    """fp32 storage moves 4 rows per 16-byte vector: ragged m exercises the
+    guarded last vector of the dot and the unguarded axpy padding."""
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    a, y, lo, hi = _nnls(m, 200, seed=m)
+    a32 = np.asfortranarray(a.astype(np.float32))
+    res = solve(Problem(a32, y, lo, hi, dtype=np.float32),
+                SolverConfig(kind="apg", inner_passes=10, gap_tol=1e-6, max_rounds=20000))
+    # converged: certified by the fp64-accumulated certificate (the reduced
+    # gap of the fp32-accumulated residual has a floor)
+    assert res.converged, (res.rounds, res.gap)
+    ref = oracle_solve(np.asfortranarray(a32.astype(np.float64)), y, lo, hi, kind="apg", inner_passes=10,
+                       gap_tol=1e-9 * max(1.0, float(res.trace[-1].primal)))
+    p32 = objective(a32.astype(np.float64), y, np.asarray(res.x, dtype=np.float64))
+    p64 = objective(a32.astype(np.float64), y, ref["x"])
+    assert abs(p32 - p64) <= 1e-4 * max(abs(p64), 1e-12), (p32, p64)
