@@ -37,9 +37,12 @@ from .solvers import SolverConfig
 
 
 def column_blocks(n, world):
-    """Contiguous, balanced column blocks [(c0, c1)] for ``world`` ranks."""
+    """Contiguous, balanced column blocks [(c0, c1)] for ``world`` ranks
+    (every rank owns at least one column: n >= world)."""
     if world < 1:
         raise ValueError("world must be >= 1")
+    if n < world:
+        raise ValueError(f"{n} columns cannot be sharded over {world} ranks (each rank needs one)")
     return [(n * r // world, n * (r + 1) // world) for r in range(world)]
 
 

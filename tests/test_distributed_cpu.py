@@ -89,8 +89,12 @@ def test_two_rank_gloo_matches_unsharded_oracle(kind):
 
 def test_column_blocks():
     from paper_2202_07258_b200.distributed import column_blocks
+    with pytest.raises(ValueError):
+        column_blocks(3, 4)  # every rank needs a column
     for n in (1, 7, 50000):
         for w in (1, 2, 3, 8):
+            if n < w:
+                continue
             b = column_blocks(n, w)
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
