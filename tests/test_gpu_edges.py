@@ -146,3 +146,40 @@ def test_wide_shapes_reach_the_oracle_optimum(family, kind):
     assert abs(pg_ - po) <= g.gap + o["gap"] + 1e-9 * max(1.0, abs(po)), (pg_, po, g.gap, o["gap"])
     assert g.gap <= 1e-3 * max(1.0, abs(po))  # and it got somewhere
     assert np.all(g.x >= lo - 1e-15) and np.all(g.x <= hi + 1e-15)
+
+
+@pytest.mark.parametrize("family", ["nnls", "bvls", "mixed"])
+@pytest.mark.parametrize("m,n", [(40, 7), (9, 9), (200, 3), (1, 1)])
+def test_active_set_edge_shapes(family, m, n):
+    from conftest import small_instance
+    rng = np.random.default_rng(m * 13 + n)
+    a, y, lo, hi = small_instance(rng, m, n, family)
+    g, o = _solve_both(a, y, lo, hi, "active-set", passes=1, tol=1e-10, max_rounds=None)
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, probs[:3]
+
+
+@pytest.mark.parametrize("layout", ["row-major", "column-major", "fp32-host"])
+def test_device_and_host_inputs_give_the_same_solve(layout):
+    """Problem accepts host arrays or CUDA tensors in either layout; the
+    device copy has the C-ABI column-major layout either way, so the solves
+    are identical (bit for bit) to the numpy-input solve."""
+    import torch
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    a, y, lo, hi = _nnls(300, 500, seed=77)
+    cfg = SolverConfig(kind="apg", inner_passes=10, gap_tol=1e-8, max_rounds=300)
+    ref = solve(Problem(a, y, lo, hi), cfg)
+    if layout == "row-major":
+        p = Problem(torch.from_numpy(np.ascontiguousarray(a)).cuda(), torch.from_numpy(y).cuda(), lo, hi)
+    elif layout == "column-major":
+        p = Problem(torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t(), torch.from_numpy(y).cuda(), lo, hi)
+    else:
+        p = Problem(a.astype(np.float32).astype(np.float64), y.astype(np.float32), lo, hi)
+    res = solve(p, cfg)
+    if layout == "fp32-host":
+        a2 = a.astype(np.float32).astype(np.float64)
+        y2 = y.astype(np.float32).astype(np.float64)
+        ref = solve(Problem(a2, y2, lo, hi), cfg)
+    assert res.rounds == ref.rounds
+    np.testing.assert_array_equal(np.asarray(res.x), np.asarray(ref.x))
+    assert [t.gap for t in res.trace] == [t.gap for t in ref.trace]
