@@ -183,3 +183,21 @@ def test_device_and_host_inputs_give_the_same_solve(layout):
     assert res.rounds == ref.rounds
     np.testing.assert_array_equal(np.asarray(res.x), np.asarray(ref.x))
     assert [t.gap for t in res.trace] == [t.gap for t in ref.trace]
+
+
+@pytest.mark.parametrize("m,n", [(400, 1200), (3000, 700)])
+def test_cd_with_screening_events(m, n):
+    """Coordinate descent on a box-constrained family whose optimum saturates
+    many coordinates: screening fires while the sweep spans many blocks, so
+    compaction, the Gram / cross-Gram recompute and the pipelined block ring
+    all run between sweeps (m = 3000 also takes the two-slot ring)."""
+    rng = np.random.default_rng(m + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) / np.sqrt(m))
+    # 70% of the planted coordinates lie outside the box [-1, 1]
+    xt = np.where(rng.random(n) < 0.7, 2.0 * np.sign(rng.standard_normal(n)), rng.uniform(-0.5, 0.5, n))
+    y = a @ xt + 0.01 * rng.standard_normal(m)
+    lo, hi = np.full(n, -1.0), np.full(n, 1.0)
+    g, o = _solve_both(a, y, lo, hi, "cd", passes=1, tol=1e-9, max_rounds=150)
+    assert o["trace"][-1]["preserved"] < n  # screening fired
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, probs[:3]
