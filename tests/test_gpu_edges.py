@@ -185,18 +185,39 @@ def test_device_and_host_inputs_give_the_same_solve(layout):
     assert [t.gap for t in res.trace] == [t.gap for t in ref.trace]
 
 
+def _saturating_bvls(m, n):
+    rng = np.random.default_rng(m + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) / np.sqrt(m))
+    # 70% of the planted coordinates lie outside the box [-1, 1]
+    xt = np.where(rng.random(n) < 0.7, 2.0 * np.sign(rng.standard_normal(n)), rng.uniform(-0.5, 0.5, n))
+    y = a @ xt + 0.01 * rng.standard_normal(m)
+    return a, y, np.full(n, -1.0), np.full(n, 1.0)
+
+
+@pytest.mark.parametrize("m,n", [(400, 1200), (3000, 700)])
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+@pytest.mark.parametrize("streamed", [False, True])
+def test_first_order_bvls_screening_both_bounds(m, n, kind, streamed, monkeypatch):
+    """Upper- and lower-bound screening (z update with nonzero bounds) on
+    both PG / FISTA paths."""
+    if streamed:
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+    else:
+        monkeypatch.delenv("BX_NO_SMALL", raising=False)
+    a, y, lo, hi = _saturating_bvls(m, n)
+    g, o = _solve_both(a, y, lo, hi, kind, passes=10, tol=1e-9, max_rounds=200)
+    assert len(o["sat_lower"]) > 0 and len(o["sat_upper"]) > 0
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, probs[:3]
+
+
 @pytest.mark.parametrize("m,n", [(400, 1200), (3000, 700)])
 def test_cd_with_screening_events(m, n):
     """Coordinate descent on a box-constrained family whose optimum saturates
     many coordinates: screening fires while the sweep spans many blocks, so
     compaction, the Gram / cross-Gram recompute and the pipelined block ring
     all run between sweeps (m = 3000 also takes the two-slot ring)."""
-    rng = np.random.default_rng(m + n)
-    a = np.asfortranarray(rng.standard_normal((m, n)) / np.sqrt(m))
-    # 70% of the planted coordinates lie outside the box [-1, 1]
-    xt = np.where(rng.random(n) < 0.7, 2.0 * np.sign(rng.standard_normal(n)), rng.uniform(-0.5, 0.5, n))
-    y = a @ xt + 0.01 * rng.standard_normal(m)
-    lo, hi = np.full(n, -1.0), np.full(n, 1.0)
+    a, y, lo, hi = _saturating_bvls(m, n)
     g, o = _solve_both(a, y, lo, hi, "cd", passes=1, tol=1e-9, max_rounds=150)
     assert o["trace"][-1]["preserved"] < n  # screening fired
     probs = compare_traces(g, o) + compare_final(g, o)
