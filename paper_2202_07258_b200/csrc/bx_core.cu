@@ -464,7 +464,6 @@ struct Carver {
   }
 };
 
-constexpr int kPartRows = 1;  // placeholder to keep layout comments aligned
 
 void carve(bx_ctx* c, Carver& w) {
   const int64_t m = c->m, n = c->n, mp = c->mp;
@@ -520,7 +519,6 @@ void carve(bx_ctx* c, Carver& w) {
   c->grp_tmp = w.take(mp * 8 + 4096);
   c->grp_ptrs = (const void**)w.take(kMaxRanks * 8);
   (void)m;
-  (void)kPartRows;
 }
 
 void shape_params(bx_ctx* c) {
@@ -1081,7 +1079,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   if (ncmax > SM_CMAX) return BX_OK;
   if (lp.max_rounds > 1 && (c->m + G - 1) / G > SM_NT) return BX_OK;
   const int colstride = (int)round_up(c->m, 2 * V);
-  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 3 * SM_NT + 8 + 7 * SM_CMAX + SM_NT + round_up(c->m, 8)) * 8 + 256;
+  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 2 * SM_NT + 8 + 7 * SM_CMAX + SM_NT + round_up(c->m, 8)) * 8 + 256;
   const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
   if (smem > c->smem_cap) return BX_OK;
   const int s = c->cur;
@@ -1108,7 +1106,6 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   a.epart = c->bpart;
   a.sc = c->sc;
   a.bar = c->bar;
-  a.epoch0 = 0;
   a.passes = passes;
   a.kind = kind;
   a.g_valid = c->g_valid ? 1 : 0;

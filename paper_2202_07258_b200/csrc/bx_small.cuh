@@ -44,7 +44,6 @@ struct SmallArgs {
   double* epart;   // [G] epsilon partials for k_dual
   DevScalars* sc;
   unsigned* bar;   // [G] per-CTA barrier epochs
-  unsigned epoch0; // epoch base of this launch (host keeps the count)
   int passes;
   int kind;        // 0 PG, 2 APG
   int g_valid;     // PG: the first step may use the stored gradient
@@ -107,8 +106,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   double* red = reinterpret_cast<double*>(smem + (((size_t)a.ncmax * a.colstride * sizeof(T) + 127) / 128) * 128);
   double* gcol = red + NW * SM_CMAX;   // [SM_CMAX] reduced dots
   double* cf = gcol + SM_CMAX;         // [SM_CMAX] axpy coefficients
-  double* rowscr = cf + SM_CMAX;       // [SM_NT] reduce-phase scratch
-  double* rsx = rowscr + SM_NT;        // [2][SM_NT] restart partials
+  double* rsx = cf + SM_CMAX;          // [2][SM_NT] restart partials
   double* sc4 = rsx + 2 * SM_NT;       // [8] block scalars
   double* cx = sc4 + 8;                // [SM_CMAX] resident x
   double* cxp = cx + SM_CMAX;          // [SM_CMAX] x_prev
