@@ -1627,7 +1627,11 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   double excluded = 0.0;  // seconds of gap evaluation left out of the trace (screening off)
   EventPair gap_ev;
   if (!cfg->screening) TRY(gap_ev.create(c));
-  const bool f32cert = c->esz == 4 && kind != BX_ACTIVE_SET;
+  static const int f32_every = [] {
+    const char* e = getenv("BX_F32_CERT_EVERY");  // 0 disables the periodic certificate
+    return e ? atoi(e) : kF32CertEvery;
+  }();
+  const bool f32cert = c->esz == 4 && kind != BX_ACTIVE_SET && f32_every > 0;
   int64_t last_cert = 0;
   SmallLoop lp;
   lp.tol = tol;
@@ -1644,7 +1648,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     } else if (!c->prof) {
       // small problems: device-resident rounds until the next event
       lp.max_rounds = (int)std::min<int64_t>(max_rounds - rnd + 1, kSmallRounds);
-      if (f32cert) lp.max_rounds = (int)std::min<int64_t>(lp.max_rounds, last_cert + kF32CertEvery - rnd);
+      if (f32cert) lp.max_rounds = (int)std::min<int64_t>(lp.max_rounds, last_cert + f32_every - rnd);
       int ran = 0, done = 0, ev = 0;
       if (lp.max_rounds > 1) TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
       if (ran) {
@@ -1708,7 +1712,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     // fp32 storage: the reduced gap of the fp32-accumulated residual has a
     // floor of ~1e-7 |Ax|^2, so the fp64-accumulated certificate is also
     // tried every kF32CertEvery rounds (it alone decides convergence)
-    if (act.gap < tol_r || (f32cert && rnd >= last_cert + kF32CertEvery)) {
+    if (act.gap < tol_r || (f32cert && rnd >= last_cert + f32_every)) {
       last_cert = rnd;
       if (!cfg->screening) CU(cudaEventRecord(gap_ev[0], c->stream));
       TRY(certified<T>(c, alpha));
