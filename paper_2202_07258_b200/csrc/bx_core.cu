@@ -304,6 +304,7 @@ struct bx_ctx {
   double* dtrace = nullptr; // small-round kernel: per-round trace records [kSmallRounds][8]
   bool dot_done = false;    // the round kernel already produced g and the eps partials
   int dot_G = 0;
+  int64_t graph_body_kernels = 0;  // nodes of the captured round (launch accounting)
   bool small_ok = true;     // cooperative small-round path allowed (env BX_NO_SMALL disables)
   unsigned bar_epoch = 0;   // grid-barrier epochs issued so far
   int64_t launches = 0;
@@ -1066,7 +1067,8 @@ struct SmallLoop {
 // *event = 1 when the following round's passes + dot pass also ran and its
 // dual / screening step is left to the host.
 template <typename T>
-int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran, int* done, int* event) {
+int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran, int* done, int* event,
+                 bool dry = false) {
   *ran = 0;
   *done = 0;
   *event = 0;
@@ -1082,6 +1084,10 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 2 * SM_NT + 8 + 7 * SM_CMAX + SM_NT + round_up(c->m, 8)) * 8 + 256;
   const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
   if (smem > c->smem_cap) return BX_OK;
+  if (dry) {  // would run (the caller only asks)
+    *ran = 1;
+    return BX_OK;
+  }
   const int s = c->cur;
   View<T> vw = act_view<T>(c);
   SmallArgs a;
@@ -1149,6 +1155,203 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   *ran = 1;
   *done = hd[0];
   *event = hd[1];
+  return BX_OK;
+}
+
+template <typename T>
+int primal_passes(bx_ctx* c, int kind, int passes);
+template <typename T>
+int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha);
+
+// ---- graph-resident rounds (streamed PG / FISTA and CD) ---------------------
+// The round sequence (primal passes, screening dot, dual point, sphere test)
+// is captured once into the body of a CUDA-graph WHILE node; a one-thread
+// kernel ends each round: it records the trace, and keeps looping while the
+// round had no event (nothing screened, gap above tolerance, no error) and
+// the round budget lasts.  The host then syncs once per batch instead of
+// once per round.  The body must be a steady-state round -- the host state
+// the capture leaves behind equals the state it started from (checked).
+struct GraphKey {
+  int64_t k, kphys;
+  const void *r, *rprev, *x, *g;
+  int cur, kind, passes, screening, g_valid, dense, act_is_orig;
+  bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+static GraphKey graph_key(const bx_ctx* c, int kind, int passes, int screening) {
+  GraphKey k;
+  memset(&k, 0, sizeof(k));
+  k.k = c->k;
+  k.kphys = c->kphys;
+  k.r = c->r;
+  k.rprev = c->rprev;
+  k.x = c->x[c->cur];
+  k.g = c->g;
+  k.cur = c->cur;
+  k.kind = kind;
+  k.passes = passes;
+  k.screening = screening;
+  k.g_valid = c->g_valid ? 1 : 0;
+  k.dense = c->dense ? 1 : 0;
+  k.act_is_orig = c->act_is_orig ? 1 : 0;
+  return k;
+}
+
+struct GraphEndArgs {
+  DevScalars* sc;
+  double* trace;  // [limit][8]
+  int* done;      // [0] event-free rounds, [1] event flag
+  cudaGraphConditionalHandle h;
+  const int* limit;  // device: rounds allowed in this launch
+  double tol;
+  int relative_gap;
+  int screening;
+};
+
+__global__ void k_graph_round_end(GraphEndArgs a) {
+  const int q = a.done[0];
+  const DualOut& d = a.sc->act;
+  const double tol_r = a.relative_gap ? a.tol * fmax(1.0, fabs(d.primal)) : a.tol;
+  const bool ev = a.sc->err != 0 || d.gap_raw < -1e-9 || d.gap < tol_r ||
+                  (a.screening && (a.sc->g_lo + a.sc->g_up) > 0);
+  if (!ev) {
+    double* tr = a.trace + 8 * q;
+    tr[0] = d.primal;
+    tr[1] = d.dual;
+    tr[2] = d.gap;
+    tr[3] = d.eps;
+    tr[4] = d.radius;
+    tr[5] = a.sc->mom_t;
+    tr[6] = (double)a.sc->restarts;
+    a.done[0] = q + 1;
+  } else {
+    a.done[1] = 1;
+  }
+  cudaGraphSetConditional(a.h, (!ev && q + 1 < *a.limit) ? 1u : 0u);
+}
+
+struct GraphState {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cs = nullptr;  // private capture / launch stream (the caller's may be the legacy default stream)
+  cudaEvent_t join[2] = {nullptr, nullptr};
+  GraphKey key{};
+  bool broken = false;  // capture not steady / unsupported: stop trying this solve
+  ~GraphState() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto& e : join)
+      if (e) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+  }
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+  }
+};
+
+// Up to `limit` rounds on the graph.  *ran = 0 when the path does not apply;
+// otherwise *done event-free rounds (trace in c->dtrace) and *event = 1 when
+// the round after them ran and had an event (its dual / screening results are
+// in the device scalars; g is valid, dot_done set).
+template <typename T>
+int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, double tol, int relative_gap,
+                 int screening, double slack_scale, double alpha, int* ran, int* done, int* event) {
+  *ran = 0;
+  *done = 0;
+  *event = 0;
+  if (gs.broken || c->prof || c->sharded() || limit < 2 || c->k == 0) return BX_OK;
+  if (kind != BX_PG && kind != BX_APG && kind != BX_CD) return BX_OK;
+  {
+    int r0 = 0, d0 = 0, e0 = 0;
+    SmallLoop probe;
+    TRY(small_rounds<T>(c, kind, passes, probe, &r0, &d0, &e0, true));
+    if (r0) return BX_OK;  // the small-problem kernel owns these rounds
+  }
+  if (limit > kSmallRounds) limit = kSmallRounds;
+  const GraphKey key = graph_key(c, kind, passes, screening);
+  if (!gs.cs) {
+    if (cudaStreamCreateWithFlags(&gs.cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gs.join[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&gs.join[1], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      gs.broken = true;
+      return BX_OK;
+    }
+  }
+  if (!gs.exec || !(gs.key == key)) {
+    gs.reset();
+    CU(cudaGraphCreate(&gs.graph, 0));
+    cudaGraphConditionalHandle h;
+    CU(cudaGraphConditionalHandleCreate(&h, gs.graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    CU(cudaGraphAddNode(&node, gs.graph, nullptr, 0, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    // capture on the private stream (the round functions launch on c->stream)
+    cudaStream_t user_stream = c->stream;
+    c->stream = gs.cs;
+    if (cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      c->stream = user_stream;
+      gs.reset();
+      gs.broken = true;
+      return BX_OK;
+    }
+    const int64_t launches0 = c->launches;
+    int st = primal_passes<T>(c, kind, passes);
+    if (st == BX_OK) st = dual_screen<T>(c, screening, slack_scale, alpha);
+    GraphEndArgs ga;
+    ga.sc = c->sc;
+    ga.trace = c->dtrace;
+    ga.done = c->done;
+    ga.h = h;
+    ga.limit = c->done + 2;
+    ga.tol = tol;
+    ga.relative_gap = relative_gap;
+    ga.screening = screening;
+    if (st == BX_OK) k_graph_round_end<<<1, 1, 0, c->stream>>>(ga);
+    cudaGraph_t cap = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &cap);
+    c->stream = user_stream;
+    c->launches = launches0;  // captured, not launched
+    if (st != BX_OK || ce != cudaSuccess || !(graph_key(c, kind, passes, screening) == key)) {
+      // not a steady-state round (or capture failed): stay on the host loop
+      cudaGetLastError();
+      gs.reset();
+      gs.broken = true;
+      c->err.clear();
+      return BX_OK;
+    }
+    size_t nn = 0;
+    CU(cudaGraphGetNodes(body, nullptr, &nn));
+    c->graph_body_kernels = (int64_t)nn;
+    CU(cudaGraphInstantiate(&gs.exec, gs.graph, 0));
+    gs.key = key;
+  }
+  const int hd0[3] = {0, 0, limit};
+  CU(cudaMemcpyAsync(c->done, hd0, sizeof(hd0), cudaMemcpyHostToDevice, c->stream));
+  // run on the private stream, joined both ways with the caller's stream
+  CU(cudaEventRecord(gs.join[0], c->stream));
+  CU(cudaStreamWaitEvent(gs.cs, gs.join[0], 0));
+  CU(cudaGraphLaunch(gs.exec, gs.cs));
+  CU(cudaEventRecord(gs.join[1], gs.cs));
+  CU(cudaStreamWaitEvent(c->stream, gs.join[1], 0));
+  int hd[2] = {0, 0};
+  CU(cudaMemcpyAsync(hd, c->done, sizeof(hd), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  // every executed round launched the body's kernels
+  c->launches += (int64_t)(hd[0] + hd[1]) * c->graph_body_kernels;
+  *ran = 1;
+  *done = hd[0];
+  *event = hd[1];
+  if (hd[1]) c->dot_done = true;  // the event round's g / eps partials are in place
   return BX_OK;
 }
 
@@ -1336,6 +1539,7 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
     TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr,
                     (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s], nullptr, c->bpart, c->has_inf,
                     &G));
+    c->dot_G = G;  // a later dual_screen on the same g (dot_done) reuses its eps partials
   }
   c->g_valid = true;
   TRY(dual_point<T>(c, 0, (const double*)c->r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g, (const double*)c->att[s],
@@ -1633,6 +1837,9 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   }();
   const bool f32cert = c->esz == 4 && kind != BX_ACTIVE_SET && f32_every > 0;
   int64_t last_cert = 0;
+  int64_t last_event = 0;  // last round the host handled an event in (graph rounds resume 2 later)
+  GraphState gstate;
+  static const bool graph_off = getenv("BX_NO_GRAPH") != nullptr;
   SmallLoop lp;
   lp.tol = tol;
   lp.relative_gap = cfg->relative_gap;
@@ -1651,6 +1858,9 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       if (f32cert) lp.max_rounds = (int)std::min<int64_t>(lp.max_rounds, last_cert + f32_every - rnd);
       int ran = 0, done = 0, ev = 0;
       if (lp.max_rounds > 1) TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
+      if (!ran && lp.max_rounds > 1 && rnd >= 2 && rnd - last_event >= 2 && !graph_off)
+        TRY(graph_rounds<T>(c, gstate, kind, passes, lp.max_rounds, tol, cfg->relative_gap, cfg->screening,
+                            slack_scale, alpha, &ran, &done, &ev));
       if (ran) {
         if (done > 0) {
           std::vector<double> tr(8 * (size_t)done);
@@ -1714,6 +1924,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     // tried every kF32CertEvery rounds (it alone decides convergence)
     if (act.gap < tol_r || (f32cert && rnd >= last_cert + f32_every)) {
       last_cert = rnd;
+      last_event = rnd;
       if (!cfg->screening) CU(cudaEventRecord(gap_ev[0], c->stream));
       TRY(certified<T>(c, alpha));
       if (!cfg->screening) CU(cudaEventRecord(gap_ev[1], c->stream));
@@ -1735,6 +1946,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       n_lo = c->hsc->g_lo;
       n_up = c->hsc->g_up;
       if (n_lo || n_up) {
+        last_event = rnd;
         const bool z_update = ((c->bound_bits & 1) && n_lo > 0) || ((c->bound_bits & 2) && n_up > 0);
         TRY(compact<T>(c, c->hsc->n_lo, c->hsc->n_up, c->hsc->n_keep, kind, z_update));
         kg = c->hsc->g_keep;
