@@ -222,3 +222,40 @@ def test_cd_with_screening_events(m, n):
     assert o["trace"][-1]["preserved"] < n  # screening fired
     probs = compare_traces(g, o) + compare_final(g, o)
     assert not probs, probs[:3]
+
+
+@pytest.mark.parametrize("m,n,K", [(1, 5, 1), (8, 15, 63), (37, 17, 65), (208, 40, 64), (50, 33, 129)])
+@pytest.mark.parametrize("screening", [True, False])
+def test_batched_edge_shapes(m, n, K, screening):
+    """Batched many-RHS FISTA: a partial last problem tile (K % 64), a
+    dictionary narrower than one 16-column chunk or with a ragged last chunk,
+    a single row, the 208-row register envelope; per problem vs the batched
+    oracle."""
+    from oracle.batched_oracle import batched_apg
+    from paper_2202_07258_b200.batched import solve_batched
+    rng = np.random.default_rng(m * 1000 + n * 10 + K)
+    a = np.abs(rng.standard_normal((m, n))) + 0.05
+    X0 = np.zeros((n, K))
+    for k in range(K):
+        sup = rng.choice(n, size=min(3, n), replace=False)
+        X0[sup, k] = rng.random(sup.size)
+    Y = a @ X0 + 0.05 * rng.standard_normal((m, K))
+    g = solve_batched(a, Y, passes=10, rounds=6, gap_tol=1e-300, screening=screening)
+    o = batched_apg(a, Y, eta=g.eta, inner_passes=10, rounds=6, gap_tol=1e-300, screening=screening)
+    # both stop early when every gap reaches exactly 0 (m = 1: exact fit)
+    assert g.rounds == len(o["gap"])
+    scale = np.maximum(np.maximum(np.abs(o["primal"][-1]), np.abs(o["dual"][-1])), 1e-3)
+    for name, gv in (("primal", g.primal), ("dual", g.dual), ("gap", g.gap)):
+        d = np.abs(gv - o[name][-1])
+        assert np.all(d <= 1e-10 * scale), (name, d.max())
+    np.testing.assert_array_equal(g.preserved, o["preserved"][-1])
+    assert np.max(np.abs(g.x - o["X"])) <= 1e-8 * max(1.0, np.abs(o["X"]).max())
+
+
+def test_batched_stops_when_every_problem_converged():
+    from paper_2202_07258_b200.batched import solve_batched
+    rng = np.random.default_rng(3)
+    a = np.abs(rng.standard_normal((60, 20))) + 0.1
+    Y = a @ np.abs(rng.standard_normal((20, 64)))
+    g = solve_batched(a, Y, passes=10, rounds=200, gap_tol=1e-3)
+    assert g.converged == 64 and g.rounds < 200 and np.all(g.gap < 1e-3)
