@@ -715,6 +715,19 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     for (int e = 0; e < V; ++e) acc[e] = 0.0;
     if (row < m) {
       int bb = warp;
+      // eight partial rows in flight per lane (the loop is L2-latency bound)
+      for (; bb + 7 * RED_SLICES < G; bb += 8 * RED_SLICES) {
+        T q[8][V];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)(bb + u * RED_SLICES) * ldp + row), q[u]);
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          acc[e] += ((static_cast<double>(q[0][e]) + static_cast<double>(q[1][e])) +
+                     (static_cast<double>(q[2][e]) + static_cast<double>(q[3][e]))) +
+                    ((static_cast<double>(q[4][e]) + static_cast<double>(q[5][e])) +
+                     (static_cast<double>(q[6][e]) + static_cast<double>(q[7][e])));
+      }
       for (; bb + 3 * RED_SLICES < G; bb += 4 * RED_SLICES) {
         T q0[V], q1[V], q2[V], q3[V];
         unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)bb * ldp + row), q0);
