@@ -73,18 +73,21 @@ struct BatchSmem {
 // This thread's 16-byte pieces of a dictionary chunk (16 columns x m rows),
 // decomposed once per kernel: the (column, row) split of a piece index is the
 // same for every chunk, so the per-chunk copy loop has no integer division.
-constexpr int BT_PMAX = (BT_CH * (BT_MT * 8 / 2) + BT_NT - 1) / BT_NT;
+__host__ __device__ constexpr int bt_pmax(int nt) { return (BT_CH * (BT_MT * 8 / 2) + nt - 1) / nt; }
+template <int NTH>
 struct BtPlan {
-  int jj[BT_PMAX];    // column within the chunk (BT_CH: no piece)
-  int soff[BT_PMAX];  // smem offset (doubles)
-  int goff[BT_PMAX];  // global offset from the chunk's first column (doubles)
+  static constexpr int PM = bt_pmax(NTH);
+  int jj[PM];    // column within the chunk (BT_CH: no piece)
+  int soff[PM];  // smem offset (doubles)
+  int goff[PM];  // global offset from the chunk's first column (doubles)
 };
-__device__ __forceinline__ BtPlan bt_plan(const BatchArgs& a) {
-  BtPlan pl;
+template <int NTH>
+__device__ __forceinline__ BtPlan<NTH> bt_plan(const BatchArgs& a) {
+  BtPlan<NTH> pl;
   const int mv = (a.m + 1) / 2;
 #pragma unroll
-  for (int i = 0; i < BT_PMAX; ++i) {
-    const int q = threadIdx.x + i * BT_NT;
+  for (int i = 0; i < BtPlan<NTH>::PM; ++i) {
+    const int q = threadIdx.x + i * NTH;
     const int jj = q < BT_CH * mv ? q / mv : BT_CH;
     const int v = q - jj * mv;
     pl.jj[i] = jj;
@@ -94,25 +97,27 @@ __device__ __forceinline__ BtPlan bt_plan(const BatchArgs& a) {
   return pl;
 }
 
-__device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BtPlan& pl, const BatchSmem& s, int buf, int c,
-                                            int k0, const double* X, const double* Xp, bool with_x) {
+template <int TILE>
+__device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BtPlan<TILE * 8>& pl, const BatchSmem& s,
+                                            int buf, int c, int k0, const double* X, const double* Xp, bool with_x) {
+  constexpr int NT_ = TILE * 8;
   const int j0 = c * BT_CH;
   const int nj = min(BT_CH, a.n - j0);
   // A chunk: 16 columns x m rows (16-byte pieces)
   double* ab = s.abuf + buf * BT_CH * a.sa;
   const double* ag = a.A + (int64_t)j0 * a.lda;
 #pragma unroll
-  for (int i = 0; i < BT_PMAX; ++i) {
+  for (int i = 0; i < BtPlan<NT_>::PM; ++i) {
     if (pl.jj[i] < nj)
       cp_async16(ab + pl.soff[i], ag + pl.goff[i]);
     else if (pl.jj[i] < BT_CH)
       *reinterpret_cast<double2*>(ab + pl.soff[i]) = make_double2(0.0, 0.0);
   }
   if (with_x) {
-    // x / x_prev chunks: 64 problems x 16 coordinates
-    double* xs = s.xs + buf * BT_TILE * BT_SX;
-    double* xp = s.xps + buf * BT_TILE * BT_SX;
-    for (int q = threadIdx.x; q < BT_TILE * 8; q += BT_NT) {
+    // x / x_prev chunks: TILE problems x 16 coordinates
+    double* xs = s.xs + buf * TILE * BT_SX;
+    double* xp = s.xps + buf * TILE * BT_SX;
+    for (int q = threadIdx.x; q < TILE * 8; q += NT_) {
       const int nn = q >> 3, v = q & 7;
       if (2 * v < nj) {
         cp_async16(xs + nn * BT_SX + 2 * v, X + (int64_t)(k0 + nn) * a.ldx + j0 + 2 * v);
@@ -120,9 +125,9 @@ __device__ __forceinline__ void bt_prefetch(const BatchArgs& a, const BtPlan& pl
       }
     }
   }
-  if (threadIdx.x < BT_TILE) {
+  if (threadIdx.x < TILE) {
     const int w = j0 >> 5;
-    s.mk[buf * BT_TILE + threadIdx.x] = a.mask[(int64_t)(k0 + threadIdx.x) * a.nw + w];
+    s.mk[buf * TILE + threadIdx.x] = a.mask[(int64_t)(k0 + threadIdx.x) * a.nw + w];
   }
   cp_async_commit();
 }
@@ -201,43 +206,50 @@ __device__ __forceinline__ void bt_gemm2(const BatchArgs& a, const double* ab, c
   }
 }
 
-__global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
+// TILE = 64: 16 warps, double-buffered dictionary chunks, one CTA per SM;
+// TILE = 32: 8 warps, single-buffered chunks, two CTAs per SM (each CTA's
+// chunk-copy waits and barriers overlap the other CTA's DMMA work)
+template <int TILE>
+__global__ void __launch_bounds__(TILE * 8, 512 / (TILE * 8)) k_batched_round(const BatchArgs a) {
+  constexpr int NT_ = TILE * 8;
+  constexpr int NTW = TILE / 8;             // problem tiles (of 8) per CTA
+  constexpr int NB = TILE == 64 ? 2 : 1;    // dictionary chunk buffers
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
-  const int nt = warp & 7, mh = warp >> 3;  // problem tile of this warp, coordinate / row half
+  const int nt = warp % NTW, mh = warp / NTW;  // problem tile of this warp, coordinate / row half
   const int n0 = nt * 8;
   BatchSmem s;
   {
     double* p = reinterpret_cast<double*>(smem_raw);
     s.rys = p;
-    p += BT_TILE * a.sa;
+    p += TILE * a.sa;
     s.abuf = p;
-    p += 2 * BT_CH * a.sa;
+    p += NB * BT_CH * a.sa;
     s.xs = p;
-    p += 2 * BT_TILE * BT_SX;
+    p += NB * TILE * BT_SX;
     s.xps = p;
-    p += 2 * BT_TILE * BT_SX;
+    p += NB * TILE * BT_SX;
     s.xns = p;
-    p += BT_TILE * BT_SX;
+    p += TILE * BT_SX;
     s.red = p;  // [8][64]: per-problem partials of the two warp halves
-    p += 8 * BT_TILE;
+    p += 8 * TILE;
     s.beta = p;
-    p += BT_TILE;
+    p += TILE;
     s.mk = reinterpret_cast<uint32_t*>(p);
   }
-  const BtPlan pl = bt_plan(a);
+  const BtPlan<NT_> pl = bt_plan<NT_>(a);
   const int mt_n = (a.m + 7) / 8;
   const int mlo = mh ? BT_MH : 0, mhi = mh ? mt_n : min(BT_MH, mt_n);
   const int nch = (a.n + BT_CH - 1) / BT_CH;
-  const int ntiles = a.K / BT_TILE;
+  const int ntiles = a.K / TILE;
   // zero both dictionary buffers once: rows in [m, sa) and columns past n are
   // never written by the chunk copies and must multiply as exact zeros
-  for (int q = tid; q < 2 * BT_CH * a.sa; q += BT_NT) s.abuf[q] = 0.0;
+  for (int q = tid; q < NB * BT_CH * a.sa; q += NT_) s.abuf[q] = 0.0;
   __syncthreads();
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int k0 = tile * BT_TILE;
+    const int k0 = tile * TILE;
     int par = a.par;
     // ---------------- FISTA steps ----------------
     for (int pass = 0; pass < a.passes; ++pass) {
@@ -245,14 +257,14 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       double* Xp = a.X[1 - par];  // read as x_prev, then overwritten by x+
       const double* R = a.R[par];
       double* Rp = a.R[1 - par];
-      if (tid < BT_TILE) {
+      if (tid < TILE) {
         const double t = a.mom[k0 + tid];
         const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
         s.beta[tid] = (t - 1.0) / tn;
       }
       __syncthreads();
       // R_y = R + beta (R - R_prev)  (rows >= m zero padded)
-      for (int q = tid; q < BT_TILE * a.sa; q += BT_NT) {
+      for (int q = tid; q < TILE * a.sa; q += NT_) {
         const int nn = q / a.sa, i = q - nn * a.sa;
         double v = 0.0;
         if (i < a.m) {
@@ -268,16 +280,20 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       for (int q = 0; q < BT_MH; ++q) acc[q][0] = acc[q][1] = 0.0;
       double gdot[2] = {0.0, 0.0}, gsc[2] = {0.0, 0.0};
       const double bt0 = s.beta[n0 + 2 * tig], bt1 = s.beta[n0 + 2 * tig + 1];
-      bt_prefetch(a, pl, s, 0, 0, k0, X, Xp, true);
+      bt_prefetch<TILE>(a, pl, s, 0, 0, k0, X, Xp, true);
       for (int c = 0; c < nch; ++c) {
-        const int buf = c & 1;
+        if (NB == 1 && c > 0) {  // the single buffer is free once every warp left chunk c-1
+          __syncthreads();
+          bt_prefetch<TILE>(a, pl, s, 0, c, k0, X, Xp, true);
+        }
+        const int buf = NB == 2 ? (c & 1) : 0;
         cp_async_wait_all();
         __syncthreads();
-        if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, X, Xp, true);
+        if (NB == 2 && c + 1 < nch) bt_prefetch<TILE>(a, pl, s, buf ^ 1, c + 1, k0, X, Xp, true);
         const double* ab = s.abuf + buf * BT_CH * a.sa;
-        const double* xs = s.xs + buf * BT_TILE * BT_SX;
-        const double* xps = s.xps + buf * BT_TILE * BT_SX;
-        const uint32_t* mk = s.mk + buf * BT_TILE;
+        const double* xs = s.xs + buf * TILE * BT_SX;
+        const double* xps = s.xps + buf * TILE * BT_SX;
+        const uint32_t* mk = s.mk + buf * TILE;
         double gt[2];
         bt_gemm1(a, ab, s.rys, n0, mh, g, tig, gt);
         // epilogue: the FISTA update of this lane's two elements
@@ -310,7 +326,7 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
         // x+ chunk -> global (the x_prev slot, already consumed for this chunk)
         {
           const int nj = min(BT_CH, a.n - j0);
-          for (int q = tid; q < BT_TILE * BT_CH; q += BT_NT) {
+          for (int q = tid; q < TILE * BT_CH; q += NT_) {
             const int nn = q / BT_CH, jj = q - nn * BT_CH;
             if (jj < nj) Xp[(int64_t)(k0 + nn) * a.ldx + j0 + jj] = s.xns[nn * BT_SX + jj];
           }
@@ -345,17 +361,17 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int nn = n0 + 2 * tig + e;
-          s.red[(0 + mh) * BT_TILE + nn] = sq[e];
-          s.red[(2 + mh) * BT_TILE + nn] = gdot[e];
-          s.red[(4 + mh) * BT_TILE + nn] = gsc[e];
+          s.red[(0 + mh) * TILE + nn] = sq[e];
+          s.red[(2 + mh) * TILE + nn] = gdot[e];
+          s.red[(4 + mh) * TILE + nn] = gsc[e];
         }
       }
       __syncthreads();
-      if (tid < BT_TILE) {
+      if (tid < TILE) {
         const int k = k0 + tid;
-        const double Pn = 0.5 * (s.red[tid] + s.red[BT_TILE + tid]);
-        const double gd = s.red[2 * BT_TILE + tid] + s.red[3 * BT_TILE + tid];
-        const double gs = s.red[4 * BT_TILE + tid] + s.red[5 * BT_TILE + tid];
+        const double Pn = 0.5 * (s.red[tid] + s.red[TILE + tid]);
+        const double gd = s.red[2 * TILE + tid] + s.red[3 * TILE + tid];
+        const double gs = s.red[4 * TILE + tid] + s.red[5 * TILE + tid];
         const double P = a.P[k];
         const double t = a.mom[k];
         const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
@@ -373,18 +389,22 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       double* Xq = a.X[1 - par];
       const double* R = a.R[par];
       // r at x into smem
-      for (int q = tid; q < BT_TILE * a.sa; q += BT_NT) {
+      for (int q = tid; q < TILE * a.sa; q += NT_) {
         const int nn = q / a.sa, i = q - nn * a.sa;
         s.rys[q] = (i < a.m) ? R[(int64_t)(k0 + nn) * a.ldy + i] : 0.0;
       }
       // sweep 1: epsilon_k = max_j (v_jk)+ / |a_j't|, v = -A'r
       double emax[2] = {0.0, 0.0};
-      bt_prefetch(a, pl, s, 0, 0, k0, X, nullptr, false);
+      bt_prefetch<TILE>(a, pl, s, 0, 0, k0, X, nullptr, false);
       for (int c = 0; c < nch; ++c) {
-        const int buf = c & 1;
+        if (NB == 1 && c > 0) {  // the single buffer is free once every warp left chunk c-1
+          __syncthreads();
+          bt_prefetch<TILE>(a, pl, s, 0, c, k0, X, nullptr, false);
+        }
+        const int buf = NB == 2 ? (c & 1) : 0;
         cp_async_wait_all();
         __syncthreads();
-        if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, X, nullptr, false);
+        if (NB == 2 && c + 1 < nch) bt_prefetch<TILE>(a, pl, s, buf ^ 1, c + 1, k0, X, nullptr, false);
         double gt[2];
         bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, mh, g, tig, gt);
         const int j = c * BT_CH + 8 * mh + g;
@@ -399,14 +419,14 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) emax[e] = fmax(emax[e], __shfl_xor_sync(0xffffffffu, emax[e], o));
       if (g == 0) {
-        s.red[mh * BT_TILE + n0 + 2 * tig] = emax[0];
-        s.red[mh * BT_TILE + n0 + 2 * tig + 1] = emax[1];
+        s.red[mh * TILE + n0 + 2 * tig] = emax[0];
+        s.red[mh * TILE + n0 + 2 * tig + 1] = emax[1];
       }
       __syncthreads();
-      if (tid < BT_TILE) s.beta[tid] = fmax(s.red[tid], s.red[BT_TILE + tid]);  // eps per problem
+      if (tid < TILE) s.beta[tid] = fmax(s.red[tid], s.red[TILE + tid]);  // eps per problem
       __syncthreads();
       // dual objective per problem: theta = -r + eps t (t = -1): theta_i = -r_i - eps
-      for (int pb = warp; pb < BT_TILE; pb += BT_NT / 32) {
+      for (int pb = warp; pb < TILE; pb += NT_ / 32) {
         const double eps = s.beta[pb];
         double s1 = 0.0, s2 = 0.0;
         for (int i = lane; i < a.m; i += 32) {
@@ -427,7 +447,7 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
           st[a.K + k] = D;
           st[2 * a.K + k] = gap;
           st[3 * a.K + k] = eps;
-          s.red[6 * BT_TILE + pb] = sqrt(2.0 * gap) + a.slack_scale * fmax(1.0, sqrt(s2));  // radius + slack
+          s.red[6 * TILE + pb] = sqrt(2.0 * gap) + a.slack_scale * fmax(1.0, sqrt(s2));  // radius + slack
         }
       }
       __syncthreads();
@@ -435,15 +455,19 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
       __shared__ int dirty;
       if (tid == 0) dirty = 0;
       if (a.screening) {
-        bt_prefetch(a, pl, s, 0, 0, k0, X, nullptr, false);
+        bt_prefetch<TILE>(a, pl, s, 0, 0, k0, X, nullptr, false);
         for (int c = 0; c < nch; ++c) {
-          const int buf = c & 1;
+          if (NB == 1 && c > 0) {  // the single buffer is free once every warp left chunk c-1
+            __syncthreads();
+            bt_prefetch<TILE>(a, pl, s, 0, c, k0, X, nullptr, false);
+          }
+          const int buf = NB == 2 ? (c & 1) : 0;
           cp_async_wait_all();
           __syncthreads();
-          if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, X, nullptr, false);
+          if (NB == 2 && c + 1 < nch) bt_prefetch<TILE>(a, pl, s, buf ^ 1, c + 1, k0, X, nullptr, false);
           double gt[2];
           bt_gemm1(a, s.abuf + buf * BT_CH * a.sa, s.rys, n0, mh, g, tig, gt);
-          const uint32_t* mk = s.mk + buf * BT_TILE;
+          const uint32_t* mk = s.mk + buf * TILE;
           const int j = c * BT_CH + 8 * mh + g;
           if (j < a.n) {
 #pragma unroll
@@ -451,7 +475,7 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
               const int nn = n0 + 2 * tig + e;
               const bool act = (mk[nn] >> (j & 31)) & 1u;
               const double v = add_rn(-gt[e], mul_rn(s.beta[nn], a.att[j]));
-              if (act && v < -s.red[6 * BT_TILE + nn] * a.nrm[j]) {
+              if (act && v < -s.red[6 * TILE + nn] * a.nrm[j]) {
                 const int64_t k = k0 + nn;
                 atomicAnd(&a.mask[k * a.nw + (j >> 5)], ~(1u << (j & 31)));
                 const_cast<double*>(X)[k * a.ldx + j] = 0.0;
@@ -471,16 +495,20 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
           double acc[BT_MH][2];
 #pragma unroll
           for (int q = 0; q < BT_MH; ++q) acc[q][0] = acc[q][1] = 0.0;
-          bt_prefetch(a, pl, s, 0, 0, k0, Xw, nullptr, true);
+          bt_prefetch<TILE>(a, pl, s, 0, 0, k0, Xw, nullptr, true);
           for (int c = 0; c < nch; ++c) {
-            const int buf = c & 1;
+            if (NB == 1 && c > 0) {  // the single buffer is free once every warp left chunk c-1
+              __syncthreads();
+              bt_prefetch<TILE>(a, pl, s, 0, c, k0, Xw, nullptr, true);
+            }
+            const int buf = NB == 2 ? (c & 1) : 0;
             cp_async_wait_all();
             __syncthreads();
-            if (c + 1 < nch) bt_prefetch(a, pl, s, buf ^ 1, c + 1, k0, Xw, nullptr, true);
+            if (NB == 2 && c + 1 < nch) bt_prefetch<TILE>(a, pl, s, buf ^ 1, c + 1, k0, Xw, nullptr, true);
             // stage the chunk in the conflict-free layout of xns
-            const double* xs = s.xs + buf * BT_TILE * BT_SX;
+            const double* xs = s.xs + buf * TILE * BT_SX;
             const int nj = min(BT_CH, a.n - c * BT_CH);
-            for (int q = tid; q < BT_TILE * BT_CH; q += BT_NT) {
+            for (int q = tid; q < TILE * BT_CH; q += NT_) {
               const int nn = q / BT_CH, jj = q - nn * BT_CH;
               s.xns[nn * BT_SX + jj] = (jj < nj) ? xs[nn * BT_SX + jj] : 0.0;
             }
@@ -506,16 +534,16 @@ __global__ void __launch_bounds__(BT_NT, 1) k_batched_round(const BatchArgs a) {
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) sq[e] += __shfl_xor_sync(0xffffffffu, sq[e], o);
           if (g == 0) {
-            s.red[mh * BT_TILE + n0 + 2 * tig] = sq[0];
-            s.red[mh * BT_TILE + n0 + 2 * tig + 1] = sq[1];
+            s.red[mh * TILE + n0 + 2 * tig] = sq[0];
+            s.red[mh * TILE + n0 + 2 * tig + 1] = sq[1];
           }
           __syncthreads();
-          if (which == 0 && tid < BT_TILE) a.P[k0 + tid] = 0.5 * (s.red[tid] + s.red[BT_TILE + tid]);
+          if (which == 0 && tid < TILE) a.P[k0 + tid] = 0.5 * (s.red[tid] + s.red[TILE + tid]);
           __syncthreads();
         }
       }
       // preserved counts
-      for (int pb = warp; pb < BT_TILE; pb += BT_NT / 32) {
+      for (int pb = warp; pb < TILE; pb += NT_ / 32) {
         int cnt = 0;
         for (int w = lane; w < a.nw; w += 32) cnt += __popc(a.mask[(int64_t)(k0 + pb) * a.nw + w]);
         cnt = warp_sum<int>(cnt);

@@ -2481,6 +2481,7 @@ struct bx_batch {
   std::string err;
   int nsm = 148;
   size_t smem = 0;
+  int tile = 64;  // problems per CTA tile of k_batched_round
 };
 
 namespace {
@@ -2634,8 +2635,18 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
   int dev = 0;
   BCU(cudaGetDevice(&dev));
   BCU(cudaDeviceGetAttribute(&b->nsm, cudaDevAttrMultiProcessorCount, dev));
-  b->smem = ((size_t)BT_TILE * A.sa + 2 * BT_CH * A.sa + 5 * BT_TILE * BT_SX + 9 * BT_TILE) * 8 + 2 * BT_TILE * 4 + 64;
-  BCU(cudaFuncSetAttribute(k_batched_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
+  // problem tile: 64 (one CTA per SM) or 32 (two CTAs per SM); BX_BT_TILE overrides
+  {
+    const char* e = getenv("BX_BT_TILE");
+    b->tile = (e && atoi(e) == 32) ? 32 : 64;
+  }
+  const int nb = b->tile == 64 ? 2 : 1;
+  b->smem = ((size_t)b->tile * A.sa + (size_t)nb * BT_CH * A.sa + (size_t)(2 * nb + 1) * b->tile * BT_SX +
+             9 * (size_t)b->tile) * 8 + 2 * (size_t)b->tile * 4 + 64;
+  if (b->tile == 64)
+    BCU(cudaFuncSetAttribute(k_batched_round<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
+  else
+    BCU(cudaFuncSetAttribute(k_batched_round<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
   BCU(cudaMallocHost((void**)&b->hred, 64));
   // padded copy of Y, t = -1, column norms and A't of the dictionary
   k_pad_copy<<<1024, 256, 0, b->stream>>>(y, ldy, m, k_rhs, const_cast<double*>(A.Y), L.ldy, L.Kp);
@@ -2668,11 +2679,15 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
   A.par = 0;
   k_batched_init<<<1024, 256, 0, b->stream>>>(A);
   b->launches = 1;
-  int grid = b->nsm < A.K / BT_TILE ? b->nsm : A.K / BT_TILE;
+  const int per_sm = b->tile == 64 ? 1 : 2;
+  int grid = per_sm * b->nsm < A.K / b->tile ? per_sm * b->nsm : A.K / b->tile;
   int64_t r = 0;
   int64_t conv = 0;
   for (r = 0; r < rounds; ++r) {
-    k_batched_round<<<grid, BT_NT, b->smem, b->stream>>>(A);
+    if (b->tile == 64)
+      k_batched_round<64><<<grid, 64 * 8, b->smem, b->stream>>>(A);
+    else
+      k_batched_round<32><<<grid, 32 * 8, b->smem, b->stream>>>(A);
     k_batched_summary<<<1, 1024, 0, b->stream>>>(A.stats, A.K, b->K_user, gap_tol, b->red);
     b->launches += 2;
     BCU(cudaGetLastError());
