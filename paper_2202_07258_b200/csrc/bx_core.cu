@@ -1282,16 +1282,25 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
   }
   if (!gs.exec || !(gs.key == key)) {
     gs.reset();
-    CU(cudaGraphCreate(&gs.graph, 0));
+    // any failure while building (e.g. a driver without conditional nodes)
+    // leaves the host loop in charge
+    auto give_up = [&]() {
+      cudaGetLastError();
+      gs.reset();
+      gs.broken = true;
+      return BX_OK;
+    };
     cudaGraphConditionalHandle h;
-    CU(cudaGraphConditionalHandleCreate(&h, gs.graph, 1, cudaGraphCondAssignDefault));
     cudaGraphNodeParams p = {};
     p.type = cudaGraphNodeTypeConditional;
-    p.conditional.handle = h;
     p.conditional.type = cudaGraphCondTypeWhile;
     p.conditional.size = 1;
     cudaGraphNode_t node;
-    CU(cudaGraphAddNode(&node, gs.graph, nullptr, 0, &p));
+    if (cudaGraphCreate(&gs.graph, 0) != cudaSuccess ||
+        cudaGraphConditionalHandleCreate(&h, gs.graph, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+      return give_up();
+    p.conditional.handle = h;
+    if (cudaGraphAddNode(&node, gs.graph, nullptr, 0, &p) != cudaSuccess) return give_up();
     cudaGraph_t body = p.conditional.phGraph_out[0];
     // capture on the private stream (the round functions launch on c->stream)
     cudaStream_t user_stream = c->stream;
@@ -1330,9 +1339,10 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
       return BX_OK;
     }
     size_t nn = 0;
-    CU(cudaGraphGetNodes(body, nullptr, &nn));
+    if (cudaGraphGetNodes(body, nullptr, &nn) != cudaSuccess ||
+        cudaGraphInstantiate(&gs.exec, gs.graph, 0) != cudaSuccess)
+      return give_up();
     c->graph_body_kernels = (int64_t)nn;
-    CU(cudaGraphInstantiate(&gs.exec, gs.graph, 0));
     gs.key = key;
   }
   const int hd0[3] = {0, 0, limit};
