@@ -534,8 +534,9 @@ void shape_params(bx_ctx* c) {
 int pick_R(int64_t m, size_t esz) {
   const int V = (int)(16 / esz);
   const int64_t per = (int64_t)NT * V;
-  const int Rs[] = {1, 2, 4, 6, 8, 10, 12};
-  for (int R : Rs)
+  // the smallest R with R * NT * V >= m: then every row-vector of the first
+  // R - 1 chunks is full (k_pass drops their row guards)
+  for (int R = 1; R <= 12; ++R)
     if ((int64_t)R * per >= m) return R;
   return -1;
 }
@@ -687,6 +688,11 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
     case 8: st = launch_pass_R<T, 8>(c, a, dot, axpy, G, smem, acc64); break;
     case 10: st = launch_pass_R<T, 10>(c, a, dot, axpy, G, smem, acc64); break;
     case 12: st = launch_pass_R<T, 12>(c, a, dot, axpy, G, smem, acc64); break;
+    case 3: st = launch_pass_R<T, 3>(c, a, dot, axpy, G, smem, acc64); break;
+    case 5: st = launch_pass_R<T, 5>(c, a, dot, axpy, G, smem, acc64); break;
+    case 7: st = launch_pass_R<T, 7>(c, a, dot, axpy, G, smem, acc64); break;
+    case 9: st = launch_pass_R<T, 9>(c, a, dot, axpy, G, smem, acc64); break;
+    case 11: st = launch_pass_R<T, 11>(c, a, dot, axpy, G, smem, acc64); break;
     default: st = fail(c, BX_ERR_UNSUPPORTED, "R=%d", R);
   }
   if (e0 >= 0) {

@@ -431,14 +431,22 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
           T dd[V];
 #pragma unroll
           for (int e = 0; e < V; ++e) dd[e] = T(0);
+          // chunks 0 .. R-2 are full for every thread (R is the smallest
+          // with R * NT * V >= m): no row guards, no divergence bookkeeping
 #pragma unroll
-          for (int i = 0; i < R; ++i) {
+          for (int i = 0; i < R - 1; ++i) {
+            T av[V];
+            unpack<T>(*reinterpret_cast<const VT*>(col + row0 + i * (NT * V)), av);
+            // packed fp32 FMA (FFMA2): same per-element fma.rn as the
+            // scalar chains, half the issue slots
+            fma2_acc(dd, av, vr[i]);
+          }
+#pragma unroll
+          for (int i = R - 1; i < R; ++i) {
             const int row = row0 + i * (NT * V);
             if (row + V <= m) {
               T av[V];
               unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
-              // packed fp32 FMA (FFMA2): same per-element fma.rn as the
-              // scalar chains, half the issue slots
               fma2_acc(dd, av, vr[i]);
             } else if (row < m) {
               T av[V];
@@ -533,7 +541,29 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       }
       __syncthreads();
     }
-    if (AXPY) {
+    if constexpr (AXPY && sizeof(T) == 4 && sizeof(AT) == 4) {
+      // fp32: chunks 0 .. R-2 unguarded (see the dot); rows >= m of the last
+      // vector only reach the padding of the partial row, which k_reduce never
+      // reads
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (c < cg) {
+          const AT cc = static_cast<AT>(cf[c]);
+          const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
+#pragma unroll
+          for (int i = 0; i < R - 1; ++i) {
+            T av[V];
+            unpack<T>(*reinterpret_cast<const VT*>(col + row0 + i * (NT * V)), av);
+            fma2_axpy(acc[i], av, cc);
+          }
+          if (row0 + (R - 1) * (NT * V) < m) {
+            T av[V];
+            unpack<T>(*reinterpret_cast<const VT*>(col + row0 + (R - 1) * (NT * V)), av);
+            fma2_axpy(acc[R - 1], av, cc);
+          }
+        }
+      }
+    } else if (AXPY) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (c < cg) {
