@@ -394,15 +394,22 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         if (c < cg) {
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
           if constexpr (sizeof(T) == 8) {
-            // fp64: one chain per thread (measured faster than split sums here)
+            // fp64: one chain per thread (measured faster than split sums
+            // here); chunks 0 .. R-2 are full (see the fp32 path): no guards
 #pragma unroll
-            for (int i = 0; i < R; ++i) {
-              const int row = row0 + i * (NT * V);
+            for (int i = 0; i < R - 1; ++i) {
+              T av[V];
+              unpack<T>(*reinterpret_cast<const VT*>(col + row0 + i * (NT * V)), av);
+#pragma unroll
+              for (int e = 0; e < V; ++e) d[c] += av[e] * vr[i][e];
+            }
+            {
+              const int row = row0 + (R - 1) * (NT * V);
               if (row < m) {
                 T av[V];
                 unpack<T>(*reinterpret_cast<const VT*>(col + row), av);
 #pragma unroll
-                for (int e = 0; e < V; ++e) d[c] += ((row + e < m) ? av[e] : T(0)) * vr[i][e];
+                for (int e = 0; e < V; ++e) d[c] += ((row + e < m) ? av[e] : T(0)) * vr[R - 1][e];
               }
             }
           } else if constexpr (sizeof(AT) == 8) {
@@ -541,7 +548,30 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       }
       __syncthreads();
     }
-    if constexpr (AXPY && sizeof(T) == 4 && sizeof(AT) == 4) {
+    if constexpr (AXPY && sizeof(T) == 8) {
+      // fp64: chunks 0 .. R-2 unguarded; the last chunk's rows >= m only
+      // reach the padding of the partial row, which k_reduce never reads
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (c < cg) {
+          const AT cc = static_cast<AT>(cf[c]);
+          const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
+#pragma unroll
+          for (int i = 0; i < R - 1; ++i) {
+            T av[V];
+            unpack<T>(*reinterpret_cast<const VT*>(col + row0 + i * (NT * V)), av);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[i][e] += av[e] * cc;
+          }
+          if (row0 + (R - 1) * (NT * V) < m) {
+            T av[V];
+            unpack<T>(*reinterpret_cast<const VT*>(col + row0 + (R - 1) * (NT * V)), av);
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[R - 1][e] += av[e] * cc;
+          }
+        }
+      }
+    } else if constexpr (AXPY && sizeof(T) == 4 && sizeof(AT) == 4) {
       // fp32: chunks 0 .. R-2 unguarded (see the dot); rows >= m of the last
       // vector only reach the padding of the partial row, which k_reduce never
       // reads
