@@ -367,22 +367,14 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     __syncthreads();
   }
 
-  // ring slot / mbarrier phase of group gi: a running counter on the fp32
-  // pass, gi % S on the fp64 pass (A/B on the B200: the counter is ~5%
-  // faster for fp32 and ~14% slower for fp64, scheduling of the 128-register
-  // fp64 kernel)
+  // ring slot / mbarrier phase of group gi: a running counter (no integer
+  // division per column; A/B on the B200 with the unguarded chunk loops:
+  // ~2% faster for fp64 under the power cap, ~5% for fp32)
   int s_run = 0;
   uint32_t ph_run = 0;
   for (int gi = 0; gi < ngroups; ++gi) {
-    int s;
-    uint32_t ph;
-    if constexpr (sizeof(T) == 4) {
-      s = s_run;
-      ph = ph_run;
-    } else {
-      s = gi % S;
-      ph = (uint32_t)((gi / S) & 1);
-    }
+    const int s = s_run;
+    const uint32_t ph = ph_run;
     const int cg = min(C, ncol - gi * C);
     mbar_wait(&bars[s], ph);
     const unsigned char* slot = smem + s * slot_bytes;
@@ -622,11 +614,9 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       }
     }
     __syncthreads();  // every thread is done with slot s
-    if constexpr (sizeof(T) == 4) {
-      if (++s_run == S) {
-        s_run = 0;
-        ph_run ^= 1u;
-      }
+    if (++s_run == S) {
+      s_run = 0;
+      ph_run ^= 1u;
     }
     if (tid == 0 && gi + S < ngroups) {
       const int gn = gi + S;
