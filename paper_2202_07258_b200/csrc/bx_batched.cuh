@@ -322,12 +322,15 @@ __global__ void __launch_bounds__(TILE * 8, 512 / (TILE * 8)) k_batched_round(co
             s.xns[nn * BT_SX + jj] = xn;
           }
         }
-        __syncthreads();
+        // only the warp pair of problem tile nt shares these xns rows: a
+        // named barrier per pair instead of a CTA barrier, so pairs drift and
+        // one pair's epilogue overlaps another's DMMA work
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + nt) : "memory");
         // x+ chunk -> global (the x_prev slot, already consumed for this chunk)
         {
           const int nj = min(BT_CH, a.n - j0);
-          for (int q = tid; q < TILE * BT_CH; q += NT_) {
-            const int nn = q / BT_CH, jj = q - nn * BT_CH;
+          for (int q = mh * 32 + lane; q < 8 * BT_CH; q += 64) {
+            const int nn = n0 + q / BT_CH, jj = q % BT_CH;
             if (jj < nj) Xp[(int64_t)(k0 + nn) * a.ldx + j0 + jj] = s.xns[nn * BT_SX + jj];
           }
         }
