@@ -220,6 +220,33 @@ struct LocalComm : Comm {
 // ---------------------------------------------------------------------------
 // the context
 // ---------------------------------------------------------------------------
+// Small pinned host blocks (the per-round scalar mirrors) come from a
+// process-wide free list: cudaMallocHost / cudaFreeHost per solve are
+// heavyweight driver calls that serialise with anything else holding the
+// driver (e.g. an nvidia-smi query) and showed up as 2x outliers in short
+// timed solves.
+constexpr size_t kPinBlock = 4096;
+static std::mutex g_pin_mu;
+static std::vector<void*> g_pin_free;
+static void* pin_acquire(size_t bytes) {
+  if (bytes > kPinBlock) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      void* p = g_pin_free.back();
+      g_pin_free.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  return cudaMallocHost(&p, kPinBlock) == cudaSuccess ? p : nullptr;
+}
+static void pin_release(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 // A communicator that outlives contexts (bx_comm_create): the NCCL
 // communicator plus the fused exchange's IPC-mapped receive buffers and
 // their epoch counter, set up once per process group and borrowed by every
@@ -1235,19 +1262,49 @@ __global__ void k_graph_round_end(GraphEndArgs a) {
   cudaGraphSetConditional(a.h, (!ev && q + 1 < *a.limit) ? 1u : 0u);
 }
 
+// private capture / launch streams (+ join events) of the graph path, pooled
+// per process like the pinned blocks (no stream / event creation per solve)
+struct GraphStream {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t join[2] = {nullptr, nullptr};
+};
+static std::mutex g_gs_mu;
+static std::vector<GraphStream> g_gs_free;
+static bool graph_stream_acquire(GraphStream* out) {
+  {
+    std::lock_guard<std::mutex> lk(g_gs_mu);
+    if (!g_gs_free.empty()) {
+      *out = g_gs_free.back();
+      g_gs_free.pop_back();
+      return true;
+    }
+  }
+  GraphStream g;
+  if (cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&g.join[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&g.join[1], cudaEventDisableTiming) != cudaSuccess)
+    return false;
+  *out = g;
+  return true;
+}
+static void graph_stream_release(const GraphStream& g) {
+  if (!g.cs) return;
+  std::lock_guard<std::mutex> lk(g_gs_mu);
+  g_gs_free.push_back(g);
+}
+
 struct GraphState {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  cudaStream_t cs = nullptr;  // private capture / launch stream (the caller's may be the legacy default stream)
-  cudaEvent_t join[2] = {nullptr, nullptr};
+  GraphStream gst;            // private capture / launch stream (the caller's may be the legacy default stream)
+  cudaStream_t& cs = gst.cs;
+  cudaEvent_t* join = gst.join;
   GraphKey key{};
   bool broken = false;  // capture not steady / unsupported: stop trying this solve
   ~GraphState() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    for (auto& e : join)
-      if (e) cudaEventDestroy(e);
-    if (cs) cudaStreamDestroy(cs);
+    graph_stream_release(gst);
   }
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -1277,14 +1334,10 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
   }
   if (limit > kSmallRounds) limit = kSmallRounds;
   const GraphKey key = graph_key(c, kind, passes, screening);
-  if (!gs.cs) {
-    if (cudaStreamCreateWithFlags(&gs.cs, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&gs.join[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&gs.join[1], cudaEventDisableTiming) != cudaSuccess) {
-      cudaGetLastError();
-      gs.broken = true;
-      return BX_OK;
-    }
+  if (!gs.cs && !graph_stream_acquire(&gs.gst)) {
+    cudaGetLastError();
+    gs.broken = true;
+    return BX_OK;
   }
   if (!gs.exec || !(gs.key == key)) {
     gs.reset();
@@ -2079,7 +2132,8 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   char* base = (char*)align_up((uintptr_t)workspace, kAlign);
   Carver w{base, 0, workspace_bytes, false};
   carve(c, w);
-  CU(cudaMallocHost((void**)&c->hsc, sizeof(DevScalars)));
+  c->hsc = (DevScalars*)pin_acquire(sizeof(DevScalars));
+  if (!c->hsc) return fail(c, BX_ERR_CUDA, "pinned scalar mirror");
   memset(c->hsc, 0, sizeof(DevScalars));
   CU(cudaMemsetAsync(c->sc, 0, sizeof(DevScalars), c->stream));
   CU(cudaMemsetAsync(c->part, 0, (size_t)c->Gmax * c->ldp * 8, c->stream));
@@ -2092,8 +2146,8 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
 int bx_ctx_destroy(bx_ctx* c) {
   if (!c) return BX_OK;
   for (auto& e : c->ev) cudaEventDestroy(e);
-  if (c->hsc) cudaFreeHost(c->hsc);
-  if (c->has) cudaFreeHost(c->has);
+  pin_release(c->hsc);
+  pin_release(c->has);
   for (void* p : c->xopened) cudaIpcCloseMemHandle(p);
   if (c->xbuf) cudaFree(c->xbuf);
   if (c->comm_owned) delete c->comm;
@@ -2240,7 +2294,10 @@ int bx_ctx_set_active_set_workspace(bx_ctx* c, void* workspace, size_t bytes) {
   c->as_s = (double*)w.take((size_t)(pcap + 1) * 8);
   c->as_frac = (double*)w.take((size_t)(pcap + 1) * 8);
   c->as = (AsState*)w.take(sizeof(AsState));
-  if (!c->has) CU(cudaMallocHost((void**)&c->has, sizeof(AsState)));
+  if (!c->has) {
+    c->has = (AsState*)pin_acquire(sizeof(AsState));
+    if (!c->has) return fail(c, BX_ERR_CUDA, "pinned active-set mirror");
+  }
   memset(c->has, 0, sizeof(AsState));
   c->as_dirty = true;
   return BX_OK;
@@ -2663,7 +2720,8 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
     BCU(cudaFuncSetAttribute(k_batched_round<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
   else
     BCU(cudaFuncSetAttribute(k_batched_round<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
-  BCU(cudaMallocHost((void**)&b->hred, 64));
+  b->hred = (double*)pin_acquire(64);
+  if (!b->hred) return BX_ERR_CUDA;
   // padded copy of Y, t = -1, column norms and A't of the dictionary
   k_pad_copy<<<1024, 256, 0, b->stream>>>(y, ldy, m, k_rhs, const_cast<double*>(A.Y), L.ldy, L.Kp);
   k_fill<double><<<4, 256, 0, b->stream>>>(L.ldy, b->t, 0.0);
@@ -2749,7 +2807,7 @@ const char* bx_batched_last_error(const bx_batch* b) { return b ? b->err.c_str()
 
 int bx_batched_destroy(bx_batch* b) {
   if (!b) return BX_OK;
-  if (b->hred) cudaFreeHost(b->hred);
+  pin_release(b->hred);
   delete b;
   return BX_OK;
 }
