@@ -9,7 +9,10 @@
 //                 x_j'  = clip(y_j - eta g_j, l_j, u_j)    (PG / FISTA update)
 //                 acc  += a_j x_j'           (the next residual's partial A x')
 //              so ONE read of A serves both products of a projected-gradient
-//              step (solvers.py:109-116 does two GEMV passes).  Modes cover
+//              step (solvers.py:109-116 does two GEMV passes).  Each thread
+//              owns R row chunks of 16-byte vectors, R the smallest count
+//              covering m, so chunks 0..R-2 run without row guards (the pass
+//              is issue-limited under the board power cap).  Modes cover
 //              the screening pass (dot + epsilon partial), power iteration
 //              (solvers.py:78-85) and plain A x (refresh, certified gap).
 //   k_reduce   sums the per-CTA partial rows in a fixed order (deterministic),

@@ -6,12 +6,15 @@
 // bound at this size: ~21 us per step for 16 MB.  Here every CTA loads its
 // contiguous block of preserved columns into shared memory ONCE per round and
 // keeps it there; each step is
-//     dots of the local columns with the (register-resident) residual
-//     -> local x update -> local partial A x+ rows  -> grid barrier
+//     dots of the local columns (one warp per column) with the residual
+//     staged in shared memory -> each column's x update by the lane that
+//     holds its dot -> local partial A x+ rows  -> grid barrier
 //     -> CTA b reduces rows [b*mb, (b+1)*mb) over all partials in a fixed order
 //        (+ z - y), and its share of ||r||^2 and the restart partials
-//     -> grid barrier -> every CTA folds the per-CTA scalars (same order, same
-//        value everywhere) and takes the same StepSizeTooLarge / restart decision
+//     -> grid barrier -> every CTA loads the next step's residual rows and
+//        folds the per-CTA scalars in the same L2 round trip (same order, same
+//        value everywhere) and takes the same StepSizeTooLarge / restart
+//        decision
 // and the round ends with the screening dot pass (g = A'r, epsilon partials)
 // consumed by k_dual.  The arithmetic is the streamed path's: same per-column
 // update, same deterministic reductions (different summation grouping).
