@@ -396,9 +396,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     P = Pn;
     rc ^= 1;
     gv = 0;
-    // next step reads the new residual written by other CTAs: the barrier
-    // above ordered it; keep the block in step before reusing smem scratch
-    __syncthreads();
+    // no CTA barrier here: every shared-memory reuse of the next step (rv,
+    // sc4, cf / rsx) is already separated from this step's reads by the
+    // barriers above
   }
   // screening dot pass at the final x: g = A'r and the epsilon partial
   double ep = 0.0;
