@@ -696,6 +696,7 @@ __device__ __forceinline__ double block_sum_rt(double v, double* sh) {
 // (warp w sums partials w, w+8, ...), then the 8 slice sums are combined in
 // warp order -- a fixed summation order, so results are deterministic.
 constexpr int RED_SLICES = RT / 32;
+constexpr int RED_ONESHOT = 20;  // partial rows per slice loaded in one go (G <= 160)
 
 template <typename T>
 __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, double Pn, double scale_div,
@@ -766,7 +767,33 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     double acc[V];  // partial rows summed in fp64 (fixed order)
 #pragma unroll
     for (int e = 0; e < V; ++e) acc[e] = 0.0;
-    if (row < m) {
+    if (row < m && G <= RED_ONESHOT * RED_SLICES) {
+      // every partial row of this lane's slice in flight at once: one L2 round
+      // trip (G = one per CTA of the pass, <= 160 on a 148-SM part); absent
+      // rows read as zero, the fixed pairwise tree keeps the order fixed
+      T q[RED_ONESHOT][V];
+#pragma unroll
+      for (int u = 0; u < RED_ONESHOT; ++u) {
+        const int b = warp + u * RED_SLICES;
+        if (b < G) {
+          unpack<T>(*reinterpret_cast<const VT*>(part + (int64_t)b * ldp + row), q[u]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) q[u][e] = T(0);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        double s[RED_ONESHOT];
+#pragma unroll
+        for (int u = 0; u < RED_ONESHOT; ++u) s[u] = static_cast<double>(q[u][e]);
+#pragma unroll
+        for (int w = 1; w < RED_ONESHOT; w *= 2)
+#pragma unroll
+          for (int u = 0; u + w < RED_ONESHOT; u += 2 * w) s[u] += s[u + w];
+        acc[e] = s[0];
+      }
+    } else if (row < m) {
       int bb = warp;
       // eight partial rows in flight per lane (the loop is L2-latency bound)
       for (; bb + 7 * RED_SLICES < G; bb += 8 * RED_SLICES) {
