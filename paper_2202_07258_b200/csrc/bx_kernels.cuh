@@ -762,8 +762,13 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     if (lane == 0) s_div = sqrt(nw2);
   }
   double sq = 0.0;
+  static_assert(RB <= RT, "one output row per thread");
   for (int64_t r0 = (int64_t)blockIdx.x * RB; r0 < m; r0 += (int64_t)gridDim.x * RB) {
     const int64_t row = r0 + lane * V;
+    // the offset row this thread adds below, requested in the same L2 round
+    // trip as the partial rows (off may alias out: read before it is written)
+    const int64_t orow = r0 + threadIdx.x;
+    const double offv = (off && threadIdx.x < RB && orow < m) ? off[orow] : 0.0;
     double acc[V];  // partial rows summed in fp64 (fixed order)
 #pragma unroll
     for (int e = 0; e < V; ++e) acc[e] = 0.0;
@@ -838,7 +843,7 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
         double s = sl[0][q];
 #pragma unroll
         for (int w = 1; w < RED_SLICES; ++w) s += sl[w][q];
-        if (off) s = add_rn(s, off[i]);
+        if (off) s = add_rn(s, offv);
         if (mode == R_POWER) s = s / s_div;
         out[i] = s;
         sq += s * s;
