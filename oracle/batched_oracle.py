@@ -26,7 +26,6 @@ Per round (inner_passes FISTA steps, then the dual point at x):
 Problems whose gap is below gap_tol are converged; the batch stops when all are.
 """
 
-import math
 
 import numpy as np
 

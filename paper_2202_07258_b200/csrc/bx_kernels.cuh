@@ -833,10 +833,7 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
     }
 #pragma unroll
     for (int e = 0; e < V; ++e) sl[warp][lane * V + e] = acc[e];
-    __syncthreads();
-    if (mode == R_POWER) {
-      // all threads read the divisor after the first barrier
-    }
+    __syncthreads();  // also publishes s_div (R_POWER) to every thread
     for (int q = threadIdx.x; q < RB; q += RT) {
       const int64_t i = r0 + q;
       if (i < m) {

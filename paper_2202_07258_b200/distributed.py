@@ -28,8 +28,6 @@ import ctypes
 import os
 import threading
 
-import numpy as np
-
 from . import _native as nat
 from .driver import _Session, _default_slack, _result
 from .model import Problem, QuadraticLoss

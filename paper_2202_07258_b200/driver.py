@@ -12,7 +12,6 @@ library or a machine without CUDA raises.
 import csv
 import ctypes
 import json
-import math
 from dataclasses import asdict, dataclass, field
 
 import numpy as np

@@ -2,7 +2,6 @@
 declares (CPU only: no compute calls), and the host-side logic that needs no
 GPU behaves like the reference."""
 
-import ctypes
 import os
 import re
 
