@@ -13,9 +13,11 @@ from conftest import small_instance
 pytestmark = pytest.mark.gpu
 
 
-def _cases(count=108, seed=20240817):
+def _cases(count=216, seed=20240817):
+    # the reference's 216 instances over nnls / bvls / mixed x pg / cd /
+    # active-set, plus the apg kind
     rng = np.random.default_rng(seed)
-    combos = list(itertools.product(("nnls", "bvls", "mixed"), ("pg", "apg", "cd")))
+    combos = list(itertools.product(("nnls", "bvls", "mixed"), ("pg", "apg", "cd", "active-set")))
     for i in range(count):
         family, kind = combos[i % len(combos)]
         n = int(rng.integers(3, 31))
@@ -46,6 +48,6 @@ def test_criterion1_screening_is_safe_and_criterion2_on_off_agree():
         o_on = 0.5 * float(np.sum((a @ on.x - y) ** 2))
         o_off = 0.5 * float(np.sum((a @ off.x - y) ** 2))
         worst = max(worst, abs(o_on - o_off) / max(1.0, abs(o_off)))
-    assert checked > 100
+    assert checked > 200
     assert violations == 0, f"{violations} of {checked} screened coordinates not saturated"
     assert worst <= 1e-8, worst
