@@ -159,3 +159,27 @@ def test_pg_screening_work_vs_saturation():
     assert len(upper) >= 2
     assert all(a[1] <= b[1] for a, b in zip(upper, upper[1:])), upper
     assert all(abs(c[1] - 1.0) < 1e-12 for c in cells if c[0] == 0.0), cells
+
+
+@pytest.mark.parametrize("kind", ["pg", "apg", "cd", "active-set"])
+@pytest.mark.parametrize("path", ["small", "streamed", "graph-off"])
+def test_traces_are_bitwise_deterministic(kind, path, monkeypatch):
+    """pkg/tests/test_driver.py:83-96: the same solve twice gives bitwise
+    identical traces and x (fixed-order reductions on every device path: the
+    SM-resident round kernel, the streamed passes with graph-captured rounds,
+    and the same without graphs)."""
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    monkeypatch.delenv("BX_NO_SMALL", raising=False)
+    monkeypatch.delenv("BX_NO_GRAPH", raising=False)
+    if path != "small":
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+    if path == "graph-off":
+        monkeypatch.setenv("BX_NO_GRAPH", "1")
+    rng = np.random.default_rng(83)
+    a, y, lo, hi = small_instance(rng, 300, 700, "mixed")
+    cfg = SolverConfig(kind=kind, inner_passes=10 if kind in ("pg", "apg") else 1, gap_tol=1e-9, max_rounds=200)
+    runs = [solve(Problem(a, y, lo, hi), cfg, screening=True) for _ in range(2)]
+    fields = ("primal", "dual", "gap", "preserved_count")
+    t0, t1 = ([[getattr(t, f) for f in fields] for t in r.trace] for r in runs)
+    assert t0 == t1
+    assert runs[0].x.tobytes() == runs[1].x.tobytes()
