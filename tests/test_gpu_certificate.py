@@ -183,3 +183,40 @@ def test_traces_are_bitwise_deterministic(kind, path, monkeypatch):
     t0, t1 = ([[getattr(t, f) for f in fields] for t in r.trace] for r in runs)
     assert t0 == t1
     assert runs[0].x.tobytes() == runs[1].x.tobytes()
+
+
+KINDS = ["pg", "apg", "cd", "active-set"]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_solve_basics_every_kind(kind):
+    """pkg/tests/test_driver.py:14-51 and :134-143 for every kind: 1-D NNLS
+    converges in one round with ratio 1; a huge tolerance returns after the
+    first round; max_rounds stops an unconverged solve; results are box
+    feasible on every family; mixed bounds screen at an upper bound only
+    where it is finite."""
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    rng = np.random.default_rng(12345)
+    res = solve(Problem([[1.0]], [-1.0], 0.0, np.inf), SolverConfig(kind=kind), screening=True)
+    assert res.converged and res.rounds == 1
+    assert res.x[0] == 0.0 and res.gap < 1e-12
+    assert res.trace[-1].screening_ratio == 1.0
+
+    a, y, lo, hi = small_instance(rng, 10, 6, "nnls")
+    res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, gap_tol=1e9), screening=True)
+    assert res.converged and res.rounds == 1
+
+    a, y, lo, hi = small_instance(rng, 20, 10, "nnls")
+    res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, gap_tol=1e-14, max_rounds=2), screening=False)
+    assert not res.converged and res.rounds == 2
+
+    for family in ("nnls", "bvls", "mixed"):
+        a, y, lo, hi = small_instance(rng, 25, 10, family)
+        res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, gap_tol=1e-6), screening=True)
+        assert res.converged and res.gap < 1e-6, family
+        assert np.all(res.x >= lo) and np.all(res.x <= hi), family
+
+    a, y, lo, hi = small_instance(rng, 30, 12, "mixed")
+    res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, gap_tol=1e-8), screening=True)
+    assert res.converged
+    assert not np.any(np.isinf(hi[res.sat_upper]))
