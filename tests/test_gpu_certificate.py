@@ -220,3 +220,33 @@ def test_solve_basics_every_kind(kind):
     res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, gap_tol=1e-8), screening=True)
     assert res.converged
     assert not np.any(np.isinf(hi[res.sat_upper]))
+
+
+def test_spectral_norm_and_step_on_device():
+    """pkg/tests/test_solvers.py:47-65: the device power iteration against
+    known norms and the SVD; the automatic step is safe."""
+    from paper_2202_07258_b200 import auto_step_size, spectral_norm_estimate
+    assert abs(spectral_norm_estimate(np.eye(3)) - 1.0) <= 1e-6
+    assert abs(spectral_norm_estimate(np.diag([3.0, 1.0])) - 3.0) <= 1e-4
+    rng = np.random.default_rng(12345)
+    for _ in range(10):
+        a = rng.standard_normal((20, 10))
+        true = np.linalg.svd(a, compute_uv=False)[0]
+        assert abs(spectral_norm_estimate(a) - true) / true < 1e-3
+    a = rng.standard_normal((15, 8))
+    assert auto_step_size(a, 1.0) <= 1.0 / np.linalg.svd(a, compute_uv=False)[0] ** 2
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_kkt_at_convergence(kind):
+    """pkg/tests/test_solvers.py:121-127 for every kind: at a 1e-10 gap the
+    gradient satisfies the NNLS KKT conditions."""
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    rng = np.random.default_rng(12345)
+    a, y, lo, hi = small_instance(rng, 15, 8, "nnls")
+    res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, gap_tol=1e-10), screening=False)
+    assert res.converged
+    g = a.T @ (y - a @ res.x)
+    at_lower = res.x <= lo + 1e-9
+    assert np.all(g[at_lower] < 1e-5)
+    assert np.all(np.abs(g[~at_lower]) < 1e-5)
