@@ -250,3 +250,17 @@ def test_kkt_at_convergence(kind):
     at_lower = res.x <= lo + 1e-9
     assert np.all(g[at_lower] < 1e-5)
     assert np.all(np.abs(g[~at_lower]) < 1e-5)
+
+
+@pytest.mark.parametrize("kind,family", [("pg", "bvls"), ("cd", "mixed")])
+def test_objective_non_increasing(kind, family):
+    """pkg/tests/test_solvers.py:85-96 / :129-138: PG (safe step) and CD never
+    increase the objective from round to round."""
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    rng = np.random.default_rng(12345)
+    a, y, lo, hi = small_instance(rng, 20, 10, family)
+    res = solve(Problem(a, y, lo, hi), SolverConfig(kind=kind, inner_passes=1, gap_tol=1e-14, max_rounds=100),
+                screening=False)
+    primal = [t.primal for t in res.trace]
+    assert len(primal) >= 10
+    assert all(b <= a_ + 1e-12 for a_, b in zip(primal, primal[1:]))
