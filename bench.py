@@ -340,6 +340,8 @@ def ncu_traffic(cfg_id):
     info = {"traffic_source": ent["source"], "traffic_kernel": ent["kernel"],
             "traffic_launch_algorithmic": ent.get("algorithmic"),
             "traffic_over_algorithmic": (t / ent["algorithmic"]) if ent.get("algorithmic") else None}
+    if ent.get("launch_list"):
+        info["launch_list"] = ent["launch_list"]  # ncu --metrics gpu__time_duration.sum of this command
     return t, info
 
 
