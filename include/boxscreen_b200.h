@@ -53,7 +53,9 @@ typedef enum {
   BX_ERR_UNSUPPORTED = 9,          /* shape outside the compiled kernel envelope   */
   BX_ERR_WORKSPACE = 10,           /* caller workspace too small / misaligned      */
   BX_ERR_NOT_INTERIOR = 11,        /* errors.py:25  NotInterior                */
-  BX_ERR_SINGULAR = 12             /* errors.py:56  SingularSubproblem (active set) */
+  BX_ERR_SINGULAR = 12,            /* errors.py:56  SingularSubproblem (active set) */
+  BX_ERR_PEER_TIMEOUT = 13         /* column-sharded fused exchange: a peer never published
+                                      (bounded wait, BX_PEER_TIMEOUT_S, default 30 s)  */
 } bx_status;
 
 typedef enum { BX_F64 = 0, BX_F32 = 1 } bx_dtype;
@@ -80,6 +82,10 @@ typedef struct {
   double slack_scale;    /* driver.py:219: 1e-12 for fp64                        */
   int32_t relative_gap;  /* 1: stop when gap <= gap_tol * max(1, P) (fp32 rule,
                             DESIGN.md); 0: absolute gap (reference rule)        */
+  int32_t restart;       /* FISTA restart rule (BX_APG): 0 = adaptive (objective
+                            increase OR the gradient test);
+                            1 = objective increase only (BASELINE config 3's
+                            stated rule, mirroring solvers.py:111-114)           */
 } bx_solve_cfg;
 
 /* TraceRecord (driver.py:28-38) plus the dual-point internals. */
@@ -105,6 +111,9 @@ typedef struct {
   double sigma;          /* last power-iteration estimate                      */
   int64_t kernel_launches;
   int64_t restarts;
+  int64_t spec_kept;     /* screening events whose speculative round-boundary step
+                            stood                                  */
+  int64_t spec_undone;   /* ... and events that undid it and took it again       */
 } bx_solve_out;
 
 /* Host callback producing the power-iteration start vector of length k:

@@ -28,9 +28,10 @@ Extensions the reference does not contain (BASELINE.json configs 3 and 5),
 defined here in the same workspace/round conventions and documented in
 DESIGN.md ("FISTA definition"):
 
-* ``apg`` -- FISTA momentum with function-value restart, residuals carried by
-  linearity (r(y) = r + beta (r - r_prev)), momentum kept across screening
-  events with r_prev recomputed on the compacted set.
+* ``apg`` -- FISTA momentum with restart on an objective increase (plus, by
+  default, the O'Donoghue-Candes gradient test), the extrapolated gradient
+  carried by linearity (g(y) = g + beta (g - g_prev)), momentum kept across
+  screening events with g_prev recomputed on the compacted set.
 
 Parity pinning: ``tests/golden/make_golden.py`` runs the real reference
 (imported from /root/reference in the build container) on seeded instances
@@ -151,9 +152,10 @@ class ActiveView:
         self.tgt = y - z            # reduced-problem target
         self.r = self.mat @ self.x + self.off
         self.g = self.mat.T @ self.r
-        # apg state (not part of the reference workspace)
+        # apg state (not part of the reference workspace): previous iterate
+        # and the gradient there
         self.x_prev = None
-        self.r_prev = None
+        self.g_prev = None
 
     def write_back(self, x_full):
         x_full[self.idx] = self.x
@@ -191,42 +193,49 @@ def cd_passes(w, passes):
     w.g = mat.T @ r
 
 
-def apg_passes(w, eta, passes, mom):
+def apg_passes(w, eta, passes, mom, restart="adaptive"):
     """FISTA extension (not in the reference; see module docstring).
 
     ``mom`` is a one-element list holding the momentum scalar t_k (t=1 means
-    no extrapolation on the next step).  Per step:
+    no extrapolation on the next step).  ``w.g`` is the gradient A'r at the
+    current x (the Workspace invariant, solvers.py:65-69) and ``w.g_prev``
+    the gradient at the previous iterate.  Per step:
         t' = (1 + sqrt(1 + 4 t^2)) / 2 ;  beta = (t - 1) / t'
-        y  = x + beta (x - x_prev) ;  r_y = r + beta (r - r_prev)
-        x+ = clip(y - eta A'r_y, lo, hi) ;  r+ = A x+ + off
+        y  = x + beta (x - x_prev) ;  g_y = g + beta (g - g_prev)
+                                      (= A'r(y): the gradient is affine in x)
+        x+ = clip(y - eta g_y, lo, hi) ;  r+ = A x+ + off ;  g+ = A'r+
         restart (t <- 1) when  P(x+) > P(x) + s_f      (objective increase,
                                                        the BASELINE config-3 rule)
                            or  g_y'(x+ - x) > s_g      (gradient test of
-                                                       O'Donoghue & Candes 2015)
+                                                       O'Donoghue & Candes 2015;
+                                                       restart="adaptive" only)
         otherwise t <- t'.  Slacks sized to each test's own round-off, so
         the CPU oracle and the GPU (different summation orders) agree:
             s_f = 1e-12 max(1, P(x))                        (noise in P ~1e-14 P)
             s_g = 1e-12 ||r|| sum_j ||a_j|| |x+_j - x_j|    (noise in g_j ~ eps ||a_j|| ||r||)
+    Each step reads A twice, like pg_step (solvers.py:109-116): A x+ and
+    A'r+.  The gradient at the new iterate is the one the next step, and the
+    round's dual point (driver.py:183-198), both need -- so the GPU streams A
+    once per step and evaluates the round's dual point from the first pass of
+    the next round ("speculative round boundary").
     The gradient test keeps restarting deep in the tail, where objective
     changes are far below s_f; without it the momentum grows unbounded and
     FISTA degrades to its O(1/k^2) regime ("FISTA definition").
-    After the passes g = A'r at the final x (for the dual point).
     """
     obj = 0.5 * float(w.r @ w.r)
     if w.x_prev is None:
         w.x_prev = w.x.copy()
-        w.r_prev = w.r.copy()
+        w.g_prev = w.g.copy()
     for _ in range(passes):
         t = mom[0]
         tn = (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
         beta = (t - 1.0) / tn
         if beta != 0.0:
             yv = w.x + beta * (w.x - w.x_prev)
-            ry = w.r + beta * (w.r - w.r_prev)
+            gy = w.g + beta * (w.g - w.g_prev)
         else:
             yv = w.x
-            ry = w.r
-        gy = w.mat.T @ ry
+            gy = w.g
         xn = np.clip(yv - eta * gy, w.lo, w.hi)
         rn = w.mat @ xn + w.off
         nobj = 0.5 * float(rn @ rn)
@@ -234,11 +243,12 @@ def apg_passes(w, eta, passes, mom):
         gdot = float(gy @ dx)
         s_f = RESTART_SLACK * max(1.0, abs(obj))
         s_g = RESTART_SLACK * math.sqrt(2.0 * obj) * float(w.nrm @ np.abs(dx))
-        w.x_prev, w.r_prev = w.x, w.r
+        w.x_prev, w.g_prev = w.x, w.g
         w.x, w.r = xn, rn
-        mom[0] = 1.0 if (nobj > obj + s_f or gdot > s_g) else tn
+        w.g = w.mat.T @ w.r
+        grad_test = restart == "adaptive" and gdot > s_g
+        mom[0] = 1.0 if (nobj > obj + s_f or grad_test) else tn
         obj = nobj
-    w.g = w.mat.T @ w.r
 
 
 def _passive_lstsq(mat, rhs, cols):
@@ -302,7 +312,7 @@ def active_set_pass(w, passive):
 
 def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
                  max_rounds=None, screening=True, step_size=None, t=None,
-                 power_iters=50, record_sets=False, round_hook=None):
+                 power_iters=50, record_sets=False, round_hook=None, restart="adaptive"):
     """Run the screened solver and return a dict with x, theta, gap, rounds,
     converged, trace (list of per-round dicts), sat_lower, sat_upper.
 
@@ -357,7 +367,7 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
         if kind == "pg":
             pg_passes(w, eta, inner_passes)
         elif kind == "apg":
-            apg_passes(w, eta, inner_passes, mom)
+            apg_passes(w, eta, inner_passes, mom, restart)
         elif kind == "cd":
             cd_passes(w, inner_passes)
         else:
@@ -424,7 +434,7 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
                     xp_full[old.idx] = old.x_prev
                     xp_full[gone] = x_full[gone]
                     w.x_prev = xp_full[keep].copy()
-                    w.r_prev = w.mat @ w.x_prev + w.off
+                    w.g_prev = w.mat.T @ (w.mat @ w.x_prev + w.off)
                 if (kind in ("pg", "apg") and step_size is None
                         and keep.size < 0.5 * basis):
                     eta = safe_step(w.mat, 1.0, power_iters)

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 BX_F64, BX_F32 = 0, 1
 BX_PG, BX_CD, BX_APG, BX_ACTIVE_SET = 0, 1, 2, 3
 KINDS = {"pg": BX_PG, "cd": BX_CD, "apg": BX_APG, "active-set": BX_ACTIVE_SET}
+RESTARTS = {"adaptive": 0, "function": 1}
 
 
 class SolveCfg(ctypes.Structure):
@@ -23,7 +24,8 @@ class SolveCfg(ctypes.Structure):
                 ("max_rounds", ctypes.c_int64), ("gap_tol", ctypes.c_double),
                 ("step_size", ctypes.c_double), ("power_iters", ctypes.c_int32),
                 ("screening", ctypes.c_int32), ("alpha", ctypes.c_double),
-                ("slack_scale", ctypes.c_double), ("relative_gap", ctypes.c_int32)]
+                ("slack_scale", ctypes.c_double), ("relative_gap", ctypes.c_int32),
+                ("restart", ctypes.c_int32)]
 
 
 class TraceRec(ctypes.Structure):
@@ -39,7 +41,8 @@ class SolveOut(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("converged", ctypes.c_int32), ("gap", ctypes.c_double),
                 ("n_sat_lower", ctypes.c_int64), ("n_sat_upper", ctypes.c_int64),
                 ("iterations", ctypes.c_int64), ("step", ctypes.c_double), ("sigma", ctypes.c_double),
-                ("kernel_launches", ctypes.c_int64), ("restarts", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("restarts", ctypes.c_int64),
+                ("spec_kept", ctypes.c_int64), ("spec_undone", ctypes.c_int64)]
 
 
 class ProfEntry(ctypes.Structure):

@@ -296,7 +296,16 @@ struct bx_ctx {
   int cur = 0;
   int32_t* idx[2] = {nullptr, nullptr};
   void *x[2] = {}, *xprev[2] = {}, *lo[2] = {}, *hi[2] = {}, *nrm[2] = {}, *att[2] = {};
+  void* gprev[2] = {};  // FISTA: gradient at x_prev (g_{k-1}), carried through compaction
   void *g = nullptr, *v = nullptr, *coef = nullptr;
+  // speculative round boundary: the round's screening gradient
+  // comes from the next round's first step, which keeps what an undo needs
+  void *xbak = nullptr, *gbak = nullptr, *rbak = nullptr;
+  double* epart = nullptr;   // epsilon partials of the speculative step
+  bool spec_on = true;       // env BX_SPEC=0 disables (a separate dot pass per round)
+  bool spec_pending = false; // the current x has taken the next round's first step
+  bool dot_spec = false;     // dot_done's g / epsilon partials came from a speculative step
+  int last_kind = BX_APG;    // kind of the last primal passes (fine-grained C ABI)
   void* gram = nullptr;  // CD Gram blocks [ceil(n/32)][32][32]
   bool gram_dirty = true;
   // full-problem vectors
@@ -336,6 +345,7 @@ struct bx_ctx {
   unsigned bar_epoch = 0;   // grid-barrier epochs issued so far
   int64_t launches = 0;
   int last_Gw = 0;  // block count of the last pass's scalar partials (bpart)
+  int last_Ge = 0;  // block count of the last speculative step's epsilon partials (epart)
   std::string err;
 
   // live per-kernel timing (CUDA events on the context stream)
@@ -370,6 +380,7 @@ struct bx_ctx {
   unsigned xepoch = 0;
   unsigned* xepoch_p = nullptr;   // the epoch counter in use (own, or the borrowed bx_comm's)
   int xnb = 1;
+  uint64_t xtimeout_ns = 30ull * 1000000000ull;  // bound of a peer wait (env BX_PEER_TIMEOUT_S)
   bool comm_owned = true;         // false: `comm` belongs to a bx_comm
 
   // multi-GPU column sharding
@@ -512,7 +523,12 @@ void carve(bx_ctx* c, Carver& w) {
     c->hi[s] = w.take(n * e);
     c->nrm[s] = w.take(n * e);
     c->att[s] = w.take(n * e);
+    c->gprev[s] = w.take(n * e);
   }
+  c->xbak = w.take(n * e);
+  c->gbak = w.take(n * e);
+  c->rbak = w.take(mp * e);
+  c->epart = (double*)w.take(4 * c->Gmax * 8);
   c->g = w.take(n * e);
   c->v = w.take(n * e);
   c->coef = w.take(n * e);
@@ -525,7 +541,7 @@ void carve(bx_ctx* c, Carver& w) {
   c->gfull = w.take(n * e);
   c->vfull = w.take(n * e);
   c->flags = (uint8_t*)w.take(n);
-  c->bcnt = (int32_t*)w.take((n / RT + 2) * 3 * 4);
+  c->bcnt = (int32_t*)w.take((n / RT + 2) * 4 * 4);
   c->scr_idx = (int32_t*)w.take(n * 4);
   c->scr_val = w.take(n * e);
   c->sat_lo = (int64_t*)w.take(n * 8);
@@ -630,11 +646,22 @@ int pass_grid(bx_ctx* c, int64_t k) {
   return (int)G;
 }
 
+// FISTA's per-column gradient state and the speculative round-boundary step
+// for a PG / FISTA pass
+struct StepExtra {
+  double* gprev = nullptr;  // g_{k-1} in, g_k out (U_APG)
+  int spec = 0;             // speculative step: keep x_{k-1}/g_{k-1}, emit g_k + epsilon partials
+  double* xbak = nullptr;
+  double* gbak = nullptr;
+  double* epart = nullptr;
+};
+
 // Launch one streamed pass.  Returns the grid used through *G_out.
 template <typename T>
 int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
                      double* xprev, const double* lo, const double* hi, double* g, const double* att,
-                     const double* coef, double* bpart, int has_inf, int* G_out, const double* nrm);
+                     const double* coef, double* bpart, int has_inf, int* G_out, const double* nrm,
+                     const StepExtra& ex);
 
 // One streamed pass over the columns of `vw`, rows [row0, row0 + mrows) (the
 // whole column by default).  accumulate >= 0 turns a U_DOT pass into a
@@ -643,19 +670,19 @@ template <typename T>
 int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
              double* xprev, const double* lo, const double* hi, double* g, const double* att, const double* coef,
              double* bpart, int has_inf, int* G_out, const double* nrm = nullptr, int64_t row0 = 0,
-             int64_t mrows = -1, int accumulate = -1, bool acc64 = false) {
+             int64_t mrows = -1, int accumulate = -1, bool acc64 = false, const StepExtra& ex = StepExtra()) {
   const int64_t mm = mrows < 0 ? c->m : mrows;
   const int R = pick_R(mm, sizeof(T));
   if (R < 0 && mrows < 0)
     return run_pass_blocked<T>(c, vw, upd, vin, vin_prev, x, xprev, lo, hi, g, att, coef, bpart, has_inf, G_out,
-                               nrm);
+                               nrm, ex);
   if (R < 0) return fail(c, BX_ERR_UNSUPPORTED, "row block of %lld rows", (long long)mm);
   const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
   const bool axpy = (upd != U_DOT);
   const int C = cols_per_slot(R);
   const uint32_t colbytes = (uint32_t)align_up((size_t)mm * sizeof(T), 16);
   const uint32_t colstride = (uint32_t)align_up(colbytes, 128);
-  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 3 * CMAX) * 8 + 64;
+  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 4 * CMAX) * 8 + 64;
   const size_t slot = (size_t)C * colstride;
   const int G = pass_grid(c, vw.k);
   int S = (int)((c->smem_cap - scratch) / slot);
@@ -663,7 +690,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   if (S < 1) return fail(c, BX_ERR_UNSUPPORTED, "column of %u bytes does not fit shared memory", colbytes);
   // stage the per-column state of each CTA when that costs no ring slot below 2
   const int64_t per_cta = (vw.k + G - 1) / G;
-  const size_t stage = align_up((size_t)per_cta * 5 * 8, 128);
+  const size_t stage = align_up((size_t)per_cta * PASS_STAGED * 8, 128);
   int pre = 0;
   {
     int S2 = (int)((c->smem_cap - scratch - stage) / slot);
@@ -703,8 +730,14 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   a.colbytes = colbytes;
   a.colstride = colstride;
   a.pre = pre;
+  a.gprev = ex.gprev;
+  a.spec = ex.spec;
+  a.xbak = ex.xbak;
+  a.gbak = ex.gbak;
+  a.epart = ex.spec ? ex.epart : nullptr;
   if (G_out) *G_out = G;
   c->last_Gw = G;
+  if (ex.spec) c->last_Ge = G;
   const int e0 = prof_begin(c);
   int st = BX_OK;
   switch (R) {
@@ -725,10 +758,10 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   if (e0 >= 0) {
     // algorithmic bytes: every streamed column once, the per-column state the
     // mode touches, the input row vector(s) and the output row vector once
-    static const int col_vec[] = {3, 5, 5, 6, 0, 1};  // U_DOT..U_AX, elements per column
+    static const int col_vec[] = {3, 5, 5, 8, 0, 1};  // U_DOT..U_AX, elements per column
     const double es = (double)sizeof(T);
     double bytes = (double)vw.k * (double)c->m * es + (double)vw.k * col_vec[upd] * es;
-    if (dot) bytes += (double)c->m * es * (upd == U_APG ? 2 : 1);
+    if (dot) bytes += (double)c->m * es;
     if (axpy) bytes += (double)c->m * es;
     prof_end(c, e0, BX_PROF_PASS_DOT + upd, bytes);
   }
@@ -742,7 +775,8 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
 template <typename T>
 int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const double* vin_prev, double* x,
                      double* xprev, const double* lo, const double* hi, double* g, const double* att,
-                     const double* coef, double* bpart, int has_inf, int* G_out, const double* nrm) {
+                     const double* coef, double* bpart, int has_inf, int* G_out, const double* nrm,
+                     const StepExtra& ex) {
   constexpr int64_t BR = (int64_t)NT * (16 / sizeof(T)) * 8;  // rows per block (R = 8)
   const bool dot = (upd == U_DOT || upd == U_PG || upd == U_APG || upd == U_POWER);
   const bool axpy = (upd != U_DOT);
@@ -751,8 +785,9 @@ int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, c
   if (dot) {
     for (int64_t r0 = 0, q = 0; r0 < c->m; r0 += BR, ++q) {
       const int64_t mr = std::min(BR, c->m - r0);
-      TRY(run_pass<T>(c, vw, U_DOT, vin, (upd == U_APG) ? vin_prev : nullptr, nullptr, nullptr, nullptr, hi, gg,
-                      att, nullptr, nullptr, 0, &G, nullptr, r0, mr, q ? 1 : 0));
+      // FISTA dots the plain residual too (gradient linearity, k_colupdate)
+      TRY(run_pass<T>(c, vw, U_DOT, vin, nullptr, nullptr, nullptr, nullptr, hi, gg, att, nullptr, nullptr, 0, &G,
+                      nullptr, r0, mr, q ? 1 : 0));
     }
   }
   const double* cf = coef ? coef : x;  // U_AX without coefficients multiplies by x
@@ -760,8 +795,9 @@ int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, c
   if (upd != U_AX) {
     const int nb = grid1d(c, vw.k);
     k_colupdate<<<nb, RT, 0, c->stream>>>(upd, vw.k, x, xprev, lo, hi, gg, att, nrm, (double*)c->coef, bpart,
-                                          has_inf, c->sc);
+                                          has_inf, c->sc, ex.gprev, ex.spec, ex.xbak, ex.gbak, ex.epart);
     LAUNCHED();
+    if (ex.spec) c->last_Ge = nb;
     if (upd == U_DOT) {
       if (G_out) *G_out = nb;
       return BX_OK;
@@ -783,9 +819,11 @@ int run_pass_blocked(bx_ctx* c, const View<T>& vw, int upd, const double* vin, c
 
 template <typename T>
 int run_xreduce(bx_ctx* c, int G, const double* off, double* out, int mode, const double* wpart, int Gw,
-                int counter) {
+                int counter, double* save) {
   XArgs a;
   memset(&a, 0, sizeof(a));
+  a.save = save;
+  a.timeout_ns = c->xtimeout_ns;
   a.part = c->part;
   a.ldp = c->ldp;
   a.G = G;
@@ -797,7 +835,7 @@ int run_xreduce(bx_ctx* c, int G, const double* off, double* out, int mode, cons
   a.bpart = c->bpart2;
   a.wpart = (wpart && Gw > 0) ? wpart : nullptr;
   a.Gw = Gw;
-  a.stride = a.wpart ? (mode == R_APG ? 2 : 1) : 0;
+  a.stride = a.wpart ? ((mode & ~R_SPEC) == R_APG ? 2 : 1) : 0;
   a.mode = mode;
   a.counter = counter;
   a.rank = c->rank;
@@ -826,9 +864,10 @@ int run_xreduce(bx_ctx* c, int G, const double* off, double* out, int mode, cons
 }
 
 template <typename T>
-int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const double* wpart, int Gw, int counter) {
+int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const double* wpart, int Gw, int counter,
+               double* save = nullptr) {
   // column-sharded with the peer exchange attached: one fused kernel
-  if (c->sharded() && c->xmode) return run_xreduce<T>(c, G, off, out, mode, wpart, Gw, counter);
+  if (c->sharded() && c->xmode) return run_xreduce<T>(c, G, off, out, mode, wpart, Gw, counter, save);
   const int64_t rb = 32 * (16 / (int64_t)sizeof(T));
   int nb = (int)((c->m + rb - 1) / rb);
   if (nb > 4 * c->nsm) nb = 4 * c->nsm;
@@ -837,9 +876,9 @@ int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const
     // phase A: this rank's partial rows; block scalars folded; both summed
     // over ranks (NCCL allreduce); phase B: offset, objective, mode logic
     k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, nullptr, (double*)c->rloc, c->sc,
-                                           c->bpart2, nullptr, 0, R_PLAIN, counter);
+                                           c->bpart2, nullptr, 0, R_PLAIN, counter, nullptr);
     LAUNCHED();
-    const int stride = (mode == R_APG) ? 2 : 1;
+    const int stride = ((mode & ~R_SPEC) == R_APG) ? 2 : 1;
     if (wpart && Gw > 0) {
       k_fold<<<1, 32, 0, c->stream>>>(wpart, Gw, stride, 0, c->scal);
       LAUNCHED();
@@ -849,13 +888,13 @@ int run_reduce(bx_ctx* c, int G, const double* off, double* out, int mode, const
     if (wpart && Gw > 0) TRY(allreduce(c, c->scal, (size_t)stride, ncclFloat64, ncclSum));
     k_reduce<double><<<nb2, RT, 0, c->stream>>>((const double*)c->rloc, c->ldp, 1, c->m, off, out, c->sc, c->bpart2,
                                            (wpart && Gw > 0) ? c->scal : nullptr, (wpart && Gw > 0) ? 1 : 0, mode,
-                                           counter);
+                                           counter, save);
     LAUNCHED();
     return BX_OK;
   }
   const int e0 = prof_begin(c);
   k_reduce<T><<<nb, RT, 0, c->stream>>>((const T*)c->part, c->ldp, G, c->m, off, out, c->sc, c->bpart2, wpart, Gw,
-                                         mode, counter);
+                                         mode, counter, save);
   LAUNCHED();
   prof_end(c, e0, BX_PROF_REDUCE, (double)c->m * sizeof(T) * (G + 2 + (off ? 1 : 0)));
   return BX_OK;
@@ -881,6 +920,9 @@ int check_dev_err(bx_ctx* c) {
     const DualOut& d = c->hsc->act.gap_raw < -1e-9 ? c->hsc->act : c->hsc->cert;
     return fail(c, BX_ERR_INTERNAL_CONSISTENCY, "duality gap %.3e below round-off slack", d.gap_raw);
   }
+  if (e == DE_PEER_TIMEOUT)
+    return fail(c, BX_ERR_PEER_TIMEOUT, "fused peer exchange: a peer rank did not publish within %.1f s",
+                1e-9 * (double)c->xtimeout_ns);
   return fail(c, BX_ERR_CUDA, "device error code %d", e);
 }
 
@@ -1105,7 +1147,9 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   *ran = 0;
   *done = 0;
   *event = 0;
-  if (!c->small_ok || c->sharded() || (kind != BX_PG && kind != BX_APG) || c->k == 0) return BX_OK;
+  // (not while a speculative step is pending: the kernel starts a round from x)
+  if (!c->small_ok || c->sharded() || (kind != BX_PG && kind != BX_APG) || c->k == 0 || c->spec_pending)
+    return BX_OK;
   constexpr int V = 16 / sizeof(T);
   const int R = (int)((c->m + SM_NT * V - 1) / (SM_NT * V));
   if (R > 4) return BX_OK;
@@ -1114,7 +1158,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   if (ncmax > SM_CMAX) return BX_OK;
   if (lp.max_rounds > 1 && (c->m + G - 1) / G > SM_NT) return BX_OK;
   const int colstride = (int)round_up(c->m, 2 * V);
-  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 2 * SM_NT + 8 + 7 * SM_CMAX + SM_NT + round_up(c->m, 8)) * 8 + 256;
+  const size_t scratch = (16 * SM_CMAX + 2 * SM_CMAX + 2 * SM_NT + 8 + 8 * SM_CMAX + SM_NT + round_up(c->m, 8)) * 8 + 256;
   const size_t smem = align_up((size_t)ncmax * colstride * sizeof(T), 128) + scratch;
   if (smem > c->smem_cap) return BX_OK;
   if (dry) {  // would run (the caller only asks)
@@ -1131,6 +1175,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   a.m = (int)c->m;
   a.x = (double*)c->x[s];
   a.xprev = (double*)c->xprev[s];
+  a.gprev = (double*)c->gprev[s];
   a.lo = (const double*)c->lo[s];
   a.hi = (const double*)c->hi[s];
   a.nrm = (const double*)c->nrm[s];
@@ -1183,6 +1228,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   }
   if (hd[2] & 1) std::swap(c->r, c->rprev);
   c->dot_done = hd[1] != 0;
+  c->dot_spec = false;
   c->dot_G = G;
   c->g_valid = true;
   *ran = 1;
@@ -1195,6 +1241,10 @@ template <typename T>
 int primal_passes(bx_ctx* c, int kind, int passes);
 template <typename T>
 int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha);
+template <typename T>
+int step_pass(bx_ctx* c, int kind, bool spec);
+template <typename T>
+bool spec_applies(bx_ctx* c, int kind, int passes);
 
 // ---- graph-resident rounds (streamed PG / FISTA and CD) ---------------------
 // The round sequence (primal passes, screening dot, dual point, sphere test)
@@ -1207,7 +1257,7 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha);
 struct GraphKey {
   int64_t k, kphys;
   const void *r, *rprev, *x, *g;
-  int cur, kind, passes, screening, g_valid, dense, act_is_orig;
+  int cur, kind, passes, screening, g_valid, dense, act_is_orig, spec_pending, dot_spec;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
 static GraphKey graph_key(const bx_ctx* c, int kind, int passes, int screening) {
@@ -1226,6 +1276,8 @@ static GraphKey graph_key(const bx_ctx* c, int kind, int passes, int screening) 
   k.g_valid = c->g_valid ? 1 : 0;
   k.dense = c->dense ? 1 : 0;
   k.act_is_orig = c->act_is_orig ? 1 : 0;
+  k.spec_pending = c->spec_pending ? 1 : 0;
+  k.dot_spec = c->dot_spec ? 1 : 0;
   return k;
 }
 
@@ -1238,13 +1290,14 @@ struct GraphEndArgs {
   double tol;
   int relative_gap;
   int screening;
+  int spec;  // the body ends with a speculative step: the round's momentum is bak_mom_t
 };
 
 __global__ void k_graph_round_end(GraphEndArgs a) {
   const int q = a.done[0];
   const DualOut& d = a.sc->act;
   const double tol_r = a.relative_gap ? a.tol * fmax(1.0, fabs(d.primal)) : a.tol;
-  const bool ev = a.sc->err != 0 || d.gap_raw < -1e-9 || d.gap < tol_r ||
+  const bool ev = a.sc->err != 0 || a.sc->err_spec != 0 || d.gap_raw < -1e-9 || d.gap < tol_r ||
                   (a.screening && (a.sc->g_lo + a.sc->g_up) > 0);
   if (!ev) {
     double* tr = a.trace + 8 * q;
@@ -1253,8 +1306,8 @@ __global__ void k_graph_round_end(GraphEndArgs a) {
     tr[2] = d.gap;
     tr[3] = d.eps;
     tr[4] = d.radius;
-    tr[5] = a.sc->mom_t;
-    tr[6] = (double)a.sc->restarts;
+    tr[5] = a.spec ? a.sc->bak_mom_t : a.sc->mom_t;
+    tr[6] = (double)(a.spec ? a.sc->bak_restarts : a.sc->restarts);
     a.done[0] = q + 1;
   } else {
     a.done[1] = 1;
@@ -1333,6 +1386,11 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
     if (r0) return BX_OK;  // the small-problem kernel owns these rounds
   }
   if (limit > kSmallRounds) limit = kSmallRounds;
+  // with the speculative round boundary the body is: the round's remaining
+  // steps, the next round's first step (speculative), the dual point of the
+  // round -- steady only when the round's first step is already done
+  const bool spec = spec_applies<T>(c, kind, passes);
+  if (spec && !c->spec_pending) return BX_OK;
   const GraphKey key = graph_key(c, kind, passes, screening);
   if (!gs.cs && !graph_stream_acquire(&gs.gst)) {
     cudaGetLastError();
@@ -1373,7 +1431,16 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
       return BX_OK;
     }
     const int64_t launches0 = c->launches;
+    // host-side state the captured calls advance (restored if the capture is
+    // abandoned: nothing captured has run)
+    struct {
+      void *r, *rprev;
+      bool spec_pending, dot_done, dot_spec, g_valid;
+      int dot_G, last_Gw, last_Ge, last_kind;
+    } saved{c->r, c->rprev, c->spec_pending, c->dot_done, c->dot_spec, c->g_valid, c->dot_G, c->last_Gw,
+            c->last_Ge, c->last_kind};
     int st = primal_passes<T>(c, kind, passes);
+    if (st == BX_OK && spec) st = step_pass<T>(c, kind, true);
     if (st == BX_OK) st = dual_screen<T>(c, screening, slack_scale, alpha);
     GraphEndArgs ga;
     ga.sc = c->sc;
@@ -1384,6 +1451,7 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
     ga.tol = tol;
     ga.relative_gap = relative_gap;
     ga.screening = screening;
+    ga.spec = spec ? 1 : 0;
     if (st == BX_OK) k_graph_round_end<<<1, 1, 0, c->stream>>>(ga);
     cudaGraph_t cap = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(c->stream, &cap);
@@ -1395,6 +1463,16 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
       gs.reset();
       gs.broken = true;
       c->err.clear();
+      c->r = saved.r;
+      c->rprev = saved.rprev;
+      c->spec_pending = saved.spec_pending;
+      c->dot_done = saved.dot_done;
+      c->dot_spec = saved.dot_spec;
+      c->g_valid = saved.g_valid;
+      c->dot_G = saved.dot_G;
+      c->last_Gw = saved.last_Gw;
+      c->last_Ge = saved.last_Ge;
+      c->last_kind = saved.last_kind;
       return BX_OK;
     }
     size_t nn = 0;
@@ -1420,43 +1498,105 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
   *ran = 1;
   *done = hd[0];
   *event = hd[1];
-  if (hd[1]) c->dot_done = true;  // the event round's g / eps partials are in place
+  // the event round's g / eps partials are in place (with spec: the round
+  // ended with its speculative step, as the capture left the host state)
+  if (hd[1]) c->dot_done = true;
   return BX_OK;
 }
 
-// one round's primal passes
+// one PG / FISTA step on the act view: pass + reduce.  spec: the
+// speculative round-boundary step -- the pass also emits the
+// round's screening gradient g_k and epsilon partials and keeps what an undo
+// needs (x_k, and for FISTA x_{k-1} / g_{k-1}; the reduce saves r_k and the
+// objective / momentum before the step).
+template <typename T>
+int step_pass(bx_ctx* c, int kind, bool spec) {
+  const int s = c->cur;
+  int G = 1;
+  StepExtra ex;
+  ex.spec = spec ? 1 : 0;
+  ex.xbak = (double*)c->xbak;
+  ex.gbak = (double*)c->gbak;
+  ex.epart = c->epart;
+  const int sm = spec ? R_SPEC : 0;
+  double* save = spec ? (double*)c->rbak : nullptr;
+  if (kind == BX_PG) {
+    if (c->g_valid && !spec) {
+      TRY(run_pass<T>(c, act_view<T>(c), U_PG_G, nullptr, nullptr, (double*)c->x[s], nullptr, (const double*)c->lo[s],
+                      (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G));
+    } else {
+      // spec: x_k goes to xprev (unused by PG) for an undo
+      TRY(run_pass<T>(c, act_view<T>(c), U_PG, (const double*)c->r, nullptr, (double*)c->x[s], (double*)c->xprev[s],
+                      (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s],
+                      nullptr, nullptr, c->has_inf, &G, nullptr, 0, -1, -1, false, ex));
+    }
+    TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_PG | sm, nullptr, 0, 2, save));
+  } else {
+    // FISTA by gradient linearity: the pass dots r_k; the new
+    // residual is reduced in place
+    ex.gprev = (double*)c->gprev[s];
+    TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const double*)c->r, nullptr, (double*)c->x[s], (double*)c->xprev[s],
+                    (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s],
+                    nullptr, c->bpart, c->has_inf, &G, (const double*)c->nrm[s], 0, -1, -1, false, ex));
+    TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_APG | sm, c->bpart, c->last_Gw, 2, save));
+  }
+  c->g_valid = false;
+  if (spec) {
+    c->spec_pending = true;
+    c->dot_done = true;  // g_k and its epsilon partials are the round's screening gradient
+    c->dot_spec = true;
+    c->dot_G = c->last_Ge;
+  }
+  return BX_OK;
+}
+
+// one round's primal passes.  After an accepted speculative step the round's
+// first step has already been taken (at the end of the previous round).
 template <typename T>
 int primal_passes(bx_ctx* c, int kind, int passes) {
-  const int s = c->cur;
-  {
+  c->last_kind = kind;
+  int p0 = 0;
+  if (c->spec_pending) {
+    p0 = 1;
+    c->spec_pending = false;
+  } else {
     int ran = 0, done = 0, ev = 0;
     SmallLoop lp;
     TRY(small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev));
     if (ran) return BX_OK;
   }
-  for (int p = 0; p < passes; ++p) {
-    int G = 1;
-    if (kind == BX_PG) {
-      if (c->g_valid) {
-        TRY(run_pass<T>(c, act_view<T>(c), U_PG_G, nullptr, nullptr, (double*)c->x[s], nullptr, (const double*)c->lo[s],
-                        (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G));
-      } else {
-        TRY(run_pass<T>(c, act_view<T>(c), U_PG, (const double*)c->r, nullptr, (double*)c->x[s], nullptr, (const double*)c->lo[s],
-                        (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G));
-      }
-      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_PG, nullptr, 0, 2));
-      c->g_valid = false;
-    } else if (kind == BX_APG) {
-      TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const double*)c->r, (const double*)c->rprev, (double*)c->x[s], (double*)c->xprev[s],
-                      (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, c->bpart, 0, &G,
-                      (const double*)c->nrm[s]));
-      // r_prev <- r, r <- new residual: write into the r_prev buffer, swap
-      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->rprev, R_APG, c->bpart, c->last_Gw, 2));
-      std::swap(c->r, c->rprev);
-    } else {
-      return cd_sweeps<T>(c, passes);  // all sweeps in one launch
-    }
-  }
+  if (kind == BX_CD) return cd_sweeps<T>(c, passes);  // all sweeps in one launch
+  for (int p = p0; p < passes; ++p) TRY(step_pass<T>(c, kind, false));
+  return BX_OK;
+}
+
+// Whether the round about to end should evaluate its screening gradient with
+// the next round's first step (speculatively) instead of a dot-only pass:
+// PG / FISTA on the streamed path, when the next round runs there too.
+template <typename T>
+bool spec_applies(bx_ctx* c, int kind, int passes) {
+  if (!c->spec_on || (kind != BX_PG && kind != BX_APG) || c->k == 0) return false;
+  int ran = 0, done = 0, ev = 0;
+  SmallLoop lp;
+  lp.max_rounds = 2;
+  if (small_rounds<T>(c, kind, passes, lp, &ran, &done, &ev, true) != BX_OK) return false;
+  return !ran;  // the cooperative small-round kernel owns the next round
+}
+
+// Undo the speculative step (k_spec_undo): the state is again the round's
+// final iterate x_k with r_k, g_{k-1} and the scalars before the step.
+template <typename T>
+int spec_undo(bx_ctx* c, int kind) {
+  if (!c->spec_pending) return BX_OK;
+  const int s = c->cur;
+  const int64_t n = c->k > c->m ? c->k : c->m;
+  k_spec_undo<<<grid1d(c, n), RT, 0, c->stream>>>(c->k, kind == BX_APG ? 1 : 0, (double*)c->x[s],
+                                                  (double*)c->xprev[s], (const double*)c->xbak,
+                                                  (double*)c->gprev[s], (const double*)c->gbak, c->m,
+                                                  (double*)c->r, (const double*)c->rbak, c->sc);
+  LAUNCHED();
+  c->spec_pending = false;
+  c->g_valid = false;
   return BX_OK;
 }
 
@@ -1584,7 +1724,7 @@ int dual_point(bx_ctx* c, int which, const double* r, const double* tgt, double*
   int nb = grid1d(c, c->m > k ? c->m : k);
   const int e0 = prof_begin(c);
   k_dual<double><<<nb, RT, 0, c->stream>>>(r, (const double*)c->t, tgt, theta, c->m, g, att, lo, hi, v, k, ep, ge, c->has_inf,
-                                       c->sc, which, c->bpart3, slack_scale, alpha, which ? 5 : 3,
+                                       c->sc, which, c->bpart3, slack_scale, alpha, which == 1 ? 5 : 3,
                                        c->sharded() ? c->dsum : nullptr);
   LAUNCHED();
   prof_end(c, e0, BX_PROF_DUAL, 8.0 * (4.0 * c->m + 6.0 * k));
@@ -1596,46 +1736,63 @@ int dual_point(bx_ctx* c, int which, const double* r, const double* tgt, double*
   return BX_OK;
 }
 
-// gradient at the current iterate + dual point + gap (+ sphere test)
+// gradient at the round's final iterate + dual point + gap (+ sphere test).
+// The gradient is a dot-only pass, or came with the round kernel / the
+// speculative step (dot_done; then with dot_spec the round's final iterate
+// is x_prev, its residual r_bak and its objective bak_P, and the sphere test
+// also counts the "dirty" screened columns that force an undo).
 template <typename T>
 int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
   const int s = c->cur;
   int G = 1;
+  const bool spec = c->dot_done && c->dot_spec;
   if (c->dot_done) {
-    G = c->dot_G;  // g and the eps partials came with the round kernel
+    G = c->dot_G;  // g and the eps partials came with the round kernel / the speculative step
     c->dot_done = false;
   } else {
     TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr,
                     (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s], nullptr, c->bpart, c->has_inf,
                     &G));
     c->dot_G = G;  // a later dual_screen on the same g (dot_done) reuses its eps partials
+    c->dot_spec = false;
   }
-  c->g_valid = true;
-  TRY(dual_point<T>(c, 0, (const double*)c->r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g, (const double*)c->att[s],
-                    (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->v, c->k, c->bpart, G, slack_scale, alpha));
+  if (!spec) c->g_valid = true;  // (after a speculative step g is at x_prev, not x)
+  const double* r = spec ? (const double*)c->rbak : (const double*)c->r;
+  TRY(dual_point<T>(c, spec ? 2 : 0, r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g,
+                    (const double*)c->att[s], (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->v, c->k,
+                    spec ? c->epart : c->bpart, G, slack_scale, alpha));
   c->theta_is_cert = false;
   if (screening && c->k > 0) {
     const int nbs = (int)((c->k + RT - 1) / RT);
     const int e1 = prof_begin(c);
-    k_sphere<double><<<nbs, RT, 0, c->stream>>>((const double*)c->v, (const double*)c->nrm[s], (const double*)c->hi[s], c->k, c->sc,
-                                            c->flags, c->bcnt);
+    const bool apg = c->last_kind == BX_APG;
+    k_sphere<double><<<nbs, RT, 0, c->stream>>>((const double*)c->v, (const double*)c->nrm[s], (const double*)c->lo[s],
+                                            (const double*)c->hi[s], c->k, c->sc, c->flags, c->bcnt,
+                                            spec ? (const double*)c->x[s] : nullptr,
+                                            spec ? (const double*)c->xprev[s] : nullptr,
+                                            (spec && apg) ? (const double*)c->xbak : nullptr);
     LAUNCHED();
     k_scan<<<1, 1024, 0, c->stream>>>(c->bcnt, nbs, c->sc);
     LAUNCHED();
     prof_end(c, e1, BX_PROF_SPHERE, (double)c->k * 25.0);
   } else {
-    CU(cudaMemsetAsync(&c->sc->n_keep, 0, 6 * sizeof(int64_t), c->stream));
+    CU(cudaMemsetAsync(&c->sc->n_keep, 0, 8 * sizeof(int64_t), c->stream));
   }
-  if (screening && c->sharded()) TRY(allreduce(c, &c->sc->g_keep, 3, ncclInt64, ncclSum));
+  if (screening && c->sharded()) TRY(allreduce(c, &c->sc->g_keep, 4, ncclInt64, ncclSum));
   return BX_OK;
 }
 
 // _certified_gap (driver.py:112-117): full-problem A x, A'(y - A x), epsilon
 // over all infinite-upper columns, dual objective
+// The round's final iterate: x, or x_prev while a speculative step is pending.
+const double* round_x(const bx_ctx* c) {
+  return (const double*)(c->spec_pending ? c->xprev[c->cur] : c->x[c->cur]);
+}
+
 template <typename T>
 int certified(bx_ctx* c, double alpha) {
   const int s = c->cur;
-  k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], (const double*)c->x[s], (double*)c->xfull);
+  k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], round_x(c), (double*)c->xfull);
   LAUNCHED();
   int G = 1;
   // fp32 storage: the certificate's A x and A'r accumulate in fp64 (a fp32
@@ -1657,12 +1814,20 @@ int certified(bx_ctx* c, double alpha) {
   return BX_OK;
 }
 
+template <typename T>
+int dot_accumulate(bx_ctx* c, const double* vin, double* g);
+
 // r += A_S (b_S - x_S) (and r_prev += A_S (b_S - x_prev_S)) over the newly
 // screened columns: the residual of the snapped iterate without a pass over the
 // preserved set.  The reference recomputes it (solvers.py:64); the next step's
 // pass recomputes r = A x + z - y from scratch anyway, so only the one dot of
 // that step sees the (rounding-level) difference.  Collective in sharded mode
 // (every rank contributes its own screened columns, possibly none).
+//
+// FISTA also carries g_{k-1} = A'r_{k-1} per preserved column; snapping the
+// screened x_{k-1} moves r_{k-1} by d = A_S (b_S - x_prev_S), so g_prev gets
+// A_act' d (one dot pass over the preserved set with d as the vector).  The
+// oracle recomputes g_prev from the snapped x_prev (same quantity).
 template <typename T>
 int refresh_incremental(bx_ctx* c, int64_t nscr, int kind) {
   View<T> vw{(const T*)c->A, c->lda, c->scr_idx, nscr};
@@ -1670,26 +1835,48 @@ int refresh_incremental(bx_ctx* c, int64_t nscr, int kind) {
   TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                   (const double*)c->scr_dx, nullptr, 0, &G));
   TRY(run_reduce<T>(c, G, (const double*)c->r, (double*)c->r, R_SET, nullptr, 0, 0));
-  if (kind == BX_APG) {
+  if (kind == BX_APG && c->k > 0) {
     TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                     (const double*)c->scr_dxp, nullptr, 0, &G));
-    TRY(run_reduce<T>(c, G, (const double*)c->rprev, (double*)c->rprev, R_PLAIN, nullptr, 0, 0));
+    TRY(run_reduce<T>(c, G, nullptr, (double*)c->u, R_PLAIN, nullptr, 0, 0));
+    TRY(dot_accumulate<T>(c, (const double*)c->u, (double*)c->gprev[c->cur]));
   }
   return BX_OK;
 }
 
-// apply_screening + Workspace.refresh (screening.py:72-94, solvers.py:54-65)
+// g[p] += a_p . vin over the preserved set (whole columns, or row blocks
+// beyond the register-resident envelope)
 template <typename T>
-int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, bool z_update) {
+int dot_accumulate(bx_ctx* c, const double* vin, double* g) {
+  if (c->k == 0) return BX_OK;
+  int G = 1;
+  if (pick_R(c->m, sizeof(T)) > 0)
+    return run_pass<T>(c, act_view<T>(c), U_DOT, vin, nullptr, nullptr, nullptr, nullptr, nullptr, g, nullptr,
+                       nullptr, nullptr, 0, &G, nullptr, 0, c->m, 1);
+  constexpr int64_t BR = (int64_t)NT * (16 / sizeof(T)) * 8;
+  for (int64_t r0 = 0; r0 < c->m; r0 += BR)
+    TRY(run_pass<T>(c, act_view<T>(c), U_DOT, vin, nullptr, nullptr, nullptr, nullptr, nullptr, g, nullptr, nullptr,
+                    nullptr, 0, &G, nullptr, r0, std::min(BR, c->m - r0), 1));
+  return BX_OK;
+}
+
+// apply_screening + Workspace.refresh (screening.py:72-94, solvers.py:54-65).
+// clean: a speculative step stands over a screened set that sat at its bound
+// on every iterate the step touched -- the residual, g_prev and the step are
+// unchanged by the screening, so there is nothing to refresh.
+template <typename T>
+int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, bool z_update, bool clean = false) {
   const int s = c->cur, d = 1 - c->cur;
   const int nbs = (int)((c->k + RT - 1) / RT);
   const int64_t nscr = n_lo + n_up;
   if (nscr > 0) {
     const bool carry2 = kind == BX_APG || kind == BX_ACTIVE_SET;  // momentum state / passive mask
     ColState<double> src{c->idx[s], (double*)c->x[s], carry2 ? (double*)c->xprev[s] : nullptr,
+                         kind == BX_APG ? (double*)c->gprev[s] : nullptr,
                          (double*)c->lo[s], (double*)c->hi[s], (double*)c->nrm[s], (double*)c->att[s],
                          c->dense ? nullptr : c->pos[s]};
-    ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->lo[d], (double*)c->hi[d],
+    ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->gprev[d],
+                         (double*)c->lo[d], (double*)c->hi[d],
                          (double*)c->nrm[d], (double*)c->att[d], c->act_is_orig ? nullptr : c->pos[d]};
     k_compact<double><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (double*)c->xfull, c->scr_idx,
                                                  (double*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo,
@@ -1715,7 +1902,7 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
                                                              (double*)c->off, (double*)c->tgt);
     LAUNCHED();
   }
-  TRY(refresh_incremental<T>(c, nscr, kind));
+  if (!clean) TRY(refresh_incremental<T>(c, nscr, kind));
   // physical rewrite of the preserved columns (solvers.py:57) once half the
   // physical buffer is dead -- or always for CD, whose kernels read A_act densely
   if (nscr > 0 && (kind == BX_CD || c->k < c->kphys / 2)) {
@@ -1737,7 +1924,7 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
 }
 
 template <typename T>
-int reset_state(bx_ctx* c, int kind) {
+int reset_state(bx_ctx* c, int kind, int restart = 0) {
   const int s = 0;
   c->cur = 0;
   c->k = c->n;
@@ -1774,14 +1961,19 @@ int reset_state(bx_ctx* c, int kind) {
   const bool f32 = sizeof(T) == 4;
   h.rise_rel = f32 ? 1e-5 : 0.0;
   h.rs_f = f32 ? 1e-6 : 1e-12;
-  h.rs_g = f32 ? 1e-5 : 1e-12;
+  // restart = 1 (objective increase only): the gradient test never fires
+  h.rs_g = restart ? INFINITY : (f32 ? 1e-5 : 1e-12);
   CU(cudaMemcpyAsync(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
   TRY(refresh_resid<T>(c));
   if (kind == BX_APG) {
+    // x_prev = x_0; g_prev is unused until a step with momentum (t_0 = 1)
     CU(cudaMemcpyAsync(c->xprev[s], c->x[s], c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->rprev, c->r, c->mp * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemsetAsync(c->gprev[s], 0, c->n * sizeof(double), c->stream));
     c->have_apg_state = true;
   }
+  c->spec_pending = false;
+  c->dot_done = false;
+  c->dot_spec = false;
   return BX_OK;
 }
 
@@ -1881,7 +2073,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   if (kind == BX_ACTIVE_SET && !c->as)
     return fail(c, BX_ERR_WORKSPACE, "active-set scratch not attached (bx_ctx_set_active_set_workspace)");
   TRY(validate(c));
-  TRY(reset_state<T>(c, kind));
+  TRY(reset_state<T>(c, kind, cfg->restart));
   double eta = cfg->step_size;
   double sigma = 0.0;
   int64_t kg = c->sharded() ? c->n_global : c->n;  // global preserved count
@@ -1895,6 +2087,11 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   }
   int64_t rounds = 0, iters = 0;
   bool converged = false;
+  int64_t spec_kept = 0, spec_undone = 0, last_restarts = 0;
+  static const bool spec_force_undo = [] {
+    const char* e = getenv("BX_SPEC_FORCE_UNDO");  // test switch: every event takes the undo path
+    return e && e[0] == '1';
+  }();
   double gap_out = INFINITY;
   int64_t ntrace = 0;
   double excluded = 0.0;  // seconds of gap evaluation left out of the trace (screening off)
@@ -1953,6 +2150,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
             t.restarts = (int64_t)tr[8 * q + 6];
           }
           gap_out = tr[8 * (done - 1) + 2];
+          last_restarts = (int64_t)tr[8 * (done - 1) + 6];
           iters += (int64_t)done * passes;
           rnd += done;
           rounds = rnd - 1;
@@ -1966,10 +2164,12 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       } else {
         TRY(primal_passes<T>(c, kind, passes));
         iters += passes;
+        if (spec_applies<T>(c, kind, passes)) TRY(step_pass<T>(c, kind, true));
       }
     } else {
       TRY(primal_passes<T>(c, kind, passes));
       iters += passes;
+      if (spec_applies<T>(c, kind, passes)) TRY(step_pass<T>(c, kind, true));
     }
     // offline-gap convention (driver.py:180-181, 237-238): without screening
     // the gap evaluation is excluded from the trace's elapsed time -- here the
@@ -2010,6 +2210,10 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       const double tol_c = cfg->relative_gap ? tol * fmax(1.0, fabs(c->hsc->cert.primal)) : tol;
       if (cert_gap < tol_c) converged = true;
     }
+    // the round's momentum / restart count (before a speculative step)
+    const double mom_round = c->spec_pending ? c->hsc->bak_mom_t : c->hsc->mom_t;
+    const int64_t restarts_round = c->spec_pending ? c->hsc->bak_restarts : c->hsc->restarts;
+    last_restarts = restarts_round;
     int64_t n_lo = 0, n_up = 0;
     if (cfg->screening && kg > 0) {
       n_lo = c->hsc->g_lo;
@@ -2017,12 +2221,21 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       if (n_lo || n_up) {
         last_event = rnd;
         const bool z_update = ((c->bound_bits & 1) && n_lo > 0) || ((c->bound_bits & 2) && n_up > 0);
-        TRY(compact<T>(c, c->hsc->n_lo, c->hsc->n_up, c->hsc->n_keep, kind, z_update));
-        kg = c->hsc->g_keep;
-        if ((kind == BX_PG || kind == BX_APG) && auto_eta && (double)kg < 0.5 * (double)basis) {
+        const int64_t kg_new = c->hsc->g_keep;
+        const bool reestimate =
+            (kind == BX_PG || kind == BX_APG) && auto_eta && (double)kg_new < 0.5 * (double)basis;
+        // the speculative step stands only if screening leaves the problem it
+        // was taken on unchanged (no screened coordinate off its bound on any
+        // iterate the step touched) and the step size stays
+        const bool clean = c->spec_pending && !converged && c->hsc->g_dirty == 0 && !reestimate && !spec_force_undo;
+        if (c->spec_pending && !clean) TRY(spec_undo<T>(c, kind));
+        TRY(compact<T>(c, c->hsc->n_lo, c->hsc->n_up, c->hsc->n_keep, kind, z_update, clean));
+        kg = kg_new;
+        if (reestimate) {
           TRY(auto_step<T>(c, cfg->power_iters, alpha, fn, user, &eta, &sigma));
           basis = kg;
         }
+        if (clean) ++spec_kept; else if (!converged) ++spec_undone;
       }
     }
     if (trace && ntrace < cap) {
@@ -2039,10 +2252,14 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       tr.radius = act.radius;
       tr.step = eta;
       tr.certified_gap = cert_gap;
-      tr.restarts = c->hsc->restarts;
-      tr.momentum = c->hsc->mom_t;
+      tr.restarts = restarts_round;
+      tr.momentum = mom_round;
     }
     if (converged) break;
+    // a StepSizeTooLarge of a speculative step that stands is the next
+    // round's (the reference raises it from that round's pg_step)
+    if (c->spec_pending && c->hsc->err_spec)
+      return fail(c, BX_ERR_STEP_TOO_LARGE, "objective rose from %.6e to %.6e", c->hsc->spec_v1, c->hsc->spec_v2);
     if (optimal) {
       // KKT-optimal active set: the certified gap alone decides (driver.py:246-252)
       TRY(certified<T>(c, alpha));
@@ -2055,6 +2272,8 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
       break;
     }
   }
+  // a speculative step past the last round is dropped: x is the last round's
+  TRY(spec_undo<T>(c, kind));
   // x_full <- current preserved iterate (ws.sync, driver.py:252)
   k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], (const double*)c->x[c->cur], (double*)c->xfull);
   LAUNCHED();
@@ -2069,7 +2288,9 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     out->step = eta;
     out->sigma = sigma;
     out->kernel_launches = c->launches;
-    out->restarts = c->hsc->restarts;
+    out->restarts = last_restarts;
+    out->spec_kept = spec_kept;
+    out->spec_undone = spec_undone;
   }
   return BX_OK;
 }
@@ -2139,6 +2360,12 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   CU(cudaMemsetAsync(c->part, 0, (size_t)c->Gmax * c->ldp * 8, c->stream));
   CU(cudaMemsetAsync(c->bar, 0, 4 * kMaxRanks * 4, c->stream));
   c->small_ok = getenv("BX_NO_SMALL") == nullptr;
+  {
+    const char* e = getenv("BX_SPEC");
+    c->spec_on = !(e && e[0] == '0');
+    const char* to = getenv("BX_PEER_TIMEOUT_S");
+    if (to && atof(to) > 0) c->xtimeout_ns = (uint64_t)(atof(to) * 1e9);
+  }
   if (dtype == BX_F64) return create_typed<double>(c, y, lower, upper, t);
   return create_typed<float>(c, y, lower, upper, t);
 }
@@ -2251,7 +2478,16 @@ int bx_solve(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* us
 }
 
 int bx_get_state(bx_ctx* c, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper) {
-  if (x) CU(cudaMemcpyAsync(x, c->xfull, c->n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (x) {
+    // x_full <- the current preserved iterate (screened entries are already
+    // at their bounds): valid after any sequence of fine-grained calls
+    if (c->k > 0) {
+      k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], round_x(c), (double*)c->xfull);
+      LAUNCHED();
+    }
+    CU(cudaMemcpyAsync(x, c->xfull, c->n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
   if (theta)
     CU(cudaMemcpyAsync(theta, c->theta_is_cert ? c->thetac : c->theta, c->m * 8, cudaMemcpyDeviceToDevice,
                        c->stream));

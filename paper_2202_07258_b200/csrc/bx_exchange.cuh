@@ -48,6 +48,8 @@ struct XArgs {
   int64_t m, mp;      // rows, padded rows (payload stride = mp + kXExtra)
   const double* off;  // offset added after the sum (NULL: none)
   double* out;        // the reduced vector (replicated on every rank)
+  double* save;       // speculative step: out's previous contents (NULL: none)
+  uint64_t timeout_ns;  // bound of every peer wait (%globaltimer); DE_PEER_TIMEOUT beyond it
   DevScalars* sc;
   double* bpart;      // [nb] per-CTA ||out||^2 partials
   const double* wpart;  // [Gw][stride] pass scalar partials (NULL: none)
@@ -71,6 +73,26 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 }
 // epochs are monotonic (mod 2^32): "reached" survives a peer running ahead
 __device__ __forceinline__ bool reached(unsigned v, unsigned epoch) { return (int)(v - epoch) >= 0; }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded wait for a peer's flag: a peer that errored, exited or took the
+// NCCL schedule never publishes, so after timeout_ns the wait gives up and
+// raises DE_PEER_TIMEOUT (the host turns it into an error on every rank that
+// tripped, instead of a kernel that never returns).  Returns false on timeout.
+__device__ __forceinline__ bool wait_flag(const unsigned* p, unsigned epoch, uint64_t t0, uint64_t timeout_ns,
+                                          DevScalars* sc) {
+  unsigned spins = 0;
+  while (!reached(ld_acquire_sys(p), epoch)) {
+    if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > timeout_ns) {
+      atomicCAS(&sc->err, 0, DE_PEER_TIMEOUT);
+      return false;
+    }
+  }
+  return true;
+}
 
 template <typename T>
 __device__ void xreduce_body(const XArgs& a, int cta) {
@@ -121,11 +143,9 @@ __device__ void xreduce_body(const XArgs& a, int cta) {
   if (tid < a.nranks) st_release_sys(&a.flag[tid][a.rank * a.nb + cta], a.epoch);
   // 4. wait for the same block (and the scalar slots of CTA 0) from every peer
   if (tid < a.nranks) {
-    while (!reached(ld_acquire_sys(&a.my_flag[tid * a.nb + cta]), a.epoch)) {
-    }
-    if (a.wpart && cta != 0)
-      while (!reached(ld_acquire_sys(&a.my_flag[tid * a.nb]), a.epoch)) {
-      }
+    const uint64_t t0 = globaltimer_ns();
+    if (wait_flag(&a.my_flag[tid * a.nb + cta], a.epoch, t0, a.timeout_ns, a.sc) && a.wpart && cta != 0)
+      wait_flag(&a.my_flag[tid * a.nb], a.epoch, t0, a.timeout_ns, a.sc);
   }
   __threadfence();
   __syncthreads();
@@ -137,18 +157,20 @@ __device__ void xreduce_body(const XArgs& a, int cta) {
     ex[tid] = v;
   }
   __syncthreads();
-  const double s_div = (a.mode == R_POWER) ? sqrt(ex[0]) : 1.0;
+  const int base = a.mode & ~R_SPEC;
+  const double s_div = (base == R_POWER) ? sqrt(ex[0]) : 1.0;
   // 5. the replicated result: peers summed in rank order (+ offset)
   double sq = 0.0;
   for (int64_t i = r0 + tid; i < r1; i += XT) {
     double s = __ldcv(rb + i);
     for (int q = 1; q < a.nranks; ++q) s += __ldcv(rb + q * pay + i);
     if (a.off) s = add_rn(s, a.off[i]);
-    if (a.mode == R_POWER) s = s / s_div;
+    if (base == R_POWER) s = s / s_div;
+    if (a.save) a.save[i] = a.out[i];
     a.out[i] = s;
     sq += s * s;
   }
-  if (a.mode == R_PLAIN) return;
+  if (base == R_PLAIN) return;
   sq = warp_sum<double>(sq);
   if (lane == 0) sh[warp] = sq;
   __syncthreads();
@@ -167,7 +189,7 @@ __device__ void xreduce_body(const XArgs& a, int cta) {
   for (int b = lane; b < a.nb; b += 32) total += __ldcg(&a.bpart[b]);
   total = warp_sum<double>(total);
   if (lane != 0) return;
-  finalize_objective<T>(a.sc, a.mode, 0.5 * total, a.mode == R_POWER ? s_div : 0.0, ex[0], ex[1]);
+  finalize_objective<T>(a.sc, a.mode, 0.5 * total, base == R_POWER ? s_div : 0.0, ex[0], ex[1]);
   a.sc->counters[a.counter] = 0u;
 }
 

@@ -37,6 +37,7 @@ constexpr int NWARPS = NT / 32;
 constexpr int CMAX = 8;            // columns per ring slot (max)
 constexpr int SMAX = 8;            // ring slots (max)
 constexpr int RT = 256;            // block size of the vector kernels
+constexpr int PASS_STAGED = 7;     // per-column state arrays a pass may stage in shared memory
 
 template <typename T> struct V16;
 template <> struct V16<double> { using type = double2; static constexpr int n = 2; };
@@ -52,9 +53,14 @@ enum PassUpd : int {
 };
 
 enum ReduceMode : int { R_PLAIN = 0, R_SET = 1, R_PG = 2, R_APG = 3, R_POWER = 4, R_CERT = 5 };
+// or-ed into R_PG / R_APG for the speculative round-boundary step: the
+// objective / momentum before the step are kept (bak_*) and a step error is
+// recorded in err_spec, because the step is undone when the round's
+// screening event changes the problem it was taken on
+constexpr int R_SPEC = 16;
 
 enum DevErr : int {
-  DE_NONE = 0, DE_STEP_TOO_LARGE = 4, DE_INTERNAL_CONSISTENCY = 5, DE_POWER_ZERO = 64
+  DE_NONE = 0, DE_STEP_TOO_LARGE = 4, DE_INTERNAL_CONSISTENCY = 5, DE_POWER_ZERO = 64, DE_PEER_TIMEOUT = 65
 };
 
 // Scalars shared by the kernels of one context (device memory).
@@ -76,10 +82,17 @@ struct DevScalars {
   double rs_f;      // FISTA restart slacks (1e-12 fp64; fp32 values sized to fp32 round-off)
   double rs_g;
   double err_v1, err_v2;  // objective values at a StepSizeTooLarge event
-  int64_t n_keep, n_lo, n_up;  // this rank's sphere-test counts
-  int64_t g_keep, g_lo, g_up;  // summed over ranks (== local on one GPU)
+  // state before the speculative round-boundary step (restored on undo)
+  double bak_P, bak_mom_t;
+  double spec_v1, spec_v2;  // objective values of a speculative StepSizeTooLarge
+  // this rank's sphere-test counts; n_dirty = screened columns whose iterate
+  // around the speculative step is off the bound (the step must be undone)
+  int64_t n_keep, n_lo, n_up, n_dirty;
+  int64_t g_keep, g_lo, g_up, g_dirty;  // summed over ranks (== local on one GPU)
   int32_t err;
   int32_t restarts;
+  int32_t bak_restarts;
+  int32_t err_spec;  // StepSizeTooLarge raised by the speculative step
   unsigned int counters[8];
 };
 
@@ -94,9 +107,10 @@ struct PassArgs {
   // storage type T -- fp32 storage halves the streamed bytes without
   // lowering the precision of the iterate ("fp32")
   const double* vin;       // dot vector (residual / power vector)
-  const double* vin_prev;  // FISTA: previous residual
+  const double* vin_prev;  // row-blocked dot with an extrapolated vector (unused by the fused modes)
   double* x;               // iterate (updated in place)
-  double* xprev;           // FISTA previous iterate
+  double* xprev;           // FISTA previous iterate (PG speculative step: x before the step)
+  double* gprev;           // FISTA: gradient at the previous iterate (read g_{k-1}, written g_k)
   const double* lo;
   const double* hi;
   double* g;               // gradient A'v (written by dot modes, read by U_PG_G)
@@ -116,6 +130,13 @@ struct PassArgs {
   int pre;                 // >= columns per CTA: the CTA's per-column state is staged in smem (0: off)
   int accumulate;          // U_DOT over a row block: g[p] = (accumulate ? g[p] : 0) + block dot, no epsilon
   int extrap;              // dot with the FISTA extrapolated residual r + beta (r - r_prev)
+  // speculative round-boundary step (U_PG / U_APG): the pass's dot is also
+  // the round's screening gradient -- g[p] = g_k, epsilon partial -> epart;
+  // FISTA keeps x_{k-1} / g_{k-1} in xbak / gbak for an undo
+  int spec;
+  double* xbak;
+  double* gbak;
+  double* epart;           // [gridDim.x] epsilon partial (block max)
 };
 
 // ----------------------------------------------------------------------------
@@ -283,8 +304,8 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * slot_bytes);
   double* red = reinterpret_cast<double*>(bars + SMAX);  // [NWARPS][C]
   double* cf = red + NWARPS * CMAX;                      // [C] axpy coefficients
-  double* bscr = cf + CMAX;                              // [2][CMAX] block scalar scratch
-  double* stg = bscr + 2 * CMAX;                         // [5][pre] staged per-column state
+  double* bscr = cf + CMAX;                              // [3][CMAX] block scalar scratch
+  double* stg = bscr + 3 * CMAX;                         // [PASS_STAGED][pre] staged per-column state
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -307,12 +328,23 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     }
   }
 
-  // the dot vector, register resident: thread owns rows (i*NT + tid)*V + e
+  // the dot vector, register resident: thread owns rows (i*NT + tid)*V + e.
+  // FISTA dots the plain residual r_k: the extrapolated gradient is formed
+  // per column by linearity, g_y = g_k + beta (g_k - g_{k-1}),
+  // so the dot is also the gradient at x_k -- the round's screening gradient
   AT vr[DOT ? R : 1][V];
-  double beta = 0.0;
-  const double eta = a.sc->eta;
+  double beta = 0.0;   // extrapolation of the dot vector (row-blocked dots only)
+  // the step eta and FISTA's momentum coefficient are read in the per-column
+  // epilogue (one thread per column; keeps them out of the register file of
+  // the streaming loop)
+  auto step_eta = [&]() { return __ldg(&a.sc->eta); };
+  auto momentum_beta = [&]() {
+    const double t = __ldg(&a.sc->mom_t);
+    const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    return (t - 1.0) / tn;
+  };
   if (DOT) {
-    if (a.upd == U_APG || a.extrap) {
+    if (a.extrap) {
       const double t = a.sc->mom_t;
       const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
       beta = (t - 1.0) / tn;
@@ -344,29 +376,33 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     for (int e = 0; e < V; ++e) acc[i][e] = AT(0);
   double run = 0.0;   // block-scalar running value (threads tid < C)
   double run2 = 0.0;  // second block scalar (FISTA restart slack)
+  double run3 = 0.0;  // speculative step: epsilon partial (max)
 
   // Stage this CTA's per-column state in shared memory once (coalesced), so
   // the per-column update between the two barriers never waits on HBM.
   const bool staged = a.pre >= ncol && a.pre > 0;
-  const double *s0 = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr;
+  // slots: U_DOT hi, att | U_PG_G x, lo, hi, g | U_PG x, lo, hi, -, -, -, att |
+  // U_APG x, lo, hi, x_prev, ||a||, g_prev, att | U_AX coef
+  // (no pointer per slot: the epilogue indexes stg directly -- fewer live
+  // registers in the R = 10..12 instantiations)
+#define BX_STG(f) stg[(f) * a.pre + ql]
+  const bool want_att = a.spec && a.has_inf;
   if (staged) {
-    const double* src[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    const double* src[PASS_STAGED] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     switch (a.upd) {
       case U_DOT: src[0] = a.hi; src[1] = a.att; break;
       case U_PG_G: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; src[3] = a.g; break;
-      case U_PG: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; break;
-      case U_APG: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; src[3] = a.xprev; src[4] = a.nrm; break;
+      case U_PG: src[0] = a.x; src[1] = a.lo; src[2] = a.hi; if (want_att) src[6] = a.att; break;
+      case U_APG:
+        src[0] = a.x; src[1] = a.lo; src[2] = a.hi; src[3] = a.xprev; src[4] = a.nrm; src[5] = a.gprev;
+        if (want_att) src[6] = a.att;
+        break;
       case U_AX: src[0] = a.coef ? a.coef : a.x; break;
       default: break;
     }
-    for (int f = 0; f < 5; ++f)
+    for (int f = 0; f < PASS_STAGED; ++f)
       if (src[f])
         for (int q = tid; q < ncol; q += NT) stg[f * a.pre + q] = src[f][p0 + q];
-    s0 = stg;
-    s1 = stg + a.pre;
-    s2 = stg + 2 * a.pre;
-    s3 = stg + 3 * a.pre;
-    s4 = stg + 4 * a.pre;
     __syncthreads();
   }
 
@@ -485,35 +521,54 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
               break;
             }
             a.g[p] = gj;
-            const double hj = staged ? s0[ql] : a.hi[p];
+            const double hj = staged ? BX_STG(0) : a.hi[p];
             if (a.has_inf && isinf(hj)) {
-              const double ratio = fmax(-gj, 0.0) / fabs(staged ? s1[ql] : a.att[p]);
+              const double ratio = fmax(-gj, 0.0) / fabs(staged ? BX_STG(1) : a.att[p]);
               run = fmax(run, ratio);
             }
           } break;
           case U_PG: {
+            const double eta = step_eta();
             a.g[p] = gj;
-            const double xo = staged ? s0[ql] : a.x[p];
-            const double xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), staged ? s1[ql] : a.lo[p],
-                                           staged ? s2[ql] : a.hi[p]);
+            const double xo = staged ? BX_STG(0) : a.x[p];
+            const double hj = staged ? BX_STG(2) : a.hi[p];
+            const double xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), staged ? BX_STG(1) : a.lo[p], hj);
+            if (a.spec) {
+              a.xprev[p] = xo;  // x_k, for an undo
+              if (a.has_inf && isinf(hj)) run3 = fmax(run3, fmax(-gj, 0.0) / fabs(staged ? BX_STG(6) : a.att[p]));
+            }
             a.x[p] = xn;
             coef = xn;
           } break;
           case U_APG: {
-            const double xo = staged ? s0[ql] : a.x[p];
-            const double xp = staged ? s3[ql] : a.xprev[p];
-            double yv = xo;
-            if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
-            const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), staged ? s1[ql] : a.lo[p],
-                                           staged ? s2[ql] : a.hi[p]);
+            // FISTA step by gradient linearity: the dot is g_k
+            const double eta = step_eta();
+            const double mbeta = momentum_beta();
+            const double xo = staged ? BX_STG(0) : a.x[p];
+            const double xp = staged ? BX_STG(3) : a.xprev[p];
+            const double gp = staged ? BX_STG(5) : a.gprev[p];
+            const double hj = staged ? BX_STG(2) : a.hi[p];
+            double yv = xo, gy = gj;
+            if (mbeta != 0.0) {
+              yv = add_rn(xo, mul_rn(mbeta, sub_rn(xo, xp)));
+              gy = add_rn(gj, mul_rn(mbeta, sub_rn(gj, gp)));
+            }
+            const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gy)), staged ? BX_STG(1) : a.lo[p], hj);
+            if (a.spec) {
+              a.xbak[p] = xp;  // x_{k-1}, g_{k-1}: an undo restores them
+              a.gbak[p] = gp;
+              a.g[p] = gj;     // the round's screening gradient (g at x_k)
+              if (a.has_inf && isinf(hj)) run3 = fmax(run3, fmax(-gj, 0.0) / fabs(staged ? BX_STG(6) : a.att[p]));
+            }
             a.xprev[p] = xo;
+            a.gprev[p] = gj;
             a.x[p] = xn;
             coef = xn;
             // gradient restart test g_y'(x+ - x) and its round-off scale
             // sum ||a_j|| |x+ - x| (FISTA)
             const double dxj = xn - xo;
-            run += gj * dxj;
-            run2 += (staged ? s4[ql] : a.nrm[p]) * fabs(dxj);
+            run += gy * dxj;
+            run2 += (staged ? BX_STG(4) : a.nrm[p]) * fabs(dxj);
           } break;
           case U_POWER: {
             coef = gj;
@@ -531,13 +586,14 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         const int64_t p = p0 + ql;
         double coef = 0.0;
         if (a.upd == U_PG_G) {
-          const double xo = staged ? s0[ql] : a.x[p];
-          const double xn = clip<double>(sub_rn(xo, mul_rn(eta, staged ? s3[ql] : a.g[p])),
-                                         staged ? s1[ql] : a.lo[p], staged ? s2[ql] : a.hi[p]);
+          const double eta = step_eta();
+          const double xo = staged ? BX_STG(0) : a.x[p];
+          const double xn = clip<double>(sub_rn(xo, mul_rn(eta, staged ? BX_STG(3) : a.g[p])),
+                                         staged ? BX_STG(1) : a.lo[p], staged ? BX_STG(2) : a.hi[p]);
           a.x[p] = xn;
           coef = xn;
         } else {
-          coef = staged ? s0[ql] : (a.coef ? a.coef[p] : a.x[p]);
+          coef = staged ? BX_STG(0) : (a.coef ? a.coef[p] : a.x[p]);
         }
         cf[tid] = coef;
       }
@@ -653,24 +709,30 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       }
     }
   }
-  if (a.bpart) {
+#undef BX_STG
+  if (a.bpart || a.epart) {
     if (tid < C) {
       bscr[tid] = run;
       bscr[CMAX + tid] = run2;
+      bscr[2 * CMAX + tid] = run3;
     }
     __syncthreads();
     if (tid == 0) {
-      double v = bscr[0], v2 = bscr[CMAX];
+      double v = bscr[0], v2 = bscr[CMAX], v3 = bscr[2 * CMAX];
       for (int c = 1; c < C; ++c) {
         v = (a.upd == U_DOT) ? fmax(v, bscr[c]) : v + bscr[c];
         v2 += bscr[CMAX + c];
+        v3 = fmax(v3, bscr[2 * CMAX + c]);
       }
-      if (a.upd == U_APG) {
-        a.bpart[2 * b] = v;
-        a.bpart[2 * b + 1] = v2;
-      } else {
-        a.bpart[b] = v;
+      if (a.bpart) {
+        if (a.upd == U_APG) {
+          a.bpart[2 * b] = v;
+          a.bpart[2 * b + 1] = v2;
+        } else {
+          a.bpart[b] = v;
+        }
       }
+      if (a.epart) a.epart[b] = v3;
     }
   }
 }
@@ -701,17 +763,33 @@ constexpr int RED_ONESHOT = 20;  // partial rows per slice loaded in one go (G <
 template <typename T>
 __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, double Pn, double scale_div,
                                                    double gdot, double gscale) {
-  switch (mode) {
+  if (mode & R_SPEC) {
+    // speculative round-boundary step: keep what an undo restores
+    sc->bak_P = sc->P;
+    sc->bak_mom_t = sc->mom_t;
+    sc->bak_restarts = sc->restarts;
+  }
+  switch (mode & ~R_SPEC) {
     case R_SET:
       sc->P = Pn;
       break;
     case R_PG:
       if (Pn > sc->P + 1e-9 + sc->rise_rel * fabs(sc->P)) {  // solvers.py:111-114
-        if (sc->err == 0) {
-          sc->err_v1 = sc->P;
-          sc->err_v2 = Pn;
+        if (mode & R_SPEC) {
+          // raised only if the step stands (the round neither converges nor
+          // undoes it): the reference raises it in the next round's pg_step
+          if (sc->err_spec == 0) {
+            sc->spec_v1 = sc->P;
+            sc->spec_v2 = Pn;
+          }
+          atomicCAS(&sc->err_spec, 0, DE_STEP_TOO_LARGE);
+        } else {
+          if (sc->err == 0) {
+            sc->err_v1 = sc->P;
+            sc->err_v2 = Pn;
+          }
+          set_err(sc, DE_STEP_TOO_LARGE);
         }
-        set_err(sc, DE_STEP_TOO_LARGE);
       }
       sc->P = Pn;
       break;
@@ -741,11 +819,12 @@ __device__ __forceinline__ void finalize_objective(DevScalars* sc, int mode, dou
   }
 }
 
+// save (speculative step, may be NULL): the previous contents of out
 template <typename T>
 __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64_t ldp, int G, int64_t m,
-                                               const double* __restrict__ off, double* __restrict__ out,
+                                               const double* off, double* out,
                                                DevScalars* sc, double* bpart, const double* wpart,
-                                               int Gw, int mode, int counter) {
+                                               int Gw, int mode, int counter, double* __restrict__ save) {
   using VT = typename V16<T>::type;
   constexpr int V = V16<T>::n;
   constexpr int RB = 32 * V;
@@ -754,7 +833,8 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
   __shared__ double s_div;
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (mode == R_POWER && warp == 0) {
+  const int base = mode & ~R_SPEC;
+  if (base == R_POWER && warp == 0) {
     double nw2 = 0.0;
     for (int b = lane; b < Gw; b += 32) nw2 += wpart[b];
     // fixed-shape tree: deterministic
@@ -841,14 +921,15 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
 #pragma unroll
         for (int w = 1; w < RED_SLICES; ++w) s += sl[w][q];
         if (off) s = add_rn(s, offv);
-        if (mode == R_POWER) s = s / s_div;
+        if (base == R_POWER) s = s / s_div;
+        if (save) save[i] = out[i];
         out[i] = s;
         sq += s * s;
       }
     }
     __syncthreads();
   }
-  if (mode == R_PLAIN) return;
+  if (base == R_PLAIN) return;
   const double tot = block_sum_rt(sq, sh);
   if (threadIdx.x == 0) {
     bpart[blockIdx.x] = tot;
@@ -862,7 +943,7 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
   // last block: warp 0 folds the block partials (lane-strided + fixed tree)
   double total = 0.0, gdot = 0.0, gscale = 0.0;
   for (int b = lane; b < (int)gridDim.x; b += 32) total += __ldcg(&bpart[b]);
-  if (mode == R_APG && wpart)
+  if (base == R_APG && wpart)
     for (int b = lane; b < Gw; b += 32) {
       gdot += __ldcg(&wpart[2 * b]);
       gscale += __ldcg(&wpart[2 * b + 1]);
@@ -871,7 +952,7 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
   gdot = warp_sum<double>(gdot);
   gscale = warp_sum<double>(gscale);
   if (lane != 0) return;
-  finalize_objective<T>(sc, mode, 0.5 * total, mode == R_POWER ? s_div : 0.0, gdot, gscale);
+  finalize_objective<T>(sc, mode, 0.5 * total, base == R_POWER ? s_div : 0.0, gdot, gscale);
   sc->counters[counter] = 0u;
 }
 
@@ -882,11 +963,14 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
 // (duality.py:154), radius (screening.py:11-15), slack (driver.py:219)
 __device__ __forceinline__ void dual_finalize(DevScalars* sc, int which, double t1, double t2, double t3, double t4,
                                               double eps, double slack_scale, double alpha) {
-  DualOut* out = which ? &sc->cert : &sc->act;
+  // which: 0 reduced problem, 1 certificate (full problem), 2 reduced problem
+  // at the iterate before a speculative round-boundary step (its objective
+  // was kept in bak_P)
+  DualOut* out = (which == 1) ? &sc->cert : &sc->act;
   double dual = t1 - 0.5 * t2;
   dual -= t3;
   dual -= t4;
-  const double primal = which ? sc->cert_P : sc->P;
+  const double primal = (which == 1) ? sc->cert_P : (which == 2 ? sc->bak_P : sc->P);
   const double raw = primal - dual;
   if (raw < -1e-9) set_err(sc, DE_INTERNAL_CONSISTENCY);
   const double gap = fmax(raw, 0.0);
@@ -1002,13 +1086,22 @@ __global__ void k_dual_fin(const double* sums, DevScalars* sc, int which, double
 // sphere test + compaction (warp ballot + block prefix sums)
 // flags: 0 keep, 1 lower, 2 upper
 // ----------------------------------------------------------------------------
+// Speculative round boundary: with sx0 != NULL the iterate
+// has already taken the next round's first step; a screened coordinate is
+// "dirty" when any of the iterates the step touched -- sx0 (after), sx1
+// (the round's final x), sx2 (FISTA: the one before) -- is off the bound it
+// is screened at.  Any dirty column means the step used a residual the
+// screening changes: the host undoes it (k_spec_undo) and takes it again.
 template <typename T>
 __global__ void __launch_bounds__(RT) k_sphere(const T* __restrict__ v, const T* __restrict__ nrm,
-                                               const T* __restrict__ hi, int64_t k, const DevScalars* sc,
-                                               uint8_t* __restrict__ flags, int32_t* __restrict__ bcnt) {
-  __shared__ int32_t wc[RT / 32][3];
+                                               const T* __restrict__ lo, const T* __restrict__ hi, int64_t k,
+                                               const DevScalars* sc, uint8_t* __restrict__ flags,
+                                               int32_t* __restrict__ bcnt, const double* __restrict__ sx0,
+                                               const double* __restrict__ sx1, const double* __restrict__ sx2) {
+  __shared__ int32_t wc[RT / 32][4];
   const int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x;
   int f = -1;
+  bool dirty = false;
   if (j < k) {
     const double thr = sc->act.thr * static_cast<double>(nrm[j]);
     const double vj = static_cast<double>(v[j]);
@@ -1018,43 +1111,50 @@ __global__ void __launch_bounds__(RT) k_sphere(const T* __restrict__ v, const T*
     else if (vj > thr && !isinf(static_cast<double>(hi[j])))
       f = 2;
     flags[j] = static_cast<uint8_t>(f);
+    if (f > 0 && sx0) {
+      const double bnd = static_cast<double>(f == 1 ? lo[j] : hi[j]);
+      dirty = sx0[j] != bnd || sx1[j] != bnd || (sx2 && sx2[j] != bnd);
+    }
   }
   const unsigned bk = __ballot_sync(0xffffffffu, f == 0);
   const unsigned bl = __ballot_sync(0xffffffffu, f == 1);
   const unsigned bu = __ballot_sync(0xffffffffu, f == 2);
+  const unsigned bd = __ballot_sync(0xffffffffu, dirty);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) {
     wc[warp][0] = __popc(bk);
     wc[warp][1] = __popc(bl);
     wc[warp][2] = __popc(bu);
+    wc[warp][3] = __popc(bd);
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
+  if (threadIdx.x < 4) {
     int s = 0;
     for (int w = 0; w < RT / 32; ++w) s += wc[w][threadIdx.x];
-    bcnt[3 * blockIdx.x + threadIdx.x] = s;
+    bcnt[4 * blockIdx.x + threadIdx.x] = s;
   }
 }
 
-// single block: exclusive scan of the per-block (keep, lower, upper) counts
-// in place; totals to sc->n_keep / n_lo / n_up
+// single block: exclusive scan of the per-block (keep, lower, upper, dirty)
+// counts in place; totals to sc->n_keep / n_lo / n_up / n_dirty
 __global__ void __launch_bounds__(1024) k_scan(int32_t* bcnt, int nb, DevScalars* sc) {
-  __shared__ int64_t wsum[32][3];
-  __shared__ int64_t carry[3];
+  __shared__ int64_t wsum[32][4];
+  __shared__ int64_t carry[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < 3) carry[threadIdx.x] = 0;
+  if (threadIdx.x < 4) carry[threadIdx.x] = 0;
   __syncthreads();
   for (int base = 0; base < nb; base += 1024) {
     const int i = base + threadIdx.x;
-    int64_t c[3] = {0, 0, 0};
+    int64_t c[4] = {0, 0, 0, 0};
     if (i < nb) {
-      c[0] = bcnt[3 * i + 0];
-      c[1] = bcnt[3 * i + 1];
-      c[2] = bcnt[3 * i + 2];
+      c[0] = bcnt[4 * i + 0];
+      c[1] = bcnt[4 * i + 1];
+      c[2] = bcnt[4 * i + 2];
+      c[3] = bcnt[4 * i + 3];
     }
-    int64_t inc[3] = {c[0], c[1], c[2]};
+    int64_t inc[4] = {c[0], c[1], c[2], c[3]};
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 4; ++q) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int64_t nb_ = __shfl_up_sync(0xffffffffu, inc[q], o);
@@ -1065,7 +1165,7 @@ __global__ void __launch_bounds__(1024) k_scan(int32_t* bcnt, int nb, DevScalars
     __syncthreads();
     if (warp == 0) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
+      for (int q = 0; q < 4; ++q) {
         int64_t w = wsum[lane][q];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1078,19 +1178,20 @@ __global__ void __launch_bounds__(1024) k_scan(int32_t* bcnt, int nb, DevScalars
     __syncthreads();
     if (i < nb) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
+      for (int q = 0; q < 4; ++q) {
         const int64_t wex = warp ? wsum[warp - 1][q] : 0;
-        bcnt[3 * i + q] = static_cast<int32_t>(carry[q] + wex + inc[q] - c[q]);
+        bcnt[4 * i + q] = static_cast<int32_t>(carry[q] + wex + inc[q] - c[q]);
       }
     }
     __syncthreads();
-    if (threadIdx.x < 3) carry[threadIdx.x] += wsum[31][threadIdx.x];
+    if (threadIdx.x < 4) carry[threadIdx.x] += wsum[31][threadIdx.x];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     sc->n_keep = sc->g_keep = carry[0];
     sc->n_lo = sc->g_lo = carry[1];
     sc->n_up = sc->g_up = carry[2];
+    sc->n_dirty = sc->g_dirty = carry[3];
   }
 }
 
@@ -1102,6 +1203,7 @@ struct ColState {
   int32_t* idx;
   T* x;
   T* xprev;
+  T* gprev;  // FISTA gradient at x_prev (NULL: not carried)
   T* lo;
   T* hi;
   T* nrm;
@@ -1138,13 +1240,14 @@ __global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flag
   }
   __syncthreads();
   if (f > 2) return;
-  const int64_t pos = (int64_t)boff[3 * blockIdx.x + f] + woff[warp][f] + __popc(bq[f] & lt);
+  const int64_t pos = (int64_t)boff[4 * blockIdx.x + f] + woff[warp][f] + __popc(bq[f] & lt);
   const int32_t id = src.idx[j];
   if (f == 0) {
     dst.idx[pos] = id;
     if (dst.pos) dst.pos[pos] = src.pos ? src.pos[j] : static_cast<int32_t>(j);
     dst.x[pos] = src.x[j];
     if (src.xprev) dst.xprev[pos] = src.xprev[j];
+    if (src.gprev) dst.gprev[pos] = src.gprev[j];
     dst.lo[pos] = src.lo[j];
     dst.hi[pos] = src.hi[j];
     dst.nrm[pos] = src.nrm[j];
@@ -1273,12 +1376,18 @@ __global__ void k_bounds_probe(int64_t n, const T* __restrict__ lo, const T* __r
 // has been accumulated over all row blocks, the per-column update of the mode
 // (the same arithmetic as k_pass's epilogue) and its block scalar partials.
 // Writes coef (the axpy coefficients of the following A x blocks).
+// FISTA: g holds g_k (the dot at r_k); the extrapolated gradient is formed by
+// linearity from gprev (g_{k-1}), which is then replaced by g_k.  spec: the
+// speculative round-boundary step (x_k -> xprev / x_{k-1}, g_{k-1} -> xbak,
+// gbak for an undo; epsilon partial of g_k -> epart).
 __global__ void __launch_bounds__(RT) k_colupdate(int upd, int64_t k, double* __restrict__ x, double* __restrict__ xprev,
                                                   const double* __restrict__ lo, const double* __restrict__ hi,
                                                   const double* __restrict__ g, const double* __restrict__ att,
                                                   const double* __restrict__ nrm, double* __restrict__ coef,
-                                                  double* __restrict__ bpart, int has_inf, const DevScalars* sc) {
-  __shared__ double sh[RT / 32][2];
+                                                  double* __restrict__ bpart, int has_inf, const DevScalars* sc,
+                                                  double* __restrict__ gprev, int spec, double* __restrict__ xbak,
+                                                  double* __restrict__ gbak, double* __restrict__ epart) {
+  __shared__ double sh[RT / 32][3];
   const double eta = sc->eta;
   double beta = 0.0;
   if (upd == U_APG) {
@@ -1286,29 +1395,40 @@ __global__ void __launch_bounds__(RT) k_colupdate(int upd, int64_t k, double* __
     const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
     beta = (t - 1.0) / tn;
   }
-  double r1 = 0.0, r2 = 0.0;
+  double r1 = 0.0, r2 = 0.0, r3 = 0.0;
   for (int64_t p = (int64_t)blockIdx.x * RT + threadIdx.x; p < k; p += (int64_t)gridDim.x * RT) {
     const double gj = g[p];
+    if (spec && has_inf && isinf(hi[p])) r3 = fmax(r3, fmax(-gj, 0.0) / fabs(att[p]));
     switch (upd) {
       case U_DOT:
         if (has_inf && isinf(hi[p])) r1 = fmax(r1, fmax(-gj, 0.0) / fabs(att[p]));
         break;
       case U_PG:
       case U_PG_G: {
-        const double xn = clip<double>(sub_rn(x[p], mul_rn(eta, gj)), lo[p], hi[p]);
+        const double xo = x[p];
+        const double xn = clip<double>(sub_rn(xo, mul_rn(eta, gj)), lo[p], hi[p]);
+        if (spec) xprev[p] = xo;
         x[p] = xn;
         coef[p] = xn;
       } break;
       case U_APG: {
-        const double xo = x[p], xp = xprev[p];
-        double yv = xo;
-        if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
-        const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), lo[p], hi[p]);
+        const double xo = x[p], xp = xprev[p], gp = gprev[p];
+        double yv = xo, gy = gj;
+        if (beta != 0.0) {
+          yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
+          gy = add_rn(gj, mul_rn(beta, sub_rn(gj, gp)));
+        }
+        const double xn = clip<double>(sub_rn(yv, mul_rn(eta, gy)), lo[p], hi[p]);
+        if (spec) {
+          xbak[p] = xp;
+          gbak[p] = gp;
+        }
         xprev[p] = xo;
+        gprev[p] = gj;
         x[p] = xn;
         coef[p] = xn;
         const double dx = xn - xo;
-        r1 += gj * dx;
+        r1 += gy * dx;
         r2 += nrm[p] * fabs(dx);
       } break;
       case U_POWER:
@@ -1327,23 +1447,56 @@ __global__ void __launch_bounds__(RT) k_colupdate(int upd, int64_t k, double* __
     r1 = warp_sum<double>(r1);
     r2 = warp_sum<double>(r2);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r3 = fmax(r3, __shfl_xor_sync(0xffffffffu, r3, o));
   if (lane == 0) {
     sh[warp][0] = r1;
     sh[warp][1] = r2;
+    sh[warp][2] = r3;
   }
   __syncthreads();
-  if (threadIdx.x == 0 && bpart) {
-    double v1 = sh[0][0], v2 = sh[0][1];
+  if (threadIdx.x == 0) {
+    double v1 = sh[0][0], v2 = sh[0][1], v3 = sh[0][2];
     for (int w = 1; w < RT / 32; ++w) {
       v1 = (upd == U_DOT) ? fmax(v1, sh[w][0]) : v1 + sh[w][0];
       v2 += sh[w][1];
+      v3 = fmax(v3, sh[w][2]);
     }
-    if (upd == U_APG) {
-      bpart[2 * blockIdx.x] = v1;
-      bpart[2 * blockIdx.x + 1] = v2;
-    } else {
-      bpart[blockIdx.x] = v1;
+    if (bpart) {
+      if (upd == U_APG) {
+        bpart[2 * blockIdx.x] = v1;
+        bpart[2 * blockIdx.x + 1] = v2;
+      } else {
+        bpart[blockIdx.x] = v1;
+      }
     }
+    if (spec && epart) epart[blockIdx.x] = v3;
+  }
+}
+
+// Undo of the speculative round-boundary step (the round's screening event
+// changed the problem the step was taken on, or the step size changes):
+// x <- x_k, and for FISTA x_prev <- x_{k-1}, g_prev <- g_{k-1}; the residual
+// r_k (saved by the step's reduce) and the scalars before the step.
+__global__ void k_spec_undo(int64_t k, int apg, double* __restrict__ x, double* __restrict__ xprev,
+                            const double* __restrict__ xbak, double* __restrict__ gprev,
+                            const double* __restrict__ gbak, int64_t m, double* __restrict__ r,
+                            const double* __restrict__ rbak, DevScalars* sc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t p = i0; p < k; p += stride) {
+    x[p] = xprev[p];
+    if (apg) {
+      xprev[p] = xbak[p];
+      gprev[p] = gbak[p];
+    }
+  }
+  for (int64_t i = i0; i < m; i += stride) r[i] = rbak[i];
+  if (i0 == 0) {
+    sc->P = sc->bak_P;
+    sc->mom_t = sc->bak_mom_t;
+    sc->restarts = sc->bak_restarts;
+    sc->err_spec = 0;
   }
 }
 

@@ -34,6 +34,7 @@ struct SmallArgs {
   int m;
   double* x;
   double* xprev;
+  double* gprev;   // FISTA: gradient at x_prev
   const double* lo;
   const double* hi;
   const double* nrm;
@@ -117,8 +118,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   double* chi = clo + SM_CMAX;
   double* cnr = chi + SM_CMAX;
   double* cat = cnr + SM_CMAX;
-  double* cg = cat + SM_CMAX;
-  double* coff = cg + SM_CMAX;         // [SM_NT] z - y of the rows this CTA reduces
+  double* cg = cat + SM_CMAX;          // gradient at the current x (when gv)
+  double* cgp = cg + SM_CMAX;          // FISTA: gradient at x_prev
+  double* coff = cgp + SM_CMAX;        // [SM_NT] z - y of the rows this CTA reduces
   double* rv = coff + SM_NT;           // [m, padded] the dot vector of this step
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = a.m;
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     cnr[tid] = a.nrm[p];
     cat[tid] = a.att[p];
     cg[tid] = a.g[p];
+    cgp[tid] = a.kind == 2 ? a.gprev[p] : 0.0;
   }
   __syncthreads();
 
@@ -209,32 +212,39 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
 
   int done_rounds = 0, event = 0;
   bool perr = false;
-  // this thread's rows (tid + q * SM_NT) of the current and the previous
-  // residual, loaded right after the barrier that completes them -- in the
-  // same L2 round trip as the objective fold instead of one after it
+  // this thread's rows (tid + q * SM_NT) of the current residual, loaded
+  // right after the barrier that completes them -- in the same L2 round trip
+  // as the objective fold instead of one after it
   constexpr int PR = R * V;
-  double pr[PR], pp[PR];
+  double pr[PR];
   bool have_pre = false;
   for (int rnd = 0; rnd < a.max_rounds; ++rnd) {
   for (int pass = 0; pass < a.passes; ++pass) {
     const double* rcur = a.r[rc];
-    const double* rprv = a.r[rc ^ 1];
     const double tn = (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom)) / 2.0;
     const double beta = (a.kind == 2) ? (t_mom - 1.0) / tn : 0.0;
-    const bool use_stored = (a.kind == 0 && gv && pass == 0);
+    // the gradient at x is known (the previous round's screening dot): the
+    // round's first step needs no dot
+    const bool use_stored = (gv && pass == 0);
     // column update (PG / FISTA), done by the lane that holds the column's
-    // dot -- no CTA barrier between the dots and the updates
+    // dot -- no CTA barrier between the dots and the updates.  FISTA forms
+    // the extrapolated gradient by linearity:
+    // g_y = g_k + beta (g_k - g_{k-1})
     auto update_col = [&](int c, double gj) {
       const double xo = cx[c];
       double xn;
       if (a.kind == 2) {
         const double xp = cxp[c];
-        double yv = xo;
-        if (beta != 0.0) yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
-        xn = clip<double>(sub_rn(yv, mul_rn(eta, gj)), clo[c], chi[c]);
+        double yv = xo, gy = gj;
+        if (beta != 0.0) {
+          yv = add_rn(xo, mul_rn(beta, sub_rn(xo, xp)));
+          gy = add_rn(gj, mul_rn(beta, sub_rn(gj, cgp[c])));
+        }
+        xn = clip<double>(sub_rn(yv, mul_rn(eta, gy)), clo[c], chi[c]);
         cxp[c] = xo;
+        cgp[c] = gj;
         const double dx = xn - xo;
-        rsx[c] = gj * dx;                  // restart partials of this CTA
+        rsx[c] = gy * dx;                  // restart partials of this CTA
         rsx[SM_NT + c] = cnr[c] * fabs(dx);
       } else {
         cg[c] = gj;
@@ -244,24 +254,16 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       cf[c] = xn;
     };
     if (!use_stored) {
-      // residual (or the extrapolated residual) -> shared memory; written by
-      // other CTAs before the barrier: read through L2
+      // residual -> shared memory; written by other CTAs before the barrier:
+      // read through L2
       if (have_pre) {
 #pragma unroll
         for (int q = 0; q < PR; ++q) {
           const int row = tid + q * SM_NT;
-          if (row < m) {
-            double v = pr[q];
-            if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, pp[q])));
-            rv[row] = v;
-          }
+          if (row < m) rv[row] = pr[q];
         }
       } else {
-        for (int row = tid; row < m; row += SM_NT) {
-          double v = __ldcg(&rcur[row]);
-          if (beta != 0.0) v = add_rn(v, mul_rn(beta, sub_rn(v, __ldcg(&rprv[row]))));
-          rv[row] = v;
-        }
+        for (int row = tid; row < m; row += SM_NT) rv[row] = __ldcg(&rcur[row]);
       }
       __syncthreads();
       for (int c = warp; c < ncol; c += NW) {
@@ -345,15 +347,12 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.bpart[4 * b + 0] = s;
     }
     grid_barrier(a.bar, nbar);
-    // the next step's residual rows: r just completed (r[rc ^ 1]) and the
-    // previous one (r[rc]), issued before the fold below
+    // the next step's residual rows (r just completed, r[rc ^ 1]), issued
+    // before the fold below
 #pragma unroll
     for (int q = 0; q < PR; ++q) {
       const int row = tid + q * SM_NT;
-      if (row < m) {
-        pr[q] = __ldcg(&a.r[rc ^ 1][row]);
-        pp[q] = (a.kind == 2) ? __ldcg(&a.r[rc][row]) : 0.0;
-      }
+      if (row < m) pr[q] = __ldcg(&a.r[rc ^ 1][row]);
     }
     have_pre = true;
     // every CTA folds the same values in the same order -> same decision
@@ -540,14 +539,17 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     tr[6] = (double)a.sc->restarts;
   }
   ++done_rounds;
-  gv = (a.kind == 0) ? 1 : 0;  // PG: the next round starts from this round's gradient
+  gv = 1;  // the next round starts from this round's screening gradient
   __syncthreads();
   }  // rounds
   // write back the resident per-column state
   if (tid < ncol) {
     const int64_t p = p0 + tid;
     a.x[p] = cx[tid];
-    if (a.kind == 2) a.xprev[p] = cxp[tid];
+    if (a.kind == 2) {
+      a.xprev[p] = cxp[tid];
+      a.gprev[p] = cgp[tid];
+    }
     a.g[p] = cg[tid];
   }
   if (b == 0 && tid == 0) {

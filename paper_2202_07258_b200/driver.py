@@ -207,6 +207,7 @@ class _Session:
         c.slack_scale = slack_scale
         rel = cfg.relative_gap
         c.relative_gap = int(self.dtype_code == nat.BX_F32 if rel is None else bool(rel))
+        c.restart = nat.RESTARTS[cfg.restart]
         cap = min(cfg.max_rounds or 1_000_000, 250_000)
         trace = np.empty(cap, dtype=TRACE_DTYPE)
         out = nat.SolveOut()
@@ -254,7 +255,8 @@ def _result(p_n, out, tr, x, theta, sl, su, prof, return_device, n_total=None):
                          float(r["gap"]), int(r["preserved_count"]), (n - int(r["preserved_count"])) / n,
                          int(r["newly_screened_lower"]), int(r["newly_screened_upper"])) for r in tr]
     info = dict(iterations=int(out.iterations), step=float(out.step), sigma=float(out.sigma),
-                kernel_launches=int(out.kernel_launches), restarts=int(out.restarts), trace_arrays=tr, profile=prof)
+                kernel_launches=int(out.kernel_launches), restarts=int(out.restarts), trace_arrays=tr, profile=prof,
+                spec_kept=int(out.spec_kept), spec_undone=int(out.spec_undone))
     if return_device:
         xo, tho = x, theta
     else:

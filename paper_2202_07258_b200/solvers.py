@@ -28,12 +28,19 @@ class SolverConfig:
     # reference's absolute rule for fp64, the relative rule for fp32 storage
     # (an absolute 1e-6 is below fp32 resolution when P* >> 1)
     relative_gap: bool | None = None
+    # FISTA ("apg") restart rule: "adaptive" restarts on an objective increase
+    # or on the O'Donoghue-Candes gradient test (the default);
+    # "function" restarts on an objective increase only -- BASELINE config 3's
+    # stated rule (the objective-rise test of solvers.py:111-114)
+    restart: str = "adaptive"
 
     def __post_init__(self):
         if self.kind not in _SOLVER_KINDS:
             raise ValueError(f"unknown solver kind {self.kind!r}")
         if self.gap_tol <= 0:
             raise ValueError("gap_tol must be positive")
+        if self.restart not in ("adaptive", "function"):
+            raise ValueError(f"unknown restart rule {self.restart!r}")
         if self.inner_passes < 1:
             raise ValueError("inner_passes must be >= 1")
 

@@ -27,7 +27,8 @@ def sharded_rounds(a, y, lo, hi, col_offset, n_global, kind, eta, rounds, passes
         return allreduce(a[:, kp] @ xk, "sum") + (z - y)
 
     r = resid(x[keep], keep)
-    x_prev, r_prev, mom = x.copy(), r.copy(), 1.0
+    g_cur = a[:, keep].T @ r            # this rank's columns of A'r (r is replicated)
+    x_prev, g_prev, mom = x.copy(), g_cur.copy(), 1.0
     out = []
     for _ in range(rounds):
         xa = x[keep]
@@ -43,8 +44,7 @@ def sharded_rounds(a, y, lo, hi, col_offset, n_global, kind, eta, rounds, passes
                 beta = (mom - 1.0) / tn
                 xp = x_prev[keep]
                 yv = xa + beta * (xa - xp) if beta != 0.0 else xa
-                ry = r + beta * (r - r_prev) if beta != 0.0 else r
-                gy = a[:, keep].T @ ry
+                gy = g_cur + beta * (g_cur - g_prev) if beta != 0.0 else g_cur
                 xn = np.clip(yv - eta * gy, lo[keep], hi[keep])
                 rn = resid(xn, keep)
                 nobj = 0.5 * float(rn @ rn)
@@ -53,9 +53,10 @@ def sharded_rounds(a, y, lo, hi, col_offset, n_global, kind, eta, rounds, passes
                 s_f = 1e-12 * max(1.0, abs(obj))
                 s_g = 1e-12 * math.sqrt(2.0 * obj) * gd[1]
                 x_prev[keep] = xa
-                r_prev = r
+                g_prev = g_cur
                 mom = 1.0 if (nobj > obj + s_f or gd[0] > s_g) else tn
                 xa, r, obj = xn, rn, nobj
+                g_cur = a[:, keep].T @ r
         x[keep] = xa
         g = a[:, keep].T @ r
         v = -g
@@ -87,7 +88,8 @@ def sharded_rounds(a, y, lo, hi, col_offset, n_global, kind, eta, rounds, passes
             x_prev[gone] = x[gone]
             keep = keep[~np.isin(keep, gone)]
             r = resid(x[keep], keep)
-            r_prev = resid(x_prev[keep], keep)
+            g_cur = a[:, keep].T @ r
+            g_prev = a[:, keep].T @ resid(x_prev[keep], keep)
         kg = allreduce(np.array([float(keep.size)]), "sum")[0]
         out.append(dict(primal=primal, dual=dual, gap=gap, preserved=int(kg)))
     return out, x

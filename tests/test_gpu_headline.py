@@ -1,0 +1,132 @@
+"""Round-by-round oracle parity for the headline path at its own shapes.
+
+The fused streamed pass is instantiated per row-chunk count R (rows per
+thread = R 16-byte vectors, csrc/bx_core.cu pick_R); BASELINE config 3
+(m = 10,000) runs the R = 10 fp64 instantiation and config 4 (m = 20,000
+fp32) the R = 10 fp32 one.  These tests compare every round of those
+instantiations -- and of every R in 6..12 -- with the CPU oracle
+(oracle/boxscreen_oracle.py, pinned to the reference): primal, dual and gap
+within 1e-10 * max(|P|, |D|) and identical preserved counts every round
+(reference round loop: /root/reference/pkg/src/boxscreen/driver.py:168-241).
+
+* R sweep, fp64, two families per m: the config-3 recipe (no screening event
+  in the first rounds: pure streaming) and a BVLS saturation family whose
+  coordinates leave the preserved set over several rounds (compaction,
+  incremental refresh and the speculative round-boundary pass at that R).
+* R sweep, fp32 storage, against the fp64 oracle on the same rounded matrix:
+  per-round objective within 1e-4 relative (north_star's fp32 tolerance).
+* config 3 itself (10000 x 50000, 4 GB): the first 60 rounds against
+  ``oracle_solve(max_rounds=60)``.
+"""
+
+import numpy as np
+import pytest
+
+from oracle.boxscreen_oracle import oracle_solve
+from parity import compare_final, compare_traces
+
+pytestmark = pytest.mark.gpu
+
+# m -> R of the fp64 pass (R = ceil(m / 1024)); ragged and exact multiples
+FP64_M = {6: 5121, 7: 6145, 8: 7169, 9: 8193, 10: 10000, 11: 11264, 12: 12288}
+# fp32 moves 4 rows per 16-byte vector: R = ceil(m / 2048)
+FP32_M = {7: 12289, 9: 16385, 10: 20000, 12: 24576}
+
+
+def saturating_bvls(m, n, seed):
+    """Gaussian unit columns, box [-1, 1], planted solution 40% at +-1.3 (so
+    its coordinates saturate and are screened over several rounds)."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    a /= np.linalg.norm(a, axis=0)
+    xt = rng.choice([-1.3, 1.3, 0.0], size=n, p=[0.4, 0.4, 0.2])
+    mid = xt == 0.0
+    xt[mid] = rng.uniform(-0.5, 0.5, int(mid.sum()))
+    y = a @ xt + 0.01 * rng.standard_normal(m)
+    return np.asfortranarray(a), y, -np.ones(n), np.ones(n)
+
+
+def _solve(a, y, lo, hi, kind, passes, tol, rounds, dtype=np.float64, restart="adaptive"):
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    p = Problem(a, y, lo, hi, dtype=dtype)
+    return solve(p, SolverConfig(kind=kind, inner_passes=passes, gap_tol=tol, max_rounds=rounds,
+                                 restart=restart))
+
+
+@pytest.mark.parametrize("R", sorted(FP64_M))
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+def test_fp64_rsweep_config3_recipe(R, kind, monkeypatch):
+    from paper_2202_07258_b200.generate import make_config
+    monkeypatch.setenv("BX_NO_SMALL", "1")
+    inst = make_config(3, m=FP64_M[R], n=1500)
+    g = _solve(inst.a, inst.y, inst.lower, inst.upper, kind, 10, 1e-6, 40)
+    o = oracle_solve(inst.a, inst.y, inst.lower, inst.upper, kind=kind, inner_passes=10, gap_tol=1e-6,
+                     max_rounds=40)
+    probs = compare_traces(g, o)
+    assert not probs, (R, probs[:3])
+    assert len(g.trace) == 40
+
+
+@pytest.mark.parametrize("R", sorted(FP64_M))
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+def test_fp64_rsweep_screening_events(R, kind, monkeypatch):
+    monkeypatch.setenv("BX_NO_SMALL", "1")
+    a, y, lo, hi = saturating_bvls(FP64_M[R], 1500, seed=R)
+    g = _solve(a, y, lo, hi, kind, 3, 1e-11, 200)
+    o = oracle_solve(a, y, lo, hi, kind=kind, inner_passes=3, gap_tol=1e-11, max_rounds=200)
+    assert sum(r["new_lower"] + r["new_upper"] > 0 for r in o["trace"]) >= 2  # several events
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, (R, probs[:3])
+
+
+@pytest.mark.parametrize("R", sorted(FP32_M))
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+def test_fp32_rsweep_tracks_fp64_oracle(R, kind):
+    from paper_2202_07258_b200.generate import make_config
+    inst = make_config(4, m=FP32_M[R], n=1500)
+    assert inst.a.dtype == np.float32
+    rounds = 30
+    g = _solve(inst.a, inst.y, inst.lower, inst.upper, kind, 10, 1e-6, rounds, dtype=np.float32)
+    a64 = np.asfortranarray(inst.a.astype(np.float64))  # the same rounded matrix
+    o = oracle_solve(a64, inst.y, inst.lower, inst.upper, kind=kind, inner_passes=10, gap_tol=1e-300,
+                     max_rounds=rounds)
+    assert len(g.trace) == rounds == len(o["trace"])
+    p32 = np.array([t.primal for t in g.trace])
+    p64 = np.array([t["primal"] for t in o["trace"]])
+    assert np.all(np.abs(p32 - p64) <= 1e-4 * np.abs(p64)), (R, np.max(np.abs(p32 - p64) / np.abs(p64)))
+
+
+def test_config3_first_60_rounds():
+    """BASELINE config 3 at its full size (R = 10 fp64 pass): the first 60
+    rounds (600 FISTA steps + 60 dual points) against the oracle."""
+    from paper_2202_07258_b200.generate import make_config
+    inst = make_config(3)
+    assert inst.a.shape == (10000, 50000)
+    g = _solve(inst.a, inst.y, inst.lower, inst.upper, "apg", 10, 1e-6, 60)
+    o = oracle_solve(inst.a, inst.y, inst.lower, inst.upper, kind="apg", inner_passes=10, gap_tol=1e-6,
+                     max_rounds=60)
+    probs = compare_traces(g, o)
+    assert not probs, probs[:3]
+    assert len(g.trace) == 60
+
+
+@pytest.mark.parametrize("path", ["resident", "streamed"])
+def test_function_restart_rule_matches_oracle(path, monkeypatch):
+    """BASELINE config 3's stated FISTA rule -- restart on an objective
+    increase only (SolverConfig(restart="function")) -- round by round on the
+    config-3 recipe at an oracle-friendly size, both device paths."""
+    from paper_2202_07258_b200.generate import make_config
+    if path == "streamed":
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+    else:
+        monkeypatch.delenv("BX_NO_SMALL", raising=False)
+    inst = make_config(3, m=500, n=2500)
+    g = _solve(inst.a, inst.y, inst.lower, inst.upper, "apg", 10, 1e-6, 400, restart="function")
+    o = oracle_solve(inst.a, inst.y, inst.lower, inst.upper, kind="apg", inner_passes=10, gap_tol=1e-6,
+                     max_rounds=400, restart="function")
+    probs = compare_traces(g, o) + (compare_final(g, o) if o["converged"] else [])
+    assert not probs, probs[:3]
+    adaptive = oracle_solve(inst.a, inst.y, inst.lower, inst.upper, kind="apg", inner_passes=10,
+                            gap_tol=1e-6, max_rounds=400)
+    # the two rules are different iterations (the gradient test fires)
+    assert [t["primal"] for t in adaptive["trace"][:50]] != [t["primal"] for t in o["trace"][:50]]
