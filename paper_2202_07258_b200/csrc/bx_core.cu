@@ -300,7 +300,9 @@ struct bx_ctx {
   void *g = nullptr, *v = nullptr, *coef = nullptr;
   // speculative round boundary: the round's screening gradient
   // comes from the next round's first step, which keeps what an undo needs
-  void *xbak = nullptr, *gbak = nullptr, *rbak = nullptr;
+  // (x_{k-1}, g_{k-1} ping-pong with compaction: a step that stands through a
+  // screening event can still be dropped at the end of the solve)
+  void *xbak[2] = {}, *gbak[2] = {}, *rbak = nullptr;
   double* epart = nullptr;   // epsilon partials of the speculative step
   bool spec_on = true;       // env BX_SPEC=0 disables (a separate dot pass per round)
   bool spec_pending = false; // the current x has taken the next round's first step
@@ -525,8 +527,10 @@ void carve(bx_ctx* c, Carver& w) {
     c->att[s] = w.take(n * e);
     c->gprev[s] = w.take(n * e);
   }
-  c->xbak = w.take(n * e);
-  c->gbak = w.take(n * e);
+  for (int s = 0; s < 2; ++s) {
+    c->xbak[s] = w.take(n * e);
+    c->gbak[s] = w.take(n * e);
+  }
   c->rbak = w.take(mp * e);
   c->epart = (double*)w.take(4 * c->Gmax * 8);
   c->g = w.take(n * e);
@@ -1257,7 +1261,7 @@ bool spec_applies(bx_ctx* c, int kind, int passes);
 struct GraphKey {
   int64_t k, kphys;
   const void *r, *rprev, *x, *g;
-  int cur, kind, passes, screening, g_valid, dense, act_is_orig, spec_pending, dot_spec;
+  int cur, kind, passes, screening, g_valid, dense, act_is_orig, spec_pending;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
 static GraphKey graph_key(const bx_ctx* c, int kind, int passes, int screening) {
@@ -1277,7 +1281,6 @@ static GraphKey graph_key(const bx_ctx* c, int kind, int passes, int screening) 
   k.dense = c->dense ? 1 : 0;
   k.act_is_orig = c->act_is_orig ? 1 : 0;
   k.spec_pending = c->spec_pending ? 1 : 0;
-  k.dot_spec = c->dot_spec ? 1 : 0;
   return k;
 }
 
@@ -1500,7 +1503,10 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
   *event = hd[1];
   // the event round's g / eps partials are in place (with spec: the round
   // ended with its speculative step, as the capture left the host state)
-  if (hd[1]) c->dot_done = true;
+  if (hd[1]) {
+    c->dot_done = true;
+    c->dot_spec = spec;
+  }
   return BX_OK;
 }
 
@@ -1515,8 +1521,8 @@ int step_pass(bx_ctx* c, int kind, bool spec) {
   int G = 1;
   StepExtra ex;
   ex.spec = spec ? 1 : 0;
-  ex.xbak = (double*)c->xbak;
-  ex.gbak = (double*)c->gbak;
+  ex.xbak = (double*)c->xbak[s];
+  ex.gbak = (double*)c->gbak[s];
   ex.epart = c->epart;
   const int sm = spec ? R_SPEC : 0;
   double* save = spec ? (double*)c->rbak : nullptr;
@@ -1591,8 +1597,8 @@ int spec_undo(bx_ctx* c, int kind) {
   const int s = c->cur;
   const int64_t n = c->k > c->m ? c->k : c->m;
   k_spec_undo<<<grid1d(c, n), RT, 0, c->stream>>>(c->k, kind == BX_APG ? 1 : 0, (double*)c->x[s],
-                                                  (double*)c->xprev[s], (const double*)c->xbak,
-                                                  (double*)c->gprev[s], (const double*)c->gbak, c->m,
+                                                  (double*)c->xprev[s], (const double*)c->xbak[s],
+                                                  (double*)c->gprev[s], (const double*)c->gbak[s], c->m,
                                                   (double*)c->r, (const double*)c->rbak, c->sc);
   LAUNCHED();
   c->spec_pending = false;
@@ -1754,8 +1760,8 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
                     (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s], nullptr, c->bpart, c->has_inf,
                     &G));
     c->dot_G = G;  // a later dual_screen on the same g (dot_done) reuses its eps partials
-    c->dot_spec = false;
   }
+  c->dot_spec = false;
   if (!spec) c->g_valid = true;  // (after a speculative step g is at x_prev, not x)
   const double* r = spec ? (const double*)c->rbak : (const double*)c->r;
   TRY(dual_point<T>(c, spec ? 2 : 0, r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g,
@@ -1770,7 +1776,7 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
                                             (const double*)c->hi[s], c->k, c->sc, c->flags, c->bcnt,
                                             spec ? (const double*)c->x[s] : nullptr,
                                             spec ? (const double*)c->xprev[s] : nullptr,
-                                            (spec && apg) ? (const double*)c->xbak : nullptr);
+                                            (spec && apg) ? (const double*)c->xbak[s] : nullptr);
     LAUNCHED();
     k_scan<<<1, 1024, 0, c->stream>>>(c->bcnt, nbs, c->sc);
     LAUNCHED();
@@ -1870,13 +1876,17 @@ int compact(bx_ctx* c, int64_t n_lo, int64_t n_up, int64_t n_keep, int kind, boo
   const int nbs = (int)((c->k + RT - 1) / RT);
   const int64_t nscr = n_lo + n_up;
   if (nscr > 0) {
-    const bool carry2 = kind == BX_APG || kind == BX_ACTIVE_SET;  // momentum state / passive mask
+    // momentum state / passive mask; a standing speculative step also keeps
+    // what dropping it at the end of the solve needs (x_k, x_{k-1}, g_{k-1})
+    const bool carry2 = kind == BX_APG || kind == BX_ACTIVE_SET || c->spec_pending;
+    const bool bak = c->spec_pending && kind == BX_APG;
     ColState<double> src{c->idx[s], (double*)c->x[s], carry2 ? (double*)c->xprev[s] : nullptr,
                          kind == BX_APG ? (double*)c->gprev[s] : nullptr,
+                         bak ? (double*)c->xbak[s] : nullptr, bak ? (double*)c->gbak[s] : nullptr,
                          (double*)c->lo[s], (double*)c->hi[s], (double*)c->nrm[s], (double*)c->att[s],
                          c->dense ? nullptr : c->pos[s]};
     ColState<double> dst{c->idx[d], (double*)c->x[d], (double*)c->xprev[d], (double*)c->gprev[d],
-                         (double*)c->lo[d], (double*)c->hi[d],
+                         (double*)c->xbak[d], (double*)c->gbak[d], (double*)c->lo[d], (double*)c->hi[d],
                          (double*)c->nrm[d], (double*)c->att[d], c->act_is_orig ? nullptr : c->pos[d]};
     k_compact<double><<<nbs, RT, 0, c->stream>>>(c->flags, c->bcnt, c->k, src, dst, (double*)c->xfull, c->scr_idx,
                                                  (double*)c->scr_val, n_lo, c->sat_lo + c->n_sat_lo,
@@ -2088,7 +2098,7 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   int64_t rounds = 0, iters = 0;
   bool converged = false;
   int64_t spec_kept = 0, spec_undone = 0, last_restarts = 0;
-  static const bool spec_force_undo = [] {
+  const bool spec_force_undo = [] {
     const char* e = getenv("BX_SPEC_FORCE_UNDO");  // test switch: every event takes the undo path
     return e && e[0] == '1';
   }();
@@ -2227,7 +2237,8 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
         // the speculative step stands only if screening leaves the problem it
         // was taken on unchanged (no screened coordinate off its bound on any
         // iterate the step touched) and the step size stays
-        const bool clean = c->spec_pending && !converged && c->hsc->g_dirty == 0 && !reestimate && !spec_force_undo;
+        const bool was_spec = c->spec_pending;
+        const bool clean = was_spec && !converged && c->hsc->g_dirty == 0 && !reestimate && !spec_force_undo;
         if (c->spec_pending && !clean) TRY(spec_undo<T>(c, kind));
         TRY(compact<T>(c, c->hsc->n_lo, c->hsc->n_up, c->hsc->n_keep, kind, z_update, clean));
         kg = kg_new;
@@ -2235,7 +2246,10 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
           TRY(auto_step<T>(c, cfg->power_iters, alpha, fn, user, &eta, &sigma));
           basis = kg;
         }
-        if (clean) ++spec_kept; else if (!converged) ++spec_undone;
+        if (clean)
+          ++spec_kept;
+        else if (was_spec && !converged)
+          ++spec_undone;
       }
     }
     if (trace && ntrace < cap) {

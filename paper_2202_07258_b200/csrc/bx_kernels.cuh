@@ -1204,6 +1204,8 @@ struct ColState {
   T* x;
   T* xprev;
   T* gprev;  // FISTA gradient at x_prev (NULL: not carried)
+  T* xbak;   // a standing speculative step's x_{k-1} / g_{k-1} (NULL: not carried)
+  T* gbak;
   T* lo;
   T* hi;
   T* nrm;
@@ -1248,6 +1250,8 @@ __global__ void __launch_bounds__(RT) k_compact(const uint8_t* __restrict__ flag
     dst.x[pos] = src.x[j];
     if (src.xprev) dst.xprev[pos] = src.xprev[j];
     if (src.gprev) dst.gprev[pos] = src.gprev[j];
+    if (src.xbak) dst.xbak[pos] = src.xbak[j];
+    if (src.gbak) dst.gbak[pos] = src.gbak[j];
     dst.lo[pos] = src.lo[j];
     dst.hi[pos] = src.hi[j];
     dst.nrm[pos] = src.nrm[j];

@@ -130,3 +130,55 @@ def test_function_restart_rule_matches_oracle(path, monkeypatch):
                             gap_tol=1e-6, max_rounds=400)
     # the two rules are different iterations (the gradient test fires)
     assert [t["primal"] for t in adaptive["trace"][:50]] != [t["primal"] for t in o["trace"][:50]]
+
+
+@pytest.fixture(params=["spec", "no_spec", "force_undo"])
+def spec_mode(request, monkeypatch):
+    """The round boundary's three schedules: the speculative step
+    (default), a dot-only screening pass per round (BX_SPEC=0), and every
+    screening event undoing the speculative step (BX_SPEC_FORCE_UNDO=1)."""
+    monkeypatch.delenv("BX_SPEC", raising=False)
+    monkeypatch.delenv("BX_SPEC_FORCE_UNDO", raising=False)
+    if request.param == "no_spec":
+        monkeypatch.setenv("BX_SPEC", "0")
+    elif request.param == "force_undo":
+        monkeypatch.setenv("BX_SPEC_FORCE_UNDO", "1")
+    return request.param
+
+
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+def test_round_boundary_schedules_match_oracle(kind, spec_mode, monkeypatch):
+    """Every round-boundary schedule follows the oracle round by round
+    through screening events at both bounds (z updates with nonzero bounds),
+    and so does the final x; with the speculative step most events keep it."""
+    monkeypatch.setenv("BX_NO_SMALL", "1")
+    a, y, lo, hi = saturating_bvls(3000, 900, seed=5)
+    g = _solve(a, y, lo, hi, kind, 4, 1e-11, 300)
+    o = oracle_solve(a, y, lo, hi, kind=kind, inner_passes=4, gap_tol=1e-11, max_rounds=300)
+    probs = compare_traces(g, o) + compare_final(g, o)
+    assert not probs, probs[:3]
+    events = sum(r["new_lower"] + r["new_upper"] > 0 for r in o["trace"])
+    assert events >= 3
+    if spec_mode == "spec":
+        assert g.info["spec_kept"] >= 1
+    elif spec_mode == "force_undo":
+        assert g.info["spec_kept"] == 0 and g.info["spec_undone"] >= 1
+    else:
+        assert g.info["spec_kept"] == g.info["spec_undone"] == 0
+
+
+@pytest.mark.parametrize("kind", ["pg", "apg"])
+def test_speculative_step_dropped_at_round_limit(kind, monkeypatch):
+    """A solve that stops at max_rounds right after a screening event whose
+    speculative step stood: the returned x is the last round's iterate (the
+    step is dropped through the compaction that followed it)."""
+    monkeypatch.setenv("BX_NO_SMALL", "1")
+    a, y, lo, hi = saturating_bvls(2000, 700, seed=9)
+    full = oracle_solve(a, y, lo, hi, kind=kind, inner_passes=3, gap_tol=1e-11, max_rounds=60)
+    ev = [r["round"] for r in full["trace"] if r["new_lower"] + r["new_upper"] > 0]
+    assert len(ev) >= 2
+    for rounds in sorted(set(ev[:4] + [e + 1 for e in ev[:2]])):
+        g = _solve(a, y, lo, hi, kind, 3, 1e-11, rounds)
+        o = oracle_solve(a, y, lo, hi, kind=kind, inner_passes=3, gap_tol=1e-11, max_rounds=rounds)
+        probs = compare_traces(g, o) + compare_final(g, o)
+        assert not probs, (rounds, probs[:3])
