@@ -686,7 +686,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   const int C = cols_per_slot(R);
   const uint32_t colbytes = (uint32_t)align_up((size_t)mm * sizeof(T), 16);
   const uint32_t colstride = (uint32_t)align_up(colbytes, 128);
-  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 4 * CMAX) * 8 + 64;
+  const size_t scratch = SMAX * 8 + (NWARPS * CMAX + 4 * CMAX + 2) * 8 + 64;
   const size_t slot = (size_t)C * colstride;
   const int G = pass_grid(c, vw.k);
   int S = (int)((c->smem_cap - scratch) / slot);

@@ -305,11 +305,19 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   double* red = reinterpret_cast<double*>(bars + SMAX);  // [NWARPS][C]
   double* cf = red + NWARPS * CMAX;                      // [C] axpy coefficients
   double* bscr = cf + CMAX;                              // [3][CMAX] block scalar scratch
-  double* stg = bscr + 3 * CMAX;                         // [PASS_STAGED][pre] staged per-column state
+  double* s_step = bscr + 3 * CMAX;                      // [2] step eta, FISTA momentum coefficient
+  double* stg = s_step + 2;                              // [PASS_STAGED][pre] staged per-column state
 
+  // step eta and FISTA's momentum coefficient, computed once per CTA and read
+  // by the per-column epilogue from shared memory (short epilogue chain, and
+  // no registers held across the streaming loop)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
+    s_step[0] = a.sc->eta;
+    const double t = a.sc->mom_t;
+    const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    s_step[1] = (t - 1.0) / tn;
   }
   __syncthreads();
 
@@ -334,15 +342,8 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   // so the dot is also the gradient at x_k -- the round's screening gradient
   AT vr[DOT ? R : 1][V];
   double beta = 0.0;   // extrapolation of the dot vector (row-blocked dots only)
-  // the step eta and FISTA's momentum coefficient are read in the per-column
-  // epilogue (one thread per column; keeps them out of the register file of
-  // the streaming loop)
-  auto step_eta = [&]() { return __ldg(&a.sc->eta); };
-  auto momentum_beta = [&]() {
-    const double t = __ldg(&a.sc->mom_t);
-    const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-    return (t - 1.0) / tn;
-  };
+  auto step_eta = [&]() { return s_step[0]; };
+  auto momentum_beta = [&]() { return s_step[1]; };
   if (DOT) {
     if (a.extrap) {
       const double t = a.sc->mom_t;
