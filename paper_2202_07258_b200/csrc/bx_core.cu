@@ -305,6 +305,7 @@ struct bx_ctx {
   void *xbak[2] = {}, *gbak[2] = {}, *rbak = nullptr;
   double* epart = nullptr;   // epsilon partials of the speculative step
   bool spec_on = true;       // env BX_SPEC=0 disables (a separate dot pass per round)
+  bool fuse_on = true;       // env BX_FUSE=0: PG / FISTA passes leave the reduce to k_reduce
   bool spec_pending = false; // the current x has taken the next round's first step
   bool dot_spec = false;     // dot_done's g / epsilon partials came from a speculative step
   int last_kind = BX_APG;    // kind of the last primal passes (fine-grained C ABI)
@@ -597,7 +598,14 @@ int launch_pass_RDX(bx_ctx* c, const PassArgs<T>& a, int G, size_t smem) {
     if (e != cudaSuccess) return fail(c, BX_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  kern<<<G, NT, smem, c->stream>>>(a);
+  if (a.fuse) {
+    // the fused reduce syncs the grid: every CTA must be resident (G <= #SMs,
+    // one CTA per SM), which a cooperative launch guarantees
+    void* args[] = {(void*)&a};
+    CU(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(NT), args, smem, c->stream));
+  } else {
+    kern<<<G, NT, smem, c->stream>>>(a);
+  }
   LAUNCHED();
   return BX_OK;
 }
@@ -658,6 +666,13 @@ struct StepExtra {
   double* xbak = nullptr;
   double* gbak = nullptr;
   double* epart = nullptr;
+  // fused reduce (k_pass reduces its own partial rows; cooperative launch)
+  int fuse = 0;
+  const double* roff = nullptr;
+  double* rout = nullptr;
+  double* rsave = nullptr;
+  int rmode = 0;
+  int rcounter = 0;
 };
 
 // Launch one streamed pass.  Returns the grid used through *G_out.
@@ -739,6 +754,13 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   a.xbak = ex.xbak;
   a.gbak = ex.gbak;
   a.epart = ex.spec ? ex.epart : nullptr;
+  a.fuse = ex.fuse;
+  a.roff = ex.roff;
+  a.rout = ex.rout;
+  a.rsave = ex.rsave;
+  a.rpart = c->bpart2;
+  a.rmode = ex.rmode;
+  a.rcounter = ex.rcounter;
   if (G_out) *G_out = G;
   c->last_Gw = G;
   if (ex.spec) c->last_Ge = G;
@@ -1526,25 +1548,37 @@ int step_pass(bx_ctx* c, int kind, bool spec) {
   ex.epart = c->epart;
   const int sm = spec ? R_SPEC : 0;
   double* save = spec ? (double*)c->rbak : nullptr;
+  // one GPU and the register-resident pass: the pass reduces its own partial
+  // rows (no k_reduce launch); sharded: the cross-rank exchange does it
+  const bool fuse = c->fuse_on && !c->sharded() && pick_R(c->m, sizeof(T)) > 0;
+  ex.fuse = fuse ? 1 : 0;
+  ex.roff = (const double*)c->off;
+  ex.rout = (double*)c->r;
+  ex.rsave = save;
+  ex.rcounter = 2;
   if (kind == BX_PG) {
+    ex.rmode = R_PG | sm;
     if (c->g_valid && !spec) {
       TRY(run_pass<T>(c, act_view<T>(c), U_PG_G, nullptr, nullptr, (double*)c->x[s], nullptr, (const double*)c->lo[s],
-                      (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G));
+                      (const double*)c->hi[s], (double*)c->g, nullptr, nullptr, nullptr, 0, &G, nullptr, 0, -1, -1,
+                      false, ex));
     } else {
       // spec: x_k goes to xprev (unused by PG) for an undo
       TRY(run_pass<T>(c, act_view<T>(c), U_PG, (const double*)c->r, nullptr, (double*)c->x[s], (double*)c->xprev[s],
                       (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s],
                       nullptr, nullptr, c->has_inf, &G, nullptr, 0, -1, -1, false, ex));
     }
-    TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_PG | sm, nullptr, 0, 2, save));
+    if (!fuse) TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_PG | sm, nullptr, 0, 2, save));
   } else {
     // FISTA by gradient linearity: the pass dots r_k; the new
     // residual is reduced in place
+    ex.rmode = R_APG | sm;
     ex.gprev = (double*)c->gprev[s];
     TRY(run_pass<T>(c, act_view<T>(c), U_APG, (const double*)c->r, nullptr, (double*)c->x[s], (double*)c->xprev[s],
                     (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s],
                     nullptr, c->bpart, c->has_inf, &G, (const double*)c->nrm[s], 0, -1, -1, false, ex));
-    TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_APG | sm, c->bpart, c->last_Gw, 2, save));
+    if (!fuse)
+      TRY(run_reduce<T>(c, G, (const double*)c->off, (double*)c->r, R_APG | sm, c->bpart, c->last_Gw, 2, save));
   }
   c->g_valid = false;
   if (spec) {
@@ -2377,6 +2411,8 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   {
     const char* e = getenv("BX_SPEC");
     c->spec_on = !(e && e[0] == '0');
+    const char* fz = getenv("BX_FUSE");
+    c->fuse_on = !(fz && fz[0] == '0');
     const char* to = getenv("BX_PEER_TIMEOUT_S");
     if (to && atof(to) > 0) c->xtimeout_ns = (uint64_t)(atof(to) * 1e9);
   }

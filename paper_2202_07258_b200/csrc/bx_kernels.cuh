@@ -27,6 +27,7 @@
 //              physical rewrite of A_act (solvers.py:57).
 #pragma once
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <stdint.h>
 #include <math.h>
 
@@ -137,7 +138,21 @@ struct PassArgs {
   double* xbak;
   double* gbak;
   double* epart;           // [gridDim.x] epsilon partial (block max)
+  // fused reduce (PG / FISTA step on one GPU, cooperative launch): after the
+  // stream, the CTAs reduce the partial rows themselves -- rout = sum of
+  // partials + roff, rsave = rout's previous contents (speculative step) --
+  // and the last CTA folds the objective / restart test (rmode, as k_reduce)
+  int fuse;
+  const double* roff;
+  double* rout;
+  double* rsave;
+  double* rpart;           // [gridDim.x] per-CTA ||r||^2 partials
+  int rmode;
+  int rcounter;
 };
+
+template <typename T>
+__device__ void pass_fused_reduce(const PassArgs<T>& a, unsigned char* scratch);
 
 // ----------------------------------------------------------------------------
 // PTX helpers: mbarrier + bulk copy (TMA bulk engine, SASS UBLKCP)
@@ -736,6 +751,10 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       if (a.epart) a.epart[b] = v3;
     }
   }
+  if constexpr (AXPY && sizeof(AT) == sizeof(T)) {
+    // (the ring is drained: its shared memory is the reduce's scratch)
+    if (a.fuse) pass_fused_reduce<T>(a, smem);
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -955,6 +974,92 @@ __global__ void __launch_bounds__(RT) k_reduce(const T* __restrict__ part, int64
   if (lane != 0) return;
   finalize_objective<T>(sc, mode, 0.5 * total, base == R_POWER ? s_div : 0.0, gdot, gscale);
   sc->counters[counter] = 0u;
+}
+
+// The reduce of k_pass's fused mode (one cooperative grid, every CTA
+// resident): grid-wide sync once every partial row is written, then CTA b
+// sums rows [b*per, (b+1)*per) over the G partials (8 groups of partial rows
+// per 64-row chunk, combined in group order: deterministic), adds the offset,
+// and the last CTA to finish folds the per-CTA ||r||^2 and restart partials
+// in a fixed order and takes the StepSizeTooLarge / restart decision --
+// k_reduce's arithmetic, without its launch and without a second pass over
+// the partial rows' launch boundary.
+template <typename T>
+__device__ void pass_fused_reduce(const PassArgs<T>& a, unsigned char* scratch) {
+  constexpr int FR = 64;        // rows per chunk
+  constexpr int FQ = NT / FR;   // partial-row groups
+  constexpr int FONESHOT = 20;  // partials per thread loaded in one go (G <= 160)
+  double* sm = reinterpret_cast<double*>(scratch);  // [FQ][FR] (+ [NWARPS] + flag)
+  double* swarp = sm + FQ * FR;
+  int* slast = reinterpret_cast<int*>(swarp + NWARPS);
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t m = a.m;
+  const int64_t per = (m + G - 1) / G;
+  const int64_t r0 = b * per < m ? b * per : m;
+  const int64_t r1 = r0 + per < m ? r0 + per : m;
+  const int rr = tid % FR, q = tid / FR;
+  double sq = 0.0;
+  for (int64_t base = r0; base < r1; base += FR) {
+    const int64_t i = base + rr;
+    double s = 0.0;
+    if (i < r1) {
+      if (G <= FQ * FONESHOT) {
+        // every partial of this thread in flight at once (one L2 round trip)
+        T v[FONESHOT];
+#pragma unroll
+        for (int u = 0; u < FONESHOT; ++u) {
+          const int64_t bb = q + (int64_t)u * FQ;
+          v[u] = bb < G ? __ldcg(a.part + bb * a.ldp + i) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < FONESHOT; ++u) s += static_cast<double>(v[u]);
+      } else {
+        for (int64_t bb = q; bb < G; bb += FQ) s += static_cast<double>(__ldcg(a.part + bb * a.ldp + i));
+      }
+    }
+    sm[q * FR + rr] = s;
+    __syncthreads();
+    if (tid < FR && i < r1) {
+      double t = sm[rr];
+#pragma unroll
+      for (int h = 1; h < FQ; ++h) t += sm[h * FR + rr];
+      t = add_rn(t, a.roff[i]);
+      if (a.rsave) a.rsave[i] = a.rout[i];
+      a.rout[i] = t;
+      sq += t * t;
+    }
+    __syncthreads();
+  }
+  sq = warp_sum<double>(sq);
+  if (lane == 0) swarp[warp] = sq;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < NWARPS; ++w) tot += swarp[w];
+    a.rpart[b] = tot;
+    __threadfence();
+    const unsigned prev = atomicAdd(&a.sc->counters[a.rcounter], 1u);
+    *slast = (prev == (unsigned)G - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (!*slast || warp != 0) return;
+  __threadfence();
+  double total = 0.0, gdot = 0.0, gscale = 0.0;
+  for (int64_t bb = lane; bb < G; bb += 32) total += __ldcg(&a.rpart[bb]);
+  if ((a.rmode & ~R_SPEC) == R_APG && a.bpart)
+    for (int64_t bb = lane; bb < G; bb += 32) {
+      gdot += __ldcg(&a.bpart[2 * bb]);
+      gscale += __ldcg(&a.bpart[2 * bb + 1]);
+    }
+  total = warp_sum<double>(total);
+  gdot = warp_sum<double>(gdot);
+  gscale = warp_sum<double>(gscale);
+  if (lane != 0) return;
+  finalize_objective<T>(a.sc, a.rmode, 0.5 * total, 0.0, gdot, gscale);
+  a.sc->counters[a.rcounter] = 0u;
 }
 
 // ----------------------------------------------------------------------------
