@@ -152,16 +152,63 @@ int bx_reset(bx_ctx* ctx);
  * pg_step (solvers.py:101-116), cd_sweep (:119-137), FISTA */
 int bx_primal_passes(bx_ctx* ctx, int32_t kind, double eta, int32_t passes);
 /* dual point + reduced gap + (optionally) the sphere test for the current
- * iterate: driver.py:183-201 and 453-461.  out_scalars_host receives
- * {primal, dual, gap, eps, radius, slack, n_new_lower, n_new_upper}. */
-int bx_dual_screen(bx_ctx* ctx, int32_t screening, double slack_scale, double* out_scalars_host);
-/* apply_screening (screening.py:72-94) + Workspace.refresh (solvers.py:54-65):
- * snaps screened x to bounds, updates z, compacts A and the per-column state
- * (ballot/prefix-sum), recomputes the residual. */
+ * iterate: driver.py:183-201 and 213-221.  alpha: the loss's
+ * strong-concavity constant (model.py:40, 1 for the quadratic loss).
+ * out_scalars_host receives {primal, dual, gap, eps, radius, slack,
+ * n_new_lower, n_new_upper}. */
+int bx_dual_screen(bx_ctx* ctx, int32_t screening, double slack_scale, double alpha,
+                   double* out_scalars_host);
+/* apply_screening (screening.py:72-94) + Workspace.refresh (solvers.py:54-65)
+ * of the last bx_dual_screen's sphere test: snaps screened x to bounds,
+ * updates z, compacts A and the per-column state of the kind the last
+ * bx_primal_passes ran (ballot/prefix-sum), updates the residual. */
 int bx_compact(bx_ctx* ctx);
 /* _certified_gap on the full problem (driver.py:112-117 ->
  * duality.py:159-209); out_host = {gap, primal, dual, eps} */
-int bx_certified_gap(bx_ctx* ctx, double* out_host);
+int bx_certified_gap(bx_ctx* ctx, double alpha, double* out_host);
+
+/* Load a preserved set and a primal point into the workspace -- the state
+ * the reference's spec-level updates take as (ScreeningState, PrimalPoint)
+ * and rebuild a Workspace from (solvers.py:48-65, 207-227): `preserved`
+ * (host, k ascending original indices), x_full (device, n) and the
+ * saturated part z = A_S x_S (device, m).  Recomputes r = A_act x + z - y
+ * and its objective; FISTA momentum restarts.  sat lists are not tracked. */
+int bx_set_state(bx_ctx* ctx, const int64_t* preserved_host, int64_t k, const double* x_full,
+                 const double* z);
+/* one outer bounded-variable Lawson-Hanson iteration on the preserved set
+ * (active_set_step, solvers.py:152-204; needs
+ * bx_ctx_set_active_set_workspace): passive_in (device, k; NULL keeps the
+ * context's mask) -> passive_out (device, k; may be NULL); *optimal = 1
+ * when nothing violates the optimality conditions. */
+int bx_active_set_step(bx_ctx* ctx, const uint8_t* passive_in, uint8_t* passive_out, int32_t* optimal);
+/* residual r (m) and the restricted gradient A_act' r (k) at the current
+ * iterate -- pg_update / cd_update's return values (solvers.py:207-227).
+ * Device pointers. */
+int bx_gradient(bx_ctx* ctx, double* resid, double* grad);
+/* out (m) = A[:, cols] coef (+ z_add when not NULL): forward_product
+ * (screening.py:97-104) and the z update of apply_screening (:84-88).
+ * cols (device int32, k entries; NULL = all n columns, k = n). */
+int bx_apply_a(bx_ctx* ctx, const int32_t* cols, int64_t k, const double* coef, const double* z_add,
+               double* out);
+/* out (n) = A' v over the full problem (eval_dual, dual_translate,
+ * is_dual_feasible: duality.py:103-185).  Device pointers. */
+int bx_apply_at(bx_ctx* ctx, const double* v, double* out);
+/* dual point of the full problem at x_full (device, n): dual translation
+ * with the context's t when some upper bound is infinite
+ * (dual_point_nnlr, duality.py:187-209), dual scaling otherwise
+ * (dual_point_bvlr, :159-168).  theta (m), a_t_theta (n) device (either may
+ * be NULL); out_host = {gap (clamped), primal, dual, eps}. */
+int bx_dual_point(bx_ctx* ctx, const double* x_full, double alpha, double* theta, double* a_t_theta,
+                  double* out_host);
+/* dual objective D(theta) (duality.py:103-124) given A'theta (device, n;
+ * NULL: computed here); *d_host receives it. */
+int bx_eval_dual(bx_ctx* ctx, const double* theta, const double* a_t_theta, double* d_host);
+/* gap-safe sphere test on given inner products (screening.py:46-69):
+ * a_t_theta (device, n), preserved (device int32, k), thresholds
+ * (radius + slack) ||a_j||, strict comparisons; flags (device, k):
+ * 0 keep, 1 lower, 2 upper. */
+int bx_sphere_test(bx_ctx* ctx, const double* a_t_theta, const int32_t* preserved, int64_t k, double radius,
+                   double slack, uint8_t* flags);
 /* preserved count, and the preserved original indices (int32, device) */
 int64_t bx_preserved_count(const bx_ctx* ctx);
 

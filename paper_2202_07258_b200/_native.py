@@ -75,9 +75,17 @@ SIGNATURES = {
     "bx_power_iter": (ctypes.c_int, [_vp, _i32, _dp, _dp]),
     "bx_reset": (ctypes.c_int, [_vp]),
     "bx_primal_passes": (ctypes.c_int, [_vp, _i32, _d, _i32]),
-    "bx_dual_screen": (ctypes.c_int, [_vp, _i32, _d, _dp]),
+    "bx_dual_screen": (ctypes.c_int, [_vp, _i32, _d, _d, _dp]),
     "bx_compact": (ctypes.c_int, [_vp]),
-    "bx_certified_gap": (ctypes.c_int, [_vp, _dp]),
+    "bx_certified_gap": (ctypes.c_int, [_vp, _d, _dp]),
+    "bx_set_state": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), _i64, _vp, _vp]),
+    "bx_gradient": (ctypes.c_int, [_vp, _vp, _vp]),
+    "bx_active_set_step": (ctypes.c_int, [_vp, _vp, _vp, ctypes.POINTER(ctypes.c_int32)]),
+    "bx_apply_a": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "bx_apply_at": (ctypes.c_int, [_vp, _vp, _vp]),
+    "bx_dual_point": (ctypes.c_int, [_vp, _vp, _d, _vp, _vp, _dp]),
+    "bx_eval_dual": (ctypes.c_int, [_vp, _vp, _vp, _dp]),
+    "bx_sphere_test": (ctypes.c_int, [_vp, _vp, _vp, _i64, _d, _d, _vp]),
     "bx_preserved_count": (_i64, [_vp]),
     "bx_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveCfg), START_FN, _vp, ctypes.POINTER(TraceRec), _i64,
                                 ctypes.POINTER(SolveOut)]),

@@ -1829,11 +1829,20 @@ const double* round_x(const bx_ctx* c) {
   return (const double*)(c->spec_pending ? c->xprev[c->cur] : c->x[c->cur]);
 }
 
+// the full-problem certificate of the iterate in x_full
+template <typename T>
+int certify_full(bx_ctx* c, double alpha);
+
 template <typename T>
 int certified(bx_ctx* c, double alpha) {
   const int s = c->cur;
   k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[s], round_x(c), (double*)c->xfull);
   LAUNCHED();
+  return certify_full<T>(c, alpha);
+}
+
+template <typename T>
+int certify_full(bx_ctx* c, double alpha) {
   int G = 1;
   // fp32 storage: the certificate's A x and A'r accumulate in fp64 (a fp32
   // sum of A x carries ~1e-7 |Ax| of noise, which puts a floor of ~1e-7
@@ -2343,6 +2352,181 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
   return BX_OK;
 }
 
+// ---- spec-level primitives (fine-grained C ABI) ------------------------------
+template <typename T>
+int set_state_typed(bx_ctx* c, const int64_t* pres, int64_t k, const double* xf, const double* z) {
+  if (k < 0 || k > c->n) return fail(c, BX_ERR_DIMENSION, "preserved count %lld outside [0, n]", (long long)k);
+  if (k > 0 && !pres) return fail(c, BX_ERR_INVALID_ARGUMENT, "preserved indices");
+  if (!xf) return fail(c, BX_ERR_INVALID_ARGUMENT, "x_full");
+  for (int64_t i = 0; i < k; ++i)
+    if (pres[i] < 0 || pres[i] >= c->n || (i && pres[i] <= pres[i - 1]))
+      return fail(c, BX_ERR_INVALID_ARGUMENT, "preserved indices must be ascending and in [0, n)");
+  c->cur = 0;
+  c->k = k;
+  c->act_is_orig = true;
+  c->dense = (k == c->n);  // ascending and k == n: the identity
+  c->kphys = c->n;
+  c->n_sat_lo = c->n_sat_up = 0;
+  c->spec_pending = c->dot_done = c->dot_spec = c->g_valid = c->theta_is_cert = false;
+  c->gram_dirty = true;
+  c->as_dirty = true;
+  if (k > 0) {
+    CU(cudaMemcpyAsync(c->sat_lo, pres, k * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    k_gather_state<<<grid1d(c, k), RT, 0, c->stream>>>(
+        k, c->sat_lo, c->idx[0], xf, (const double*)c->lofull, (const double*)c->hifull, (const double*)c->nrmfull,
+        (const double*)c->attfull, (double*)c->x[0], (double*)c->lo[0], (double*)c->hi[0], (double*)c->nrm[0],
+        (double*)c->att[0], (double*)c->xprev[0], (double*)c->gprev[0]);
+    LAUNCHED();
+  }
+  CU(cudaMemcpyAsync(c->xfull, xf, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemsetAsync(c->z, 0, c->mp * sizeof(double), c->stream));
+  if (z) CU(cudaMemcpyAsync(c->z, z, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  k_offsets<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, (const double*)c->y, (const double*)c->z,
+                                                           (double*)c->off, (double*)c->tgt);
+  LAUNCHED();
+  DevScalars h;
+  memset(&h, 0, sizeof(h));
+  const bool f32 = sizeof(T) == 4;
+  h.mom_t = 1.0;
+  h.P = INFINITY;
+  h.rise_rel = f32 ? 1e-5 : 0.0;
+  h.rs_f = f32 ? 1e-6 : 1e-12;
+  h.rs_g = f32 ? 1e-5 : 1e-12;
+  CU(cudaMemcpyAsync(c->sc, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  TRY(refresh_resid<T>(c));
+  TRY(sync_scalars<T>(c));
+  return check_dev_err(c);
+}
+
+template <typename T>
+int gradient_typed(bx_ctx* c, double* resid, double* grad) {
+  const int s = c->cur;
+  if (c->k > 0) {
+    int G = 1;
+    TRY(run_pass<T>(c, act_view<T>(c), U_DOT, (const double*)c->r, nullptr, nullptr, nullptr, nullptr,
+                    (const double*)c->hi[s], (double*)c->g, (const double*)c->att[s], nullptr, nullptr, 0, &G));
+    c->g_valid = true;
+  }
+  if (resid) CU(cudaMemcpyAsync(resid, c->r, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (grad && c->k > 0) CU(cudaMemcpyAsync(grad, c->g, c->k * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+template <typename T>
+int apply_a_typed(bx_ctx* c, const int32_t* cols, int64_t k, const double* coef, const double* z_add, double* out) {
+  if (!out) return fail(c, BX_ERR_INVALID_ARGUMENT, "out");
+  if (!cols && k != c->n) return fail(c, BX_ERR_DIMENSION, "all columns: k must be n");
+  if (k == 0) {
+    if (z_add)
+      CU(cudaMemcpyAsync(out, z_add, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    else
+      CU(cudaMemsetAsync(out, 0, c->m * sizeof(double), c->stream));
+  } else {
+    if (!coef) return fail(c, BX_ERR_INVALID_ARGUMENT, "coef");
+    View<T> vw{(const T*)c->A, c->lda, cols, k};
+    int G = 1;
+    const bool acc64 = sizeof(T) == 4 && c->m <= (int64_t)NT * 4 * 12;  // fp32 storage: fp64 sums (as certified())
+    TRY(run_pass<T>(c, vw, U_AX, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, coef,
+                    nullptr, 0, &G, nullptr, 0, -1, -1, acc64));
+    if (acc64)
+      TRY(run_reduce<double>(c, G, z_add, out, R_PLAIN, nullptr, 0, 0));
+    else
+      TRY(run_reduce<T>(c, G, z_add, out, R_PLAIN, nullptr, 0, 0));
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+template <typename T>
+int apply_at_typed(bx_ctx* c, const double* v, double* out) {
+  if (!v || !out) return fail(c, BX_ERR_INVALID_ARGUMENT, "v / out");
+  int G = 1;
+  const bool acc64 = sizeof(T) == 4 && c->m <= (int64_t)NT * 4 * 12;
+  TRY(run_pass<T>(c, full_view<T>(c), U_DOT, v, nullptr, nullptr, nullptr, nullptr, (const double*)c->hifull, out,
+                  (const double*)c->attfull, nullptr, nullptr, 0, &G, nullptr, 0, -1, -1, acc64));
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
+template <typename T>
+int dual_point_typed(bx_ctx* c, const double* xf, double alpha, double* theta, double* atheta, double* out) {
+  if (!xf) return fail(c, BX_ERR_INVALID_ARGUMENT, "x_full");
+  CU(cudaMemcpyAsync(c->xfull, xf, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemsetAsync(&c->sc->err, 0, sizeof(int32_t), c->stream));
+  TRY(certify_full<T>(c, alpha));
+  if (theta) CU(cudaMemcpyAsync(theta, c->thetac, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (atheta) CU(cudaMemcpyAsync(atheta, c->vfull, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  TRY(sync_scalars<T>(c));
+  const int st = check_dev_err(c);
+  if (out) {
+    out[0] = c->hsc->cert.gap;
+    out[1] = c->hsc->cert.primal;
+    out[2] = c->hsc->cert.dual;
+    out[3] = c->hsc->cert.eps;
+  }
+  return st;
+}
+
+template <typename T>
+int eval_dual_typed(bx_ctx* c, const double* theta, const double* atheta, double* d) {
+  if (!theta) return fail(c, BX_ERR_INVALID_ARGUMENT, "theta");
+  // k_dual evaluates theta = -r and v = -g with no translation (eps = 0)
+  k_neg<double><<<grid1d(c, c->m), RT, 0, c->stream>>>(c->m, theta, (double*)c->rc);
+  LAUNCHED();
+  if (atheta) {
+    k_neg<double><<<grid1d(c, c->n), RT, 0, c->stream>>>(c->n, atheta, (double*)c->gfull);
+    LAUNCHED();
+  } else {
+    int G = 1;
+    const bool acc64 = sizeof(T) == 4 && c->m <= (int64_t)NT * 4 * 12;
+    TRY(run_pass<T>(c, full_view<T>(c), U_DOT, (const double*)c->rc, nullptr, nullptr, nullptr, nullptr,
+                    (const double*)c->hifull, (double*)c->gfull, (const double*)c->attfull, nullptr, nullptr, 0, &G,
+                    nullptr, 0, -1, -1, acc64));
+  }
+  const double inf = INFINITY;  // no primal here: the weak-duality check cannot fire
+  CU(cudaMemcpyAsync(&c->sc->cert_P, &inf, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int nb = grid1d(c, c->m > c->n ? c->m : c->n);
+  k_dual<double><<<nb, RT, 0, c->stream>>>((const double*)c->rc, (const double*)c->t, (const double*)c->y,
+                                           (double*)c->thetac, c->m, (const double*)c->gfull,
+                                           (const double*)c->attfull, (const double*)c->lofull,
+                                           (const double*)c->hifull, (double*)c->vfull, c->n, nullptr, 0, 0, c->sc, 1,
+                                           c->bpart3, 0.0, 1.0, 5, nullptr);
+  LAUNCHED();
+  TRY(sync_scalars<T>(c));
+  if (d) *d = c->hsc->cert.dual;
+  return BX_OK;
+}
+
+__global__ void k_mask_io(int64_t k, const uint8_t* __restrict__ in, double* __restrict__ pmask,
+                          uint8_t* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x) {
+    if (in) pmask[p] = in[p] ? 1.0 : 0.0;
+    if (out) out[p] = pmask[p] != 0.0 ? 1 : 0;
+  }
+}
+
+template <typename T>
+int active_set_step_typed(bx_ctx* c, const uint8_t* pin, uint8_t* pout, int32_t* optimal) {
+  if (!c->as) return fail(c, BX_ERR_WORKSPACE, "active-set scratch not attached (bx_ctx_set_active_set_workspace)");
+  c->last_kind = BX_ACTIVE_SET;
+  double* pmask = (double*)c->xprev[c->cur];
+  if (pin && c->k > 0) {
+    k_mask_io<<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, pin, pmask, nullptr);
+    LAUNCHED();
+    c->as_dirty = true;
+  }
+  bool opt = false;
+  TRY(as_step<T>(c, &opt));
+  if (pout && c->k > 0) {
+    k_mask_io<<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, nullptr, pmask, pout);
+    LAUNCHED();
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  if (optimal) *optimal = opt ? 1 : 0;
+  return BX_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -2466,9 +2650,11 @@ int bx_primal_passes(bx_ctx* c, int32_t kind, double eta, int32_t passes) {
   return check_dev_err(c);
 }
 
-int bx_dual_screen(bx_ctx* c, int32_t screening, double slack_scale, double* o) {
-  int s = (c->dtype == BX_F64) ? dual_screen<double>(c, screening, slack_scale, 1.0)
-                               : dual_screen<float>(c, screening, slack_scale, 1.0);
+int bx_dual_screen(bx_ctx* c, int32_t screening, double slack_scale, double alpha, double* o) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (!(alpha > 0)) return fail(c, BX_ERR_INVALID_ARGUMENT, "alpha must be positive");
+  int s = (c->dtype == BX_F64) ? dual_screen<double>(c, screening, slack_scale, alpha)
+                               : dual_screen<float>(c, screening, slack_scale, alpha);
   if (s != BX_OK) return s;
   CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -2491,15 +2677,17 @@ int bx_compact(bx_ctx* c) {
   const int64_t lo = c->hsc->n_lo, up = c->hsc->n_up, keep = c->hsc->n_keep;
   if (lo + up == 0) return BX_OK;
   const bool zu = ((c->bound_bits & 1) && lo > 0) || ((c->bound_bits & 2) && up > 0);
-  int s = (c->dtype == BX_F64) ? compact<double>(c, lo, up, keep, BX_APG, zu)
-                               : compact<float>(c, lo, up, keep, BX_APG, zu);
+  int s = (c->dtype == BX_F64) ? compact<double>(c, lo, up, keep, c->last_kind, zu)
+                               : compact<float>(c, lo, up, keep, c->last_kind, zu);
   if (s != BX_OK) return s;
   CU(cudaStreamSynchronize(c->stream));
   return BX_OK;
 }
 
-int bx_certified_gap(bx_ctx* c, double* o) {
-  int s = (c->dtype == BX_F64) ? certified<double>(c, 1.0) : certified<float>(c, 1.0);
+int bx_certified_gap(bx_ctx* c, double alpha, double* o) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (!(alpha > 0)) return fail(c, BX_ERR_INVALID_ARGUMENT, "alpha must be positive");
+  int s = (c->dtype == BX_F64) ? certified<double>(c, alpha) : certified<float>(c, alpha);
   if (s != BX_OK) return s;
   CU(cudaMemcpyAsync(c->hsc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -2514,6 +2702,60 @@ int bx_certified_gap(bx_ctx* c, double* o) {
 }
 
 int64_t bx_preserved_count(const bx_ctx* c) { return c ? c->k : -1; }
+
+int bx_set_state(bx_ctx* c, const int64_t* pres, int64_t k, const double* xf, const double* z) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  return c->dtype == BX_F64 ? set_state_typed<double>(c, pres, k, xf, z) : set_state_typed<float>(c, pres, k, xf, z);
+}
+
+int bx_active_set_step(bx_ctx* c, const uint8_t* passive_in, uint8_t* passive_out, int32_t* optimal) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  return c->dtype == BX_F64 ? active_set_step_typed<double>(c, passive_in, passive_out, optimal)
+                            : active_set_step_typed<float>(c, passive_in, passive_out, optimal);
+}
+
+int bx_gradient(bx_ctx* c, double* resid, double* grad) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  return c->dtype == BX_F64 ? gradient_typed<double>(c, resid, grad) : gradient_typed<float>(c, resid, grad);
+}
+
+int bx_apply_a(bx_ctx* c, const int32_t* cols, int64_t k, const double* coef, const double* z_add, double* out) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (k < 0 || k > c->n) return fail(c, BX_ERR_DIMENSION, "column count %lld", (long long)k);
+  return c->dtype == BX_F64 ? apply_a_typed<double>(c, cols, k, coef, z_add, out)
+                            : apply_a_typed<float>(c, cols, k, coef, z_add, out);
+}
+
+int bx_apply_at(bx_ctx* c, const double* v, double* out) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  return c->dtype == BX_F64 ? apply_at_typed<double>(c, v, out) : apply_at_typed<float>(c, v, out);
+}
+
+int bx_dual_point(bx_ctx* c, const double* xf, double alpha, double* theta, double* atheta, double* out) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (!(alpha > 0)) return fail(c, BX_ERR_INVALID_ARGUMENT, "alpha must be positive");
+  return c->dtype == BX_F64 ? dual_point_typed<double>(c, xf, alpha, theta, atheta, out)
+                            : dual_point_typed<float>(c, xf, alpha, theta, atheta, out);
+}
+
+int bx_eval_dual(bx_ctx* c, const double* theta, const double* atheta, double* d) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  return c->dtype == BX_F64 ? eval_dual_typed<double>(c, theta, atheta, d)
+                            : eval_dual_typed<float>(c, theta, atheta, d);
+}
+
+int bx_sphere_test(bx_ctx* c, const double* v, const int32_t* pres, int64_t k, double radius, double slack,
+                   uint8_t* flags) {
+  if (!c) return BX_ERR_INVALID_ARGUMENT;
+  if (k < 0 || k > c->n) return fail(c, BX_ERR_DIMENSION, "preserved count %lld", (long long)k);
+  if (k == 0) return BX_OK;
+  if (!v || !pres || !flags) return fail(c, BX_ERR_INVALID_ARGUMENT, "a_t_theta / preserved / flags");
+  k_sphere_given<<<grid1d(c, k), RT, 0, c->stream>>>(v, (const double*)c->nrmfull, (const double*)c->hifull, pres, k,
+                                                    radius, slack, flags);
+  LAUNCHED();
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
 
 int bx_solve(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void* user, bx_trace_rec* trace,
              int64_t cap, bx_solve_out* out) {

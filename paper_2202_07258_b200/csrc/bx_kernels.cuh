@@ -1440,6 +1440,46 @@ __global__ void k_init_cols(int64_t n, const T* __restrict__ lo, const T* __rest
   }
 }
 
+// bx_set_state: the per-column state of a given preserved set (Workspace,
+// solvers.py:51-63): x, bounds, norms and A't gathered from the full arrays
+__global__ void k_gather_state(int64_t k, const int64_t* __restrict__ pres, int32_t* __restrict__ idx,
+                               const double* __restrict__ xf, const double* __restrict__ lof,
+                               const double* __restrict__ hif, const double* __restrict__ nrmf,
+                               const double* __restrict__ attf, double* __restrict__ x, double* __restrict__ lo,
+                               double* __restrict__ hi, double* __restrict__ nrm, double* __restrict__ att,
+                               double* __restrict__ xprev, double* __restrict__ gprev) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = pres[p];
+    idx[p] = static_cast<int32_t>(j);
+    x[p] = xf[j];
+    xprev[p] = xf[j];
+    gprev[p] = 0.0;
+    lo[p] = lof[j];
+    hi[p] = hif[j];
+    nrm[p] = nrmf[j];
+    att[p] = attf[j];
+  }
+}
+
+// sphere test on caller-given inner products (screening.py:60-69):
+// thr_j = (radius + slack) ||a_j||, strict comparisons, upper only for
+// finite u_j
+__global__ void k_sphere_given(const double* __restrict__ v, const double* __restrict__ nrm,
+                               const double* __restrict__ hi, const int32_t* __restrict__ pres, int64_t k,
+                               double radius, double slack, uint8_t* __restrict__ flags) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = pres[p];
+    const double thr = (radius + slack) * nrm[j];
+    const double vj = v[j];
+    uint8_t f = 0;
+    if (vj < -thr)
+      f = 1;
+    else if (vj > thr && !isinf(hi[j]))
+      f = 2;
+    flags[p] = f;
+  }
+}
+
 template <typename T>
 __global__ void k_offsets(int64_t m, const T* __restrict__ y, const T* __restrict__ z, T* __restrict__ off,
                           T* __restrict__ tgt) {

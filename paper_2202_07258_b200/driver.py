@@ -173,6 +173,12 @@ class _Session:
             nat.lib().bx_ctx_destroy(self.ctx)
             self.ctx = None
 
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
     def power_iter(self, iters, v0):
         nat.check(nat.lib().bx_reset(self.ctx), self.ctx, "bx_reset")
         v0 = np.ascontiguousarray(v0, dtype=np.float64)
@@ -229,6 +235,21 @@ class _Session:
         nat.check(L.bx_get_state(self.ctx, x.data_ptr(), theta.data_ptr(), sl.data_ptr(), su.data_ptr()),
                   self.ctx, "bx_get_state")
         return out, trace[: min(out.rounds, cap)], x, theta, sl[: out.n_sat_lower], su[: out.n_sat_upper]
+
+
+def device_session(p, t=None):
+    """A native context over ``p`` (and translation vector ``t``), created
+    once and cached on the Problem: the spec-level primitives
+    (primitives.py) run their passes on it."""
+    import types
+    key = None if t is None else np.asarray(t, dtype=np.float64).ravel().tobytes()
+    cache = p.__dict__.setdefault("_sessions", {})
+    s = cache.get(key)
+    if s is None or s.ctx is None:
+        tv = None if t is None else types.SimpleNamespace(t=np.asarray(t, dtype=np.float64).ravel())
+        s = _Session(p, tv=tv)
+        cache[key] = s
+    return s
 
 
 def column_stats(p, t=None):

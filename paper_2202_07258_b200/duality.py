@@ -94,3 +94,8 @@ def select_translation_vector(p, strategy="neg-ones", column=None, t=None):
     else:
         raise ValueError(f"unknown strategy {strategy!r}; choose from {STRATEGIES}")
     return TranslationVector(p, cand, strategy=strategy)
+
+
+# the dual-point family of the per-round API (duality.py:29-209), on the GPU
+from .primitives import (DualState, dual_point_bvlr, dual_point_nnlr, dual_translate,  # noqa: E402,F401
+                         duality_gap, eval_dual, is_dual_feasible)

@@ -61,6 +61,23 @@ def _is_torch(x):
         return False
 
 
+def _validate_device(a, y, lo, hi):
+    """The reference's input checks (model.py:58-76) on CUDA tensors, in the
+    same order and with the same messages as the host path; each check is a
+    device reduction, only its boolean comes back."""
+    import torch
+    if bool(torch.isnan(a).any()) or bool(torch.isnan(y).any()):
+        raise ValueError("NaN entries in A or y")
+    if bool(torch.isnan(lo).any()) or bool(torch.isnan(hi).any()):
+        raise ValueError("NaN entries in bounds")
+    if not bool(torch.isfinite(lo).all()):
+        raise ValueError("lower bounds must be finite")
+    if bool(torch.isinf(a).any()) or bool(torch.isinf(y).any()):
+        raise ValueError("A and y must be finite")
+    if not bool((lo < hi).all()):
+        raise ValueError("need lower_j < upper_j for every coordinate")
+
+
 class Problem:
     """min 0.5 ||A x - y||^2  s.t.  lower <= x <= upper  (model.py:47-99)."""
 
@@ -121,6 +138,7 @@ class Problem:
         yv = torch.as_tensor(y, device=dev).to(f64).reshape(-1).contiguous()
         if yv.shape[0] != m:
             raise DimensionMismatch(f"y has length {yv.shape[0]}, expected {m}")
+        _validate_device(a, yv, lo, hi)
         self._dev = dict(a=self._device_layout(a.to(tdt)), y=yv, lo=lo, hi=hi, device=dev)
         self.a_matrix = None
         self.y = None
@@ -146,6 +164,9 @@ class Problem:
         lo = torch.as_tensor(lower, dtype=f64, device=dev).broadcast_to((n,)).contiguous()
         hi = torch.as_tensor(upper, dtype=f64, device=dev).broadcast_to((n,)).contiguous()
         yv = torch.as_tensor(y, device=dev).to(f64).reshape(-1).contiguous()
+        if yv.shape[0] != m:
+            raise DimensionMismatch(f"y has length {yv.shape[0]}, expected {m}")
+        _validate_device(storage[:, :m], yv, lo, hi)
         p._dev = dict(a=storage, y=yv, lo=lo, hi=hi, device=dev)
         p.a_matrix = None
         p.y = None
@@ -206,7 +227,9 @@ class Problem:
 
     @property
     def col_norms(self):
-        return np.linalg.norm(self.a_matrix, axis=0)
+        """||a_j||_2 (model.py:89-92), from the GPU setup pass."""
+        from .primitives import device_col_norms
+        return device_col_norms(self)
 
     def is_box_feasible(self, x):
         x = np.asarray(x, dtype=float)
@@ -227,8 +250,13 @@ def eval_primal(p, pt):
     """0.5 ||A x - y||^2 with an exact box check (model.py:109-120)."""
     if not p.is_box_feasible(pt.x):
         raise InfeasiblePoint("primal point violates the box constraint")
-    ax = pt.ax_cache if pt.ax_cache is not None else p.a_matrix @ pt.x
+    if pt.ax_cache is not None:
+        ax = pt.ax_cache
+    else:
+        from .primitives import device_forward  # A x on the GPU (bx_apply_a)
+        ax = device_forward(p, pt.x)
     if ax.shape != (p.m,):
         raise DimensionMismatch("ax_cache has wrong length")
-    r = ax - p.y
+    y = p.y if p.y is not None else p.device_arrays()["y"].cpu().numpy()
+    r = ax - y
     return 0.5 * float(r @ r)

@@ -72,3 +72,7 @@ def auto_step_size(a_sub, alpha, power_iters=50):
     if sigma == 0.0:
         return 1.0
     return 0.99 * alpha / sigma ** 2
+
+
+# the spec-level one-shot updates (solvers.py:38-45, 207-240), on the GPU
+from .primitives import ActiveSetState, active_set_update, cd_update, pg_update  # noqa: E402,F401

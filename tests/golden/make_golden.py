@@ -28,6 +28,11 @@ Fixtures
   cfg1_trace.npz      BASELINE config 1 at full size (1000 x 2000, PG, 10
                       passes/round, gap 1e-6): the reference's whole trajectory
   cfg2_trace.npz      BASELINE config 2 at full size (2000 x 4000, CD, gap 1e-7)
+  primitives.npz      the spec-level per-round API (__init__.py exports):
+                      pg_update / cd_update / active_set_update, dual points
+                      (nnlr / bvlr), eval_dual, is_dual_feasible,
+                      duality_gap, dual_translate, safe_screen_test,
+                      apply_screening, forward_product on small instances
 """
 
 import hashlib
@@ -279,8 +284,72 @@ def full_config(cfg_id, fname, kind=None, gap_tol=None):
     print(fname, "rounds", res.rounds, "converged", res.converged, "elapsed %.1fs" % el)
 
 
+def primitives():
+    """One scripted sequence of the reference's per-round primitives per
+    (family, seed): every input and output stored."""
+    out = {}
+    for fam in ("nnls", "bvls", "mixed"):
+        for seed in range(2):
+            rng = np.random.default_rng(1000 + seed + 10 * ("nnls", "bvls", "mixed").index(fam))
+            a, y, lo, hi = small_instance(rng, 60, 40, fam)
+            key = f"{fam}_{seed}"
+            p = bs.Problem(a, y, lo, hi)
+            st = bs.ScreeningState(p)
+            pt = bs.PrimalPoint(np.clip(np.zeros(p.n), lo, hi))
+            cfg = bs.SolverConfig(kind="pg", inner_passes=3000)
+            step = bs.auto_step_size(a, 1.0)
+            r1, g1 = bs.pg_update(p, st, pt, cfg, step)
+            rec = dict(a=a, y=y, lo=lo, hi=hi, step=np.array(step), pg_r=r1, pg_g=g1, pg_x=pt.x.copy())
+            tv = None
+            if p.j_inf.size:
+                tv = bs.select_translation_vector(p, "neg-ones")
+                ds = bs.dual_point_nnlr(p, tv, pt)
+                rec["t"] = tv.t
+            else:
+                ds = bs.dual_point_bvlr(p, pt)
+            rec.update(theta=ds.theta, d_value=np.array(ds.d_value), gap=np.array(ds.gap),
+                       a_t_theta=ds.a_t_theta_cache)
+            rec["eval_dual"] = np.array(bs.eval_dual(p, ds.theta))
+            rec["eval_dual_cached"] = np.array(bs.eval_dual(p, ds.theta, ds.a_t_theta_cache))
+            rec["feasible"] = np.array(bs.is_dual_feasible(p, ds.theta))
+            rec["feasible_neg"] = np.array(bs.is_dual_feasible(p, -ds.theta))
+            rec["duality_gap"] = np.array(bs.duality_gap(p, pt, ds.theta))
+            zg = y - a @ pt.x
+            rec["zgrad"] = zg
+            if tv is not None:
+                rec["translated"] = bs.dual_translate(p, tv, zg)
+            st.radius = bs.gap_safe_radius(ds.gap, 1.0)
+            slack = 1e-12 * max(1.0, float(np.linalg.norm(ds.theta)))
+            nl, nu = bs.safe_screen_test(st, ds.a_t_theta_cache, p, slack=slack)
+            rec.update(radius=np.array(st.radius), slack=np.array(slack), new_lower=nl, new_upper=nu)
+            # a synthetic test vector with decisions on both sides of the sphere
+            vt = np.random.default_rng(seed).standard_normal(p.n) * st.col_norms
+            st.radius = 0.5
+            nl2, nu2 = bs.safe_screen_test(st, vt, p, slack=0.25)
+            rec.update(vtest=vt, new_lower2=nl2, new_upper2=nu2)
+            bs.apply_screening(st, nl, nu, pt, p)
+            rec.update(z=st.z.copy(), preserved=st.preserved.copy(), x_screened=pt.x.copy())
+            rec["forward"] = bs.forward_product(st, p, pt.x[st.preserved])
+            r2, g2 = bs.cd_update(p, st, pt, bs.SolverConfig(kind="cd", inner_passes=3))
+            rec.update(cd_r=r2, cd_g=g2, cd_x=pt.x.copy())
+            # three active-set iterations from the reference's start (x = l)
+            st3 = bs.ScreeningState(p)
+            pt3 = bs.PrimalPoint(lo.copy())
+            ass = bs.ActiveSetState(p.n)
+            for it in range(3):
+                r3, g3, opt = bs.active_set_update(p, st3, pt3, ass, bs.SolverConfig(kind="active-set"))
+                rec.update({f"as{it}_r": r3, f"as{it}_g": g3, f"as{it}_x": pt3.x.copy(),
+                            f"as{it}_passive": ass.passive.copy(), f"as{it}_opt": np.array(opt)})
+            for k, v in rec.items():
+                out[f"{key}/{k}"] = np.asarray(v)
+    np.savez_compressed(os.path.join(HERE, "primitives.npz"), **out)
+    print("primitives.npz", len(out), "arrays")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "kat", "optimum", "active", "frontends", "cfg1as", "cfg2", "cfg1"]
+    which = sys.argv[1:] or ["small", "kat", "optimum", "active", "frontends", "cfg1as", "cfg2", "cfg1", "primitives"]
+    if "primitives" in which:
+        primitives()
     if "small" in which:
         small_cases()
     if "kat" in which:
