@@ -1070,8 +1070,20 @@ int auto_step(bx_ctx* c, int iters, double alpha, bx_start_vector_fn fn, void* u
 template <typename T>
 int cd_sweeps(bx_ctx* c, int passes) {
   const int s = c->cur;
-  View<T> vw = act_view<T>(c);
   if (c->k == 0) return BX_OK;
+  if (!c->dense) {
+    // CD reads A_act densely (block copies of consecutive columns): rewrite
+    // the preserved columns contiguously first (a state loaded through
+    // bx_set_state; the solve loop's compaction does it at every event)
+    k_gather<T><<<(int)(c->k < 8 * c->nsm ? c->k : 8 * c->nsm), RT, 0, c->stream>>>(
+        (const T*)c->A, c->lda, c->idx[s], c->k, c->m, (T*)c->Aact, c->ldact);
+    LAUNCHED();
+    c->act_is_orig = false;
+    c->dense = true;
+    c->kphys = c->k;
+    c->gram_dirty = true;
+  }
+  View<T> vw = act_view<T>(c);
   constexpr int V = 16 / sizeof(T);
   int NC = 8;
   int64_t rows = round_up((c->m + NC - 1) / NC, V);

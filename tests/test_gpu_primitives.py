@@ -165,7 +165,11 @@ def test_rounds_through_fine_grained_abi(family, kind, monkeypatch):
     monkeypatch.setenv("BX_NO_SMALL", "1")
     rng = np.random.default_rng(77 + ["nnls", "bvls", "mixed"].index(family))
     a, y, lo, hi = small_instance(rng, 120, 300, family)
-    passes, tol, rounds = 10, 1e-9, 80
+    # FISTA amplifies round-off differences between any two summation orders
+    # (~10x per 10 rounds on these instances, PG stays at 1e-14:
+    # profiles/r02_fista_roundoff_drift.txt), so its per-round 1e-10 check
+    # covers the first 40 rounds
+    passes, tol, rounds = 10, 1e-9, (80 if kind == "pg" else 40)
     o = oracle_solve(a, y, lo, hi, kind=kind, inner_passes=passes, gap_tol=tol, max_rounds=rounds)
     L = nat.lib()
     s = _Session(Problem(a, y, lo, hi))
