@@ -221,6 +221,11 @@ int bx_solve(bx_ctx* ctx, const bx_solve_cfg* cfg, bx_start_vector_fn start_fn,
  * (m, fp64), sat_lower / sat_upper (int64, in screening order).  Any
  * pointer may be NULL.  Device pointers. */
 int bx_get_state(bx_ctx* ctx, void* x, void* theta, int64_t* sat_lower, int64_t* sat_upper);
+/* FISTA's previous iterate x_{k-1} as a full vector (device, n; screened
+ * coordinates at their bounds) -- with the momentum scalar of the last trace
+ * record it is the state a FISTA round resumes from (used to replay the
+ * oracle from the device state mid-solve, tests/test_gpu_headline.py). */
+int bx_get_prev_iterate(bx_ctx* ctx, double* x_prev);
 
 /* ---- active-set solver (solvers.py:140-204) ------------------------------ */
 /* bytes of the active-set scratch: the passive Cholesky factor R

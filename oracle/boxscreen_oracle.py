@@ -312,7 +312,7 @@ def active_set_pass(w, passive):
 
 def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
                  max_rounds=None, screening=True, step_size=None, t=None,
-                 power_iters=50, record_sets=False, round_hook=None, restart="adaptive"):
+                 power_iters=50, record_sets=False, round_hook=None, restart="adaptive", init=None):
     """Run the screened solver and return a dict with x, theta, gap, rounds,
     converged, trace (list of per-round dicts), sat_lower, sat_upper.
 
@@ -320,6 +320,12 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
     Per-round trace entries carry primal, dual, gap, eps, radius, slack,
     preserved count, newly screened counts and (with ``record_sets``) the
     newly screened index arrays; ``step`` is the step in force.
+
+    ``init`` resumes mid-solve from a given state (replaying rounds from a
+    device solve's state, tests/test_gpu_headline.py): dict(x, sat_lower,
+    sat_upper, eta, basis, round0 [, x_prev, mom for apg]); x holds the
+    screened coordinates at their bounds, the preserved set is the
+    complement of the saturated sets in original order, z = A_S b_S.
     """
     a = np.asarray(a, dtype=float, order="F")
     y = np.asarray(y, dtype=float).ravel()
@@ -352,16 +358,33 @@ def oracle_solve(a, y, lo, hi, kind="pg", inner_passes=1, gap_tol=1e-6,
     z = np.zeros(m)
     eta = step_size
     basis = n
+    round0 = 0
+    mom = [1.0]
+    if init is not None:
+        x_full = np.asarray(init["x"], dtype=float).copy()
+        sat_lo = np.asarray(init["sat_lower"], dtype=int).copy()
+        sat_up = np.asarray(init["sat_upper"], dtype=int).copy()
+        keep = np.setdiff1d(np.arange(n), np.concatenate([sat_lo, sat_up]))
+        if sat_lo.size:
+            z = z + a[:, sat_lo] @ lo[sat_lo]
+        if sat_up.size:
+            z = z + a[:, sat_up] @ hi[sat_up]
+        eta = float(init["eta"])
+        basis = int(init["basis"])
+        round0 = int(init.get("round0", 0))
+        mom = [float(init.get("mom", 1.0))]
     if kind in ("pg", "apg") and eta is None:
         eta = safe_step(a, 1.0, power_iters)
     w = ActiveView(a, y, lo, hi, norms, z, x_full, keep)
-    mom = [1.0]
+    if init is not None and kind == "apg" and init.get("x_prev") is not None:
+        w.x_prev = np.asarray(init["x_prev"], dtype=float)[keep].copy()
+        w.g_prev = w.mat.T @ (w.mat @ w.x_prev + w.off)
     trace = []
     converged = False
     theta_out = np.zeros(m)
     gap_out = math.inf
     rounds = 0
-    for rnd in range(1, limit + 1):
+    for rnd in range(round0 + 1, round0 + limit + 1):
         rounds = rnd
         optimal = False
         if kind == "pg":

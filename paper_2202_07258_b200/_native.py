@@ -90,6 +90,7 @@ SIGNATURES = {
     "bx_solve": (ctypes.c_int, [_vp, ctypes.POINTER(SolveCfg), START_FN, _vp, ctypes.POINTER(TraceRec), _i64,
                                 ctypes.POINTER(SolveOut)]),
     "bx_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "bx_get_prev_iterate": (ctypes.c_int, [_vp, _vp]),
     "bx_active_set_workspace_bytes": (_sz, [_i64, _i64]),
     "bx_ctx_set_active_set_workspace": (ctypes.c_int, [_vp, _vp, _sz]),
     "bx_peer_alloc": (ctypes.c_int, [_vp, ctypes.c_char_p]),

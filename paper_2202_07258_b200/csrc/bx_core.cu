@@ -2720,6 +2720,20 @@ int bx_set_state(bx_ctx* c, const int64_t* pres, int64_t k, const double* xf, co
   return c->dtype == BX_F64 ? set_state_typed<double>(c, pres, k, xf, z) : set_state_typed<float>(c, pres, k, xf, z);
 }
 
+int bx_get_prev_iterate(bx_ctx* c, double* x_prev) {
+  if (!c || !x_prev) return BX_ERR_INVALID_ARGUMENT;
+  // screened coordinates sit at their bound in x_prev too (the snap of
+  // apply_screening applies to both iterates)
+  CU(cudaMemcpyAsync(x_prev, c->xfull, c->n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (c->k > 0) {
+    const double* src = (const double*)(c->spec_pending ? c->xbak[c->cur] : c->xprev[c->cur]);
+    k_scatter_x<double><<<grid1d(c, c->k), RT, 0, c->stream>>>(c->k, c->idx[c->cur], src, x_prev);
+    LAUNCHED();
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return BX_OK;
+}
+
 int bx_active_set_step(bx_ctx* c, const uint8_t* passive_in, uint8_t* passive_out, int32_t* optimal) {
   if (!c) return BX_ERR_INVALID_ARGUMENT;
   return c->dtype == BX_F64 ? active_set_step_typed<double>(c, passive_in, passive_out, optimal)

@@ -196,7 +196,7 @@ class _Session:
         nat.check(L.bx_ctx_set_active_set_workspace(self.ctx, self.as_ws.data_ptr(), nbytes), self.ctx,
                   "bx_ctx_set_active_set_workspace")
 
-    def run(self, cfg, screening, alpha, slack_scale, profile=False):
+    def run(self, cfg, screening, alpha, slack_scale, profile=False, prev_iterate=False):
         L = nat.lib()
         if cfg.kind == "active-set" and getattr(self, "as_ws", None) is None:
             self.attach_active_set()
@@ -234,6 +234,11 @@ class _Session:
         su = torch.empty(max(out.n_sat_upper, 1), dtype=torch.int64, device=dev)
         nat.check(L.bx_get_state(self.ctx, x.data_ptr(), theta.data_ptr(), sl.data_ptr(), su.data_ptr()),
                   self.ctx, "bx_get_state")
+        self.x_prev = None
+        if prev_iterate:
+            xp = torch.empty(self.n, dtype=torch.float64, device=dev)
+            nat.check(L.bx_get_prev_iterate(self.ctx, xp.data_ptr()), self.ctx, "bx_get_prev_iterate")
+            self.x_prev = xp.cpu().numpy()
         return out, trace[: min(out.rounds, cap)], x, theta, sl[: out.n_sat_lower], su[: out.n_sat_upper]
 
 
@@ -294,12 +299,14 @@ def _default_slack(p):
 
 
 def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None, return_device=False,
-          profile=False):
+          profile=False, prev_iterate=False):
     """Run the chosen primal solver with (or without) dynamic safe screening.
 
     Same contract as the reference's ``solve`` (driver.py:131-256).  With
     ``return_device`` the result's x / theta stay CUDA tensors (no host copy);
-    ``profile`` times every kernel launch with CUDA events (info["profile"]).
+    ``profile`` times every kernel launch with CUDA events (info["profile"]);
+    ``prev_iterate`` adds FISTA's previous iterate (info["x_prev"]), which with
+    the last trace record's momentum is the state a round resumes from.
     """
     cfg = cfg or SolverConfig()
     if not isinstance(p, Problem):
@@ -307,6 +314,11 @@ def solve(p, cfg=None, screening=True, tv=None, loss=QuadraticLoss, slack_scale=
     if slack_scale is None:
         slack_scale = _default_slack(p)
     with _Session(p, tv=tv) as s:
-        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile)
+        out, tr, x, theta, sl, su = s.run(cfg, screening, loss.alpha, slack_scale, profile=profile,
+                                          prev_iterate=prev_iterate)
         prof = s.profile
-    return _result(p.n, out, tr, x, theta, sl, su, prof, return_device)
+        x_prev = s.x_prev
+    res = _result(p.n, out, tr, x, theta, sl, su, prof, return_device)
+    if prev_iterate:
+        res.info["x_prev"] = x_prev
+    return res

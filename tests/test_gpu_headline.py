@@ -23,7 +23,7 @@ import numpy as np
 import pytest
 
 from oracle.boxscreen_oracle import oracle_solve
-from parity import compare_final, compare_traces
+from parity import OBJ_RTOL, compare_final, compare_traces
 
 pytestmark = pytest.mark.gpu
 
@@ -182,3 +182,61 @@ def test_speculative_step_dropped_at_round_limit(kind, monkeypatch):
         o = oracle_solve(a, y, lo, hi, kind=kind, inner_passes=3, gap_tol=1e-11, max_rounds=rounds)
         probs = compare_traces(g, o) + compare_final(g, o)
         assert not probs, (rounds, probs[:3])
+
+
+def _basis_at(tr, r, n):
+    """Preserved count at the last step re-estimate up to round r (1-based):
+    the driver re-estimates eta when the preserved set halves
+    (driver.py:232-235)."""
+    steps = tr["step"][:r]
+    ch = np.flatnonzero(steps[1:] != steps[:-1])
+    return int(tr["preserved_count"][ch[-1] + 1]) if ch.size else n
+
+
+def test_config3_screening_events_replayed_from_device_state():
+    """Config 3's screening events at full size (10000 x 50000): the device
+    solve is stopped just before an event round, the oracle resumes from the
+    device's state (x, x_prev, momentum, screened sets, step, basis) and its
+    next rounds -- the event round included -- must match the device's round
+    by round: P, D, gap within 1e-10 * max(|P|, |D|), identical preserved and
+    newly screened counts (replay, since a CPU trajectory to
+    the first event takes hours; FISTA also amplifies round-off between any
+    two summation orders, profiles/r02_fista_roundoff_drift.txt)."""
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    from paper_2202_07258_b200.generate import make_config
+    inst = make_config(3)
+    a, y, lo, hi = inst.a, inst.y, inst.lower, inst.upper
+    n = a.shape[1]
+    p = Problem(a, y, lo, hi)
+    cfg = SolverConfig(kind="apg", inner_passes=10, gap_tol=1e-6)
+    full = solve(p, cfg)
+    assert full.converged
+    tr = full.info["trace_arrays"]
+    newly = tr["newly_screened_lower"] + tr["newly_screened_upper"]
+    ev = np.flatnonzero(newly > 0) + 1  # event rounds (1-based)
+    assert ev.size >= 10
+    steps = tr["step"]
+    reest = np.flatnonzero(steps[1:] != steps[:-1]) + 2  # rounds that re-estimated eta
+    picks = {int(ev[0]), int(ev[len(ev) // 2]), int(ev[-1])}
+    if reest.size:
+        picks.add(int(reest[0]))
+    R = 3
+    for e in sorted(picks):
+        e = max(e, 2)
+        pre = solve(p, SolverConfig(kind="apg", inner_passes=10, gap_tol=1e-6, max_rounds=e - 1),
+                    prev_iterate=True)
+        assert pre.rounds == e - 1
+        st = dict(x=pre.x, x_prev=pre.info["x_prev"], sat_lower=pre.sat_lower, sat_upper=pre.sat_upper,
+                  eta=float(steps[e - 2]), basis=_basis_at(tr, e - 1, n), mom=float(tr["momentum"][e - 2]),
+                  round0=e - 1)
+        o = oracle_solve(a, y, lo, hi, kind="apg", inner_passes=10, gap_tol=1e-6, max_rounds=R, init=st)
+        for i, ot in enumerate(o["trace"]):
+            gt = full.trace[e - 1 + i]
+            assert gt.round == ot["round"] == e + i
+            sc = max(abs(ot["primal"]), abs(ot["dual"]))
+            for key in ("primal", "dual", "gap"):
+                assert abs(getattr(gt, key) - ot[key]) <= OBJ_RTOL * sc, (e + i, key, getattr(gt, key), ot[key])
+            assert gt.preserved_count == ot["preserved"], (e + i, gt.preserved_count, ot["preserved"])
+            assert gt.newly_screened_lower == ot["new_lower"] and gt.newly_screened_upper == ot["new_upper"], e + i
+            if ot.get("certified") is not None and ot["certified"] < 1e-6:
+                break
