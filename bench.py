@@ -16,7 +16,12 @@ JSON line keys: value = screened FISTA iterations per second over whole solves
 (inputs resident in HBM), ms_per_step = time-to-gap, e2e = the same through the
 public API from pinned host buffers (H2D of A, y, bounds and D2H of x, theta
 inside the timed region), roofline = the fused FISTA pass kernel timed live
-with CUDA events, cpu_baseline = the oracle port on the host cores.
+with CUDA events, cpu_baseline = the unmodified reference (baseline/_ref) on
+the host cores when it is installed, else the oracle port.  Extra keys
+measure what screening buys on the GPU (time_to_gap_unscreened_s, the
+reference's off/on protocol, bench.py:96-115) and, for config 3, the FISTA
+restart rule BASELINE states (time_to_gap_stated_restart_s: restart on an
+objective increase only).
 """
 
 import argparse
@@ -50,6 +55,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=4, help="solves in the e2e leg (after one untimed)")
+    ap.add_argument("--no-study", action="store_true", help="skip the screening-off / stated-restart solves")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--write-trajectory", action="store_true")
     ap.add_argument("--sharded", action="store_true",
@@ -137,6 +144,78 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # the CPU side: oracle port timed on the host cores (cpu_baseline / reference arm)
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+# the unmodified reference (baseline/_ref, installed from /root/reference/pkg)
+# ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_module():
+    """The reference package ``boxscreen`` from baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "boxscreen")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import boxscreen
+        import boxscreen.solvers  # noqa: F401
+        return boxscreen
+    except Exception:
+        return None
+
+
+def ref_step_rate(bs, inst, k_bins, budget_s, kmax=None):
+    """The reference's own per-iteration work on the solve's trajectory:
+    ``pg_step`` (solvers.py:101-116: clip, A_act x, A_act' r -- the two GEMVs
+    an iteration costs in the reference; it has no FISTA, whose oracle step is
+    the same two products) timed on the reference's Workspace
+    (solvers.py:48-65) over k-column preserved sets at the solve's
+    preserved-count bins, weighted by the iterations the solve spends there.
+    Bins wider than ``kmax`` columns are timed on kmax and scaled by k / kmax
+    (GEMVs are linear in k).  Returns (iterations/s, details)."""
+    a, y, lo, hi = inst.a, inst.y, inst.lower, inst.upper
+    n = a.shape[1]
+    perm = np.random.default_rng(1).permutation(n)
+    total_it = sum(it for _, it in k_bins)
+    per_bin = budget_s / max(1, len(k_bins))
+    details, tsum = [], 0.0
+    for k, it in k_bins:
+        kt = min(k, kmax or k)
+        keep = np.sort(perm[:kt])
+        p = bs.Problem(np.asarray(a[:, keep], dtype=np.float64), y, lo[keep], hi[keep])
+        st = bs.ScreeningState(p)
+        ws = bs.solvers.Workspace(p, st, bs.PrimalPoint(np.clip(np.zeros(kt), lo[keep], hi[keep])))
+        eta = 1e-6  # timing only (a small step keeps the objective monotone); cost is step-independent
+        bs.solvers.pg_step(ws, eta, 1)  # warm
+        t0 = time.perf_counter()
+        done = 0
+        while True:
+            bs.solvers.pg_step(ws, eta, 1)
+            done += 1
+            el = time.perf_counter() - t0
+            if el > per_bin or done >= it:
+                break
+        sec = el / done * (k / kt)
+        details.append(dict(k=int(k), timed_columns=int(kt), iterations_in_solve=int(it), timed_iterations=done,
+                            sec_per_iteration=sec))
+        tsum += it * sec
+        del ws, st, p
+    return total_it / tsum, details
+
+
+def ref_solve_rate(bs, inst, screening, max_rounds=None):
+    """The reference's ``solve`` (driver.py:131-256) on the config, timed by
+    its own convention (trace[-1].elapsed, the offline-gap rule with screening
+    off; bench.py:86-93).  Returns (iterations/s, elapsed, result)."""
+    p = bs.Problem(inst.a, inst.y, inst.lower, inst.upper)
+    cfg = bs.SolverConfig(kind=inst.kind, inner_passes=inst.inner_passes, gap_tol=inst.gap_tol,
+                          max_rounds=max_rounds or 10 ** 6)
+    res = bs.solve(p, cfg, screening=screening)
+    el = res.trace[-1].elapsed
+    iters = res.rounds * inst.inner_passes
+    return iters / el, el, res
+
+
 def cpu_rate(inst, k_bins, budget_s, passes=None, kmax=8000):
     """Oracle FISTA iterations/s over the solve's preserved-set trajectory.
 
@@ -271,10 +350,16 @@ def config_block(cfg_id, inst):
             "step": CFG4_STEP if cfg_id == 4 else "one full solve to certified gap <= gap_tol"}
 
 
+STEP_LABEL = {"pg": "PG passes", "apg": "FISTA passes", "cd": "CD sweeps", "active-set": "active-set iterations"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    bs = reference_module()
+    if bs is not None:
+        return run_reference_unmodified(args, bs, world)
     inst = make_instance(args.config)
     try:
         with open(traj_path(args.config)) as fh:
@@ -298,9 +383,9 @@ def run_reference(args):
     rate = float(np.median(rates))
     cores, model = cpu_info()
     thr = blas_threads()
-    sample = (f"oracle FISTA passes (numpy/OpenBLAS, reference Workspace arithmetic) timed at {len(bins)} "
-              f"preserved-count bins weighted by {src}; {sum(d['timed_iterations'] for d in details)} "
-              f"iterations per step")
+    sample = (f"oracle {STEP_LABEL[inst.kind]} (numpy/OpenBLAS, reference Workspace arithmetic) timed at "
+              f"{len(bins)} preserved-count bins weighted by {src}; "
+              f"{sum(d['timed_iterations'] for d in details)} iterations per step")
     line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": unit_name(args.config),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
@@ -308,6 +393,63 @@ def run_reference(args):
             "config": config_block(args.config, inst),
             "cpu_baseline": {"value": rate, "unit": unit_name(args.config), "cores": thr, "kind": "port", "sample": sample,
                              "cpu_model": model, "nproc": cores, "bins": details},
+            "e2e": {"value": rate, "unit": unit_name(args.config), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_bins(cfg_id, inst):
+    try:
+        with open(traj_path(cfg_id)) as fh:
+            traj = json.load(fh)
+        if traj.get("config") != cfg_id:
+            raise ValueError("trajectory of another config")
+        return ([tuple(b) for b in traj["k_bins"]],
+                f"preserved-count trajectory of the GPU solve (profiles/cfg{cfg_id}_trajectory.json)")
+    except Exception:
+        return [(inst.a.shape[1], 100)], "unscreened working set (no trajectory file)"
+
+
+def run_reference_unmodified(args, bs, world):
+    """--impl reference with the unmodified reference installed in
+    baseline/_ref: its own code on the host cores (all BLAS threads).
+    Configs 3 / 4 (no FISTA / no fp32 in the reference): its pg_step on the
+    solve's preserved-count trajectory; configs 1 / 2: its solve() on a
+    bounded number of rounds per step."""
+    inst = make_instance(args.config)
+    cores, model = cpu_info()
+    thr = blas_threads()
+    extra = {}
+    t0 = time.perf_counter()
+    rates = []
+    if args.config in (3, 4):
+        bins, src = load_bins(args.config, inst)
+        budget = max(3.0, args.cpu_budget / max(1, args.steps))
+        kmax = 16000 if args.config == 4 else None
+        for _ in range(args.steps):
+            r, det = ref_step_rate(bs, inst, bins, budget, kmax=kmax)
+            rates.append(r)
+        sample = (f"unmodified reference pg_step (solvers.py:101-116, 2 GEMVs per iteration) on its Workspace at "
+                  f"{len(bins)} preserved-count bins weighted by {src}; "
+                  f"{sum(d['timed_iterations'] for d in det)} iterations per step"
+                  + ("; fp64 (the reference copies A to fp64), bins > 16000 columns scaled" if args.config == 4 else ""))
+        extra["bins"] = det
+    else:
+        rounds = 2000 if args.config == 1 else 100
+        for _ in range(args.steps):
+            r, _, _ = ref_solve_rate(bs, inst, True, max_rounds=rounds)
+            rates.append(r)
+        sample = (f"unmodified reference solve() (driver.py:131-256), first {rounds} screened rounds per step, "
+                  f"timed by trace[-1].elapsed")
+    wall = time.perf_counter() - t0
+    rate = float(np.median(rates))
+    line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": unit_name(args.config),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config recipe)",
+            "config": config_block(args.config, inst),
+            "cpu_baseline": {"value": rate, "unit": unit_name(args.config), "cores": thr, "kind": "reference",
+                             "sample": sample, "cpu_model": model, "nproc": cores, **extra},
             "e2e": {"value": rate, "unit": unit_name(args.config), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -684,7 +826,8 @@ def run_ours(args):
         p_host = Problem(inst.a, inst.y, inst.lower, inst.upper, dtype=inst.a.dtype, pin=True)
         h2d = p_host.a_matrix.nbytes + 8 * (m + 2 * n)
         e_it, e_t, d2h = 0, 0.0, 0
-        for s in range(args.steps + 1):
+        e_steps = min(args.steps, args.e2e_steps)
+        for s in range(e_steps + 1):
             p_host.release_device()
             torch.cuda.synchronize()
             t0 = torch.cuda.Event(enable_timing=True)
@@ -700,16 +843,57 @@ def run_ours(args):
             d2h = r.x.nbytes + r.theta.nbytes + 8 * (r.sat_lower.size + r.sat_upper.size)
         p_host.release_device()
         e2e = {"value": world * e_it / e_t, "unit": unit_name(args.config), "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000.0 * e_t / args.steps}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000.0 * e_t / e_steps, "steps": e_steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, det = cpu_rate(inst, bins, args.cpu_budget)
         cores, model = cpu_info()
-        cpu = {"value": rate, "unit": unit_name(args.config), "cores": blas_threads(), "kind": "port",
-               "sample": (f"oracle FISTA passes at {len(bins)} preserved-count bins of this solve, "
-                          f"{sum(d['timed_iterations'] for d in det)} iterations, ~{args.cpu_budget:.0f}s"),
-               "cpu_model": model, "nproc": cores}
+        bs = reference_module()
+        if bs is not None and args.config in (3, 4):
+            rate, det = ref_step_rate(bs, inst, bins, args.cpu_budget, kmax=16000 if args.config == 4 else None)
+            cpu = {"value": rate, "unit": unit_name(args.config), "cores": blas_threads(), "kind": "reference",
+                   "sample": (f"unmodified reference pg_step (solvers.py:101-116, 2 GEMVs per iteration) at "
+                              f"{len(bins)} preserved-count bins of this solve, "
+                              f"{sum(d['timed_iterations'] for d in det)} iterations, ~{args.cpu_budget:.0f}s"),
+                   "cpu_model": model, "nproc": cores}
+        elif bs is not None:
+            rate, el, rr = ref_solve_rate(bs, inst, True, max_rounds=2000 if args.config == 1 else 100)
+            cpu = {"value": rate, "unit": unit_name(args.config), "cores": blas_threads(), "kind": "reference",
+                   "sample": (f"unmodified reference solve(), first {rr.rounds} screened rounds "
+                              f"({rr.rounds * inst.inner_passes} {STEP_LABEL[inst.kind]}), trace[-1].elapsed"),
+                   "cpu_model": model, "nproc": cores}
+        else:
+            rate, det = cpu_rate(inst, bins, args.cpu_budget)
+            cpu = {"value": rate, "unit": unit_name(args.config), "cores": blas_threads(), "kind": "port",
+                   "sample": (f"oracle {STEP_LABEL[inst.kind]} at {len(bins)} preserved-count bins of this solve, "
+                              f"{sum(d['timed_iterations'] for d in det)} iterations, ~{args.cpu_budget:.0f}s"),
+                   "cpu_model": model, "nproc": cores}
+
+    # what screening buys on the GPU (the reference's paired off / on
+    # protocol, bench.py:96-115) and, for config 3, BASELINE's stated FISTA
+    # restart rule: one solve each, timed with CUDA events
+    study = {}
+    if rank == 0 and not args.no_study and args.config in (1, 2, 3):
+        import dataclasses
+
+        def timed(c, screening=True):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = solve(p_dev, c, screening=screening, return_device=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / 1000.0, r
+
+        t_off, r_off = timed(cfg, screening=False)
+        study.update(time_to_gap_unscreened_s=t_off, iterations_unscreened=r_off.info["iterations"],
+                     converged_unscreened=r_off.converged,
+                     screening_speedup=t_off / (ms_per_step / 1000.0))
+        if args.config == 3:
+            t_fn, r_fn = timed(dataclasses.replace(cfg, restart="function"))
+            study.update(time_to_gap_stated_restart_s=t_fn, iterations_stated_restart=r_fn.info["iterations"],
+                         converged_stated_restart=r_fn.converged, certified_gap_stated_restart=r_fn.gap,
+                         stated_restart_rule="FISTA restart on an objective increase only (BASELINE config 3)")
 
     r0 = results[0]
     line = {"metric": metric_name(args.config), "value": value, "unit": unit_name(args.config), "n_gpus": world,
@@ -720,7 +904,7 @@ def run_ours(args):
             "config": config_block(args.config, inst),
             "time_to_gap_s": ms_per_step / 1000.0, "converged": conv, "rounds": r0.rounds,
             "iterations_per_solve": r0.info["iterations"], "final_preserved": r0.trace[-1].preserved_count,
-            "certified_gap": r0.gap, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "certified_gap": r0.gap, "gpu_launches": launches, **study, "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
