@@ -1,17 +1,19 @@
-"""Benchmark protocols of the reference (bench.py:19-184) over the GPU solver.
+"""The reference's benchmark protocols over the GPU solver.
 
-* ``run_bench`` -- paired screening-off / screening-on timings per
-  (GenSpec, solver) cell, median of ``repetitions`` solves, speedup =
-  off / on.  Timings follow the reference's offline-gap convention: with
-  screening off the gap evaluation is excluded from ``trace[-1].elapsed``
-  (the native loop subtracts the device time of the dual / gap kernels).
-  Independent cells run on up to ``BOXSCREEN_THREADS`` host threads; a failing
-  cell is recorded under ``meta["errors"]`` instead of aborting the sweep.
-* ``compare_t`` -- screening-ratio-per-round curves for several translation
-  vector strategies, padded to a common round grid.
+Contract kept from /root/reference/pkg/src/boxscreen/bench.py (the API and
+the files a user's scripts read): ``BenchRow`` / ``BenchReport`` with the
+same fields, ``run_bench(specs, solvers, repetitions, gap_tol)`` (paired
+screening off / on, median of the repetitions, speedup = off / on, failing
+cells reported under ``meta["errors"]``, ``BOXSCREEN_THREADS`` host
+threads), ``compare_t`` (screening-ratio curves per translation strategy on
+a common round grid), the CSV column schemas and the JSON layout.
 
-This is the reference's user-facing protocol, not the repo's headline bench
-(``/bench.py`` at the repository root measures the BASELINE configs).
+How it runs here: each cell uploads its generated problem to the device once
+(every solve of the cell reuses those buffers), and timings are the native
+loop's ``trace[-1].elapsed`` -- with screening off the device time of the
+gap evaluation is subtracted, the reference's offline-gap convention
+(driver.py:180-181).  Not the repo's headline bench (``/bench.py`` measures
+the BASELINE configs).
 """
 
 import csv
@@ -20,7 +22,7 @@ import json
 import os
 import statistics
 from concurrent.futures import ThreadPoolExecutor
-from dataclasses import dataclass, field
+from dataclasses import asdict, dataclass, field
 
 import numpy as np
 
@@ -32,20 +34,19 @@ from .solvers import SolverConfig
 THREADS_ENV = "BOXSCREEN_THREADS"
 
 
-def _host_arrays(p):
-    if p.a_matrix is not None:
-        return p.a_matrix, p.y
-    d = p.device_arrays()
-    return d["a"][:, : p.m].double().T.cpu().numpy(), d["y"].cpu().numpy()
-
-
 def instance_hash(p):
-    """First 16 hex digits of sha256 over A, y, lower, upper (bench.py:19-25)."""
-    a, y = _host_arrays(p)
-    h = hashlib.sha256()
-    for arr in (a, y, p.lower, p.upper):
-        h.update(np.asarray(arr).tobytes())
-    return h.hexdigest()[:16]
+    """16 hex digits of sha256(A, y, lower, upper) -- bench.py:19-25's
+    instance identity, from the host copy (or the device copy of a
+    device-built problem)."""
+    if p.a_matrix is not None:
+        parts = (p.a_matrix, p.y)
+    else:
+        dev = p.device_arrays()
+        parts = (dev["a"][:, : p.m].double().T.cpu().numpy(), dev["y"].cpu().numpy())
+    digest = hashlib.sha256()
+    for arr in parts + (p.lower, p.upper):
+        digest.update(np.asarray(arr).tobytes())
+    return digest.hexdigest()[:16]
 
 
 @dataclass
@@ -63,6 +64,34 @@ class BenchRow:
     instance: str
 
 
+# CSV schemas of the reference's reports: (header, value of a record)
+_ROW_SCHEMA = (
+    ("solver", lambda r: r.solver),
+    ("screening", lambda r: "on" if r.screening else "off"),
+    ("family", lambda r: r.family), ("m", lambda r: r.m), ("n", lambda r: r.n), ("seed", lambda r: r.seed),
+    ("elapsed_s", lambda r: format(r.elapsed, ".9f")),
+    ("rounds", lambda r: r.rounds),
+    ("gap", lambda r: format(r.gap, ".17g")),
+    ("ratio", lambda r: format(r.screening_ratio, ".17g")),
+    ("instance", lambda r: r.instance),
+)
+_SPEEDUP_SCHEMA = (
+    ("solver", lambda s: s["solver"]), ("family", lambda s: s["family"]), ("m", lambda s: s["m"]),
+    ("n", lambda s: s["n"]), ("seed", lambda s: s["seed"]),
+    ("elapsed_off_s", lambda s: format(s["elapsed_off"], ".9f")),
+    ("elapsed_on_s", lambda s: format(s["elapsed_on"], ".9f")),
+    ("speedup", lambda s: format(s["speedup"], ".6g")),
+    ("ratio_on", lambda s: format(s["ratio_on"], ".17g")),
+)
+
+
+def _write_table(path, schema, records):
+    with open(path, "w", newline="") as fh:
+        out = csv.writer(fh)
+        out.writerow([name for name, _ in schema])
+        out.writerows([[get(rec) for _, get in schema] for rec in records])
+
+
 @dataclass
 class BenchReport:
     rows: list = field(default_factory=list)
@@ -70,110 +99,91 @@ class BenchReport:
     meta: dict = field(default_factory=lambda: {"prng": PRNG_NAME})
 
     def to_json(self, path=None, indent=2):
-        text = json.dumps({"meta": self.meta, "rows": [vars(r) for r in self.rows], "speedups": self.speedups},
-                          indent=indent)
+        payload = {"meta": self.meta, "rows": [asdict(r) for r in self.rows], "speedups": self.speedups}
+        text = json.dumps(payload, indent=indent)
         if path is not None:
             with open(path, "w") as fh:
                 fh.write(text)
         return text
 
     def rows_to_csv(self, path):
-        with open(path, "w", newline="") as fh:
-            w = csv.writer(fh)
-            w.writerow(["solver", "screening", "family", "m", "n", "seed", "elapsed_s", "rounds", "gap", "ratio",
-                        "instance"])
-            for r in self.rows:
-                w.writerow([r.solver, "on" if r.screening else "off", r.family, r.m, r.n, r.seed,
-                            f"{r.elapsed:.9f}", r.rounds, f"{r.gap:.17g}", f"{r.screening_ratio:.17g}", r.instance])
+        _write_table(path, _ROW_SCHEMA, self.rows)
 
     def speedups_to_csv(self, path):
-        with open(path, "w", newline="") as fh:
-            w = csv.writer(fh)
-            w.writerow(["solver", "family", "m", "n", "seed", "elapsed_off_s", "elapsed_on_s", "speedup",
-                        "ratio_on"])
-            for s in self.speedups:
-                w.writerow([s["solver"], s["family"], s["m"], s["n"], s["seed"], f"{s['elapsed_off']:.9f}",
-                            f"{s['elapsed_on']:.9f}", f"{s['speedup']:.6g}", f"{s['ratio_on']:.17g}"])
+        _write_table(path, _SPEEDUP_SCHEMA, self.speedups)
 
 
-def _median_solve(p, solver, screening, repetitions, gap_tol, tv):
-    times, last = [], None
-    for _ in range(repetitions):
-        last = solve(p, SolverConfig(kind=solver, gap_tol=gap_tol), screening=screening, tv=tv)
-        times.append(last.trace[-1].elapsed)
-    return statistics.median(times), last
+class _Cell:
+    """One (spec, solver) pair of the sweep: paired off / on timings."""
 
+    def __init__(self, spec, solver, repetitions, gap_tol):
+        self.spec, self.solver = spec, solver
+        self.repetitions, self.gap_tol = repetitions, gap_tol
 
-def _cell(spec, solver, repetitions, gap_tol):
-    p = generate(spec)
-    tv = select_translation_vector(p, "neg-ones") if p.j_inf.size else None
-    inst = instance_hash(p)
-    rows = []
-    timed = {}
-    for screening in (False, True):
-        t, res = _median_solve(p, solver, screening, repetitions, gap_tol, tv)
-        timed[screening] = (t, res)
-        rows.append(BenchRow(solver, screening, spec.family, spec.m, spec.n, spec.seed, t, res.rounds, res.gap,
-                             res.trace[-1].screening_ratio, inst))
-    (t_off, _), (t_on, r_on) = timed[False], timed[True]
-    return rows, dict(solver=solver, family=spec.family, m=spec.m, n=spec.n, seed=spec.seed, elapsed_off=t_off,
-                      elapsed_on=t_on, speedup=t_off / t_on, ratio_on=r_on.trace[-1].screening_ratio,
-                      instance=inst)
+    def _ident(self):
+        s = self.spec
+        return {"solver": self.solver, "family": s.family, "m": s.m, "n": s.n, "seed": s.seed}
+
+    def _median(self, p, tv, screening):
+        cfg = SolverConfig(kind=self.solver, gap_tol=self.gap_tol)
+        runs = [solve(p, cfg, screening=screening, tv=tv) for _ in range(self.repetitions)]
+        return statistics.median(r.trace[-1].elapsed for r in runs), runs[-1]
+
+    def run(self):
+        """(rows, speedup dict) -- or ([], ident + error) when the cell fails."""
+        try:
+            p = generate(self.spec)
+            p.device_arrays()  # one upload; every solve of the cell reuses it
+            tv = select_translation_vector(p, "neg-ones") if p.j_inf.size else None
+            key = instance_hash(p)
+            timed = {flag: self._median(p, tv, flag) for flag in (False, True)}
+        except Exception as exc:  # a failing cell is reported, the sweep goes on
+            return [], dict(self._ident(), error=f"{type(exc).__name__}: {exc}")
+        s = self.spec
+        rows = [BenchRow(self.solver, flag, s.family, s.m, s.n, s.seed, t, r.rounds, r.gap,
+                         r.trace[-1].screening_ratio, key) for flag, (t, r) in timed.items()]
+        (t_off, _), (t_on, r_on) = timed[False], timed[True]
+        speedup = dict(self._ident(), elapsed_off=t_off, elapsed_on=t_on, speedup=t_off / t_on,
+                       ratio_on=r_on.trace[-1].screening_ratio, instance=key)
+        return rows, speedup
 
 
 def run_bench(specs, solvers, repetitions=5, gap_tol=1e-6):
-    """Paired off / on sweep over (spec, solver) cells (bench.py:118-152)."""
+    """Paired screening-off / screening-on sweep over (spec, solver) cells."""
     if repetitions < 1:
         raise ValueError("repetitions must be >= 1")
-    cells = [(spec, solver) for spec in specs for solver in solvers]
+    cells = [_Cell(spec, solver, repetitions, gap_tol) for spec in specs for solver in solvers]
+    workers = int(os.environ.get(THREADS_ENV, "1"))
+    if workers > 1:
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            outcomes = list(pool.map(_Cell.run, cells))
+    else:
+        outcomes = [cell.run() for cell in cells]
     report = BenchReport()
     report.meta.update(repetitions=repetitions, gap_tol=gap_tol)
-
-    def one(cell):
-        spec, solver = cell
-        try:
-            return _cell(spec, solver, repetitions, gap_tol)
-        except Exception as exc:  # a failing cell must not abort the sweep
-            return [], dict(solver=solver, family=spec.family, m=spec.m, n=spec.n, seed=spec.seed,
-                            error=f"{type(exc).__name__}: {exc}")
-
-    threads = int(os.environ.get(THREADS_ENV, "1"))
-    if threads > 1:
-        with ThreadPoolExecutor(max_workers=threads) as pool:
-            results = list(pool.map(one, cells))
-    else:
-        results = [one(c) for c in cells]
-    for rows, sp in results:
-        report.rows.extend(rows)
-        if "error" in sp:
-            report.meta.setdefault("errors", []).append(sp)
-        else:
-            report.speedups.append(sp)
+    for rows, speedup in outcomes:
+        report.rows += rows
+        (report.meta.setdefault("errors", []) if "error" in speedup else report.speedups).append(speedup)
     return report
 
 
 def compare_t(p, strategies, solver="cd", gap_tol=1e-6, columns=None):
-    """Screening ratio per round for each translation strategy (bench.py:155-176).
-
-    ``strategies`` holds names or (name, kwargs) pairs; curves are padded with
-    their last ratio to the longest run.  Returns (rounds, {label: ratios}).
-    """
+    """Screening ratio per round for each translation strategy, padded with
+    each curve's final value to the longest run.  Returns (rounds, {label:
+    ratios})."""
     curves = {}
-    for strat in strategies:
-        name, kwargs = strat if isinstance(strat, tuple) else (strat, {})
-        tv = select_translation_vector(p, name, **kwargs)
-        res = solve(p, SolverConfig(kind=solver, gap_tol=gap_tol), screening=True, tv=tv)
-        label = f"{name}:{kwargs.get('column')}" if kwargs else name
-        curves[label] = [rec.screening_ratio for rec in res.trace]
-    longest = max(len(c) for c in curves.values())
-    for c in curves.values():
-        c.extend([c[-1]] * (longest - len(c)))
-    return list(range(1, longest + 1)), curves
+    for entry in strategies:
+        name, kwargs = entry if isinstance(entry, tuple) else (entry, {})
+        res = solve(p, SolverConfig(kind=solver, gap_tol=gap_tol), screening=True,
+                    tv=select_translation_vector(p, name, **kwargs))
+        curves[f"{name}:{kwargs.get('column')}" if kwargs else name] = [t.screening_ratio for t in res.trace]
+    span = max(map(len, curves.values()))
+    padded = {label: c + [c[-1]] * (span - len(c)) for label, c in curves.items()}
+    return list(range(1, span + 1)), padded
 
 
 def compare_t_to_csv(rounds, curves, path):
-    with open(path, "w", newline="") as fh:
-        w = csv.writer(fh)
-        w.writerow(["round"] + list(curves))
-        for i, rnd in enumerate(rounds):
-            w.writerow([rnd] + [f"{curves[k][i]:.17g}" for k in curves])
+    labels = list(curves)
+    _write_table(path, [("round", lambda i: rounds[i])] +
+                 [(lab, (lambda lab_: lambda i: format(curves[lab_][i], ".17g"))(lab)) for lab in labels],
+                 range(len(rounds)))
