@@ -58,7 +58,7 @@ def solve_batched(a, Y, passes=10, rounds=10, gap_tol=1e-6, screening=True, eta=
     lda = m + (m % 2)
     a_dev = torch.zeros((n, lda), dtype=torch.float64, device=dev)
     a_dev[:, :m].copy_(a_t.t().to(dev))
-    y_dev = y_t.t().contiguous().to(dev)   # (K, m) == column-major Y, ldy = m
+    y_dev = y_t.t().contiguous().to(dev, torch.float64)   # (K, m) == column-major Y, ldy = m
     if eta is None:
         eta = auto_step_size(a_dev[:, :m].t(), 1.0)
     nbytes = L.bx_batched_workspace_bytes(m, n, K)

@@ -340,7 +340,11 @@ struct bx_ctx {
   bool have_apg_state = false;
   unsigned* bar = nullptr;  // grid barrier of the cooperative small-round kernel
   int* done = nullptr;      // small-round kernel: completed rounds, event flag, residual parity
-  double* dtrace = nullptr; // small-round kernel: per-round trace records [kSmallRounds][8]
+  double* dtrace = nullptr; // small-round kernel / graph rounds: per-round records [kSmallRounds][TRACE_W]
+  unsigned long long* stamps = nullptr;  // [0] batch start, [1..2] dual point begin / end, [3] excluded ns
+  bool dual_stamps = false;  // (graph capture, screening off) stamp the dual point with k_stamp
+  std::chrono::steady_clock::time_point batch_t;  // host clock when a device-resident batch was launched
+  cudaEvent_t* dual_ev = nullptr;  // (host loop, screening off) events around the dual point
   bool dot_done = false;    // the round kernel already produced g and the eps partials
   int dot_G = 0;
   int64_t graph_body_kernels = 0;  // nodes of the captured round (launch accounting)
@@ -556,7 +560,8 @@ void carve(bx_ctx* c, Carver& w) {
   c->part = w.take((size_t)c->Gmax * c->ldp * 8);  // fp64 sized: also the small-round path's partial rows
   c->bar = (unsigned*)w.take(4 * kMaxRanks * 4);
   c->done = (int*)w.take(64);
-  c->dtrace = (double*)w.take(kSmallRounds * 8 * 8);
+  c->dtrace = (double*)w.take(kSmallRounds * TRACE_W * 8);
+  c->stamps = (unsigned long long*)w.take(8 * 8);
   c->bpart = (double*)w.take(c->Gmax * 8 * 4);
   c->bpart2 = (double*)w.take(4096 * 8);
   c->bpart3 = (double*)w.take(4096 * 4 * 8);
@@ -1158,6 +1163,7 @@ int launch_small_R(bx_ctx* c, SmallArgs& a, int G, size_t smem) {
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&a};
   CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), c->stream));  // the launch's barrier counter
+  c->batch_t = std::chrono::steady_clock::now();
   const int e0 = prof_begin(c);
   CU(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(SM_NT), args, smem, c->stream));
   LAUNCHED();
@@ -1242,6 +1248,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   a.theta = (double*)c->theta;
   a.dpart = c->bpart3 + 8 * c->Gmax;
   a.trace = c->dtrace;
+  a.stamp0 = c->stamps;
   a.done = c->done;
   a.tol = lp.tol;
   a.relative_gap = lp.relative_gap;
@@ -1320,7 +1327,8 @@ static GraphKey graph_key(const bx_ctx* c, int kind, int passes, int screening) 
 
 struct GraphEndArgs {
   DevScalars* sc;
-  double* trace;  // [limit][8]
+  double* trace;  // [limit][TRACE_W]
+  unsigned long long* stamps;  // [1..2] the round's dual-point stamps, [3] excluded ns so far
   int* done;      // [0] event-free rounds, [1] event flag
   cudaGraphConditionalHandle h;
   const int* limit;  // device: rounds allowed in this launch
@@ -1337,7 +1345,11 @@ __global__ void k_graph_round_end(GraphEndArgs a) {
   const bool ev = a.sc->err != 0 || a.sc->err_spec != 0 || d.gap_raw < -1e-9 || d.gap < tol_r ||
                   (a.screening && (a.sc->g_lo + a.sc->g_up) > 0);
   if (!ev) {
-    double* tr = a.trace + 8 * q;
+    double* tr = a.trace + TRACE_W * q;
+    const unsigned long long now = globaltimer();
+    if (!a.screening) a.stamps[3] += a.stamps[2] - a.stamps[1];
+    tr[7] = (double)now;
+    tr[8] = (double)a.stamps[3];
     tr[0] = d.primal;
     tr[1] = d.dual;
     tr[2] = d.gap;
@@ -1478,10 +1490,13 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
             c->last_Ge, c->last_kind};
     int st = primal_passes<T>(c, kind, passes);
     if (st == BX_OK && spec) st = step_pass<T>(c, kind, true);
+    c->dual_stamps = !screening;
     if (st == BX_OK) st = dual_screen<T>(c, screening, slack_scale, alpha);
+    c->dual_stamps = false;
     GraphEndArgs ga;
     ga.sc = c->sc;
     ga.trace = c->dtrace;
+    ga.stamps = c->stamps;
     ga.done = c->done;
     ga.h = h;
     ga.limit = c->done + 2;
@@ -1521,6 +1536,10 @@ int graph_rounds(bx_ctx* c, GraphState& gs, int kind, int passes, int limit, dou
   }
   const int hd0[3] = {0, 0, limit};
   CU(cudaMemcpyAsync(c->done, hd0, sizeof(hd0), cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemsetAsync(c->stamps, 0, 8 * sizeof(unsigned long long), c->stream));
+  c->batch_t = std::chrono::steady_clock::now();
+  k_stamp<<<1, 1, 0, c->stream>>>(c->stamps);  // the batch's start on the device clock
+  LAUNCHED();
   // run on the private stream, joined both ways with the caller's stream
   CU(cudaEventRecord(gs.join[0], c->stream));
   CU(cudaStreamWaitEvent(gs.cs, gs.join[0], 0));
@@ -1810,9 +1829,21 @@ int dual_screen(bx_ctx* c, int screening, double slack_scale, double alpha) {
   c->dot_spec = false;
   if (!spec) c->g_valid = true;  // (after a speculative step g is at x_prev, not x)
   const double* r = spec ? (const double*)c->rbak : (const double*)c->r;
+  // the gap evaluation proper -- the gradient above is the step's, as in the
+  // reference's pg_step -- is what the offline-gap convention excludes
+  if (c->dual_stamps) {
+    k_stamp<<<1, 1, 0, c->stream>>>(c->stamps + 1);
+    LAUNCHED();
+  }
+  if (c->dual_ev) CU(cudaEventRecord(c->dual_ev[0], c->stream));
   TRY(dual_point<T>(c, spec ? 2 : 0, r, (const double*)c->tgt, (double*)c->theta, (const double*)c->g,
                     (const double*)c->att[s], (const double*)c->lo[s], (const double*)c->hi[s], (double*)c->v, c->k,
                     spec ? c->epart : c->bpart, G, slack_scale, alpha));
+  if (c->dual_ev) CU(cudaEventRecord(c->dual_ev[1], c->stream));
+  if (c->dual_stamps) {
+    k_stamp<<<1, 1, 0, c->stream>>>(c->stamps + 2);
+    LAUNCHED();
+  }
   c->theta_is_cert = false;
   if (screening && c->k > 0) {
     const int nbs = (int)((c->k + RT - 1) / RT);
@@ -2194,28 +2225,35 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
                             slack_scale, alpha, &ran, &done, &ev));
       if (ran) {
         if (done > 0) {
-          std::vector<double> tr(8 * (size_t)done);
+          std::vector<double> tr(TRACE_W * (size_t)done);
+          unsigned long long stamp0 = 0;
           CU(cudaMemcpyAsync(tr.data(), c->dtrace, tr.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+          CU(cudaMemcpyAsync(&stamp0, c->stamps, sizeof(stamp0), cudaMemcpyDeviceToHost, c->stream));
           CU(cudaStreamSynchronize(c->stream));
-          const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() - excluded;
+          // each round's elapsed from the device clock: the batch's host
+          // launch time + the round's end on the device clock, minus the gap
+          // evaluations excluded so far (screening off)
+          const double tb = std::chrono::duration<double>(c->batch_t - t0).count();
           for (int q = 0; q < done && trace && ntrace < cap; ++q) {
+            const double* row = tr.data() + (size_t)TRACE_W * q;
             bx_trace_rec& t = trace[ntrace++];
             t.round = rnd + q;
-            t.elapsed = el;
-            t.primal = tr[8 * q + 0];
-            t.dual = tr[8 * q + 1];
-            t.gap = tr[8 * q + 2];
+            t.elapsed = tb + 1e-9 * (row[7] - (double)stamp0) - excluded - 1e-9 * row[8];
+            t.primal = row[0];
+            t.dual = row[1];
+            t.gap = row[2];
             t.preserved_count = kg;
             t.newly_screened_lower = t.newly_screened_upper = 0;
-            t.eps = tr[8 * q + 3];
-            t.radius = tr[8 * q + 4];
+            t.eps = row[3];
+            t.radius = row[4];
             t.step = eta;
             t.certified_gap = NAN;
-            t.momentum = tr[8 * q + 5];
-            t.restarts = (int64_t)tr[8 * q + 6];
+            t.momentum = row[5];
+            t.restarts = (int64_t)row[6];
           }
-          gap_out = tr[8 * (done - 1) + 2];
-          last_restarts = (int64_t)tr[8 * (done - 1) + 6];
+          excluded += 1e-9 * tr[(size_t)TRACE_W * (done - 1) + 8];
+          gap_out = tr[(size_t)TRACE_W * (done - 1) + 2];
+          last_restarts = (int64_t)tr[(size_t)TRACE_W * (done - 1) + 6];
           iters += (int64_t)done * passes;
           rnd += done;
           rounds = rnd - 1;
@@ -2238,10 +2276,11 @@ int solve_typed(bx_ctx* c, const bx_solve_cfg* cfg, bx_start_vector_fn fn, void*
     }
     // offline-gap convention (driver.py:180-181, 237-238): without screening
     // the gap evaluation is excluded from the trace's elapsed time -- here the
-    // device time of the dual / certificate kernels, bracketed by events
-    if (!cfg->screening) CU(cudaEventRecord(gap_ev[0], c->stream));
+    // device time of the dual-point / certificate kernels, bracketed by events
+    // (the gradient is the step's own, as in the reference's pg_step)
+    c->dual_ev = cfg->screening ? nullptr : gap_ev.e;
     TRY(dual_screen<T>(c, cfg->screening, slack_scale, alpha));
-    if (!cfg->screening) CU(cudaEventRecord(gap_ev[1], c->stream));
+    c->dual_ev = nullptr;
     TRY(sync_scalars<T>(c));
     TRY(check_dev_err(c));
     if (!cfg->screening) {

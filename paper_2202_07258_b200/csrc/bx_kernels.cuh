@@ -39,6 +39,19 @@ constexpr int CMAX = 8;            // columns per ring slot (max)
 constexpr int SMAX = 8;            // ring slots (max)
 constexpr int RT = 256;            // block size of the vector kernels
 constexpr int PASS_STAGED = 7;     // per-column state arrays a pass may stage in shared memory
+// device-resident round records (small-round kernel, graph rounds): primal,
+// dual, gap, eps, radius, momentum, restarts, %globaltimer at the round's
+// end (ns), gap-evaluation time excluded so far in the batch (ns, screening
+// off: the reference's offline-gap convention, driver.py:180-181)
+constexpr int TRACE_W = 10;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_stamp(unsigned long long* slot) { *slot = globaltimer(); }
 
 template <typename T> struct V16;
 template <> struct V16<double> { using type = double2; static constexpr int n = 2; };

@@ -65,7 +65,8 @@ struct SmallArgs {
   const double* tgt;  // y - z (rows)
   double* theta;      // dual point (rows)
   double* dpart;      // [G][8] dual / count partials
-  double* trace;      // [max_rounds][8] per completed round
+  double* trace;      // [max_rounds][TRACE_W] per completed round
+  unsigned long long* stamp0;  // %globaltimer at the kernel's start
   int* done;          // [2]: completed event-free rounds, event flag
   double tol;
   int relative_gap;
@@ -212,6 +213,8 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
 
   int done_rounds = 0, event = 0;
   bool perr = false;
+  if (b == 0 && tid == 0 && a.stamp0) *a.stamp0 = globaltimer();
+  double excl_ns = 0.0;  // dual-point time of this launch (block 0's view; screening off)
   // this thread's rows (tid + q * SM_NT) of the current residual, loaded
   // right after the barrier that completes them -- in the same L2 round trip
   // as the objective fold instead of one after it
@@ -434,6 +437,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   }
   // ---- device dual point (driver.py:183-201), gap, stop and sphere tests ----
   grid_barrier(a.bar, nbar);
+  const unsigned long long t_dual0 = (b == 0 && tid == 0) ? globaltimer() : 0ull;
   if (warp == 0) {
     double e = 0.0;
     for (int q = lane; q < G; q += 32) e = fmax(e, __ldcg(&a.epart[q]));
@@ -529,7 +533,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     break;
   }
   if (b == 0 && tid == 0) {
-    double* tr = a.trace + 8 * rnd;
+    const unsigned long long t_end = globaltimer();
+    if (!a.screening) excl_ns += (double)(t_end - t_dual0);
+    double* tr = a.trace + TRACE_W * rnd;
     tr[0] = P;
     tr[1] = dual;
     tr[2] = gap;
@@ -537,6 +543,8 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     tr[4] = radius;
     tr[5] = t_mom;
     tr[6] = (double)a.sc->restarts;
+    tr[7] = (double)t_end;
+    tr[8] = excl_ns;
   }
   ++done_rounds;
   gv = 1;  // the next round starts from this round's screening gradient

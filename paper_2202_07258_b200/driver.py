@@ -112,6 +112,10 @@ class _Session:
         self.t_dev = None
         if tv is not None:
             self.t_dev = torch.as_tensor(np.asarray(tv.t, dtype=np.float64), device=a.device).contiguous()
+        if stream is not None:
+            # the device arrays (upload / layout copy) and t were produced on
+            # the current stream: order the context's first kernels after them
+            stream.wait_stream(torch.cuda.current_stream(a.device))
         self.ctx = ctypes.c_void_p()
         st = L.bx_ctx_create(ctypes.byref(self.ctx), self.m, self.n, self.dtype_code, a.data_ptr(), lda,
                              d["y"].data_ptr(), d["lo"].data_ptr(), d["hi"].data_ptr(),

@@ -264,3 +264,31 @@ def test_objective_non_increasing(kind, family):
     primal = [t.primal for t in res.trace]
     assert len(primal) >= 10
     assert all(b <= a_ + 1e-12 for a_, b in zip(primal, primal[1:]))
+
+
+@pytest.mark.parametrize("path", ["resident", "graph"])
+@pytest.mark.parametrize("screening", [True, False])
+def test_trace_elapsed_per_round_on_device_batches(path, screening, monkeypatch):
+    """Rounds that ran inside one device-resident batch (small-round kernel
+    or CUDA-graph rounds) get their own elapsed from the device clock -- not
+    one value for the whole batch -- and with screening off the gap
+    evaluation is left out of it (driver.py:180-181): elapsed is
+    non-decreasing, mostly strictly increasing, and below the wall time."""
+    import time
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    from paper_2202_07258_b200.generate import make_config
+    if path == "graph":
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+        inst = make_config(3, m=2000, n=6000)
+    else:
+        monkeypatch.delenv("BX_NO_SMALL", raising=False)
+        inst = make_config(1, m=300, n=600)
+    p = Problem(inst.a, inst.y, inst.lower, inst.upper)
+    t0 = time.perf_counter()
+    res = solve(p, SolverConfig(kind="apg", inner_passes=10, gap_tol=1e-12, max_rounds=120), screening=screening)
+    wall = time.perf_counter() - t0
+    el = np.array([t.elapsed for t in res.trace])
+    assert len(el) == 120
+    assert np.all(np.diff(el) >= -1e-6), np.diff(el).min()
+    assert np.mean(np.diff(el) > 0) > 0.9  # no step function over a batch
+    assert 0 < el[-1] <= wall
