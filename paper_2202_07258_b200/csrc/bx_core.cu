@@ -790,10 +790,10 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
     // algorithmic bytes: every streamed column once, the per-column state the
     // mode touches, the input row vector(s) and the output row vector once
     static const int col_vec[] = {3, 5, 5, 8, 0, 1};  // U_DOT..U_AX, elements per column
-    const double es = (double)sizeof(T);
-    double bytes = (double)vw.k * (double)c->m * es + (double)vw.k * col_vec[upd] * es;
-    if (dot) bytes += (double)c->m * es;
-    if (axpy) bytes += (double)c->m * es;
+    const double es = (double)sizeof(T);  // storage of A; every vector is fp64
+    double bytes = (double)vw.k * (double)c->m * es + (double)vw.k * col_vec[upd] * 8.0;
+    if (dot) bytes += (double)c->m * 8.0;
+    if (axpy) bytes += (double)c->m * 8.0;
     prof_end(c, e0, BX_PROF_PASS_DOT + upd, bytes);
   }
   return st;
