@@ -589,7 +589,7 @@ int pick_R(int64_t m, size_t esz) {
   const int64_t per = (int64_t)NT * V;
   // the smallest R with R * NT * V >= m: then every row-vector of the first
   // R - 1 chunks is full (k_pass drops their row guards)
-  for (int R = 1; R <= 12; ++R)
+  for (int R = 1; R <= RMAX; ++R)
     if ((int64_t)R * per >= m) return R;
   return -1;
 }
@@ -779,6 +779,12 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
     case 8: st = launch_pass_R<T, 8>(c, a, dot, axpy, G, smem, acc64); break;
     case 10: st = launch_pass_R<T, 10>(c, a, dot, axpy, G, smem, acc64); break;
     case 12: st = launch_pass_R<T, 12>(c, a, dot, axpy, G, smem, acc64); break;
+#if BX_NT < 512
+    case 13: st = launch_pass_R<T, 13>(c, a, dot, axpy, G, smem, acc64); break;
+    case 14: st = launch_pass_R<T, 14>(c, a, dot, axpy, G, smem, acc64); break;
+    case 15: st = launch_pass_R<T, 15>(c, a, dot, axpy, G, smem, acc64); break;
+    case 16: st = launch_pass_R<T, 16>(c, a, dot, axpy, G, smem, acc64); break;
+#endif
     case 3: st = launch_pass_R<T, 3>(c, a, dot, axpy, G, smem, acc64); break;
     case 5: st = launch_pass_R<T, 5>(c, a, dot, axpy, G, smem, acc64); break;
     case 7: st = launch_pass_R<T, 7>(c, a, dot, axpy, G, smem, acc64); break;

@@ -33,12 +33,17 @@
 
 namespace bx {
 
-constexpr int NT = 512;            // k_pass block size
+#ifndef BX_NT
+#define BX_NT 512
+#endif
+constexpr int NT = BX_NT;          // k_pass block size
+constexpr int RMAX = 12 * 512 / NT;  // register-resident envelope: R * NT * V covers m <= 12288 fp64 / 24576 fp32
 constexpr int NWARPS = NT / 32;
 constexpr int CMAX = 8;            // columns per ring slot (max)
 constexpr int SMAX = 8;            // ring slots (max)
 constexpr int RT = 256;            // block size of the vector kernels
 constexpr int PASS_STAGED = 7;     // per-column state arrays a pass may stage in shared memory
+
 // device-resident round records (small-round kernel, graph rounds): primal,
 // dual, gap, eps, radius, momentum, restarts, %globaltimer at the round's
 // end (ns), gap-evaluation time excluded so far in the batch (ns, screening
@@ -403,6 +408,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
   for (int i = 0; i < (AXPY ? R : 1); ++i)
 #pragma unroll
     for (int e = 0; e < V; ++e) acc[i][e] = AT(0);
+
   double run = 0.0;   // block-scalar running value (threads tid < C)
   double run2 = 0.0;  // second block scalar (FISTA restart slack)
   double run3 = 0.0;  // speculative step: epsilon partial (max)
@@ -1001,7 +1007,7 @@ template <typename T>
 __device__ void pass_fused_reduce(const PassArgs<T>& a, unsigned char* scratch) {
   constexpr int FR = 64;        // rows per chunk
   constexpr int FQ = NT / FR;   // partial-row groups
-  constexpr int FONESHOT = 20;  // partials per thread loaded in one go (G <= 160)
+  constexpr int FONESHOT = (160 + FQ - 1) / FQ;  // partials per thread loaded in one go (G <= 160)
   double* sm = reinterpret_cast<double*>(scratch);  // [FQ][FR] (+ [NWARPS] + flag)
   double* swarp = sm + FQ * FR;
   int* slast = reinterpret_cast<int*>(swarp + NWARPS);
