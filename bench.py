@@ -873,6 +873,21 @@ def run_ours(args):
     # protocol, bench.py:96-115) and, for config 3, BASELINE's stated FISTA
     # restart rule: one solve each, timed with CUDA events
     study = {}
+    if rank == 0 and not args.no_study and args.config == 4:
+        # BASELINE's PG does not reach a relative gap of 1e-3 in 200,000
+        # iterations on this coherent matrix (profiles/r02_cfg4_gap_probe.txt):
+        # its step is a fixed round budget.  FISTA on the same shard reaches
+        # the fp32 objective tolerance (relative certified gap 1e-4):
+        import dataclasses
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r4 = solve(p_dev, dataclasses.replace(cfg, kind="apg", gap_tol=1e-4, relative_gap=True, max_rounds=20000),
+                   return_device=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        study.update(time_to_rel_gap_1e4_apg_s=e0.elapsed_time(e1) / 1000.0,
+                     iterations_rel_gap_1e4_apg=r4.info["iterations"], converged_rel_gap_1e4_apg=r4.converged)
     if rank == 0 and not args.no_study and args.config in (1, 2, 3):
         import dataclasses
 
