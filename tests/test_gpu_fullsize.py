@@ -91,3 +91,30 @@ def test_config5_full_K_sample_matches_batched_oracle():
         assert np.all(d <= 1e-10 * scale), (name, d.max())
     np.testing.assert_array_equal(g.preserved[idx], o["preserved"][-1])
     assert np.max(np.abs(g.x[:, idx] - o["X"])) <= 1e-8 * max(1.0, np.abs(o["X"]).max())
+
+
+def test_config4_full_shard_fp32_against_fp64_oracle():
+    """Config 4's full 20000 x 62,500 fp32 shard against the fp64 oracle
+    directly (not only through the fp64 device path): the first 10 rounds'
+    objectives within north_star's 1e-4 relative fp32 tolerance."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    argv, sys.argv = sys.argv, sys.argv[:1]
+    try:
+        import bench
+    finally:
+        sys.argv = argv
+    from oracle.boxscreen_oracle import oracle_solve
+    from paper_2202_07258_b200 import Problem, SolverConfig, solve
+    inst = bench.make_instance(4)
+    rounds = 10
+    r32 = solve(Problem(inst.a, inst.y, inst.lower, inst.upper, dtype=np.float32),
+                SolverConfig(kind="pg", inner_passes=10, gap_tol=1e-6, max_rounds=rounds))
+    a64 = np.asfortranarray(inst.a, dtype=np.float64)  # the same rounded matrix
+    o = oracle_solve(a64, inst.y, inst.lower, inst.upper, kind="pg", inner_passes=10, gap_tol=1e-300,
+                     max_rounds=rounds)
+    p32 = np.array([t.primal for t in r32.trace])
+    p64 = np.array([t["primal"] for t in o["trace"]])
+    assert p32.shape == p64.shape == (rounds,)
+    assert np.all(np.abs(p32 - p64) <= 1e-4 * np.abs(p64)), np.max(np.abs(p32 - p64) / np.abs(p64))
