@@ -49,6 +49,12 @@ struct BatchArgs {
   int par;             // buffer parity at entry: X[par], R[par] hold x, r; X[1-par], R[1-par] hold x_prev, r_prev
   int screening;
   double rs_f, rs_g, slack_scale;
+  // second schedule (bx_batched2.cuh): the dictionary packed chunk by chunk
+  // in the ring's stage layout (k_b2_pack), a whole number of 16-column chunks
+  const double* Ap;
+  int nch;             // chunks
+  unsigned long long* dbg;  // BX_BT_DEBUG: per-warp wait counters of the second schedule (null otherwise)
+  int sa2;             // column stride of the second schedule's tiles (>= m8, == 4 mod 8)
 };
 
 // not volatile: a pure function of its operands, so the compiler may

@@ -34,6 +34,7 @@
 #include "bx_kernels.cuh"
 #include "bx_cd.cuh"
 #include "bx_batched.cuh"
+#include "bx_batched2.cuh"
 #include "bx_small.cuh"
 #include "bx_active.cuh"
 #include "bx_exchange.cuh"
@@ -3154,6 +3155,9 @@ struct bx_batch {
   int nsm = 148;
   size_t smem = 0;
   int tile = 64;  // problems per CTA tile of k_batched_round
+  int sched = 2;  // 2: warp-per-octet schedule over a TMA chunk ring (bx_batched2.cuh); 1: the first schedule
+  size_t smem2 = 0;
+  int mtc = 0;    // compile-time row-tile count of the launched instantiation (0: run-time m)
 };
 
 namespace {
@@ -3174,8 +3178,10 @@ BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* bas
   double* R0 = (double*)w.take(L.Kp * L.ldy * 8);
   double* R1 = (double*)w.take(L.Kp * L.ldy * 8);
   uint32_t* mask = (uint32_t*)w.take(L.Kp * L.nw * 4);
-  double* nrm = (double*)w.take(n * 8);
-  double* att = (double*)w.take(n * 8);
+  const int64_t n_pad = round_up(n, BT_CH), sa2 = round_up(m, 8) + 4;
+  double* nrm = (double*)w.take(n_pad * 8);
+  double* att = (double*)w.take(n_pad * 8);
+  double* Ap = (double*)w.take(n_pad * sa2 * 8);
   double* t = (double*)w.take(L.ldy * 8);
   double* mom = (double*)w.take(L.Kp * 8);
   double* P = (double*)w.take(L.Kp * 8);
@@ -3192,6 +3198,9 @@ BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* bas
     b->a.mask = mask;
     b->a.nrm = nrm;
     b->a.att = att;
+    b->a.Ap = Ap;
+    b->a.sa2 = (int)sa2;
+    b->a.nch = (int)(n_pad / BT_CH);
     b->a.mom = mom;
     b->a.P = P;
     b->a.stats = stats;
@@ -3311,7 +3320,17 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
   {
     const char* e = getenv("BX_BT_TILE");
     b->tile = (e && atoi(e) == 32) ? 32 : 64;
+    const char* v1 = getenv("BX_BT_V1");
+    b->sched = (v1 && atoi(v1) == 1) ? 1 : 2;
+    if (b->sched == 2) b->tile = 64;
   }
+  b->smem2 = ((size_t)(B2_NST * BT_CH + BT_TILE) * A.sa2) * 8 + B2_NST * 12 + 16;
+  // the config-5 row count (25 row tiles) has its own fully unrolled instantiation
+  b->mtc = (m8 / 8 == 25 && !getenv("BX_BT_GENERIC")) ? 25 : 0;
+  if (b->mtc == 25)
+    BCU(cudaFuncSetAttribute(k_batched_round2<25>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem2));
+  else
+    BCU(cudaFuncSetAttribute(k_batched_round2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem2));
   const int nb = b->tile == 64 ? 2 : 1;
   b->smem = ((size_t)b->tile * A.sa + (size_t)nb * BT_CH * A.sa + (size_t)(2 * nb + 1) * b->tile * BT_SX +
              9 * (size_t)b->tile) * 8 + 2 * (size_t)b->tile * 4 + 64;
@@ -3328,6 +3347,7 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
   BCU(cudaMemsetAsync(b->flags, 0, 64, b->stream));
   k_colstats<double><<<(int)((n * 32 + 255) / 256 < 2048 ? (n * 32 + 255) / 256 : 2048), 256, 0, b->stream>>>(
       a, lda, n, m, b->t, const_cast<double*>(A.nrm), const_cast<double*>(A.att), 1, b->flags);
+  k_b2_pack<<<1024, 256, 0, b->stream>>>(a, lda, (int)m, (int)n, A.nrm, A.att, const_cast<double*>(A.Ap), A.sa2, A.nch);
   int fl = 0;
   BCU(cudaMemcpyAsync(&fl, b->flags, 4, cudaMemcpyDeviceToHost, b->stream));
   BCU(cudaStreamSynchronize(b->stream));
@@ -3350,6 +3370,8 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
   A.passes = passes;
   A.screening = screening;
   A.par = 0;
+  A.dbg = nullptr;
+  if (getenv("BX_BT_DEBUG")) BCU(cudaMalloc(&A.dbg, 148 * 8 * 4 * 8));
   k_batched_init<<<1024, 256, 0, b->stream>>>(A);
   b->launches = 1;
   const int per_sm = b->tile == 64 ? 1 : 2;
@@ -3357,7 +3379,11 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
   int64_t r = 0;
   int64_t conv = 0;
   for (r = 0; r < rounds; ++r) {
-    if (b->tile == 64)
+    if (b->sched == 2 && b->mtc == 25)
+      k_batched_round2<25><<<grid, B2_NT, b->smem2, b->stream>>>(A);
+    else if (b->sched == 2)
+      k_batched_round2<0><<<grid, B2_NT, b->smem2, b->stream>>>(A);
+    else if (b->tile == 64)
       k_batched_round<64><<<grid, 64 * 8, b->smem, b->stream>>>(A);
     else
       k_batched_round<32><<<grid, 32 * 8, b->smem, b->stream>>>(A);
@@ -3378,6 +3404,18 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
       ++r;
       break;
     }
+  }
+  if (A.dbg) {
+    std::vector<unsigned long long> h(148 * 8 * 4);
+    BCU(cudaMemcpy(h.data(), A.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int cta : {0, 1, 77, 147})
+      for (int w = 0; w < 8; ++w) {
+        const unsigned long long* o = &h[(size_t)(cta * 8 + w) * 4];
+        fprintf(stderr, "cta %3d warp %d: wait %6.2f%% of %llu clk, long waits %llu of %llu chunks\n", cta, w,
+                100.0 * (double)o[0] / (double)o[2], o[2], o[1], o[3]);
+      }
+    cudaFree(A.dbg);
+    A.dbg = nullptr;
   }
   if (out) {
     out->rounds = r;
