@@ -64,14 +64,18 @@ __device__ __forceinline__ void b2_issue(const BatchArgs& a, const B2Ring& rg, i
 
 __device__ __forceinline__ const double* b2_acquire(const BatchArgs& a, const B2Ring& rg) {
   const int s = rg.it % B2_NST;
+#ifndef B2_ABL_NORING
   mbar_wait(&rg.full[s], (uint32_t)((rg.it / B2_NST) & 1));
+#endif
   return rg.stage + (size_t)s * rg.sstride;
 }
 
 // stage of chunk q (anywhere ahead in the sequence: waiting does not consume)
 __device__ __forceinline__ const double* b2_acquire_at(const B2Ring& rg, int q) {
   const int s = q % B2_NST;
+#ifndef B2_ABL_NORING
   mbar_wait(&rg.full[s], (uint32_t)((q / B2_NST) & 1));
+#endif
   return rg.stage + (size_t)s * rg.sstride;
 }
 
@@ -84,8 +88,17 @@ __device__ __forceinline__ int b2_release_begin(B2Ring& rg, int lane) {
   const int s = rg.it % B2_NST;
   __syncwarp();
   int old = 0;
-  if (lane == 0)
+#ifdef B2_ABL_NORING
+  ++rg.it;
+  return -1;
+#endif
+  if (lane == 0) {
+#ifdef B2_RELAXED_ARRIVE
+    asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rg.cnt[s])) : "memory");
+#else
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rg.cnt[s])) : "memory");
+#endif
+  }
   ++rg.it;
   return old;
 }
@@ -107,52 +120,48 @@ __device__ __forceinline__ void b2_release(const BatchArgs& a, B2Ring& rg, int l
   b2_release_end(a, rg, old, q, lane, pol);
 }
 
+__device__ __forceinline__ double2 b2_ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
 // d[t][e] (problem g, coordinate 8 t + 2 tig + e of the chunk) = sum_i Ry[i][g] A_J[i][.]
-// rw = warp's R_y + g * sa + tig ; b0 = stage + slot(g) * sa + tig.  Two k-step
-// parities x two coordinate tiles = 4 independent DMMA chains per warp.
-template <int M4C>
-__device__ __forceinline__ void b2_gemm1(const double* __restrict__ rw, const double* __restrict__ b0, int sa8, int m4,
-                                         double (&d)[2][2]) {
+// ry = warp's R_y + g * sa ; b0 = stage + slot(g) * sa.  The K index is a
+// summation index, so which rows form a k-step is free: within a 16-row block
+// lane tig takes the row pairs at ro = 2 (tig & 1) + 8 (tig >> 1) and ro + 4,
+// one LDS.128 per operand for two k-steps (bank-conflict free for a column
+// stride == 4 mod 8: a quarter warp's eight 16-byte units are distinct mod
+// 8).  An odd row-tile count leaves 8 rows: pairs at 2 tig (2-way conflict,
+// once per chunk).  Chains: (pair element, coordinate tile) = 4 independent.
+template <int MTC>
+__device__ __forceinline__ void b2_gemm1(const double* __restrict__ ry, const double* __restrict__ b0, int sa8, int mt_n,
+                                         int tig, double (&d)[2][2]) {
   double acc[2][2][2];
 #pragma unroll
   for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int t = 0; t < 2; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
-  if constexpr (M4C > 0) {
-    // compile-time K: fully unrolled, every fragment load an immediate offset
-    const double* b1 = b0 + sa8;
+  const int ro = 2 * (tig & 1) + 8 * (tig >> 1);
+  const double* b1 = b0 + sa8;
+  auto step2 = [&](int off) {
+    const double2 ra = b2_ld2(ry + off), x0 = b2_ld2(b0 + off), x1 = b2_ld2(b1 + off);
+    dmma(acc[0][0][0], acc[0][0][1], ra.x, x0.x);
+    dmma(acc[0][1][0], acc[0][1][1], ra.x, x1.x);
+    dmma(acc[1][0][0], acc[1][0][1], ra.y, x0.y);
+    dmma(acc[1][1][0], acc[1][1][1], ra.y, x1.y);
+  };
+  if constexpr (MTC > 0) {
 #pragma unroll
-    for (int kk = 0; kk < M4C; ++kk) {
-      const double ra = rw[4 * kk];
-      dmma(acc[kk & 1][0][0], acc[kk & 1][0][1], ra, b0[4 * kk]);
-      dmma(acc[kk & 1][1][0], acc[kk & 1][1][1], ra, b1[4 * kk]);
+    for (int b = 0; b < MTC / 2; ++b) {
+      step2(16 * b + ro);
+      step2(16 * b + ro + 4);
     }
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) d[t][e] = acc[0][t][e] + acc[1][t][e];
-    return;
-  }
-  int kk = 0;
+    if constexpr (MTC & 1) step2(16 * (MTC / 2) + 2 * tig);
+  } else {
+    const int nb = mt_n >> 1;
 #pragma unroll 2
-  for (; kk + 2 <= m4; kk += 2) {
-    double ra[2], x0[2], x1[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      ra[u] = rw[4 * (kk + u)];
-      x0[u] = b0[4 * (kk + u)];
-      x1[u] = b0[sa8 + 4 * (kk + u)];
+    for (int b = 0; b < nb; ++b) {
+      step2(16 * b + ro);
+      step2(16 * b + ro + 4);
     }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      dmma(acc[u][0][0], acc[u][0][1], ra[u], x0[u]);
-      dmma(acc[u][1][0], acc[u][1][1], ra[u], x1[u]);
-    }
-  }
-  if (kk < m4) {
-    const double ra = rw[4 * kk];
-    dmma(acc[0][0][0], acc[0][0][1], ra, b0[4 * kk]);
-    dmma(acc[0][1][0], acc[0][1][1], ra, b0[sa8 + 4 * kk]);
+    if (mt_n & 1) step2(16 * nb + 2 * tig);
   }
 #pragma unroll
   for (int t = 0; t < 2; ++t)
@@ -160,11 +169,19 @@ __device__ __forceinline__ void b2_gemm1(const double* __restrict__ rw, const do
     for (int e = 0; e < 2; ++e) d[t][e] = acc[0][t][e] + acc[1][t][e];
 }
 
-// acc (rows 8 q + g, problems 2 tig + e) += A_J X_J, K = (tile, parity) pairs:
-// k-step (t, e) covers coordinates 8 t + 2 tig + e, whose x values are this
-// lane's xn[t][e] (problem g).  st = stage + g ; so[t][e] = slot * sa.
+// Row of accumulator tile q held by lane row g.  The M index is free as
+// well: row tiles are taken in pairs over 16 rows, lane g holding rows
+// 16 q' + 2 g (tile 2 q') and 16 q' + 2 g + 1 (tile 2 q' + 1), so one LDS.128
+// feeds two DMMAs; an odd last tile keeps rows 8 q + g.
+__device__ __forceinline__ int b2_row(int q, int g, int mt_n) {
+  return (q | 1) < mt_n ? 16 * (q >> 1) + 2 * g + (q & 1) : 8 * q + g;
+}
+
+// acc (rows b2_row(q, g), problems 2 tig + e) += A_J X_J, K = (tile, parity)
+// pairs: k-step (t, e) covers coordinates 8 t + 2 tig + e, whose x values are
+// this lane's xn[t][e] (problem g).  st = stage ; so[t][e] = slot * sa.
 template <int NQ>
-__device__ __forceinline__ void b2_gemm2_n(const double* __restrict__ st, const int (&so)[2][2],
+__device__ __forceinline__ void b2_gemm2_n(const double* __restrict__ st, int g, const int (&so)[2][2],
                                            const double (&xn)[2][2], double (&acc)[B2_MT][2]) {
 #pragma unroll
   for (int t = 0; t < 2; ++t)
@@ -173,18 +190,23 @@ __device__ __forceinline__ void b2_gemm2_n(const double* __restrict__ st, const 
       const double* aj = st + so[t][e];
       const double b = xn[t][e];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) dmma(acc[q][0], acc[q][1], aj[8 * q], b);
+      for (int p = 0; p < NQ / 2; ++p) {
+        const double2 v = b2_ld2(aj + 16 * p + 2 * g);
+        dmma(acc[2 * p][0], acc[2 * p][1], v.x, b);
+        dmma(acc[2 * p + 1][0], acc[2 * p + 1][1], v.y, b);
+      }
+      if constexpr (NQ & 1) dmma(acc[NQ - 1][0], acc[NQ - 1][1], aj[8 * (NQ - 1) + g], b);
     }
 }
 template <int MTC>
-__device__ __forceinline__ void b2_gemm2(const double* __restrict__ st, const int (&so)[2][2], const double (&xn)[2][2],
-                                         double (&acc)[B2_MT][2], int mt_n) {
+__device__ __forceinline__ void b2_gemm2(const double* __restrict__ st, int g, const int (&so)[2][2],
+                                         const double (&xn)[2][2], double (&acc)[B2_MT][2], int mt_n) {
   if constexpr (MTC > 0) {
-    b2_gemm2_n<MTC>(st, so, xn, acc);
+    b2_gemm2_n<MTC>(st, g, so, xn, acc);
     return;
   }
 #define B2_CASE(N) \
-  case N: b2_gemm2_n<N>(st, so, xn, acc); break;
+  case N: b2_gemm2_n<N>(st, g, so, xn, acc); break;
   switch (mt_n) {  // warp-uniform
     B2_CASE(26) B2_CASE(25) B2_CASE(24) B2_CASE(23) B2_CASE(22) B2_CASE(21) B2_CASE(20) B2_CASE(19) B2_CASE(18)
     B2_CASE(17) B2_CASE(16) B2_CASE(15) B2_CASE(14) B2_CASE(13) B2_CASE(12) B2_CASE(11) B2_CASE(10) B2_CASE(9)
@@ -232,7 +254,7 @@ __device__ __forceinline__ double b2_store_r(const BatchArgs& a, const double (&
   double sq[2] = {0.0, 0.0};
 #pragma unroll
   for (int q = 0; q < B2_MT; ++q) {
-    const int i = 8 * q + g;
+    const int i = b2_row(q, g, mt_n);
     if (q < mt_n && i < a.m) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -248,7 +270,7 @@ __device__ __forceinline__ double b2_store_r(const BatchArgs& a, const double (&
 
 // MTC > 0: the row-tile count ceil(m / 8) at compile time (column stride
 // 8 MTC + 4, both products fully unrolled); MTC = 0: any m <= 208 at run time
-template <int MTC>
+template <int MTC, bool PIPE = true>
 __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ int dirty_epoch;
@@ -282,14 +304,15 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
   __syncthreads();
   if (warp == 0)
     for (int q = 0; q < B2_NST; ++q) b2_issue(a, rg, q, lane, pol);
+#ifdef B2_ABL_NORING
+  for (int q = 0; q < B2_NST; ++q) mbar_wait(&rg.full[q], 0);
+#endif
 
   double* rw0 = rys + (size_t)warp * 8 * sa;           // this warp's residual tile
-  const double* rw = rw0 + g * sa + tig;               // GEMM1 A-fragment base
+  const double* rw = rw0 + g * sa;                     // GEMM1 A-fragment base (problem g's residual)
   const int sa8 = 8 * sa;
-  const int m4 = MTC ? 2 * MTC : (a.m + 3) / 4;
   const int mt_n = MTC ? MTC : (a.m + 7) / 8;
-  constexpr int M4C = 2 * MTC;
-  const int bo = b2_slot(g) * sa + tig;                // GEMM1 B-fragment offset in a stage
+  const int bo = b2_slot(g) * sa;                      // GEMM1 B-fragment base in a stage (coordinate g's column)
   const int no = sa - 2;                               // row of ||a_j|| in a column slot; a_j't one further
   int so[2][2];                                        // GEMM2 A-fragment offsets
 #pragma unroll
@@ -339,14 +362,19 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
       // does not have to be in the right phase).  The last iteration's
       // GEMM1 runs on the next sweep's first chunk and is discarded (the
       // ring cycles through the same chunks for every sweep).
-      const double* st = b2_acquire(a, rg);
+      // (PIPE = false, the A/B control: GEMM1, update and GEMM2 of the same
+      // chunk in sequence.)
+      const double* st = nullptr;
       double d[2][2];
-      b2_gemm1<M4C>(rw, st + bo, sa8, m4, d);
+      if constexpr (PIPE) {
+        st = b2_acquire(a, rg);
+        b2_gemm1<MTC>(rw, st + bo, sa8, mt_n, tig, d);
+      }
       int pend_old = 0, pend_q = -1;
       for (int c = 0; c < a.nch; ++c) {
         const int j0 = c * BT_CH;
         const long long tw0 = a.dbg ? clock64() : 0;
-        const double* stn = b2_acquire_at(rg, rg.it + 1);
+        const double* stn = b2_acquire_at(rg, rg.it + (PIPE ? 1 : 0));
         if (a.dbg) {
           const long long dt = clock64() - tw0;
           dbg_wait += dt;
@@ -354,7 +382,15 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
         }
         if (pend_q >= 0) b2_release_end(a, rg, pend_old, pend_q, lane, pol);
         double dn[2][2];
-        b2_gemm1<M4C>(rw, stn + bo, sa8, m4, dn);
+        b2_gemm1<MTC>(rw, stn + bo, sa8, mt_n, tig, dn);
+        if constexpr (!PIPE) {
+          st = stn;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            d[t][0] = dn[t][0];
+            d[t][1] = dn[t][1];
+          }
+        }
         // the FISTA update of this lane's four coordinates of problem g
         double xn[2][2];
         {
@@ -366,6 +402,9 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
             for (int e = 0; e < 2; ++e) {
               const bool act = (mb >> (8 * t + 2 * tig + e)) & 1u;
               const double x = e ? xc[t].y : xc[t].x, xp = e ? xpc[t].y : xpc[t].x;
+#ifdef B2_ABL_NOEPI
+              double v = d[t][e] + x + xp + nr[e] + (act ? 1.0 : 0.0);
+#else
               double yv = x;
               if (bt != 0.0) yv = add_rn(x, mul_rn(bt, sub_rn(x, xp)));
               double v = 0.0;
@@ -376,14 +415,22 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
               const double dx = v - x;
               gdot += d[t][e] * dx;
               gsc += nr[e] * fabs(dx);
+#endif
               xn[t][e] = v;
             }
             // x+ into the x_prev slot (this chunk's x_prev is already in registers)
+#ifndef B2_ABL_NOX
             *reinterpret_cast<double2*>(xpg + j0 + 8 * t) = make_double2(xn[t][0], xn[t][1]);
+#endif
           }
         }
         // next chunk's x, x_prev and mask word: in flight during GEMM2 and the next GEMM1
-        if (c + 1 < a.nch) {
+#ifndef B2_ABL_NOX
+        if (c + 1 < a.nch)
+#else
+        if (c + 1 < a.nch && a.eta == 12345.0)
+#endif
+        {
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             xc[t] = *reinterpret_cast<const double2*>(xg + j0 + BT_CH + 8 * t);
@@ -391,7 +438,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
           }
           mw = __ldcg(mkg + ((j0 + BT_CH) >> 5));
         }
-        b2_gemm2<MTC>(st + g, so, xn, acc, mt_n);
+        b2_gemm2<MTC>(st, g, so, xn, acc, mt_n);
         pend_q = rg.it;
         pend_old = b2_release_begin(rg, lane);
         st = stn;
@@ -428,7 +475,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
         const int j0 = c * BT_CH;
         const double* st = b2_acquire(a, rg);
         double d[2][2];
-        b2_gemm1<M4C>(rw, st + bo, sa8, m4, d);
+        b2_gemm1<MTC>(rw, st + bo, sa8, mt_n, tig, d);
         double at[2][2];
 #pragma unroll
         for (int t = 0; t < 2; ++t)
@@ -476,7 +523,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
           const int j0 = c * BT_CH;
           const double* st = b2_acquire(a, rg);
           double d[2][2];
-          b2_gemm1<M4C>(rw, st + bo, sa8, m4, d);
+          b2_gemm1<MTC>(rw, st + bo, sa8, mt_n, tig, d);
           double at[2][2], nr[2][2];
 #pragma unroll
           for (int t = 0; t < 2; ++t)
@@ -528,7 +575,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
               xn[t][1] = v.y;
             }
             const double* st = b2_acquire(a, rg);
-            b2_gemm2<MTC>(st + g, so, xn, acc, mt_n);
+            b2_gemm2<MTC>(st, g, so, xn, acc, mt_n);
             b2_release(a, rg, lane, pol);
           }
           const double sqg = b2_store_r(a, acc, Rw, kw, mt_n, g, tig);
@@ -556,10 +603,12 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
     o[3] = (unsigned long long)rg.it;
   }
   // the ring always runs NST chunks ahead: wait for the copies still in flight
+#ifndef B2_ABL_NORING
   for (int q = 0; q < B2_NST; ++q) {
     const int s = (rg.it + q) % B2_NST;
     mbar_wait(&rg.full[s], (uint32_t)(((rg.it + q) / B2_NST) & 1));
   }
+#endif
 }
 
 // The dictionary as the ring wants it: chunk c is one contiguous block

@@ -3157,6 +3157,7 @@ struct bx_batch {
   int tile = 64;  // problems per CTA tile of k_batched_round
   int sched = 2;  // 2: warp-per-octet schedule over a TMA chunk ring (bx_batched2.cuh); 1: the first schedule
   size_t smem2 = 0;
+  bool pipe = true;  // software-pipelined chunk loop (BX_BT_PIPE=0: the A/B control)
   int mtc = 0;    // compile-time row-tile count of the launched instantiation (0: run-time m)
 };
 
@@ -3327,7 +3328,11 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
   b->smem2 = ((size_t)(B2_NST * BT_CH + BT_TILE) * A.sa2) * 8 + B2_NST * 12 + 16;
   // the config-5 row count (25 row tiles) has its own fully unrolled instantiation
   b->mtc = (m8 / 8 == 25 && !getenv("BX_BT_GENERIC")) ? 25 : 0;
-  if (b->mtc == 25)
+  b->pipe = !(getenv("BX_BT_PIPE") && atoi(getenv("BX_BT_PIPE")) == 0);
+  if (b->mtc == 25 && !b->pipe)
+    BCU(cudaFuncSetAttribute(k_batched_round2<25, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)b->smem2));
+  else if (b->mtc == 25)
     BCU(cudaFuncSetAttribute(k_batched_round2<25>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem2));
   else
     BCU(cudaFuncSetAttribute(k_batched_round2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem2));
@@ -3379,7 +3384,9 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
   int64_t r = 0;
   int64_t conv = 0;
   for (r = 0; r < rounds; ++r) {
-    if (b->sched == 2 && b->mtc == 25)
+    if (b->sched == 2 && b->mtc == 25 && !b->pipe)
+      k_batched_round2<25, false><<<grid, B2_NT, b->smem2, b->stream>>>(A);
+    else if (b->sched == 2 && b->mtc == 25)
       k_batched_round2<25><<<grid, B2_NT, b->smem2, b->stream>>>(A);
     else if (b->sched == 2)
       k_batched_round2<0><<<grid, B2_NT, b->smem2, b->stream>>>(A);

@@ -28,11 +28,11 @@ __global__ void __launch_bounds__(256, 1) k(double* out, int iters, int sa) {
     const double* st = stage + (it & 3) * 16 * sa;
     if (MODE & 1) {
       double d[2][2];
-      b2_gemm1(rw, st + bo, 8 * sa, 50, d);
+      b2_gemm1<25>(rw - tig, st + bo - tig, 8 * sa, 25, tig, d);
       if (MODE & 4) { xn[0][0] = d[0][0]; xn[0][1] = d[0][1]; xn[1][0] = d[1][0]; xn[1][1] = d[1][1]; }
       else s += d[0][0] + d[0][1] + d[1][0] + d[1][1];
     }
-    if (MODE & 2) b2_gemm2_n<25>(st + g, so, xn, acc);
+    if (MODE & 2) b2_gemm2_n<25>(st, g, so, xn, acc);
   }
   for (int q = 0; q < B2_MT; ++q) s += acc[q][0] + acc[q][1];
   out[blockIdx.x * 256 + tid] = s;
