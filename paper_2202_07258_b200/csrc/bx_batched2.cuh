@@ -64,18 +64,14 @@ __device__ __forceinline__ void b2_issue(const BatchArgs& a, const B2Ring& rg, i
 
 __device__ __forceinline__ const double* b2_acquire(const BatchArgs& a, const B2Ring& rg) {
   const int s = rg.it % B2_NST;
-#ifndef B2_ABL_NORING
   mbar_wait(&rg.full[s], (uint32_t)((rg.it / B2_NST) & 1));
-#endif
   return rg.stage + (size_t)s * rg.sstride;
 }
 
 // stage of chunk q (anywhere ahead in the sequence: waiting does not consume)
 __device__ __forceinline__ const double* b2_acquire_at(const B2Ring& rg, int q) {
   const int s = q % B2_NST;
-#ifndef B2_ABL_NORING
   mbar_wait(&rg.full[s], (uint32_t)((q / B2_NST) & 1));
-#endif
   return rg.stage + (size_t)s * rg.sstride;
 }
 
@@ -88,17 +84,8 @@ __device__ __forceinline__ int b2_release_begin(B2Ring& rg, int lane) {
   const int s = rg.it % B2_NST;
   __syncwarp();
   int old = 0;
-#ifdef B2_ABL_NORING
-  ++rg.it;
-  return -1;
-#endif
-  if (lane == 0) {
-#ifdef B2_RELAXED_ARRIVE
-    asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rg.cnt[s])) : "memory");
-#else
+  if (lane == 0)
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&rg.cnt[s])) : "memory");
-#endif
-  }
   ++rg.it;
   return old;
 }
@@ -304,9 +291,6 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
   __syncthreads();
   if (warp == 0)
     for (int q = 0; q < B2_NST; ++q) b2_issue(a, rg, q, lane, pol);
-#ifdef B2_ABL_NORING
-  for (int q = 0; q < B2_NST; ++q) mbar_wait(&rg.full[q], 0);
-#endif
 
   double* rw0 = rys + (size_t)warp * 8 * sa;           // this warp's residual tile
   const double* rw = rw0 + g * sa;                     // GEMM1 A-fragment base (problem g's residual)
@@ -402,9 +386,6 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
             for (int e = 0; e < 2; ++e) {
               const bool act = (mb >> (8 * t + 2 * tig + e)) & 1u;
               const double x = e ? xc[t].y : xc[t].x, xp = e ? xpc[t].y : xpc[t].x;
-#ifdef B2_ABL_NOEPI
-              double v = d[t][e] + x + xp + nr[e] + (act ? 1.0 : 0.0);
-#else
               double yv = x;
               if (bt != 0.0) yv = add_rn(x, mul_rn(bt, sub_rn(x, xp)));
               double v = 0.0;
@@ -415,22 +396,14 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
               const double dx = v - x;
               gdot += d[t][e] * dx;
               gsc += nr[e] * fabs(dx);
-#endif
               xn[t][e] = v;
             }
             // x+ into the x_prev slot (this chunk's x_prev is already in registers)
-#ifndef B2_ABL_NOX
             *reinterpret_cast<double2*>(xpg + j0 + 8 * t) = make_double2(xn[t][0], xn[t][1]);
-#endif
           }
         }
         // next chunk's x, x_prev and mask word: in flight during GEMM2 and the next GEMM1
-#ifndef B2_ABL_NOX
-        if (c + 1 < a.nch)
-#else
-        if (c + 1 < a.nch && a.eta == 12345.0)
-#endif
-        {
+        if (c + 1 < a.nch) {
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             xc[t] = *reinterpret_cast<const double2*>(xg + j0 + BT_CH + 8 * t);
@@ -603,12 +576,10 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
     o[3] = (unsigned long long)rg.it;
   }
   // the ring always runs NST chunks ahead: wait for the copies still in flight
-#ifndef B2_ABL_NORING
   for (int q = 0; q < B2_NST; ++q) {
     const int s = (rg.it + q) % B2_NST;
     mbar_wait(&rg.full[s], (uint32_t)(((rg.it + q) / B2_NST) & 1));
   }
-#endif
 }
 
 // The dictionary as the ring wants it: chunk c is one contiguous block

@@ -109,6 +109,11 @@ struct bx_group {
   std::vector<void*> xbufs;    // each rank's exchange buffer (registered by bx_peer_open)
   std::vector<XArgs> xargs;    // each rank's arguments of the current call
   XArgs* xargs_dev = nullptr;  // device copy (rank 0 launches)
+  // BX_GROUP_XREDUCE=rank: every rank thread launches the PRODUCTION kernel
+  // (k_xreduce, the one the NCCL build runs per GPU) on its own stream, the
+  // ranks' grids co-resident on this GPU and exchanging through the flags;
+  // default: all ranks in one cooperative launch (k_xreduce_group)
+  bool per_rank = false;
   ~bx_group() {
     if (xargs_dev) cudaFree(xargs_dev);
   }
@@ -190,6 +195,27 @@ struct LocalComm : Comm {
     g->xargs[rank] = mine;
     g->barrier();
     int rc = 0;
+    if (g->per_rank) {
+      // Every rank's pass has completed (stream syncs + barrier above), so the
+      // SMs are free and the n grids of nb small CTAs are co-resident: no
+      // rank's flag wait can depend on an unscheduled CTA, and the bounded
+      // waits turn any surprise into DE_PEER_TIMEOUT instead of a hang.
+      XArgs a = mine;
+      for (int p = 0; p < g->n; ++p) {
+        char* base = static_cast<char*>(g->xbufs[p]);
+        a.recv[p] = reinterpret_cast<double*>(base);
+        a.flag[p] = reinterpret_cast<unsigned*>(base + xrecv_doubles(a.mp) * 8);
+      }
+      a.my_recv = a.recv[rank];
+      a.my_flag = a.flag[rank];
+      void* kargs[] = {(void*)&a};
+      const void* fn = f32 ? (const void*)k_xreduce<float> : (const void*)k_xreduce<double>;
+      if (cudaLaunchCooperativeKernel(fn, dim3(a.nb), dim3(XT), kargs, 0, stream) != cudaSuccess) rc = 1;
+      if (!rc && cudaStreamSynchronize(stream) != cudaSuccess) rc = 1;
+      if (rc) err = "LocalComm: per-rank exchange launch";
+      g->barrier();
+      return rc;
+    }
     if (rank == 0) {
       const int n = g->n;
       for (int q = 0; q < n; ++q) {
@@ -3095,6 +3121,10 @@ int bx_group_create(bx_group** out, int32_t nranks) {
   bx_group* g = new bx_group();
   g->n = nranks;
   g->ptrs.assign(nranks, nullptr);
+  {
+    const char* e = getenv("BX_GROUP_XREDUCE");
+    g->per_rank = e && strcmp(e, "rank") == 0;
+  }
   *out = g;
   return BX_OK;
 }

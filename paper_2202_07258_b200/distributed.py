@@ -61,22 +61,38 @@ def shard(p, c0, c1):
     return Problem.from_device_storage(d["a"][c0:c1], p.m, d["y"], d["lo"][c0:c1], d["hi"][c0:c1])
 
 
-def _exchange(exchange):
+def _exchange(exchange, group=False):
     ex = exchange or os.environ.get("BX_EXCHANGE", "fused")
-    if ex not in ("fused", "nccl"):
-        raise ValueError(f"exchange must be 'fused' or 'nccl', not {ex!r}")
+    allowed = ("fused", "nccl", "peer") if group else ("fused", "nccl")
+    if ex not in allowed:
+        raise ValueError(f"exchange must be one of {allowed}, not {ex!r}")
     return ex
 
 
 def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLoss, slack_scale=None,
                 return_shards=False, exchange=None):
-    """Column-sharded solve with ``nranks`` ranks as threads on the current GPU."""
+    """Column-sharded solve with ``nranks`` ranks as threads on the current GPU.
+
+    ``exchange``: "fused" (every rank's reduce + exchange in one cooperative
+    launch), "nccl" (the collective schedule through the group's allreduce) or
+    "peer" -- each rank thread launches the production exchange kernel
+    (``k_xreduce``, what a multi-GPU run launches per GPU) on its own stream;
+    the ranks' grids are co-resident and talk through the peer flags."""
     import torch
     cfg = cfg or SolverConfig()
     slack_scale = _default_slack(p) if slack_scale is None else slack_scale
     L = nat.lib()
     group = ctypes.c_void_p()
-    nat.check(L.bx_group_create(ctypes.byref(group), nranks), None, "bx_group_create")
+    ex = _exchange(exchange, group=True)
+    prev = os.environ.get("BX_GROUP_XREDUCE")
+    os.environ["BX_GROUP_XREDUCE"] = "rank" if ex == "peer" else "group"
+    try:
+        nat.check(L.bx_group_create(ctypes.byref(group), nranks), None, "bx_group_create")
+    finally:
+        if prev is None:
+            os.environ.pop("BX_GROUP_XREDUCE", None)
+        else:
+            os.environ["BX_GROUP_XREDUCE"] = prev
     blocks = column_blocks(p.n, nranks)
     sessions, results, errors = [], [None] * nranks, [None] * nranks
     try:
@@ -84,7 +100,7 @@ def solve_group(p, cfg=None, nranks=2, screening=True, tv=None, loss=QuadraticLo
             s = _Session(shard(p, c0, c1), tv=tv, stream=torch.cuda.Stream())
             s.attach_group(group, r, c0, p.n)
             sessions.append(s)
-            if _exchange(exchange) == "fused":
+            if ex in ("fused", "peer"):
                 s.attach_peers()
 
         def work(r):

@@ -59,7 +59,12 @@ def _solve_linear(p):
     b = -torch.ones(p.n, 1, dtype=torch.float64, device=a.device)
     gram = a.T @ a
     chol, info = torch.linalg.cholesky_ex(gram)
-    if int(info) != 0:
+    # LAPACK's potrf (the reference's cho_factor) stops at a pivot <= 0; the
+    # device factorisation can leave a round-off-sized positive pivot on an
+    # exactly rank-deficient Gram matrix (duplicated column) and then solve
+    # the consistent system by luck, so a pivot at round-off level relative to
+    # the diagonal counts as singular too (rank(A) = n is the requirement)
+    if int(info) != 0 or float(torch.diagonal(chol).min()) ** 2 <= 1e-13 * float(torch.diagonal(gram).max()):
         raise SingularGram("A' A is singular; solve-linear needs rank(A) = n <= m")
     cand = a @ torch.cholesky_solve(b, chol)
     # a near-singular Gram matrix can still factor: check the solve itself
