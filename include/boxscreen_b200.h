@@ -319,6 +319,10 @@ typedef struct bx_batch bx_batch;
 typedef struct {
   int64_t rounds, converged, iterations, kernel_launches;
   double max_gap;
+  /* tile-rounds (64 right-hand sides each) that ran the per-coordinate sphere
+   * test; the others were cleared by the per-problem bound (no coordinate
+   * could be screened); tiles = K / 64 */
+  int64_t sphere_sweeps, tiles;
 } bx_batched_out;
 size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs);
 /* A: device, column-major (lda even); Y: device m x K column-major (ldy) */

@@ -55,7 +55,8 @@ PROF_NAMES = ["pass_dot", "pass_pg_g", "pass_pg", "pass_apg", "pass_power", "pas
 
 class BatchedOut(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("converged", ctypes.c_int64), ("iterations", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("max_gap", ctypes.c_double)]
+                ("kernel_launches", ctypes.c_int64), ("max_gap", ctypes.c_double),
+                ("sphere_sweeps", ctypes.c_int64), ("tiles", ctypes.c_int64)]
 
 
 START_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),

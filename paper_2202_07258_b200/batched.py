@@ -29,6 +29,8 @@ class BatchedResult:
     eta: float
     trace: np.ndarray = field(default_factory=lambda: np.zeros((0, 4)))  # per round: converged, max/mean gap, mean preserved
     kernel_launches: int = 0
+    sphere_sweeps: int = 0    # tile-rounds that ran the per-coordinate sphere test (others cleared by the bound)
+    tiles: int = 0            # tiles (64 right-hand sides) per round
 
 
 def _check(st, h, what):
@@ -92,4 +94,5 @@ def solve_batched(a, Y, passes=10, rounds=10, gap_tol=1e-6, screening=True, eta=
         xo = host.numpy().T
     return BatchedResult(x=xo, primal=st[0], dual=st[1], gap=st[2], eps=st[3], preserved=st[4].astype(np.int64),
                          rounds=int(out.rounds), converged=int(out.converged), iterations=int(out.iterations),
-                         eta=float(eta), trace=trace[: int(out.rounds)], kernel_launches=int(out.kernel_launches))
+                         eta=float(eta), trace=trace[: int(out.rounds)], kernel_launches=int(out.kernel_launches),
+                         sphere_sweeps=int(out.sphere_sweeps), tiles=int(out.tiles))

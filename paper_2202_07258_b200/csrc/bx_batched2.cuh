@@ -115,8 +115,7 @@ __device__ __forceinline__ double2 b2_ld2(const double* p) { return *reinterpret
 // lane tig takes the row pairs at ro = 2 (tig & 1) + 8 (tig >> 1) and ro + 4,
 // one LDS.128 per operand for two k-steps (bank-conflict free for a column
 // stride == 4 mod 8: a quarter warp's eight 16-byte units are distinct mod
-// 8).  An odd row-tile count leaves 8 rows: pairs at 2 tig (2-way conflict,
-// once per chunk).  Chains: (pair element, coordinate tile) = 4 independent.
+// 8).  Chains: (pair element, coordinate tile) = 4 independent.
 template <int MTC>
 __device__ __forceinline__ void b2_gemm1(const double* __restrict__ ry, const double* __restrict__ b0, int sa8, int mt_n,
                                          int tig, double (&d)[2][2]) {
@@ -134,13 +133,23 @@ __device__ __forceinline__ void b2_gemm1(const double* __restrict__ ry, const do
     dmma(acc[1][0][0], acc[1][0][1], ra.y, x0.y);
     dmma(acc[1][1][0], acc[1][1][1], ra.y, x1.y);
   };
+  // the 8 rows an odd row-tile count leaves: two plain k-steps (rows tig and
+  // 4 + tig), 8-byte loads (16-byte pairs would conflict 2-way here)
+  auto tail = [&](int off) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double ra = ry[off + 4 * h + tig];
+      dmma(acc[h][0][0], acc[h][0][1], ra, b0[off + 4 * h + tig]);
+      dmma(acc[h][1][0], acc[h][1][1], ra, b1[off + 4 * h + tig]);
+    }
+  };
   if constexpr (MTC > 0) {
 #pragma unroll
     for (int b = 0; b < MTC / 2; ++b) {
       step2(16 * b + ro);
       step2(16 * b + ro + 4);
     }
-    if constexpr (MTC & 1) step2(16 * (MTC / 2) + 2 * tig);
+    if constexpr (MTC & 1) tail(16 * (MTC / 2));
   } else {
     const int nb = mt_n >> 1;
 #pragma unroll 2
@@ -148,7 +157,7 @@ __device__ __forceinline__ void b2_gemm1(const double* __restrict__ ry, const do
       step2(16 * b + ro);
       step2(16 * b + ro + 4);
     }
-    if (mt_n & 1) step2(16 * nb + 2 * tig);
+    if (mt_n & 1) tail(16 * nb);
   }
 #pragma unroll
   for (int t = 0; t < 2; ++t)
@@ -260,7 +269,7 @@ __device__ __forceinline__ double b2_store_r(const BatchArgs& a, const double (&
 template <int MTC, bool PIPE = true>
 __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ int dirty_epoch;
+  __shared__ int dirty_epoch, sweep_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int sa = MTC ? 8 * MTC + 4 : a.sa2;
@@ -285,6 +294,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
       rg.cnt[s] = 0;
     }
     dirty_epoch = 0;
+    sweep_epoch = 0;
     fence_mbar_init();
   }
   fence_proxy_async_smem();
@@ -443,7 +453,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
       const double* R = a.R[par];
       b2_load_ry(a, sa, rw0, R, nullptr, kw, 0.0, lane);
       // sweep 1: epsilon_k = max_j (v_jk)+ / |a_j't|, v = -A'r
-      double emax = 0.0;
+      double emax = 0.0, vmin = 0.0;
       for (int c = 0; c < a.nch; ++c) {
         const int j0 = c * BT_CH;
         const double* st = b2_acquire(a, rg);
@@ -458,10 +468,16 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
 #pragma unroll
         for (int t = 0; t < 2; ++t)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) emax = fmax(emax, fmax(-d[t][e], 0.0) * (1.0 / fabs(at[t][e])));
+          for (int e = 0; e < 2; ++e) {
+            emax = fmax(emax, fmax(-d[t][e], 0.0) * (1.0 / fabs(at[t][e])));
+            vmin = fmin(vmin, -d[t][e]);
+          }
       }
 #pragma unroll
-      for (int o = 1; o < 4; o <<= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+      for (int o = 1; o < 4; o <<= 1) {
+        emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+        vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+      }
       const double eps = emax;  // of problem g
       // dual objective per problem: theta = -r + eps t (t = -1)
       double thr = 0.0;         // radius + slack of problem g
@@ -489,8 +505,25 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
         }
         if (g == pb) thr = sqrt(2.0 * gap) + a.slack_scale * fmax(1.0, sqrt(s2));
       }
-      // sweep 2: v = -g + eps a't ; screen v < -(radius + slack) ||a_j||
+      // sweep 2: v = -g + eps a't ; screen v < -(radius + slack) ||a_j||.
+      // Sweep 1 already bounds the test of a whole problem: every statistic
+      // v_j + eps a_j't + thr ||a_j|| is at least
+      //     min_j v_j - eps max_j |a_j't| + thr min_j ||a_j||,
+      // so when that is positive (with a margin far above the round-off of
+      // the per-coordinate expression) no coordinate of the problem can be
+      // screened, and when it holds for all 64 problems of the tile the
+      // per-coordinate sweep -- a full A'R product -- is skipped.  Exact: a
+      // skipped sweep would have screened nothing.
+      bool need2 = false;
       if (a.screening) {
+        const double lo = vmin - eps * a.att_max + thr * a.nrm_min;
+        const bool clear = a.bound_skip && lo > 1e-9 * (fabs(vmin) + eps * a.att_max + thr * a.nrm_min);
+        if (!clear) atomicMax(&sweep_epoch, epoch);
+        __syncthreads();
+        need2 = sweep_epoch == epoch;
+        if (need2 && tid == 0 && a.sweeps2) atomicAdd(a.sweeps2, 1ull);
+      }
+      if (need2) {
         const uint32_t* mkg = a.mask + kg * a.nw;
         for (int c = 0; c < a.nch; ++c) {
           const int j0 = c * BT_CH;

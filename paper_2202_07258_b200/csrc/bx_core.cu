@@ -3219,6 +3219,7 @@ BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* bas
   double* stats = (double*)w.take(5 * L.Kp * 8);
   int* flags = (int*)w.take(64);
   double* red = (double*)w.take(64);
+  unsigned long long* sweeps2 = (unsigned long long*)w.take(64);
   L.bytes = w.off + kAlign;
   if (b) {
     b->a.Y = Y;
@@ -3232,6 +3233,7 @@ BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* bas
     b->a.Ap = Ap;
     b->a.sa2 = (int)sa2;
     b->a.nch = (int)(n_pad / BT_CH);
+    b->a.sweeps2 = sweeps2;
     b->a.mom = mom;
     b->a.P = P;
     b->a.stats = stats;
@@ -3394,6 +3396,21 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
     b->err = "zero column in A";
     return BX_ERR_ZERO_COLUMN;
   }
+  {
+    // constants of the sphere-test bound (second schedule)
+    std::vector<double> hn(n), ha(n);
+    BCU(cudaMemcpyAsync(hn.data(), A.nrm, n * 8, cudaMemcpyDeviceToHost, b->stream));
+    BCU(cudaMemcpyAsync(ha.data(), A.att, n * 8, cudaMemcpyDeviceToHost, b->stream));
+    BCU(cudaStreamSynchronize(b->stream));
+    double amax = 0.0, nmin = hn[0];
+    for (int64_t j = 0; j < n; ++j) {
+      amax = std::max(amax, std::fabs(ha[j]));
+      nmin = std::min(nmin, hn[j]);
+    }
+    A.att_max = amax;
+    A.nrm_min = nmin;
+    A.bound_skip = getenv("BX_BT_NOSKIP") ? 0 : 1;
+  }
   return BX_OK;
 }
 
@@ -3405,6 +3422,7 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
   A.passes = passes;
   A.screening = screening;
   A.par = 0;
+  BCU(cudaMemsetAsync(A.sweeps2, 0, 8, b->stream));
   A.dbg = nullptr;
   if (getenv("BX_BT_DEBUG")) BCU(cudaMalloc(&A.dbg, 148 * 8 * 4 * 8));
   k_batched_init<<<1024, 256, 0, b->stream>>>(A);
@@ -3460,6 +3478,10 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
     out->iterations = r * passes;
     out->kernel_launches = b->launches;
     out->max_gap = b->hred[1];
+    unsigned long long sw = 0;
+    BCU(cudaMemcpy(&sw, A.sweeps2, 8, cudaMemcpyDeviceToHost));
+    out->sphere_sweeps = b->sched == 2 ? (int64_t)sw : (screening ? r * (A.K / b->tile) : 0);
+    out->tiles = A.K / b->tile;
   }
   return BX_OK;
 }

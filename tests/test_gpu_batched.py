@@ -57,3 +57,29 @@ def test_bump_dictionary_config5_shape():
     g = solve_batched(a, Y, passes=10, rounds=4, gap_tol=1e-6)
     assert g.rounds == 4
     assert g.trace[-1, 2] < g.trace[0, 2]   # mean gap decreased
+
+
+def test_sphere_sweep_bound_is_exact(monkeypatch):
+    """The per-problem bound of the dual sweep (min_j v_j - eps max|a_j't| +
+    thr min||a_j|| > 0: nothing can be screened) only skips sweeps that screen
+    nothing: with the bound switched off (BX_BT_NOSKIP=1, every tile runs the
+    per-coordinate test) every trace value, mask count and x is bit-identical
+    -- on an instance that screens (the sweep must run) and on the config-5
+    dictionary (the bound clears every tile)."""
+    from paper_2202_07258_b200.batched import solve_batched
+    from paper_2202_07258_b200.generate import batched_rhs, bump_dictionary
+    a, Y = _instance(60, 40, 128, seed=5)
+    on = solve_batched(a, Y, passes=10, rounds=60, gap_tol=1e-300)
+    assert on.preserved.mean() < 40 and on.sphere_sweeps > 0          # screening fired through the sweep
+    ab = bump_dictionary(200, 5000)
+    Yb, _ = batched_rhs(ab, 128)
+    onb = solve_batched(ab, Yb, passes=10, rounds=3, gap_tol=1e-6)
+    assert onb.sphere_sweeps == 0 and onb.tiles == 2                   # cleared by the bound
+    monkeypatch.setenv("BX_BT_NOSKIP", "1")
+    off = solve_batched(a, Y, passes=10, rounds=60, gap_tol=1e-300)
+    offb = solve_batched(ab, Yb, passes=10, rounds=3, gap_tol=1e-6)
+    assert off.sphere_sweeps == 60 * off.tiles and offb.sphere_sweeps == 3 * offb.tiles
+    for u, v in ((on, off), (onb, offb)):
+        for f in ("primal", "dual", "gap", "preserved"):
+            np.testing.assert_array_equal(getattr(u, f), getattr(v, f))
+        np.testing.assert_array_equal(u.x, v.x)
