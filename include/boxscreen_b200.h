@@ -323,6 +323,8 @@ typedef struct {
    * test; the others were cleared by the per-problem bound (no coordinate
    * could be screened); tiles = K / 64 */
   int64_t sphere_sweeps, tiles;
+  /* summed duration of the round kernels (CUDA events on the solve's stream) */
+  double round_kernel_ms;
 } bx_batched_out;
 size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs);
 /* A: device, column-major (lda even); Y: device m x K column-major (ldy) */
@@ -334,6 +336,13 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
  * per round): {converged, max gap, mean gap, mean preserved}. */
 int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
                    double* trace_host, int64_t trace_cap, bx_batched_out* out_host);
+/* bx_batched_run with the result delivered to the host: x_host (pinned,
+ * n x K column-major, column stride ldx_host >= n) holds X when the call
+ * returns.  In the last round of the budget the tiles run wave by wave and
+ * each wave's columns of X are copied out while the next waves compute. */
+int bx_batched_run_to_host(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening,
+                           double gap_tol, double* trace_host, int64_t trace_cap, bx_batched_out* out_host,
+                           double* x_host, int64_t ldx_host);
 /* x: n x K (device, column stride ldx_out); stats: 5 x K (device) per-problem
  * {primal, dual, gap, eps, preserved} of the last round */
 int bx_batched_get(bx_batch* b, double* x, int64_t ldx_out, double* stats);

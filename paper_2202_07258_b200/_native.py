@@ -56,7 +56,7 @@ PROF_NAMES = ["pass_dot", "pass_pg_g", "pass_pg", "pass_apg", "pass_power", "pas
 class BatchedOut(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int64), ("converged", ctypes.c_int64), ("iterations", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("max_gap", ctypes.c_double),
-                ("sphere_sweeps", ctypes.c_int64), ("tiles", ctypes.c_int64)]
+                ("sphere_sweeps", ctypes.c_int64), ("tiles", ctypes.c_int64), ("round_kernel_ms", ctypes.c_double)]
 
 
 START_FN = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
@@ -114,6 +114,8 @@ SIGNATURES = {
     "bx_batched_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _sz,
                                          _vp]),
     "bx_batched_run": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _d, _dp, _i64, ctypes.POINTER(BatchedOut)]),
+    "bx_batched_run_to_host": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _d, _dp, _i64, ctypes.POINTER(BatchedOut),
+                                              _vp, _i64]),
     "bx_batched_get": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
     "bx_batched_last_error": (ctypes.c_char_p, [_vp]),
     "bx_batched_destroy": (ctypes.c_int, [_vp]),

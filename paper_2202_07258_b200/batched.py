@@ -31,6 +31,7 @@ class BatchedResult:
     kernel_launches: int = 0
     sphere_sweeps: int = 0    # tile-rounds that ran the per-coordinate sphere test (others cleared by the bound)
     tiles: int = 0            # tiles (64 right-hand sides) per round
+    round_kernel_ms: float = 0.0   # summed duration of the round kernels (CUDA events)
 
 
 def _check(st, h, what):
@@ -72,27 +73,34 @@ def solve_batched(a, Y, passes=10, rounds=10, gap_tol=1e-6, screening=True, eta=
                                    ws.data_ptr(), nbytes, stream.cuda_stream), h, "bx_batched_create")
         trace = np.zeros((rounds, 4))
         out = nat.BatchedOut()
-        _check(L.bx_batched_run(h, float(eta), passes, rounds, 1 if screening else 0, gap_tol,
-                                trace.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), rounds, ctypes.byref(out)),
-               h, "bx_batched_run")
-        x = torch.empty((K, n), dtype=torch.float64, device=dev)  # column-major n x K
+        tr_p = trace.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         stats = torch.empty((5, K), dtype=torch.float64, device=dev)
-        _check(L.bx_batched_get(h, x.data_ptr(), n, stats.data_ptr()), h, "bx_batched_get")
+        if return_device:
+            _check(L.bx_batched_run(h, float(eta), passes, rounds, 1 if screening else 0, gap_tol, tr_p, rounds,
+                                    ctypes.byref(out)), h, "bx_batched_run")
+            x = torch.empty((K, n), dtype=torch.float64, device=dev)  # column-major n x K
+            _check(L.bx_batched_get(h, x.data_ptr(), n, stats.data_ptr()), h, "bx_batched_get")
+            xo = x.t()
+        else:
+            # n x K fp64 is GBs at config 5: the result goes to pinned host
+            # memory (torch's caching host allocator reuses it across calls),
+            # and the last round of the budget streams it out wave by wave
+            # behind the remaining tensor work (bx_batched_run_to_host)
+            host = x_out if x_out is not None else torch.empty((K, n), dtype=torch.float64, pin_memory=True)
+            if tuple(host.shape) != (K, n) or host.dtype != torch.float64 or host.device.type != "cpu" or \
+                    not host.is_contiguous():
+                raise ValueError("x_out must be a contiguous (K, n) float64 host tensor")
+            if not host.is_pinned():
+                raise ValueError("x_out must be pinned host memory (torch.empty(..., pin_memory=True))")
+            _check(L.bx_batched_run_to_host(h, float(eta), passes, rounds, 1 if screening else 0, gap_tol, tr_p, rounds,
+                                            ctypes.byref(out), host.data_ptr(), n), h, "bx_batched_run_to_host")
+            _check(L.bx_batched_get(h, None, n, stats.data_ptr()), h, "bx_batched_get")
+            xo = host.numpy().T
     finally:
         L.bx_batched_destroy(h)
     st = stats.cpu().numpy()
-    if return_device:
-        xo = x.t()
-    else:
-        # n x K fp64 is GBs at config 5: copy into pinned host memory (torch's
-        # caching host allocator reuses it across calls) at full PCIe rate
-        host = x_out if x_out is not None else torch.empty((K, n), dtype=torch.float64, pin_memory=True)
-        if tuple(host.shape) != (K, n) or host.dtype != torch.float64 or host.device.type != "cpu":
-            raise ValueError("x_out must be a (K, n) float64 host tensor")
-        host.copy_(x, non_blocking=True)
-        stream.synchronize()
-        xo = host.numpy().T
     return BatchedResult(x=xo, primal=st[0], dual=st[1], gap=st[2], eps=st[3], preserved=st[4].astype(np.int64),
                          rounds=int(out.rounds), converged=int(out.converged), iterations=int(out.iterations),
                          eta=float(eta), trace=trace[: int(out.rounds)], kernel_launches=int(out.kernel_launches),
-                         sphere_sweeps=int(out.sphere_sweeps), tiles=int(out.tiles))
+                         sphere_sweeps=int(out.sphere_sweeps), tiles=int(out.tiles),
+                         round_kernel_ms=float(out.round_kernel_ms))

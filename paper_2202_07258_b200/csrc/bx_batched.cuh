@@ -53,6 +53,7 @@ struct BatchArgs {
   // in the ring's stage layout (k_b2_pack), a whole number of 16-column chunks
   const double* Ap;
   int nch;             // chunks
+  int tile0, tile1;    // tile range of this launch (second schedule)
   double att_max, nrm_min;        // max_j |a_j't|, min_j ||a_j|| over the real columns (sphere-test bound)
   int bound_skip;                 // 1: skip the per-coordinate sphere sweep of tiles the bound clears
   unsigned long long* sweeps2;    // tiles that ran the per-coordinate sweep (counter; may be null)

@@ -313,12 +313,11 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
   for (int t = 0; t < 2; ++t)
 #pragma unroll
     for (int e = 0; e < 2; ++e) so[t][e] = b2_slot(8 * t + 2 * tig + e) * sa;
-  const int ntiles = a.K / BT_TILE;
   int epoch = 0;
   long long dbg_wait = 0, dbg_nlong = 0;
   const long long dbg_t0 = clock64();
 
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tile = a.tile0 + blockIdx.x; tile < a.tile1; tile += gridDim.x) {
     ++epoch;
     const int64_t kw = (int64_t)tile * BT_TILE + warp * 8;   // first problem of the octet
     const int64_t kg = kw + g;                               // the problem of this lane's coordinate pairs

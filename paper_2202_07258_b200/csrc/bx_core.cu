@@ -3187,6 +3187,10 @@ struct bx_batch {
   int tile = 64;  // problems per CTA tile of k_batched_round
   int sched = 2;  // 2: warp-per-octet schedule over a TMA chunk ring (bx_batched2.cuh); 1: the first schedule
   size_t smem2 = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // around every round kernel (live duration for the roofline)
+  cudaStream_t copy_stream = nullptr;      // result rows leaving for the host during the last round
+  cudaEvent_t ev_wave = nullptr, ev_copy = nullptr;
+  double round_ms = 0.0;
   bool pipe = true;  // software-pipelined chunk loop (BX_BT_PIPE=0: the A/B control)
   int mtc = 0;    // compile-time row-tile count of the launched instantiation (0: run-time m)
 };
@@ -3309,6 +3313,12 @@ size_t bx_batched_workspace_bytes(int64_t m, int64_t n, int64_t k_rhs) {
     }                                                                                        \
   } while (0)
 
+#define TRY_B(call)            \
+  do {                         \
+    const int st_ = (call);    \
+    if (st_ != BX_OK) return st_; \
+  } while (0)
+
 int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const double* a, int64_t lda,
                       const double* y, int64_t ldy, void* workspace, size_t workspace_bytes, void* stream) {
   if (!out) return BX_ERR_INVALID_ARGUMENT;
@@ -3377,6 +3387,8 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
     BCU(cudaFuncSetAttribute(k_batched_round<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
   b->hred = (double*)pin_acquire(64);
   if (!b->hred) return BX_ERR_CUDA;
+  BCU(cudaEventCreate(&b->ev[0]));
+  BCU(cudaEventCreate(&b->ev[1]));
   // padded copy of Y, t = -1, column norms and A't of the dictionary
   k_pad_copy<<<1024, 256, 0, b->stream>>>(y, ldy, m, k_rhs, const_cast<double*>(A.Y), L.ldy, L.Kp);
   k_fill<double><<<4, 256, 0, b->stream>>>(L.ldy, b->t, 0.0);
@@ -3414,10 +3426,43 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
   return BX_OK;
 }
 
-int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
-                   double* trace_host, int64_t trace_cap, bx_batched_out* out) {
+}  // extern "C"
+
+namespace {
+// one round over tiles [t0, t1) with the selected schedule
+int batched_launch(bx_batch* b, int t0, int t1) {
+  BatchArgs& A = b->a;
+  const int per_sm = b->tile == 64 ? 1 : 2;
+  const int nt = t1 - t0;
+  const int grid = per_sm * b->nsm < nt ? per_sm * b->nsm : nt;
+  A.tile0 = t0;
+  A.tile1 = t1;
+  if (b->sched == 2 && b->mtc == 25 && !b->pipe)
+    k_batched_round2<25, false><<<grid, B2_NT, b->smem2, b->stream>>>(A);
+  else if (b->sched == 2 && b->mtc == 25)
+    k_batched_round2<25><<<grid, B2_NT, b->smem2, b->stream>>>(A);
+  else if (b->sched == 2)
+    k_batched_round2<0><<<grid, B2_NT, b->smem2, b->stream>>>(A);
+  else if (b->tile == 64)
+    k_batched_round<64><<<grid, 64 * 8, b->smem, b->stream>>>(A);
+  else
+    k_batched_round<32><<<grid, 32 * 8, b->smem, b->stream>>>(A);
+  ++b->launches;
+  BCU(cudaGetLastError());
+  return BX_OK;
+}
+
+// x_host (optional, pinned, n x K column-major with stride ldx_host): the
+// result on the host when the call returns.  In the last round of the budget
+// the tiles are launched wave by wave and each wave's rows of X leave for the
+// host while the next waves compute (the 4 GB of config 5 cross PCIe behind
+// ~150 ms of tensor work instead of after it); a solve that converges earlier
+// copies after its last round.
+int batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
+                double* trace_host, int64_t trace_cap, bx_batched_out* out, double* x_host, int64_t ldx_host) {
   if (!b) return BX_ERR_INVALID_ARGUMENT;
   BatchArgs& A = b->a;
+  if (x_host && ldx_host < A.n) return BX_ERR_INVALID_ARGUMENT;
   A.eta = eta;
   A.passes = passes;
   A.screening = screening;
@@ -3427,28 +3472,51 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
   if (getenv("BX_BT_DEBUG")) BCU(cudaMalloc(&A.dbg, 148 * 8 * 4 * 8));
   k_batched_init<<<1024, 256, 0, b->stream>>>(A);
   b->launches = 1;
-  const int per_sm = b->tile == 64 ? 1 : 2;
-  int grid = per_sm * b->nsm < A.K / b->tile ? per_sm * b->nsm : A.K / b->tile;
+  b->round_ms = 0.0;
+  const int ntiles = A.K / b->tile;
+  const int wave = (b->tile == 64 ? 1 : 2) * b->nsm;
+  bool streamed = false;
   int64_t r = 0;
   int64_t conv = 0;
   for (r = 0; r < rounds; ++r) {
-    if (b->sched == 2 && b->mtc == 25 && !b->pipe)
-      k_batched_round2<25, false><<<grid, B2_NT, b->smem2, b->stream>>>(A);
-    else if (b->sched == 2 && b->mtc == 25)
-      k_batched_round2<25><<<grid, B2_NT, b->smem2, b->stream>>>(A);
-    else if (b->sched == 2)
-      k_batched_round2<0><<<grid, B2_NT, b->smem2, b->stream>>>(A);
-    else if (b->tile == 64)
-      k_batched_round<64><<<grid, 64 * 8, b->smem, b->stream>>>(A);
-    else
-      k_batched_round<32><<<grid, 32 * 8, b->smem, b->stream>>>(A);
+    BCU(cudaEventRecord(b->ev[0], b->stream));
+    if (x_host && b->sched == 2 && r == rounds - 1 && ntiles > wave) {
+      if (!b->copy_stream) {
+        BCU(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+        BCU(cudaEventCreateWithFlags(&b->ev_wave, cudaEventDisableTiming));
+        BCU(cudaEventCreateWithFlags(&b->ev_copy, cudaEventDisableTiming));
+      }
+      const int par_after = (passes & 1) ? A.par ^ 1 : A.par;
+      for (int t0 = 0; t0 < ntiles; t0 += wave) {
+        const int t1 = t0 + wave < ntiles ? t0 + wave : ntiles;
+        TRY_B(batched_launch(b, t0, t1));
+        BCU(cudaEventRecord(b->ev_wave, b->stream));
+        BCU(cudaStreamWaitEvent(b->copy_stream, b->ev_wave, 0));
+        const int64_t k0 = (int64_t)t0 * b->tile;
+        const int64_t k1 = std::min<int64_t>((int64_t)t1 * b->tile, b->K_user);
+        if (k1 > k0)
+          BCU(cudaMemcpy2DAsync(x_host + k0 * ldx_host, ldx_host * 8, A.X[par_after] + k0 * A.ldx, A.ldx * 8,
+                                A.n * 8, k1 - k0, cudaMemcpyDeviceToHost, b->copy_stream));
+      }
+      BCU(cudaEventRecord(b->ev_copy, b->copy_stream));
+      BCU(cudaStreamWaitEvent(b->stream, b->ev_copy, 0));
+      streamed = true;
+    } else {
+      TRY_B(batched_launch(b, 0, ntiles));
+    }
+    BCU(cudaEventRecord(b->ev[1], b->stream));
     k_batched_summary<<<1, 1024, 0, b->stream>>>(A.stats, A.K, b->K_user, gap_tol, b->red);
-    b->launches += 2;
+    ++b->launches;
     BCU(cudaGetLastError());
     if (passes & 1) A.par ^= 1;
     BCU(cudaMemcpyAsync(b->hred, b->red, 4 * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
     BCU(cudaStreamSynchronize(b->stream));
     conv = (int64_t)b->hred[0];
+    {
+      float ms = 0.f;
+      BCU(cudaEventElapsedTime(&ms, b->ev[0], b->ev[1]));
+      b->round_ms += ms;
+    }
     if (trace_host && r < trace_cap) {
       trace_host[4 * r + 0] = b->hred[0];
       trace_host[4 * r + 1] = b->hred[1];
@@ -3459,6 +3527,11 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
       ++r;
       break;
     }
+  }
+  if (x_host && !streamed) {
+    BCU(cudaMemcpy2DAsync(x_host, ldx_host * 8, A.X[A.par], A.ldx * 8, A.n * 8, b->K_user, cudaMemcpyDeviceToHost,
+                          b->stream));
+    BCU(cudaStreamSynchronize(b->stream));
   }
   if (A.dbg) {
     std::vector<unsigned long long> h(148 * 8 * 4);
@@ -3482,8 +3555,24 @@ int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int3
     BCU(cudaMemcpy(&sw, A.sweeps2, 8, cudaMemcpyDeviceToHost));
     out->sphere_sweeps = b->sched == 2 ? (int64_t)sw : (screening ? r * (A.K / b->tile) : 0);
     out->tiles = A.K / b->tile;
+    out->round_kernel_ms = b->round_ms;
   }
   return BX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
+                   double* trace_host, int64_t trace_cap, bx_batched_out* out) {
+  return batched_run(b, eta, passes, rounds, screening, gap_tol, trace_host, trace_cap, out, nullptr, 0);
+}
+
+int bx_batched_run_to_host(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
+                           double* trace_host, int64_t trace_cap, bx_batched_out* out, double* x_host,
+                           int64_t ldx_host) {
+  if (!x_host) return BX_ERR_INVALID_ARGUMENT;
+  return batched_run(b, eta, passes, rounds, screening, gap_tol, trace_host, trace_cap, out, x_host, ldx_host);
 }
 
 int bx_batched_get(bx_batch* b, double* x, int64_t ldx_out, double* stats) {
@@ -3504,6 +3593,9 @@ const char* bx_batched_last_error(const bx_batch* b) { return b ? b->err.c_str()
 int bx_batched_destroy(bx_batch* b) {
   if (!b) return BX_OK;
   pin_release(b->hred);
+  for (cudaEvent_t e : {b->ev[0], b->ev[1], b->ev_wave, b->ev_copy})
+    if (e) cudaEventDestroy(e);
+  if (b->copy_stream) cudaStreamDestroy(b->copy_stream);
   delete b;
   return BX_OK;
 }

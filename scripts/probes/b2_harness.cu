@@ -13,7 +13,7 @@ int main(int argc, char** argv) {
   const int m8 = 200, sa = m8 + 4, nch = (n + 15) / 16, npad = nch * 16;
   BatchArgs a{};
   a.m = m; a.n = n; a.K = K; a.sa = 212; a.sa2 = sa; a.nch = nch; a.ldy = m8; a.ldx = npad; a.nw = (n + 31) / 32;
-  a.eta = 1e-3; a.passes = passes; a.par = 0; a.screening = 1; a.rs_f = a.rs_g = a.slack_scale = 1e-12; a.dbg = nullptr;
+  a.eta = 1e-3; a.passes = passes; a.par = 0; a.tile0 = 0; a.tile1 = K / 64; a.att_max = 14.0; a.nrm_min = 1.0; a.bound_skip = 0; a.sweeps2 = nullptr; a.screening = 1; a.rs_f = a.rs_g = a.slack_scale = 1e-12; a.dbg = nullptr;
   std::vector<double> hA((size_t)npad * sa);
   for (size_t i = 0; i < hA.size(); ++i) hA[i] = ((i * 2654435761u) % 1000) * 1e-3;
   double *Ap, *Y, *X0, *X1, *R0, *R1, *nrm, *att, *mom, *P, *stats; uint32_t* mask;

@@ -83,3 +83,26 @@ def test_sphere_sweep_bound_is_exact(monkeypatch):
         for f in ("primal", "dual", "gap", "preserved"):
             np.testing.assert_array_equal(getattr(u, f), getattr(v, f))
         np.testing.assert_array_equal(u.x, v.x)
+
+
+def test_result_streamed_to_host_during_last_round():
+    """More tiles than SMs: the last round of the budget runs wave by wave and
+    each wave's columns of X are copied to the (pinned) host buffer while the
+    next waves compute (bx_batched_run_to_host); same bits as the device
+    result, also when the solve stops before the budget (copy after the last
+    round) and into a caller-supplied buffer."""
+    import torch
+    from paper_2202_07258_b200.batched import solve_batched
+    K = 149 * 64 + 7
+    a, Y = _instance(16, 40, K, seed=11)
+    dev = solve_batched(a, Y, passes=10, rounds=3, gap_tol=1e-300, return_device=True)
+    host = solve_batched(a, Y, passes=10, rounds=3, gap_tol=1e-300)
+    np.testing.assert_array_equal(host.x, dev.x.cpu().numpy())
+    np.testing.assert_array_equal(host.gap, dev.gap)
+    buf = torch.empty((K, 40), dtype=torch.float64, pin_memory=True)
+    early = solve_batched(a, Y, passes=10, rounds=50, gap_tol=1e30, x_out=buf)      # converged after round 1
+    assert early.rounds == 1
+    one = solve_batched(a, Y, passes=10, rounds=1, gap_tol=1e-300, return_device=True)
+    np.testing.assert_array_equal(early.x, one.x.cpu().numpy())
+    with pytest.raises(ValueError):
+        solve_batched(a, Y, passes=10, rounds=1, x_out=torch.empty((K, 40), dtype=torch.float64))
