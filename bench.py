@@ -388,7 +388,8 @@ def run_reference(args):
               f"{sum(d['timed_iterations'] for d in details)} iterations per step")
     line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": unit_name(args.config),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True,
+            "scaling": "strong" if args.config in (3, 5) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config recipe)",
             "config": config_block(args.config, inst),
             "cpu_baseline": {"value": rate, "unit": unit_name(args.config), "cores": thr, "kind": "port", "sample": sample,
@@ -445,7 +446,8 @@ def run_reference_unmodified(args, bs, world):
     rate = float(np.median(rates))
     line = {"impl": "reference", "metric": metric_name(args.config), "value": rate, "unit": unit_name(args.config),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True,
+            "scaling": "strong" if args.config in (3, 5) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config recipe)",
             "config": config_block(args.config, inst),
             "cpu_baseline": {"value": rate, "unit": unit_name(args.config), "cores": thr, "kind": "reference",
