@@ -51,7 +51,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--rounds", type=int, default=2, help="config 5: rounds (x10 FISTA steps) per step")
+    ap.add_argument("--rounds", type=int, default=8, help="config 5: rounds (x10 FISTA steps) per step")
+    ap.add_argument("--check-every", type=int, default=0,
+                    help="config 5: rounds between convergence checks / host round trips (0: min(rounds, 16))")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -668,8 +670,10 @@ def run_batched(args, rank, world, dev):
     y_dev = torch.from_numpy(np.ascontiguousarray(Y)).to(dev)
     stream = torch.cuda.current_stream(dev)
     rounds = args.rounds
+    every = args.check_every if args.check_every > 0 else min(rounds, 16)
     for _ in range(args.warmup):
-        solve_batched(a_dev, y_dev, passes=10, rounds=rounds, gap_tol=c["gap_tol"], eta=eta, return_device=True)
+        solve_batched(a_dev, y_dev, passes=10, rounds=rounds, gap_tol=c["gap_tol"], eta=eta, return_device=True,
+                      check_every=every)
     torch.cuda.synchronize()
     res = []
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
@@ -681,7 +685,7 @@ def run_batched(args, rank, world, dev):
         e0.record(stream)
         for _ in range(args.steps):
             res.append(solve_batched(a_dev, y_dev, passes=10, rounds=rounds, gap_tol=c["gap_tol"], eta=eta,
-                                     return_device=True))
+                                     return_device=True, check_every=every))
         e1.record(stream)
         torch.cuda.synchronize()
     el = e0.elapsed_time(e1) / 1000.0
@@ -723,7 +727,8 @@ def run_batched(args, rank, world, dev):
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record(stream)
             r = solve_batched(a_pin.to(dev, non_blocking=True), y_pin.to(dev, non_blocking=True), passes=10,
-                              rounds=rounds, gap_tol=c["gap_tol"], eta=eta, return_device=False, x_out=x_pin)
+                              rounds=rounds, gap_tol=c["gap_tol"], eta=eta, return_device=False, x_out=x_pin,
+                              check_every=every)
             t1.record(stream)
             torch.cuda.synchronize()
             if s_:
@@ -748,7 +753,7 @@ def run_batched(args, rank, world, dev):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded bump dictionary + Dirichlet RHS, BASELINE config 5 recipe)",
             "config": {"workload": c["name"], "m": m, "n": n, "k_rhs": K, "solver": "apg (batched)",
-                       "inner_passes": 10, "rounds_per_step": rounds,
+                       "inner_passes": 10, "rounds_per_step": rounds, "check_every": every,
                        "parallelism": f"right-hand sides sharded x{world}, no communication",
                        "step": f"{rounds} screened rounds ({10 * rounds} FISTA steps) on every right-hand side"},
             "max_gap": float(r0.gap.max()), "mean_gap": float(r0.gap.mean()),

@@ -336,6 +336,14 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
  * per round): {converged, max gap, mean gap, mean preserved}. */
 int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
                    double* trace_host, int64_t trace_cap, bx_batched_out* out_host);
+/* Convergence is checked (and the host synchronised) every rounds_per_check
+ * rounds (default 1, at most 16).  With more than one, a launch runs that many
+ * rounds and the rounds of different tiles overlap across it: SMs that finish
+ * a round's last wave of tiles start the next round's first tiles (a tile's
+ * round r + 1 depends only on its own round r).  The per-round trace is still
+ * complete; a batch that converges at one of its inner rounds still runs to
+ * the batch's last round. */
+int bx_batched_set_check_every(bx_batch* b, int32_t rounds_per_check);
 /* bx_batched_run with the result delivered to the host: x_host (pinned,
  * n x K column-major, column stride ldx_host >= n) holds X when the call
  * returns.  In the last round of the budget the tiles run wave by wave and

@@ -114,6 +114,7 @@ SIGNATURES = {
     "bx_batched_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _sz,
                                          _vp]),
     "bx_batched_run": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _d, _dp, _i64, ctypes.POINTER(BatchedOut)]),
+    "bx_batched_set_check_every": (ctypes.c_int, [_vp, _i32]),
     "bx_batched_run_to_host": (ctypes.c_int, [_vp, _d, _i32, _i32, _i32, _d, _dp, _i64, ctypes.POINTER(BatchedOut),
                                               _vp, _i64]),
     "bx_batched_get": (ctypes.c_int, [_vp, _vp, _i64, _vp]),

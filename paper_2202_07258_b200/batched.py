@@ -41,9 +41,15 @@ def _check(st, h, what):
 
 
 def solve_batched(a, Y, passes=10, rounds=10, gap_tol=1e-6, screening=True, eta=None, return_device=False,
-                  x_out=None):
+                  x_out=None, check_every=1):
     """Run up to ``rounds`` rounds of ``passes`` FISTA steps on every column of
     Y (m x K); stops early when every problem's gap < gap_tol.
+
+    ``check_every``: rounds between convergence checks (1..16).  With more
+    than one the device runs that many rounds per launch without a host round
+    trip and overlaps the rounds of different tiles (the last, partly filled
+    wave of a round runs beside the next round's first tiles); a batch that
+    converges at an inner round still finishes its batch.
 
     ``x_out``: optional pinned host tensor (K x n, fp64) that receives X
     (returned as its n x K numpy view); reusing one across calls keeps the
@@ -71,6 +77,8 @@ def solve_batched(a, Y, passes=10, rounds=10, gap_tol=1e-6, screening=True, eta=
     try:
         _check(L.bx_batched_create(ctypes.byref(h), m, n, K, a_dev.data_ptr(), lda, y_dev.data_ptr(), m,
                                    ws.data_ptr(), nbytes, stream.cuda_stream), h, "bx_batched_create")
+        if check_every != 1:
+            _check(L.bx_batched_set_check_every(h, int(check_every)), h, "bx_batched_set_check_every")
         trace = np.zeros((rounds, 4))
         out = nat.BatchedOut()
         tr_p = trace.ctypes.data_as(ctypes.POINTER(ctypes.c_double))

@@ -54,6 +54,15 @@ struct BatchArgs {
   const double* Ap;
   int nch;             // chunks
   int tile0, tile1;    // tile range of this launch (second schedule)
+  // rounds per launch (second schedule): units (round, tile) in round-major
+  // order; round0 = rounds completed before this launch; per-octet completed
+  // round flags; per-octet round summaries [osum_rounds][K / 8][4]
+  int nrl, round0;
+  unsigned* oct_round;
+  double* osum;
+  int osum_rounds;
+  int64_t K_user;
+  double gap_tol;
   double att_max, nrm_min;        // max_j |a_j't|, min_j ||a_j|| over the real columns (sphere-test bound)
   int bound_skip;                 // 1: skip the per-coordinate sphere sweep of tiles the bound clears
   unsigned long long* sweeps2;    // tiles that ran the per-coordinate sweep (counter; may be null)

@@ -108,6 +108,14 @@ __device__ __forceinline__ void b2_release(const BatchArgs& a, B2Ring& rg, int l
 }
 
 __device__ __forceinline__ double2 b2_ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // d[t][e] (problem g, coordinate 8 t + 2 tig + e of the chunk) = sum_i Ry[i][g] A_J[i][.]
 // ry = warp's R_y + g * sa ; b0 = stage + slot(g) * sa.  The K index is a
@@ -223,8 +231,8 @@ __device__ __forceinline__ void b2_load_ry(const BatchArgs& a, int sa, double* r
     for (int i = lane; i < sa; i += 32) {
       double v = 0.0;
       if (i < a.m) {
-        v = r[i];
-        if (bt != 0.0) v = add_rn(v, mul_rn(bt, sub_rn(v, Rp[(kw + pp) * a.ldy + i])));
+        v = __ldcg(r + i);
+        if (bt != 0.0) v = add_rn(v, mul_rn(bt, sub_rn(v, __ldcg(Rp + (kw + pp) * a.ldy + i))));
       }
       rw0[pp * sa + i] = v;
     }
@@ -317,12 +325,34 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
   long long dbg_wait = 0, dbg_nlong = 0;
   const long long dbg_t0 = clock64();
 
-  for (int tile = a.tile0 + blockIdx.x; tile < a.tile1; tile += gridDim.x) {
+  // Work units of this launch: (round, tile) pairs in round-major order, unit
+  // u -> round u / ntl of the launch, tile tile0 + u % ntl; CTA b takes units
+  // b, b + grid, ...  One round per launch (nrl = 1) is the plain tile loop.
+  // With several rounds per launch the CTAs that finish a round's last wave
+  // early go on with the next round's first tiles instead of idling (1,563
+  // tiles on 148 SMs leave the 11th wave 56% full): a tile's round r + 1 only
+  // needs ITS round r, which another CTA finished ~10 waves earlier; each
+  // octet publishes its completed rounds in a flag the next round's warp
+  // acquires (everything an octet owns is written and later read by the warp
+  // of the same index, so the flags are per octet and no CTA barrier is
+  // involved), and every load of state another CTA may have written bypasses
+  // L1 (ld.global.cg).
+  const int ntl = a.tile1 - a.tile0;
+  for (int u = blockIdx.x; u < a.nrl * ntl; u += gridDim.x) {
     ++epoch;
+    const int rl = u / ntl;
+    const int tile = a.tile0 + (u - rl * ntl);
+    const int oct = tile * B2_NW + warp;
+    if (rl > 0) {
+      if (lane == 0)
+        while ((int)ld_acquire_gpu_u32(a.oct_round + oct) < a.round0 + rl) {
+        }
+      __syncwarp();
+    }
     const int64_t kw = (int64_t)tile * BT_TILE + warp * 8;   // first problem of the octet
     const int64_t kg = kw + g;                               // the problem of this lane's coordinate pairs
-    int par = a.par;
-    double mom = a.mom[kg], P = a.P[kg];
+    int par = a.par ^ ((rl * a.passes) & 1);
+    double mom = __ldcg(a.mom + kg), P = __ldcg(a.P + kg);
     // ---------------- FISTA steps ----------------
     for (int pass = 0; pass < a.passes; ++pass) {
       const double* X = a.X[par];
@@ -344,8 +374,8 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
       uint32_t mw;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        xc[t] = *reinterpret_cast<const double2*>(xg + 8 * t);
-        xpc[t] = *reinterpret_cast<const double2*>(xpg + 8 * t);
+        xc[t] = __ldcg(reinterpret_cast<const double2*>(xg + 8 * t));
+        xpc[t] = __ldcg(reinterpret_cast<const double2*>(xpg + 8 * t));
       }
       mw = __ldcg(mkg);
       // Software pipeline: iteration c runs GEMM1 of chunk c + 1, the update
@@ -415,8 +445,8 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
         if (c + 1 < a.nch) {
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            xc[t] = *reinterpret_cast<const double2*>(xg + j0 + BT_CH + 8 * t);
-            xpc[t] = *reinterpret_cast<const double2*>(xpg + j0 + BT_CH + 8 * t);
+            xc[t] = __ldcg(reinterpret_cast<const double2*>(xg + j0 + BT_CH + 8 * t));
+            xpc[t] = __ldcg(reinterpret_cast<const double2*>(xpg + j0 + BT_CH + 8 * t));
           }
           mw = __ldcg(mkg + ((j0 + BT_CH) >> 5));
         }
@@ -480,6 +510,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
       const double eps = emax;  // of problem g
       // dual objective per problem: theta = -r + eps t (t = -1)
       double thr = 0.0;         // radius + slack of problem g
+      double sm_conv = 0.0, sm_max = 0.0, sm_gap = 0.0, sm_pres = 0.0;
       for (int pb = 0; pb < 8; ++pb) {
         const double ep = __shfl_sync(0xffffffffu, eps, pb << 2);
         const double Pp = __shfl_sync(0xffffffffu, P, pb << 2);
@@ -494,6 +525,11 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
         s2 = warp_sum<double>(s2);
         const double D = s1 - 0.5 * s2;
         const double gap = fmax(Pp - D, 0.0);
+        if (kw + pb < a.K_user) {
+          sm_conv += gap < a.gap_tol ? 1.0 : 0.0;
+          sm_max = fmax(sm_max, gap);
+          sm_gap += gap;
+        }
         if (lane == 0) {
           const int64_t k = kw + pb;
           double* stt = a.stats;
@@ -575,7 +611,7 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
             double xn[2][2];
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
-              const double2 v = *reinterpret_cast<const double2*>(Xw + c * BT_CH + 8 * t);
+              const double2 v = __ldcg(reinterpret_cast<const double2*>(Xw + c * BT_CH + 8 * t));
               xn[t][0] = v.x;
               xn[t][1] = v.y;
             }
@@ -592,11 +628,26 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
         int cnt = 0;
         for (int w = lane; w < a.nw; w += 32) cnt += __popc(__ldcg(a.mask + (kw + pb) * a.nw + w));
         cnt = warp_sum<int>(cnt);
+        if (kw + pb < a.K_user) sm_pres += cnt;
         if (lane == 0) a.stats[4 * a.K + kw + pb] = cnt;
       }
       if (tig == 0) {
         a.mom[kg] = mom;
         a.P[kg] = P;
+      }
+      // this octet's share of the round summary {converged, max gap, sum gap,
+      // sum preserved} (problems past K_user are padding), then its flag
+      if (lane == 0) {
+        double* o = a.osum + ((size_t)((a.round0 + rl) % a.osum_rounds) * (a.K / 8) + oct) * 4;
+        o[0] = sm_conv;
+        o[1] = sm_max;
+        o[2] = sm_gap;
+        o[3] = sm_pres;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release_gpu_u32(a.oct_round + oct, (unsigned)(a.round0 + rl + 1));
       }
     }
   }
@@ -611,6 +662,45 @@ __global__ void __launch_bounds__(B2_NT, 1) k_batched_round2(const BatchArgs a) 
   for (int q = 0; q < B2_NST; ++q) {
     const int s = (rg.it + q) % B2_NST;
     mbar_wait(&rg.full[s], (uint32_t)(((rg.it + q) / B2_NST) & 1));
+  }
+}
+
+// Round summary from the per-octet partials, fixed order (one block):
+// out = {converged problems, max gap, sum gap, sum preserved}
+__global__ void k_b2_summary(const double* __restrict__ osum, int noct, double* __restrict__ out) {
+  __shared__ double sh[4][32];
+  double c = 0.0, mx = 0.0, sg = 0.0, sp = 0.0;
+  for (int o = threadIdx.x; o < noct; o += blockDim.x) {
+    c += osum[4 * o + 0];
+    mx = fmax(mx, osum[4 * o + 1]);
+    sg += osum[4 * o + 2];
+    sp += osum[4 * o + 3];
+  }
+  c = warp_sum<double>(c);
+  sg = warp_sum<double>(sg);
+  sp = warp_sum<double>(sp);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[0][warp] = c;
+    sh[1][warp] = mx;
+    sh[2][warp] = sg;
+    sh[3][warp] = sp;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a0 += sh[0][w];
+      a1 = fmax(a1, sh[1][w]);
+      a2 += sh[2][w];
+      a3 += sh[3][w];
+    }
+    out[0] = a0;
+    out[1] = a1;
+    out[2] = a2;
+    out[3] = a3;
   }
 }
 

@@ -3192,10 +3192,14 @@ struct bx_batch {
   cudaEvent_t ev_wave = nullptr, ev_copy = nullptr;
   double round_ms = 0.0;
   bool pipe = true;  // software-pipelined chunk loop (BX_BT_PIPE=0: the A/B control)
+  double last_max_gap = 0.0;
+  int check_every = 1;  // rounds per launch between convergence checks (second schedule)
   int mtc = 0;    // compile-time row-tile count of the launched instantiation (0: run-time m)
 };
 
 namespace {
+// rounds one launch of the second schedule may run (check_every is capped by it)
+constexpr int kBatchRoundsPerLaunch = 16;
 struct BatchLayout {
   int64_t Kp, ldx, ldy, nw;
   size_t bytes;
@@ -3222,8 +3226,10 @@ BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* bas
   double* P = (double*)w.take(L.Kp * 8);
   double* stats = (double*)w.take(5 * L.Kp * 8);
   int* flags = (int*)w.take(64);
-  double* red = (double*)w.take(64);
+  double* red = (double*)w.take(4 * kBatchRoundsPerLaunch * 8);
   unsigned long long* sweeps2 = (unsigned long long*)w.take(64);
+  unsigned* oct_round = (unsigned*)w.take((L.Kp / 8) * 4);
+  double* osum = (double*)w.take((size_t)kBatchRoundsPerLaunch * (L.Kp / 8) * 4 * 8);
   L.bytes = w.off + kAlign;
   if (b) {
     b->a.Y = Y;
@@ -3238,6 +3244,9 @@ BatchLayout batch_layout(int64_t m, int64_t n, int64_t K, bx_batch* b, char* bas
     b->a.sa2 = (int)sa2;
     b->a.nch = (int)(n_pad / BT_CH);
     b->a.sweeps2 = sweeps2;
+    b->a.oct_round = oct_round;
+    b->a.osum = osum;
+    b->a.osum_rounds = kBatchRoundsPerLaunch;
     b->a.mom = mom;
     b->a.P = P;
     b->a.stats = stats;
@@ -3385,7 +3394,7 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
     BCU(cudaFuncSetAttribute(k_batched_round<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
   else
     BCU(cudaFuncSetAttribute(k_batched_round<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
-  b->hred = (double*)pin_acquire(64);
+  b->hred = (double*)pin_acquire(4 * kBatchRoundsPerLaunch * 8);
   if (!b->hred) return BX_ERR_CUDA;
   BCU(cudaEventCreate(&b->ev[0]));
   BCU(cudaEventCreate(&b->ev[1]));
@@ -3430,20 +3439,28 @@ int bx_batched_create(bx_batch** out, int64_t m, int64_t n, int64_t k_rhs, const
 
 namespace {
 // one round over tiles [t0, t1) with the selected schedule
-int batched_launch(bx_batch* b, int t0, int t1) {
+int batched_launch(bx_batch* b, int t0, int t1, int round0, int nrl) {
   BatchArgs& A = b->a;
   const int per_sm = b->tile == 64 ? 1 : 2;
-  const int nt = t1 - t0;
-  const int grid = per_sm * b->nsm < nt ? per_sm * b->nsm : nt;
+  const int64_t units = (int64_t)(t1 - t0) * nrl;
+  const int grid = per_sm * b->nsm < units ? per_sm * b->nsm : (int)units;
   A.tile0 = t0;
   A.tile1 = t1;
-  if (b->sched == 2 && b->mtc == 25 && !b->pipe)
-    k_batched_round2<25, false><<<grid, B2_NT, b->smem2, b->stream>>>(A);
-  else if (b->sched == 2 && b->mtc == 25)
-    k_batched_round2<25><<<grid, B2_NT, b->smem2, b->stream>>>(A);
-  else if (b->sched == 2)
-    k_batched_round2<0><<<grid, B2_NT, b->smem2, b->stream>>>(A);
-  else if (b->tile == 64)
+  A.round0 = round0;
+  A.nrl = nrl;
+  if (b->sched == 2) {
+    // several rounds per launch: CTAs wait on flags other CTAs of the launch
+    // publish, so the grid must be co-resident -- a cooperative launch
+    // guarantees it (or fails) instead of assuming idle SMs
+    const void* fn = (b->mtc == 25 && !b->pipe) ? (const void*)k_batched_round2<25, false>
+                     : b->mtc == 25             ? (const void*)k_batched_round2<25, true>
+                                                : (const void*)k_batched_round2<0, true>;
+    void* kargs[] = {(void*)&A};
+    if (nrl > 1)
+      BCU(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(B2_NT), kargs, b->smem2, b->stream));
+    else
+      BCU(cudaLaunchKernel(fn, dim3(grid), dim3(B2_NT), kargs, b->smem2, b->stream));
+  } else if (b->tile == 64)
     k_batched_round<64><<<grid, 64 * 8, b->smem, b->stream>>>(A);
   else
     k_batched_round<32><<<grid, 32 * 8, b->smem, b->stream>>>(A);
@@ -3478,9 +3495,24 @@ int batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t
   bool streamed = false;
   int64_t r = 0;
   int64_t conv = 0;
-  for (r = 0; r < rounds; ++r) {
+  A.K_user = b->K_user;
+  A.gap_tol = gap_tol;
+  BCU(cudaMemsetAsync(A.oct_round, 0, (A.K / 8) * 4, b->stream));
+  const int noct = A.K / 8;
+  const bool stream_last = x_host && b->sched == 2 && ntiles > wave;
+  while (r < rounds) {
+    // rounds of this launch: one, or (second schedule) up to check_every with
+    // the tiles' rounds overlapping across the launch; the budget's last round
+    // runs alone when its result streams out
+    int nb = 1;
+    const bool last_alone = stream_last && r == rounds - 1;
+    if (b->sched == 2 && !last_alone) {
+      nb = (int)std::min<int64_t>({(int64_t)b->check_every, (int64_t)kBatchRoundsPerLaunch,
+                                   rounds - r - (stream_last ? 1 : 0)});
+      if (nb < 1) nb = 1;
+    }
     BCU(cudaEventRecord(b->ev[0], b->stream));
-    if (x_host && b->sched == 2 && r == rounds - 1 && ntiles > wave) {
+    if (last_alone) {
       if (!b->copy_stream) {
         BCU(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
         BCU(cudaEventCreateWithFlags(&b->ev_wave, cudaEventDisableTiming));
@@ -3489,7 +3521,7 @@ int batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t
       const int par_after = (passes & 1) ? A.par ^ 1 : A.par;
       for (int t0 = 0; t0 < ntiles; t0 += wave) {
         const int t1 = t0 + wave < ntiles ? t0 + wave : ntiles;
-        TRY_B(batched_launch(b, t0, t1));
+        TRY_B(batched_launch(b, t0, t1, (int)r, 1));
         BCU(cudaEventRecord(b->ev_wave, b->stream));
         BCU(cudaStreamWaitEvent(b->copy_stream, b->ev_wave, 0));
         const int64_t k0 = (int64_t)t0 * b->tile;
@@ -3502,31 +3534,39 @@ int batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t
       BCU(cudaStreamWaitEvent(b->stream, b->ev_copy, 0));
       streamed = true;
     } else {
-      TRY_B(batched_launch(b, 0, ntiles));
+      TRY_B(batched_launch(b, 0, ntiles, (int)r, nb));
     }
     BCU(cudaEventRecord(b->ev[1], b->stream));
-    k_batched_summary<<<1, 1024, 0, b->stream>>>(A.stats, A.K, b->K_user, gap_tol, b->red);
-    ++b->launches;
+    for (int q = 0; q < nb; ++q) {
+      if (b->sched == 2)
+        k_b2_summary<<<1, 1024, 0, b->stream>>>(
+            A.osum + (size_t)((r + q) % kBatchRoundsPerLaunch) * noct * 4, noct, b->red + 4 * q);
+      else
+        k_batched_summary<<<1, 1024, 0, b->stream>>>(A.stats, A.K, b->K_user, gap_tol, b->red);
+      ++b->launches;
+    }
     BCU(cudaGetLastError());
-    if (passes & 1) A.par ^= 1;
-    BCU(cudaMemcpyAsync(b->hred, b->red, 4 * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+    if ((nb * passes) & 1) A.par ^= 1;
+    BCU(cudaMemcpyAsync(b->hred, b->red, 4 * nb * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
     BCU(cudaStreamSynchronize(b->stream));
-    conv = (int64_t)b->hred[0];
     {
       float ms = 0.f;
       BCU(cudaEventElapsedTime(&ms, b->ev[0], b->ev[1]));
       b->round_ms += ms;
     }
-    if (trace_host && r < trace_cap) {
-      trace_host[4 * r + 0] = b->hred[0];
-      trace_host[4 * r + 1] = b->hred[1];
-      trace_host[4 * r + 2] = b->hred[2] / (double)b->K_user;
-      trace_host[4 * r + 3] = b->hred[3] / (double)b->K_user;
+    for (int q = 0; q < nb; ++q) {
+      const double* h = b->hred + 4 * q;
+      if (trace_host && r + q < trace_cap) {
+        trace_host[4 * (r + q) + 0] = h[0];
+        trace_host[4 * (r + q) + 1] = h[1];
+        trace_host[4 * (r + q) + 2] = h[2] / (double)b->K_user;
+        trace_host[4 * (r + q) + 3] = h[3] / (double)b->K_user;
+      }
     }
-    if (conv == b->K_user) {
-      ++r;
-      break;
-    }
+    r += nb;
+    conv = (int64_t)b->hred[4 * (nb - 1)];
+    b->last_max_gap = b->hred[4 * (nb - 1) + 1];
+    if (conv == b->K_user) break;
   }
   if (x_host && !streamed) {
     BCU(cudaMemcpy2DAsync(x_host, ldx_host * 8, A.X[A.par], A.ldx * 8, A.n * 8, b->K_user, cudaMemcpyDeviceToHost,
@@ -3550,7 +3590,7 @@ int batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t
     out->converged = conv;
     out->iterations = r * passes;
     out->kernel_launches = b->launches;
-    out->max_gap = b->hred[1];
+    out->max_gap = b->last_max_gap;
     unsigned long long sw = 0;
     BCU(cudaMemcpy(&sw, A.sweeps2, 8, cudaMemcpyDeviceToHost));
     out->sphere_sweeps = b->sched == 2 ? (int64_t)sw : (screening ? r * (A.K / b->tile) : 0);
@@ -3562,6 +3602,12 @@ int batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t
 }  // namespace
 
 extern "C" {
+
+int bx_batched_set_check_every(bx_batch* b, int32_t rounds_per_check) {
+  if (!b || rounds_per_check < 1) return BX_ERR_INVALID_ARGUMENT;
+  b->check_every = rounds_per_check < kBatchRoundsPerLaunch ? rounds_per_check : kBatchRoundsPerLaunch;
+  return BX_OK;
+}
 
 int bx_batched_run(bx_batch* b, double eta, int32_t passes, int32_t rounds, int32_t screening, double gap_tol,
                    double* trace_host, int64_t trace_cap, bx_batched_out* out) {

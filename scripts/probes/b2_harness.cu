@@ -13,7 +13,7 @@ int main(int argc, char** argv) {
   const int m8 = 200, sa = m8 + 4, nch = (n + 15) / 16, npad = nch * 16;
   BatchArgs a{};
   a.m = m; a.n = n; a.K = K; a.sa = 212; a.sa2 = sa; a.nch = nch; a.ldy = m8; a.ldx = npad; a.nw = (n + 31) / 32;
-  a.eta = 1e-3; a.passes = passes; a.par = 0; a.tile0 = 0; a.tile1 = K / 64; a.att_max = 14.0; a.nrm_min = 1.0; a.bound_skip = 0; a.sweeps2 = nullptr; a.screening = 1; a.rs_f = a.rs_g = a.slack_scale = 1e-12; a.dbg = nullptr;
+  a.eta = 1e-3; a.passes = passes; a.par = 0; a.tile0 = 0; a.tile1 = K / 64; a.nrl = 1; a.round0 = 0; a.K_user = K; a.gap_tol = 1e-6; a.osum_rounds = 1; a.att_max = 14.0; a.nrm_min = 1.0; a.bound_skip = 0; a.sweeps2 = nullptr; a.screening = 1; a.rs_f = a.rs_g = a.slack_scale = 1e-12; a.dbg = nullptr;
   std::vector<double> hA((size_t)npad * sa);
   for (size_t i = 0; i < hA.size(); ++i) hA[i] = ((i * 2654435761u) % 1000) * 1e-3;
   double *Ap, *Y, *X0, *X1, *R0, *R1, *nrm, *att, *mom, *P, *stats; uint32_t* mask;
@@ -25,6 +25,9 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&R1, (size_t)K * m8 * 8)); CK(cudaMemset(R1, 0, (size_t)K * m8 * 8));
   CK(cudaMalloc(&mask, (size_t)K * a.nw * 4)); CK(cudaMemset(mask, 0xff, (size_t)K * a.nw * 4));
   CK(cudaMalloc(&nrm, npad * 8)); CK(cudaMalloc(&att, npad * 8));
+  unsigned* octr; double* osum;
+  CK(cudaMalloc(&octr, K / 8 * 4)); CK(cudaMemset(octr, 0, K / 8 * 4)); CK(cudaMalloc(&osum, (size_t)K / 8 * 4 * 8));
+  a.oct_round = octr; a.osum = osum;
   CK(cudaMalloc(&mom, K * 8)); CK(cudaMalloc(&P, K * 8)); CK(cudaMalloc(&stats, 5 * (size_t)K * 8));
   std::vector<double> ones(K > npad ? K : npad, 1.0);
   CK(cudaMemcpy(nrm, ones.data(), npad * 8, cudaMemcpyHostToDevice));

@@ -106,3 +106,26 @@ def test_result_streamed_to_host_during_last_round():
     np.testing.assert_array_equal(early.x, one.x.cpu().numpy())
     with pytest.raises(ValueError):
         solve_batched(a, Y, passes=10, rounds=1, x_out=torch.empty((K, 40), dtype=torch.float64))
+
+
+@pytest.mark.parametrize("m,n,K,check_every", [(40, 120, 192, 4), (37, 250, 70, 16), (16, 40, 149 * 64 + 7, 3)])
+def test_rounds_overlapping_across_a_launch(m, n, K, check_every):
+    """check_every > 1: one launch runs several rounds and a tile's next round
+    starts as soon as its own previous round is done (per-octet flags), on
+    whichever SM is free.  Same arithmetic per problem, so every trace row,
+    every per-problem value and x are bit-identical to one launch per round --
+    with fewer tiles than SMs, with more (units wrap around the grid), and
+    with the result streamed to the host."""
+    from paper_2202_07258_b200.batched import solve_batched
+    a, Y = _instance(m, n, K, seed=21)
+    rounds = 11
+    one = solve_batched(a, Y, passes=10, rounds=rounds, gap_tol=1e-300)
+    many = solve_batched(a, Y, passes=10, rounds=rounds, gap_tol=1e-300, check_every=check_every)
+    assert many.rounds == one.rounds == rounds
+    np.testing.assert_array_equal(many.trace, one.trace)
+    for f in ("primal", "dual", "gap", "eps", "preserved"):
+        np.testing.assert_array_equal(getattr(many, f), getattr(one, f))
+    np.testing.assert_array_equal(many.x, one.x)
+    odd = solve_batched(a, Y, passes=3, rounds=5, gap_tol=1e-300, check_every=2, return_device=True)   # odd passes: buffer parity per round
+    ref = solve_batched(a, Y, passes=3, rounds=5, gap_tol=1e-300, return_device=True)
+    np.testing.assert_array_equal(odd.x.cpu().numpy(), ref.x.cpu().numpy())
