@@ -51,6 +51,7 @@ struct CdArgs {
   int passes;
   int rows_per_cta;  // multiple of 2
   int slots;         // shared-memory block slots (the kernel's NS): 3, or 2 for large m
+  unsigned long long* dbg;  // BX_CD_DEBUG: per-phase clock sums of rank 0's warp 0 (null otherwise)
 };
 
 // cp.async 16-byte global->shared copy (LDGSTS)
@@ -84,34 +85,27 @@ __device__ __forceinline__ double cd_state_load(const CdArgs<T>& a, int64_t blk,
 // thread t >= 32 owns rows (t - 32) + q * CD_RT
 constexpr int CD_RT = CD_NT - 32;
 
+// Block `blk` of this CTA's rows (32 columns) plus its Gram pair into a slot:
+// one cp.async.bulk per column and one for the 16 KB Gram pair, issued by one
+// warp (lane = column) and completing on the slot's mbarrier.  (The per-thread
+// cp.async version cost every thread ~1,600 clocks of address arithmetic and
+// issue per block, on the critical path of the sequential update and of the
+// row warps alike.)
 template <typename T>
 __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* gdst, int64_t blk, int64_t row0,
-                                            int nrows) {
-  // the block's Gram matrix and its cross-Gram with the next block ride along
-  for (int q = threadIdx.x; q < 2 * CD_B * CD_B / 2; q += CD_NT)
-    cp_async16(gdst + 2 * q, a.gram + blk * 2 * CD_B * CD_B + 2 * q);
+                                            int nrows, uint64_t* bar, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  constexpr int V = 16 / sizeof(T);
   const int64_t c0 = blk * CD_B;
   const int nc = (int)min((int64_t)CD_B, a.k - c0);
-  // dst[c * rows_pad + i] = A[row0 + i, 32*blk + c]; (column, vector) of
-  // piece q advanced incrementally (no integer division per piece)
-  constexpr int V = 16 / sizeof(T);
-  const int nvec = (nrows + V - 1) / V;  // rows_per_cta is a multiple of V
-  if (nvec > 0) {
-    const int rows_pad = a.rows_per_cta;
-    const int dc = CD_NT / nvec, dv = CD_NT - dc * nvec;
-    int c = threadIdx.x / nvec, v = threadIdx.x - c * nvec;
-    const T* src = a.A + c0 * a.ld + row0;
-    while (c < nc) {
-      cp_async16(dst + (int64_t)c * rows_pad + v * V, src + c * a.ld + v * V);
-      c += dc;
-      v += dv;
-      if (v >= nvec) {
-        v -= nvec;
-        ++c;
-      }
-    }
-  }
-  cp_async_commit();
+  const uint32_t colbytes = (uint32_t)(((nrows + V - 1) / V) * 16);  // rows_per_cta is a multiple of V
+  const uint32_t gbytes = 2 * CD_B * CD_B * 8;
+  fence_proxy_async_smem();  // the slot's previous readers (generic proxy) come first
+  if (lane == 0) mbar_expect_tx(bar, gbytes + (uint32_t)nc * colbytes);
+  __syncwarp();
+  if (lane == 0) bulk_g2s(gdst, a.gram + blk * 2 * CD_B * CD_B, gbytes, bar, pol);
+  if (lane < nc && colbytes > 0)
+    bulk_g2s(dst + (int64_t)lane * a.rows_per_cta, a.A + (c0 + lane) * a.ld + row0, colbytes, bar, pol);
 }
 
 __device__ __forceinline__ void cluster_arrive_release() {
@@ -143,7 +137,17 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   double* allpart = delta + CD_B;                                           // [2][16][CD_B] pushed partial dots
   double* cst = allpart + 2 * 16 * CD_B;                                    // [3][CD_ST][CD_B] column state
   __shared__ double wpart[CD_NT / 32][CD_B];
+  __shared__ uint64_t fullb[3];  // per slot: the block's bulk copies have landed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int PFW = CD_NT / 32 - 1;  // the warp that issues the block copies
+  const uint64_t pol = policy_evict_last();  // A and the Gram blocks are re-read every sweep: keep them in L2
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) mbar_init(&fullb[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // block b lands in slot b % NS; its barrier phase is (b / NS) & 1
+  auto wait_block = [&](int64_t b) { mbar_wait(&fullb[(int)b % NS], (uint32_t)(((int)b / NS) & 1)); };
   const int64_t row0 = (int64_t)rank * rows_pad;
   const int nrows = (int)max((int64_t)0, min((int64_t)rows_pad, a.m - row0));
   const int rt = tid - 32;  // row thread index (warps 1..7)
@@ -154,6 +158,12 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   for (int q = 0; q < CD_RMAX; ++q) {
     const int i = rt + q * CD_RT;
     rr[q] = (rt >= 0 && i < nrows) ? a.r[row0 + i] : 0.0;
+  }
+  // rank slots past the cluster size are never pushed to: they read as zeros
+  // in combine() (nobody else writes them, so no ordering with the pushes)
+  for (int q = NC * CD_B + tid; q < 16 * CD_B; q += CD_NT) {
+    allpart[q] = 0.0;
+    allpart[16 * CD_B + q] = 0.0;
   }
   const int64_t nblk = (a.k + CD_B - 1) / CD_B;
   const int64_t total = nblk * a.passes;  // blocks over all passes, in order
@@ -168,7 +178,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
 
   // partial dots of block `it` over this CTA's rows -> pushed into slot
   // parity(it) of every CTA (warps 1..7; named barrier 1 among them)
+  long long trw[6] = {0, 0, 0, 0, 0, 0};
+  const bool timed_r = a.dbg && rank == 0 && tid == 32;
   auto dots_push = [&](int64_t it) {
+    const long long r0 = timed_r ? clock64() : 0;
     const T* cur = slot_a(it);
     const int nc = (int)min((int64_t)CD_B, a.k - blk_of(it) * CD_B);
     double pd[CD_B];
@@ -184,6 +197,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           if (c < nc) pd[c] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * rv;
       }
     }
+    const long long r1 = timed_r ? clock64() : 0;
     // butterfly transpose-reduction: column c's warp sum lands in lane c
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -196,28 +210,42 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       }
     }
     wpart[warp][lane] = pd[0];
+    const long long r2 = timed_r ? clock64() : 0;
     asm volatile("bar.sync 1, %0;" ::"r"(CD_RT) : "memory");
+    const long long r3 = timed_r ? clock64() : 0;
     if (warp == 1) {
       double s = 0.0;
       for (int w = 1; w < CD_NT / 32; ++w) s += wpart[w][lane];
       double* slot = allpart + (it & 1) * 16 * CD_B + rank * CD_B;
       for (int q = 0; q < NC; ++q) cluster.map_shared_rank(slot, q)[lane] = s;
     }
+    if (timed_r) {
+      const long long r4 = clock64();
+      trw[0] += r1 - r0;  // partial dots (FMAs)
+      trw[1] += r2 - r1;  // butterfly
+      trw[2] += r3 - r2;  // named barrier
+      trw[3] += r4 - r3;  // combine + remote stores
+    }
   };
   // warp 0: combine the pushed partials of block `it` in rank order
   auto combine = [&](int64_t it) {
+    // all 16 rank slots (slots past NC hold zeros), four chains (rank mod 4)
+    // combined in a fixed order
     const double* ap = allpart + (it & 1) * 16 * CD_B + lane;
-    double d = 0.0;
-    for (int q = 0; q < NC; ++q) d += ap[q * CD_B];
-    return d;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s4[q & 3] += ap[q * CD_B];
+    return (s4[0] + s4[1]) + (s4[2] + s4[3]);
   };
 
   double pfv = 0.0;   // column state of the block after next (threads < CD_ST * CD_B)
   double cdot = 0.0;  // warp 0: the current block's dot, lane = column
   if (total > 0) {
     // prologue: blocks 0 and 1 in flight, block 0's column state, block 0's dots
-    cd_prefetch(a, slot_a(0), slot_g(0), blk_of(0), row0, nrows);
-    if (total > 1) cd_prefetch(a, slot_a(1), slot_g(1), blk_of(1), row0, nrows);
+    if (warp == PFW) {
+      cd_prefetch(a, slot_a(0), slot_g(0), blk_of(0), row0, nrows, &fullb[0], pol);
+      if (total > 1) cd_prefetch(a, slot_a(1), slot_g(1), blk_of(1), row0, nrows, &fullb[1 % NS], pol);
+    }
     if (tid < CD_ST * CD_B) {
       const double v = cd_state_load(a, blk_of(0), pass_of(0));
       cst[tid] = tid >= 3 * CD_B ? cd_isq(v) : v;
@@ -226,7 +254,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         cst[CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(w) : w;
       }
     }
-    if (total > 1) cp_async_wait_1(); else cp_async_wait_all();
+    wait_block(0);
     __syncthreads();
     if (warp == 0) {
       cluster_arrive_relaxed();
@@ -237,27 +265,44 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     cluster_wait();
     if (warp == 0) cdot = combine(0);
   }
+  long long tph[6] = {0, 0, 0, 0, 0, 0};
+  long long tph7 = 0;
+  long long tch[3] = {0, 0, 0};
+  const bool timed = a.dbg && rank == 0 && tid == 0;
   for (int64_t it = 0; it < total; ++it) {
+    const long long tq0 = timed ? clock64() : 0;
     const int64_t blk = blk_of(it);
     const int pass = pass_of(it);
     const int64_t c0 = blk * CD_B;
     const int nc = (int)min((int64_t)CD_B, a.k - c0);
     const bool has_next = it + 1 < total;
     // block it+1's data (issued one iteration ago) must have landed
-    cp_async_wait_all();
+    if (has_next) wait_block(it + 1);
     __syncthreads();
+    const long long tq1 = timed ? clock64() : 0;
     if (it + 2 < total) {
       // three slots: block it+2 goes into the slot block it-1 freed; two
       // slots: it must wait for block it's axpy (end of this iteration)
-      if constexpr (NS == 3) cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows);
+      if constexpr (NS == 3)
+        if (warp == PFW)
+          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol);
       pfv = cd_state_load(a, blk_of(it + 2), pass_of(it + 2));
     }
+    const long long tq1a = timed ? clock64() : 0;
     if (warp == 0) {
       cluster_arrive_relaxed();  // warp 0 publishes nothing this phase
+      const long long tc0 = timed ? clock64() : 0;
       // ---- sequential block update (lane = column), redundantly per CTA ----
       const int64_t j = c0 + lane;
       double* xout = (pass & 1) ? a.x : a.x2;
       const double* cs = cst + (it % 3) * CD_ST * CD_B;
+      // lane = column: each lane keeps its own dot current.  Straight-line,
+      // no guard for the columns past nc of a last, partial block: their
+      // state is (x, lo, hi, 1/||a||^2) = (0, 0, 0, 1) and their dots and
+      // Gram entries are zero, so their step is an exact zero.  (Measured in
+      // isolation, scripts/probes/cdchain2_probe.cu: 105 clocks per step this
+      // way, 172 as a rolled loop -- its counter lives in the uniform
+      // datapath -- and 190 with a per-step branch on nc.)
       double xj = 0.0, loj = 0.0, hij = 0.0, isq = 1.0;
       if (lane < nc) {
         xj = cs[lane];
@@ -265,27 +310,29 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         hij = cs[2 * CD_B + lane];
         isq = cs[3 * CD_B + lane];  // 1 / ||a_j||^2
       }
-      const double* gcur = slot_g(it);
-      double grow[CD_B];
-#pragma unroll
-      for (int i = 0; i < CD_B; ++i) grow[i] = gcur[lane * CD_B + i];
+      const double* grow = slot_g(it) + lane * CD_B;  // G[lane][.]: read per step, off the dependency chain
       double dl = 0.0;
+      const long long tc1 = timed ? clock64() : 0;
 #pragma unroll
       for (int i = 0; i < CD_B; ++i) {
-        if (i < nc) {
-          // every lane evaluates its tentative coordinate step (no
-          // divergence); only lane i's -- whose dot now carries the
-          // corrections of all earlier coordinates -- is broadcast and kept
-          double nv = fma(-cdot, isq, xj);  // x - (a.r)/||a||^2 (solvers.py:131-132)
-          nv = nv < loj ? loj : nv;
-          nv = nv > hij ? hij : nv;
-          const double dt = nv - xj;  // solvers.py:133
-          const double di = __shfl_sync(0xffffffffu, dt, i);
-          const bool me = lane == i;
-          xj = (me && dt != 0.0) ? nv : xj;
-          dl = me ? dt : dl;
-          cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
-        }
+        // every lane evaluates its tentative coordinate step (no
+        // divergence); only lane i's -- whose dot now carries the
+        // corrections of all earlier coordinates -- is broadcast and kept
+        double nv = fma(-cdot, isq, xj);  // x - (a.r)/||a||^2 (solvers.py:131-132)
+        nv = nv < loj ? loj : nv;
+        nv = nv > hij ? hij : nv;
+        const double dt = nv - xj;  // solvers.py:133
+        const double di = __shfl_sync(0xffffffffu, dt, i);
+        const bool me = lane == i;
+        xj = (me && dt != 0.0) ? nv : xj;
+        dl = me ? dt : dl;
+        cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
+      }
+      if (timed) {
+        const long long tc2 = clock64();
+        tch[0] += tc0 - tq1a;  // cluster arrive
+        tch[1] += tc1 - tc0;   // state / first Gram entry from shared memory
+        tch[2] += tc2 - tc1;   // the 32 dependent steps
       }
       delta[lane] = dl;
       if (lane < nc && rank == 0) xout[j] = xj;
@@ -296,21 +343,28 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     } else {
       // ---- block it+1's partial dots against r without delta_it ----
       if (has_next) dots_push(it + 1);
+      const long long r5 = timed_r ? clock64() : 0;
       cluster_arrive_release();
+      if (timed_r) trw[4] += clock64() - r5;  // arrive.release
     }
+    const long long tq2 = timed ? clock64() : 0;
     cluster_wait();
+    const long long tq3 = timed ? clock64() : 0;
     if (warp == 0 && has_next) {
       // d_{it+1} = pushed partial dots + X_it delta_it (rank order, then the
       // cross-Gram term in column order)
       __syncwarp();  // delta[] of every lane
       double d = combine(it + 1);
       const double* xg = slot_g(it) + CD_B * CD_B + lane * CD_B;
-      double corr = 0.0;
+      // four independent chains (l mod 4), combined in a fixed order
+      double corr[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int l = 0; l < CD_B; ++l) corr = fma(xg[l], delta[l], corr);
-      cdot = d + corr;
+      for (int l = 0; l < CD_B; ++l) corr[l & 3] = fma(xg[l], delta[l], corr[l & 3]);
+      cdot = d + ((corr[0] + corr[1]) + (corr[2] + corr[3]));
     }
+    const long long tq4 = timed ? clock64() : 0;
     __syncthreads();  // delta visible to the row warps
+    const long long tq5 = timed ? clock64() : 0;
     // r += A_J delta_J on this CTA's rows
     if (warp > 0) {
       const T* cur = slot_a(it);
@@ -323,8 +377,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int c = 0; c < CD_B; ++c) {
-            const double dc = delta[c];
-            if (c < nc && dc != 0.0) acc[c & 3] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * dc;
+            if (c < nc) acc[c & 3] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * delta[c];
           }
           rr[q] += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
@@ -338,10 +391,29 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       cst[((it + 2) % 3) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
     if (NS == 2 && it + 2 < total) {  // (compile-time NS)
       __syncthreads();  // block it's slot is free
-      cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows);
+      if (warp == PFW)
+        cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol);
     }
     __syncthreads();
+    if (timed) {
+      const long long tq6 = clock64();
+      tph[0] += tq1 - tq0;  // block data landed + CTA barrier
+      tph[1] += tq2 - tq1;  // warp 0: prefetch issue + sequential block update
+      tph7 += tq1a - tq1;   // of which: prefetch / state-load issue
+      tph[2] += tq3 - tq2;  // cluster barrier wait (the row warps' dots, pushes, release)
+      tph[3] += tq4 - tq3;  // combine + cross-Gram correction
+      tph[4] += tq5 - tq4;  // CTA barrier
+      tph[5] += tq6 - tq5;  // axpy phase (warp 0 waits for the row warps)
+    }
   }
+  if (timed)
+    for (int q = 0; q < 6; ++q) atomicAdd(a.dbg + q, (unsigned long long)tph[q]);
+  if (timed) atomicAdd(a.dbg + 6, (unsigned long long)total);
+  if (timed) atomicAdd(a.dbg + 7, (unsigned long long)tph7);
+  if (timed)
+    for (int q = 0; q < 3; ++q) atomicAdd(a.dbg + 13 + q, (unsigned long long)tch[q]);
+  if (timed_r)
+    for (int q = 0; q < 5; ++q) atomicAdd(a.dbg + 8 + q, (unsigned long long)trw[q]);
   // write back the residual rows and the objective 0.5 ||r||^2
   double sq = 0.0;
 #pragma unroll

@@ -1164,6 +1164,35 @@ int cd_sweeps(bx_ctx* c, int passes) {
   a.passes = passes;
   a.rows_per_cta = (int)rows;
   a.slots = slots;
+  a.dbg = nullptr;
+  {
+    // BX_CD_DEBUG=1: per-phase clock sums of the sweep's critical path, printed at exit
+    static unsigned long long* g_cd_dbg = nullptr;
+    static bool g_cd_dbg_on = getenv("BX_CD_DEBUG") != nullptr;
+    if (g_cd_dbg_on && !g_cd_dbg) {
+      CU(cudaMalloc(&g_cd_dbg, 16 * 8));
+      CU(cudaMemset(g_cd_dbg, 0, 16 * 8));
+
+      static unsigned long long* keep = g_cd_dbg;
+      atexit([] {
+        unsigned long long h[16];
+        if (cudaMemcpy(h, keep, 128, cudaMemcpyDeviceToHost) == cudaSuccess && h[6]) {
+          fprintf(stderr, "k_cd row warp per block (clk): dots %.0f | butterfly %.0f | named barrier %.0f | combine+push %.0f | arrive.release %.0f\n",
+                  (double)h[8] / h[6], (double)h[9] / h[6], (double)h[10] / h[6], (double)h[11] / h[6], (double)h[12] / h[6]);
+          fprintf(stderr, "k_cd warp 0 per block (clk): cluster arrive %.0f | state loads %.0f | 32 dependent steps %.0f\n",
+                  (double)h[13] / h[6], (double)h[14] / h[6], (double)h[15] / h[6]);
+        }
+        if (h[6])
+          fprintf(stderr,
+                  "k_cd per block (clk): load+sync %.0f | update chain %.0f (prefetch issue %.0f) | cluster wait %.0f | combine+corr %.0f | "
+                  "sync %.0f | axpy phase %.0f | total %.0f over %llu blocks\n",
+                  (double)h[0] / h[6], (double)h[1] / h[6], (double)h[7] / h[6], (double)h[2] / h[6], (double)h[3] / h[6],
+                  (double)h[4] / h[6], (double)h[5] / h[6],
+                  (double)(h[0] + h[1] + h[2] + h[3] + h[4] + h[5]) / h[6], h[6]);
+      });
+    }
+    a.dbg = g_cd_dbg;
+  }
   const size_t smem = smem_for(rows);
   auto kern = slots == 3 ? k_cd<T, 3> : k_cd<T, 2>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
