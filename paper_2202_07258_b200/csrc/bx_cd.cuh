@@ -106,6 +106,11 @@ __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* 
   if (lane == 0) bulk_g2s(gdst, a.gram + blk * 2 * CD_B * CD_B, gbytes, bar, pol);
   if (lane < nc && colbytes > 0)
     bulk_g2s(dst + (int64_t)lane * a.rows_per_cta, a.A + (c0 + lane) * a.ld + row0, colbytes, bar, pol);
+  // a last, partial block: its unused column slots read as zero columns, so
+  // the dots and the axpy need no per-column guard (a guard turns each of
+  // their 32 columns into a branch plus a dependent load: ~100 clocks each)
+  if (lane >= nc)
+    for (int i = 0; i < a.rows_per_cta; ++i) dst[(int64_t)lane * a.rows_per_cta + i] = T(0);
 }
 
 __device__ __forceinline__ void cluster_arrive_release() {
@@ -123,7 +128,12 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 //     d_{J+1} = A_{J+1}'(r + A_J delta_J) = A_{J+1}'r + X_J delta_J,
 // (exact arithmetic identity) before r += A_J delta_J.  Three shared-memory
 // slots: block J (axpy), J+1 (dots), J+2 (in flight).
-template <typename T, int NS>
+// RQ: row slots per row thread actually held (rows_per_cta <= RQ * CD_RT): 1
+// for m <= 224 rows per CTA.  The loop body is straight-line code that every
+// warp runs once per block, so its size is paid in instruction fetches: the
+// fourfold unrolling for the 4-slot envelope cost ~10 clocks per instruction
+// in the row warps' dots and axpy.
+template <typename T, int NS, int RQ>
 __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -133,13 +143,18 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   T* abuf = reinterpret_cast<T*>(smem);                                      // [3][CD_B][rows_pad]
   double* gbuf = reinterpret_cast<double*>(abuf + NS * CD_B * rows_pad);    // [NS][2][CD_B][CD_B]
   double* part = gbuf + NS * 2 * CD_B * CD_B;                               // [2] scratch
-  double* delta = part + 2;                                                 // [CD_B]
-  double* allpart = delta + CD_B;                                           // [2][16][CD_B] pushed partial dots
+  double* delta = part + 2;                                                 // [2][CD_B] steps of block it in delta[it & 1]
+  double* allpart = delta + 2 * CD_B;                                           // [2][16][CD_B] pushed partial dots
   double* cst = allpart + 2 * 16 * CD_B;                                    // [3][CD_ST][CD_B] column state
   __shared__ double wpart[CD_NT / 32][CD_B];
   __shared__ uint64_t fullb[3];  // per slot: the block's bulk copies have landed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int PFW = CD_NT / 32 - 1;  // the warp that issues the block copies
+  // Three slots: the axpy of block it runs at the start of iteration it + 1 in
+  // the row warps, overlapped with warp 0's sequential update of block it + 1
+  // (it was ~2,300 clocks per block with warp 0 idle); the slot it frees then
+  // takes block it + 3.  Two slots (tall m): the axpy stays in its iteration.
+  constexpr bool DEFER = NS == 3;
   const uint64_t pol = policy_evict_last();  // A and the Gram blocks are re-read every sweep: keep them in L2
   if (tid == 0) {
     for (int q = 0; q < 3; ++q) mbar_init(&fullb[q], 1);
@@ -153,9 +168,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   const int rt = tid - 32;  // row thread index (warps 1..7)
 
   // residual rows in registers (warps 1..7)
-  double rr[CD_RMAX];
+  double rr[RQ];
 #pragma unroll
-  for (int q = 0; q < CD_RMAX; ++q) {
+  for (int q = 0; q < RQ; ++q) {
     const int i = rt + q * CD_RT;
     rr[q] = (rt >= 0 && i < nrows) ? a.r[row0 + i] : 0.0;
   }
@@ -183,18 +198,17 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   auto dots_push = [&](int64_t it) {
     const long long r0 = timed_r ? clock64() : 0;
     const T* cur = slot_a(it);
-    const int nc = (int)min((int64_t)CD_B, a.k - blk_of(it) * CD_B);
     double pd[CD_B];
 #pragma unroll
     for (int c = 0; c < CD_B; ++c) pd[c] = 0.0;
 #pragma unroll
-    for (int q = 0; q < CD_RMAX; ++q) {
+    for (int q = 0; q < RQ; ++q) {
       const int i = rt + q * CD_RT;
       if (i < nrows) {
         const double rv = rr[q];
+        const T* colp = cur + i;
 #pragma unroll
-        for (int c = 0; c < CD_B; ++c)
-          if (c < nc) pd[c] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * rv;
+        for (int c = 0; c < CD_B; ++c) pd[c] += static_cast<double>(colp[c * rows_pad]) * rv;
       }
     }
     const long long r1 = timed_r ? clock64() : 0;
@@ -225,6 +239,24 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       trw[1] += r2 - r1;  // butterfly
       trw[2] += r3 - r2;  // named barrier
       trw[3] += r4 - r3;  // combine + remote stores
+    }
+  };
+  // r += A_b delta_b on this CTA's rows (row warps)
+  auto axpy = [&](int64_t b) {
+    const T* cur = slot_a(b);
+    const double* dl_b = delta + (b & 1) * CD_B;
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      const int i = rt + q * CD_RT;
+      if (i < nrows) {
+        // four independent chains over the block's columns (c mod 4),
+        // combined in a fixed order; a zero step adds an exact zero
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const T* colp = cur + i;
+#pragma unroll
+        for (int c = 0; c < CD_B; ++c) acc[c & 3] += static_cast<double>(colp[c * rows_pad]) * dl_b[c];
+        rr[q] += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
     }
   };
   // warp 0: combine the pushed partials of block `it` in rank order
@@ -283,9 +315,6 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     if (it + 2 < total) {
       // three slots: block it+2 goes into the slot block it-1 freed; two
       // slots: it must wait for block it's axpy (end of this iteration)
-      if constexpr (NS == 3)
-        if (warp == PFW)
-          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol);
       pfv = cd_state_load(a, blk_of(it + 2), pass_of(it + 2));
     }
     const long long tq1a = timed ? clock64() : 0;
@@ -310,7 +339,10 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         hij = cs[2 * CD_B + lane];
         isq = cs[3 * CD_B + lane];  // 1 / ||a_j||^2
       }
-      const double* grow = slot_g(it) + lane * CD_B;  // G[lane][.]: read per step, off the dependency chain
+      // G[.][lane]: the block Gram matrix is bitwise symmetric (k_gram), and
+      // reading row i across the lanes is bank-conflict free (G[lane][i] is a
+      // 32-way conflict: a 256-byte lane stride)
+      const double* gcol = slot_g(it) + lane;
       double dl = 0.0;
       const long long tc1 = timed ? clock64() : 0;
 #pragma unroll
@@ -326,15 +358,14 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         const bool me = lane == i;
         xj = (me && dt != 0.0) ? nv : xj;
         dl = me ? dt : dl;
-        cdot = fma(grow[i], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
+        cdot = fma(gcol[i * CD_B], di, cdot);  // lanes <= i are finished; di == 0 leaves cdot unchanged
       }
       if (timed) {
         const long long tc2 = clock64();
-        tch[0] += tc0 - tq1a;  // cluster arrive
         tch[1] += tc1 - tc0;   // state / first Gram entry from shared memory
         tch[2] += tc2 - tc1;   // the 32 dependent steps
       }
-      delta[lane] = dl;
+      delta[(it & 1) * CD_B + lane] = dl;
       if (lane < nc && rank == 0) xout[j] = xj;
       // short passes (<= 3 blocks): the x this block produces is read again
       // within the state look-ahead; every CTA computed it redundantly, so
@@ -342,6 +373,13 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       if (nblk <= 3 && it + nblk < total) cst[((it + nblk) % 3) * CD_ST * CD_B + lane] = xj;
     } else {
       // ---- block it+1's partial dots against r without delta_it ----
+      if constexpr (DEFER) {
+        if (it > 0) axpy(it - 1);
+        // every row warp is done with block it-1's slot: it takes block it+2
+        asm volatile("bar.sync 1, %0;" ::"r"(CD_RT) : "memory");
+        if (it + 2 < total && warp == PFW)
+          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol);
+      }
       if (has_next) dots_push(it + 1);
       const long long r5 = timed_r ? clock64() : 0;
       cluster_arrive_release();
@@ -354,35 +392,28 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       // d_{it+1} = pushed partial dots + X_it delta_it (rank order, then the
       // cross-Gram term in column order)
       __syncwarp();  // delta[] of every lane
+      const long long tk0 = timed ? clock64() : 0;
       double d = combine(it + 1);
-      const double* xg = slot_g(it) + CD_B * CD_B + lane * CD_B;
+      if (timed) {
+        asm volatile("" ::"d"(d));
+        tch[0] += clock64() - tk0;  // (debug: reuses the cluster-arrive slot) combine only
+      }
+      const double* xg = slot_g(it) + CD_B * CD_B + lane;  // X stored transposed: [l][next-block column]
       // four independent chains (l mod 4), combined in a fixed order
       double corr[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* dl_it = delta + (it & 1) * CD_B;
 #pragma unroll
-      for (int l = 0; l < CD_B; ++l) corr[l & 3] = fma(xg[l], delta[l], corr[l & 3]);
+      for (int l = 0; l < CD_B; ++l) corr[l & 3] = fma(xg[l * CD_B], dl_it[l], corr[l & 3]);
       cdot = d + ((corr[0] + corr[1]) + (corr[2] + corr[3]));
     }
     const long long tq4 = timed ? clock64() : 0;
-    __syncthreads();  // delta visible to the row warps
+    if constexpr (!DEFER) __syncthreads();  // delta visible to the row warps
     const long long tq5 = timed ? clock64() : 0;
-    // r += A_J delta_J on this CTA's rows
-    if (warp > 0) {
-      const T* cur = slot_a(it);
-#pragma unroll
-      for (int q = 0; q < CD_RMAX; ++q) {
-        const int i = rt + q * CD_RT;
-        if (i < nrows) {
-          // four independent chains over the block's columns (c mod 4),
-          // combined in a fixed order
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-          for (int c = 0; c < CD_B; ++c) {
-            if (c < nc) acc[c & 3] += static_cast<double>(cur[(int64_t)c * rows_pad + i]) * delta[c];
-          }
-          rr[q] += (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-      }
-    }
+    // r += A_J delta_J on this CTA's rows (two slots: here; three slots: by
+    // the row warps at the start of the next iteration, beside warp 0's
+    // sequential update)
+    if constexpr (!DEFER)
+      if (warp > 0) axpy(it);
     // park block it+2's column state (its slot last held block it-1).  x of
     // a later pass comes from global memory only when rank 0 wrote it at
     // least two iterations ago (ordered by the cluster barriers since);
@@ -414,10 +445,12 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     for (int q = 0; q < 3; ++q) atomicAdd(a.dbg + 13 + q, (unsigned long long)tch[q]);
   if (timed_r)
     for (int q = 0; q < 5; ++q) atomicAdd(a.dbg + 8 + q, (unsigned long long)trw[q]);
+  if constexpr (DEFER)
+    if (total > 0 && warp > 0) axpy(total - 1);  // (the loop's closing barrier made its steps visible)
   // write back the residual rows and the objective 0.5 ||r||^2
   double sq = 0.0;
 #pragma unroll
-  for (int q = 0; q < CD_RMAX; ++q) {
+  for (int q = 0; q < RQ; ++q) {
     const int i = rt + q * CD_RT;
     if (rt >= 0 && i < nrows) {
       a.r[row0 + i] = rr[q];
@@ -443,7 +476,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
 }
 
 // Gram blocks for consecutive blocks of CD_B preserved columns:
-// [blk][0] = G_JJ = A_J'A_J and [blk][1] = X_J = A_next'A_J with next = J+1
+// [blk][0] = G_JJ = A_J'A_J and [blk][1] = X_J' = (A_next'A_J)' with next = J+1
 // (block 0 after the last: the next pass starts over)
 template <typename T>
 __global__ void __launch_bounds__(256) k_gram(const T* __restrict__ A, int64_t ld, int64_t m, int64_t k,
@@ -484,7 +517,9 @@ __global__ void __launch_bounds__(256) k_gram(const T* __restrict__ A, int64_t l
   for (int u = 0; u < 4; ++u) {
     const int p = threadIdx.x * 4 + u;
     gram[blk * 2 * CD_B * CD_B + p] = acc[0][u];
-    gram[blk * 2 * CD_B * CD_B + CD_B * CD_B + p] = acc[1][u];
+    // the cross-Gram block transposed ([l][i]): the correction reads column
+    // i = lane for every l, conflict free
+    gram[blk * 2 * CD_B * CD_B + CD_B * CD_B + (p % CD_B) * CD_B + p / CD_B] = acc[1][u];
   }
 }
 

@@ -1125,7 +1125,7 @@ int cd_sweeps(bx_ctx* c, int passes) {
   constexpr int V = 16 / sizeof(T);
   int NC = 8;
   int64_t rows = round_up((c->m + NC - 1) / NC, V);
-  const size_t fixed = (2 + CD_B + 2 * 16 * CD_B + 3 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
+  const size_t fixed = (2 + 2 * CD_B + 2 * 16 * CD_B + 3 * CD_ST * CD_B) * 8 + 256 + 4096;  // + static smem of k_cd
   // three block slots (blocks J, J+1 and J+2 in flight) when they fit,
   // else two (the next block's copy then waits for this block's axpy)
   int slots = 3;
@@ -1194,7 +1194,9 @@ int cd_sweeps(bx_ctx* c, int passes) {
     a.dbg = g_cd_dbg;
   }
   const size_t smem = smem_for(rows);
-  auto kern = slots == 3 ? k_cd<T, 3> : k_cd<T, 2>;
+  const bool one_slot = rows <= CD_RT;  // one residual row per row thread: the small instantiation
+  auto kern = slots == 3 ? (one_slot ? k_cd<T, 3, 1> : k_cd<T, 3, CD_RMAX>)
+                         : (one_slot ? k_cd<T, 2, 1> : k_cd<T, 2, CD_RMAX>);
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t lc = {};
