@@ -1276,6 +1276,28 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   const int s = c->cur;
   View<T> vw = act_view<T>(c);
   SmallArgs a;
+  a.dbg = nullptr;
+  {
+    // BX_SMALL_DEBUG=1: per-phase clock sums of a resident step (CTA 0), printed at exit
+    static unsigned long long* g_sm_dbg = nullptr;
+    static bool g_sm_dbg_on = getenv("BX_SMALL_DEBUG") != nullptr;
+    if (g_sm_dbg_on && !g_sm_dbg) {
+      CU(cudaMalloc(&g_sm_dbg, 8 * 8));
+      CU(cudaMemset(g_sm_dbg, 0, 8 * 8));
+      static unsigned long long* keep = g_sm_dbg;
+      atexit([] {
+        unsigned long long h[8];
+        if (cudaMemcpy(h, keep, 64, cudaMemcpyDeviceToHost) == cudaSuccess && h[6])
+          fprintf(stderr,
+                  "k_round_small per step (clk): dots+update %.0f | partial rows %.0f | barrier 1 %.0f | row reduce %.0f | "
+                  "barrier 2 %.0f | residual load + fold %.0f | total %.0f over %llu steps\n",
+                  (double)h[0] / h[6], (double)h[1] / h[6], (double)h[2] / h[6], (double)h[3] / h[6],
+                  (double)h[4] / h[6], (double)h[5] / h[6],
+                  (double)(h[0] + h[1] + h[2] + h[3] + h[4] + h[5]) / h[6], h[6]);
+      });
+    }
+    a.dbg = g_sm_dbg;
+  }
   a.A = vw.A;
   a.ld = vw.ld;
   a.colmap = vw.colmap;

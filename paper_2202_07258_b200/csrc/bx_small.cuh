@@ -73,6 +73,7 @@ struct SmallArgs {
   int screening;
   double slack_scale;
   double alpha;
+  unsigned long long* dbg;  // BX_SMALL_DEBUG: per-phase clock sums of CTA 0 (null otherwise)
 };
 
 // Grid barrier: one monotonic arrival counter per launch (zeroed by the host
@@ -212,6 +213,8 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   };
 
   int done_rounds = 0, event = 0;
+  const bool timed = a.dbg && b == 0 && tid == 0;
+  long long tsm[7] = {0, 0, 0, 0, 0, 0, 0};
   bool perr = false;
   if (b == 0 && tid == 0 && a.stamp0) *a.stamp0 = globaltimer();
   double excl_ns = 0.0;  // dual-point time of this launch (block 0's view; screening off)
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   bool have_pre = false;
   for (int rnd = 0; rnd < a.max_rounds; ++rnd) {
   for (int pass = 0; pass < a.passes; ++pass) {
+    const long long tp0 = timed ? clock64() : 0;
     const double* rcur = a.r[rc];
     const double tn = (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom)) / 2.0;
     const double beta = (a.kind == 2) ? (t_mom - 1.0) / tn : 0.0;
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
         if (lane == 0) update_col(c, cg[c]);
     }
     __syncthreads();
+    const long long tp1 = timed ? clock64() : 0;
     // restart partials of this CTA (fixed order: lane-strided, then one
     // butterfly in warp 0; lane 0 = thread 0 also publishes them below)
     if (warp == 0) {
@@ -330,7 +335,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       a.bpart[4 * b + 1] = sc4[0];
       a.bpart[4 * b + 2] = sc4[1];
     }
+    const long long tp2 = timed ? clock64() : 0;
     grid_barrier(a.bar, nbar);
+    const long long tp3 = timed ? clock64() : 0;
     // distributed reduce of this CTA's rows: one warp per row, lanes over
     // the G partials (independent L2 loads), one butterfly
     double sq = 0.0;
@@ -349,7 +356,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
       for (int w = 0; w < NW; ++w) s += red[w];
       a.bpart[4 * b + 0] = s;
     }
+    const long long tp4 = timed ? clock64() : 0;
     grid_barrier(a.bar, nbar);
+    const long long tp5 = timed ? clock64() : 0;
     // the next step's residual rows (r just completed, r[rc ^ 1]), issued
     // before the fold below
 #pragma unroll
@@ -398,6 +407,16 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     P = Pn;
     rc ^= 1;
     gv = 0;
+    if (timed) {
+      const long long tp6 = clock64();
+      tsm[0] += tp1 - tp0;  // residual to shared memory, dots, column updates
+      tsm[1] += tp2 - tp1;  // local partial rows of A x+
+      tsm[2] += tp3 - tp2;  // grid barrier 1
+      tsm[3] += tp4 - tp3;  // distributed row reduce
+      tsm[4] += tp5 - tp4;  // grid barrier 2
+      tsm[5] += tp6 - tp5;  // next residual rows + scalar fold
+      ++tsm[6];
+    }
     // no CTA barrier here: every shared-memory reuse of the next step (rv,
     // sc4, cf / rsx) is already separated from this step's reads by the
     // barriers above
@@ -550,6 +569,8 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   gv = 1;  // the next round starts from this round's screening gradient
   __syncthreads();
   }  // rounds
+  if (timed)
+    for (int q = 0; q < 7; ++q) atomicAdd(a.dbg + q, (unsigned long long)tsm[q]);
   // write back the resident per-column state
   if (tid < ncol) {
     const int64_t p = p0 + tid;
