@@ -86,14 +86,18 @@ __device__ __forceinline__ double cd_state_load(const CdArgs<T>& a, int64_t blk,
 constexpr int CD_RT = CD_NT - 32;
 
 // Block `blk` of this CTA's rows (32 columns) plus its Gram pair into a slot:
-// one cp.async.bulk per column and one for the 16 KB Gram pair, issued by one
-// warp (lane = column) and completing on the slot's mbarrier.  (The per-thread
-// cp.async version cost every thread ~1,600 clocks of address arithmetic and
-// issue per block, on the critical path of the sequential update and of the
-// row warps alike.)
+// one cp.async.bulk per column and one for the 16 KB Gram pair, completing on
+// the slot's mbarrier.  (The per-thread cp.async version cost every thread
+// ~1,600 clocks of address arithmetic and issue per block, on the critical
+// path of the sequential update and of the row warps alike.)  A bulk copy
+// takes uniform operands, so a warp issues its lanes' copies one after the
+// other (~40 clocks each): the columns are dealt round robin to the NW warps
+// that call this (part = 0 .. NW-1; part 0 also arms the barrier and copies
+// the Gram pair) -- issued by one warp, the 33 copies held that warp, and
+// with it the row warps' named barrier, for ~1,600 clocks per block.
 template <typename T>
 __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* gdst, int64_t blk, int64_t row0,
-                                            int nrows, uint64_t* bar, uint64_t pol) {
+                                            int nrows, uint64_t* bar, uint64_t pol, int part, int NW) {
   const int lane = threadIdx.x & 31;
   constexpr int V = 16 / sizeof(T);
   const int64_t c0 = blk * CD_B;
@@ -101,16 +105,22 @@ __device__ __forceinline__ void cd_prefetch(const CdArgs<T>& a, T* dst, double* 
   const uint32_t colbytes = (uint32_t)(((nrows + V - 1) / V) * 16);  // rows_per_cta is a multiple of V
   const uint32_t gbytes = 2 * CD_B * CD_B * 8;
   fence_proxy_async_smem();  // the slot's previous readers (generic proxy) come first
-  if (lane == 0) mbar_expect_tx(bar, gbytes + (uint32_t)nc * colbytes);
-  __syncwarp();
-  if (lane == 0) bulk_g2s(gdst, a.gram + blk * 2 * CD_B * CD_B, gbytes, bar, pol);
-  if (lane < nc && colbytes > 0)
-    bulk_g2s(dst + (int64_t)lane * a.rows_per_cta, a.A + (c0 + lane) * a.ld + row0, colbytes, bar, pol);
+  if (part == 0) {
+    // the tx-count may run negative until this arrives: completions of the
+    // other warps' copies can come first
+    if (lane == 0) {
+      mbar_expect_tx(bar, gbytes + (uint32_t)nc * colbytes);
+      bulk_g2s(gdst, a.gram + blk * 2 * CD_B * CD_B, gbytes, bar, pol);
+    }
+  }
+  const int c = part + NW * lane;
+  if (c < nc && colbytes > 0)
+    bulk_g2s(dst + (int64_t)c * a.rows_per_cta, a.A + (c0 + c) * a.ld + row0, colbytes, bar, pol);
   // a last, partial block: its unused column slots read as zero columns, so
   // the dots and the axpy need no per-column guard (a guard turns each of
   // their 32 columns into a branch plus a dependent load: ~100 clocks each)
-  if (lane >= nc)
-    for (int i = 0; i < a.rows_per_cta; ++i) dst[(int64_t)lane * a.rows_per_cta + i] = T(0);
+  if (c >= nc && c < CD_B)
+    for (int i = 0; i < a.rows_per_cta; ++i) dst[(int64_t)c * a.rows_per_cta + i] = T(0);
 }
 
 __device__ __forceinline__ void cluster_arrive_release() {
@@ -149,7 +159,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   __shared__ double wpart[CD_NT / 32][CD_B];
   __shared__ uint64_t fullb[3];  // per slot: the block's bulk copies have landed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int PFW = CD_NT / 32 - 1;  // the warp that issues the block copies
+  constexpr int NRW = CD_NT / 32 - 1;  // row warps (1 .. NRW); they share the issue of the block copies
   // Three slots: the axpy of block it runs at the start of iteration it + 1 in
   // the row warps, overlapped with warp 0's sequential update of block it + 1
   // (it was ~2,300 clocks per block with warp 0 idle); the slot it frees then
@@ -274,9 +284,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   double cdot = 0.0;  // warp 0: the current block's dot, lane = column
   if (total > 0) {
     // prologue: blocks 0 and 1 in flight, block 0's column state, block 0's dots
-    if (warp == PFW) {
-      cd_prefetch(a, slot_a(0), slot_g(0), blk_of(0), row0, nrows, &fullb[0], pol);
-      if (total > 1) cd_prefetch(a, slot_a(1), slot_g(1), blk_of(1), row0, nrows, &fullb[1 % NS], pol);
+    if (warp > 0) {
+      cd_prefetch(a, slot_a(0), slot_g(0), blk_of(0), row0, nrows, &fullb[0], pol, warp - 1, NRW);
+      if (total > 1) cd_prefetch(a, slot_a(1), slot_g(1), blk_of(1), row0, nrows, &fullb[1 % NS], pol, warp - 1, NRW);
     }
     if (tid < CD_ST * CD_B) {
       const double v = cd_state_load(a, blk_of(0), pass_of(0));
@@ -377,8 +387,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
         if (it > 0) axpy(it - 1);
         // every row warp is done with block it-1's slot: it takes block it+2
         asm volatile("bar.sync 1, %0;" ::"r"(CD_RT) : "memory");
-        if (it + 2 < total && warp == PFW)
-          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol);
+        if (it + 2 < total)
+          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol,
+                      warp - 1, NRW);
       }
       if (has_next) dots_push(it + 1);
       const long long r5 = timed_r ? clock64() : 0;
@@ -422,8 +433,9 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       cst[((it + 2) % 3) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
     if (NS == 2 && it + 2 < total) {  // (compile-time NS)
       __syncthreads();  // block it's slot is free
-      if (warp == PFW)
-        cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol);
+      if (warp > 0)
+        cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol,
+                    warp - 1, NRW);
     }
     __syncthreads();
     if (timed) {
