@@ -311,10 +311,14 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
   long long tph7 = 0;
   long long tch[3] = {0, 0, 0};
   const bool timed = a.dbg && rank == 0 && tid == 0;
+  // (block, pass) of iteration it and of it + 2, advanced incrementally (an
+  // integer division per use was ~300 clocks of warp 0's path per block)
+  int blk_c = 0, pass_c = 0;
+  int blk_2 = (int)blk_of(2), pass_2 = pass_of(2);
   for (int64_t it = 0; it < total; ++it) {
     const long long tq0 = timed ? clock64() : 0;
-    const int64_t blk = blk_of(it);
-    const int pass = pass_of(it);
+    const int64_t blk = blk_c;
+    const int pass = pass_c;
     const int64_t c0 = blk * CD_B;
     const int nc = (int)min((int64_t)CD_B, a.k - c0);
     const bool has_next = it + 1 < total;
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     if (it + 2 < total) {
       // three slots: block it+2 goes into the slot block it-1 freed; two
       // slots: it must wait for block it's axpy (end of this iteration)
-      pfv = cd_state_load(a, blk_of(it + 2), pass_of(it + 2));
+      pfv = cd_state_load(a, blk_2, pass_2);
     }
     const long long tq1a = timed ? clock64() : 0;
     if (warp == 0) {
@@ -385,16 +389,22 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
       // ---- block it+1's partial dots against r without delta_it ----
       if constexpr (DEFER) {
         if (it > 0) axpy(it - 1);
-        // every row warp is done with block it-1's slot: it takes block it+2
-        asm volatile("bar.sync 1, %0;" ::"r"(CD_RT) : "memory");
-        if (it + 2 < total)
-          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol,
-                      warp - 1, NRW);
       }
       if (has_next) dots_push(it + 1);
       const long long r5 = timed_r ? clock64() : 0;
       cluster_arrive_release();
       if (timed_r) trw[4] += clock64() - r5;  // arrive.release
+      if constexpr (DEFER) {
+        // Block it+2 goes into the slot block it-1's axpy has just left (the
+        // named barrier of dots_push came after every row warp's axpy; the
+        // last block has no dots: its own barrier).  Issued between the
+        // cluster barrier's arrive and wait: the other CTAs do not wait for
+        // it, and the copy still has the rest of the iteration to land.
+        if (!has_next) asm volatile("bar.sync 1, %0;" ::"r"(CD_RT) : "memory");
+        if (it + 2 < total)
+          cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_2, row0, nrows, &fullb[(int)(it + 2) % NS], pol,
+                      warp - 1, NRW);
+      }
     }
     const long long tq2 = timed ? clock64() : 0;
     cluster_wait();
@@ -429,13 +439,21 @@ __global__ void __launch_bounds__(CD_NT, 1) k_cd(const CdArgs<T> a) {
     // a later pass comes from global memory only when rank 0 wrote it at
     // least two iterations ago (ordered by the cluster barriers since);
     // otherwise warp 0 has written it above
-    if (it + 2 < total && tid < CD_ST * CD_B && (tid >= CD_B || nblk >= 4 || pass_of(it + 2) == 0))
+    if (it + 2 < total && tid < CD_ST * CD_B && (tid >= CD_B || nblk >= 4 || pass_2 == 0))
       cst[((it + 2) % 3) * CD_ST * CD_B + tid] = tid >= 3 * CD_B ? cd_isq(pfv) : pfv;
     if (NS == 2 && it + 2 < total) {  // (compile-time NS)
       __syncthreads();  // block it's slot is free
       if (warp > 0)
-        cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_of(it + 2), row0, nrows, &fullb[(int)(it + 2) % NS], pol,
+        cd_prefetch(a, slot_a(it + 2), slot_g(it + 2), blk_2, row0, nrows, &fullb[(int)(it + 2) % NS], pol,
                     warp - 1, NRW);
+    }
+    if (++blk_c == nb32) {
+      blk_c = 0;
+      ++pass_c;
+    }
+    if (++blk_2 == nb32) {
+      blk_2 = 0;
+      ++pass_2;
     }
     __syncthreads();
     if (timed) {
