@@ -1282,12 +1282,15 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
     static unsigned long long* g_sm_dbg = nullptr;
     static bool g_sm_dbg_on = getenv("BX_SMALL_DEBUG") != nullptr;
     if (g_sm_dbg_on && !g_sm_dbg) {
-      CU(cudaMalloc(&g_sm_dbg, 8 * 8));
-      CU(cudaMemset(g_sm_dbg, 0, 8 * 8));
+      CU(cudaMalloc(&g_sm_dbg, 16 * 8));
+      CU(cudaMemset(g_sm_dbg, 0, 16 * 8));
       static unsigned long long* keep = g_sm_dbg;
       atexit([] {
-        unsigned long long h[8];
-        if (cudaMemcpy(h, keep, 64, cudaMemcpyDeviceToHost) == cudaSuccess && h[6])
+        unsigned long long h[16];
+        if (cudaMemcpy(h, keep, 128, cudaMemcpyDeviceToHost) == cudaSuccess && h[6])
+          fprintf(stderr, "k_round_small thread 0 per step (clk): residual to smem + barrier %.0f | column dot %.0f | update %.0f | fold + partial-row loop %.0f\n",
+                  (double)h[8] / h[6], (double)h[9] / h[6], (double)h[10] / h[6], (double)h[11] / h[6]);
+        if (h[6])
           fprintf(stderr,
                   "k_round_small per step (clk): dots+update %.0f | partial rows %.0f | barrier 1 %.0f | row reduce %.0f | "
                   "barrier 2 %.0f | residual load + fold %.0f | total %.0f over %llu steps\n",

@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   int done_rounds = 0, event = 0;
   const bool timed = a.dbg && b == 0 && tid == 0;
   long long tsm[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long tsx[4] = {0, 0, 0, 0};
   bool perr = false;
   if (b == 0 && tid == 0 && a.stamp0) *a.stamp0 = globaltimer();
   double excl_ns = 0.0;  // dual-point time of this launch (block 0's view; screening off)
@@ -273,10 +274,17 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
         for (int row = tid; row < m; row += SM_NT) rv[row] = __ldcg(&rcur[row]);
       }
       __syncthreads();
+      const long long td0 = timed ? clock64() : 0;
       for (int c = warp; c < ncol; c += NW) {
         const double gj = col_dot(c);
+        const long long td1 = timed ? clock64() : 0;
         if (lane == 0) update_col(c, gj);
+        if (timed) {
+          tsx[1] += td1 - td0;        // warp 0's column dot
+          tsx[2] += clock64() - td1;  // its update
+        }
       }
+      if (timed) tsx[0] += td0 - tp0;  // residual to shared memory + barrier
     } else {
       for (int c = warp; c < ncol; c += NW)
         if (lane == 0) update_col(c, cg[c]);
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
           }
         }
       }
+      if (timed) tsx[3] += clock64() - tp1;  // restart fold + the partial-row loop
       double* out = a.part + (int64_t)b * a.ldp;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
@@ -571,6 +580,8 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
   }  // rounds
   if (timed)
     for (int q = 0; q < 7; ++q) atomicAdd(a.dbg + q, (unsigned long long)tsm[q]);
+  if (timed)
+    for (int q = 0; q < 4; ++q) atomicAdd(a.dbg + 8 + q, (unsigned long long)tsx[q]);
   // write back the resident per-column state
   if (tid < ncol) {
     const int64_t p = p0 + tid;
