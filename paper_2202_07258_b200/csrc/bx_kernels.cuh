@@ -639,7 +639,10 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       // reach the padding of the partial row, which k_reduce never reads
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        if (c < cg) {
+        // a column whose coefficient is zero (most of an NNLS iterate sits on
+        // its bound) adds exactly nothing: skip its shared-memory reads and
+        // FMAs (CTA-uniform branch)
+        if (c < cg && cf[c] != 0.0) {
           const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       // reads
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        if (c < cg) {
+        if (c < cg && cf[c] != 0.0) {
           const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     } else if (AXPY) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        if (c < cg) {
+        if (c < cg && cf[c] != 0.0) {
           const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll
@@ -707,7 +710,17 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         }
       }
     }
-    __syncthreads();  // every thread is done with slot s
+    // every thread is done with slot s.  A fused step whose columns all got a
+    // zero coefficient read the slot only for the dots, which barrier 1
+    // already closed (cf / red reuse is ordered by the next column's
+    // barriers): no third barrier for those columns
+    bool slot_reread = true;
+    if constexpr (DOT && AXPY) {
+      slot_reread = false;
+#pragma unroll
+      for (int c = 0; c < C; ++c) slot_reread = slot_reread || (c < cg && cf[c] != 0.0);
+    }
+    if (slot_reread) __syncthreads();
     if (++s_run == S) {
       s_run = 0;
       ph_run ^= 1u;

@@ -293,13 +293,12 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     const long long tp1 = timed ? clock64() : 0;
     // restart partials of this CTA (fixed order: lane-strided, then one
     // butterfly in warp 0; lane 0 = thread 0 also publishes them below)
-    if (warp == 0) {
+    if (warp == 0 && a.kind == 2) {
       double s1 = 0.0, s2 = 0.0;
-      if (a.kind == 2)
-        for (int c = lane; c < ncol; c += 32) {
-          s1 += rsx[c];
-          s2 += rsx[SM_NT + c];
-        }
+      for (int c = lane; c < ncol; c += 32) {
+        s1 += rsx[c];
+        s2 += rsx[SM_NT + c];
+      }
       s1 = warp_sum<double>(s1);
       s2 = warp_sum<double>(s2);
       if (lane == 0) {
@@ -316,6 +315,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
         for (int e = 0; e < V; ++e) acc[i][e] = 0.0;
       for (int c = 0; c < ncol; ++c) {
         const double xc = cf[c];
+        if (xc == 0.0) continue;  // a coordinate on its zero bound adds exactly nothing (CTA-uniform)
         const T* col = cols + (size_t)c * a.colstride;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     }
     // thread 0 wrote sc4 itself (warp 0's fold); the grid barrier's entry
     // CTA barrier orders every thread's partial rows before the arrival
-    if (tid == 0) {
+    if (tid == 0 && a.kind == 2) {
       a.bpart[4 * b + 1] = sc4[0];
       a.bpart[4 * b + 2] = sc4[1];
     }
@@ -360,10 +360,10 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     }
     if (lane == 0) red[warp] = sq;
     __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int w = 0; w < NW; ++w) s += red[w];
-      a.bpart[4 * b + 0] = s;
+    // fold of the NW warp sums: one butterfly in warp 0 (fixed order)
+    if (warp == 0) {
+      const double s = warp_sum<double>(lane < NW ? red[lane] : 0.0);
+      if (lane == 0) a.bpart[4 * b + 0] = s;
     }
     const long long tp4 = timed ? clock64() : 0;
     grid_barrier(a.bar, nbar);
@@ -379,14 +379,18 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
     // every CTA folds the same values in the same order -> same decision
     if (warp == 0) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      for (int q = lane; q < G; q += 32) {
-        s0 += __ldcg(&a.bpart[4 * q + 0]);
-        s1 += __ldcg(&a.bpart[4 * q + 1]);
-        s2 += __ldcg(&a.bpart[4 * q + 2]);
+      if (a.kind == 2) {
+        for (int q = lane; q < G; q += 32) {
+          s0 += __ldcg(&a.bpart[4 * q + 0]);
+          s1 += __ldcg(&a.bpart[4 * q + 1]);
+          s2 += __ldcg(&a.bpart[4 * q + 2]);
+        }
+        s1 = warp_sum<double>(s1);
+        s2 = warp_sum<double>(s2);
+      } else {
+        for (int q = lane; q < G; q += 32) s0 += __ldcg(&a.bpart[4 * q + 0]);
       }
       s0 = warp_sum<double>(s0);
-      s1 = warp_sum<double>(s1);
-      s2 = warp_sum<double>(s2);
       if (lane == 0) {
         sc4[4] = s0;
         sc4[5] = s1;
