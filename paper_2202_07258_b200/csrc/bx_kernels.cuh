@@ -710,17 +710,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         }
       }
     }
-    // every thread is done with slot s.  A fused step whose columns all got a
-    // zero coefficient read the slot only for the dots, which barrier 1
-    // already closed (cf / red reuse is ordered by the next column's
-    // barriers): no third barrier for those columns
-    bool slot_reread = true;
-    if constexpr (DOT && AXPY) {
-      slot_reread = false;
-#pragma unroll
-      for (int c = 0; c < C; ++c) slot_reread = slot_reread || (c < cg && cf[c] != 0.0);
-    }
-    if (slot_reread) __syncthreads();
+    __syncthreads();  // every thread is done with slot s
     if (++s_run == S) {
       s_run = 0;
       ph_run ^= 1u;
