@@ -332,6 +332,7 @@ struct bx_ctx {
   void *xbak[2] = {}, *gbak[2] = {}, *rbak = nullptr;
   double* epart = nullptr;   // epsilon partials of the speculative step
   bool spec_on = true;       // env BX_SPEC=0 disables (a separate dot pass per round)
+  bool zskip_on = true;      // env BX_NO_ZSKIP: the axpy of zero coefficients is computed (exactness test)
   bool fuse_on = true;       // env BX_FUSE=0: PG / FISTA passes leave the reduce to k_reduce
   bool spec_pending = false; // the current x has taken the next round's first step
   bool dot_spec = false;     // dot_done's g / epsilon partials came from a speculative step
@@ -783,6 +784,7 @@ int run_pass(bx_ctx* c, const View<T>& vw, int upd, const double* vin, const dou
   a.pre = pre;
   a.gprev = ex.gprev;
   a.spec = ex.spec;
+  a.zskip = c->zskip_on ? 1 : 0;
   a.xbak = ex.xbak;
   a.gbak = ex.gbak;
   a.epart = ex.spec ? ex.epart : nullptr;
@@ -1277,6 +1279,7 @@ int small_rounds(bx_ctx* c, int kind, int passes, const SmallLoop& lp, int* ran,
   View<T> vw = act_view<T>(c);
   SmallArgs a;
   a.dbg = nullptr;
+  a.zskip = c->zskip_on ? 1 : 0;
   {
     // BX_SMALL_DEBUG=1: per-phase clock sums of a resident step (CTA 0), printed at exit
     static unsigned long long* g_sm_dbg = nullptr;
@@ -2735,6 +2738,7 @@ int bx_ctx_create(bx_ctx** out, int64_t m, int64_t n, int32_t dtype, const void*
   {
     const char* e = getenv("BX_SPEC");
     c->spec_on = !(e && e[0] == '0');
+    c->zskip_on = getenv("BX_NO_ZSKIP") == nullptr;
     const char* fz = getenv("BX_FUSE");
     c->fuse_on = !(fz && fz[0] == '0');
     const char* to = getenv("BX_PEER_TIMEOUT_S");

@@ -153,6 +153,7 @@ struct PassArgs {
   // the round's screening gradient -- g[p] = g_k, epsilon partial -> epart;
   // FISTA keeps x_{k-1} / g_{k-1} in xbak / gbak for an undo
   int spec;
+  int zskip;               // skip the axpy of zero coefficients (0 only with env BX_NO_ZSKIP: exactness test)
   double* xbak;
   double* gbak;
   double* epart;           // [gridDim.x] epsilon partial (block max)
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
         // a column whose coefficient is zero (most of an NNLS iterate sits on
         // its bound) adds exactly nothing: skip its shared-memory reads and
         // FMAs (CTA-uniform branch)
-        if (c < cg && cf[c] != 0.0) {
+        if (c < cg && (cf[c] != 0.0 || !a.zskip)) {
           const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
       // reads
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        if (c < cg && cf[c] != 0.0) {
+        if (c < cg && (cf[c] != 0.0 || !a.zskip)) {
           const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(NT, 1) k_pass(const PassArgs<T> a) {
     } else if (AXPY) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        if (c < cg && cf[c] != 0.0) {
+        if (c < cg && (cf[c] != 0.0 || !a.zskip)) {
           const AT cc = static_cast<AT>(cf[c]);
           const T* col = reinterpret_cast<const T*>(slot + c * a.colstride);
 #pragma unroll

@@ -73,6 +73,7 @@ struct SmallArgs {
   int screening;
   double slack_scale;
   double alpha;
+  int zskip;          // skip zero coefficients in the partial-row loop (0 only with env BX_NO_ZSKIP)
   unsigned long long* dbg;  // BX_SMALL_DEBUG: per-phase clock sums of CTA 0 (null otherwise)
 };
 
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(SM_NT, 1) k_round_small(const SmallArgs a) {
         for (int e = 0; e < V; ++e) acc[i][e] = 0.0;
       for (int c = 0; c < ncol; ++c) {
         const double xc = cf[c];
-        if (xc == 0.0) continue;  // a coordinate on its zero bound adds exactly nothing (CTA-uniform)
+        if (xc == 0.0 && a.zskip) continue;  // a coordinate on its zero bound adds exactly nothing (CTA-uniform)
         const T* col = cols + (size_t)c * a.colstride;
 #pragma unroll
         for (int i = 0; i < R; ++i) {

@@ -23,7 +23,7 @@ BX_NO_GRAPH=1 python scripts/ncu_target.py 3 100 > $O/plain3c.log 2>&1 && \
 python scripts/ncu_summary.py $O/r02_prof_cfg3_kpass_late.ncu-rep > $O/r02_cfg3_ncu_kpass_late.md 2>> $O/ncu_f3c.log
 # config 1: the small-round kernel
 python scripts/ncu_target.py 1 40 > $O/plain1.log 2>&1 && \
-  timeout 900 $N -k regex:k_round_small -s 2 -c 1 -f -o $O/r02_prof_cfg1_small python scripts/ncu_target.py 1 40 > $O/ncu_f1.log 2>&1
+  timeout 900 $N -k regex:k_round_small -c 1 -f -o $O/r02_prof_cfg1_small python scripts/ncu_target.py 1 40 > $O/ncu_f1.log 2>&1
 python scripts/ncu_summary.py $O/r02_prof_cfg1_small.ncu-rep > $O/r02_ncu_cfg1_small.md 2>> $O/ncu_f1.log
 rm -f $O/r02_prof_cfg1_small.ncu-rep
 ls -la $O/

@@ -240,3 +240,36 @@ def test_config3_screening_events_replayed_from_device_state():
             assert gt.newly_screened_lower == ot["new_lower"] and gt.newly_screened_upper == ot["new_upper"], e + i
             if ot.get("certified") is not None and ot["certified"] < 1e-6:
                 break
+
+
+@pytest.mark.parametrize("path", ["streamed", "small"])
+@pytest.mark.parametrize("kind,dtype", [("pg", np.float64), ("apg", np.float64), ("pg", np.float32)])
+def test_zero_coefficient_skip_is_exact(path, kind, dtype, monkeypatch):
+    """The fused step (and the small-round kernel's partial-row loop) skips the
+    axpy of a column whose new coefficient is zero.  a_j * 0 adds nothing to a
+    partial row, so the trajectory must not change by one bit: every trace
+    value, x and theta of a sparse NNLS solve are compared bitwise with the
+    skip switched off (BX_NO_ZSKIP, read when the context is created)."""
+    from paper_2202_07258_b200.generate import make_config
+    if path == "streamed":
+        monkeypatch.setenv("BX_NO_SMALL", "1")
+    if path == "small" and dtype == np.float32:
+        pytest.skip("the small-round kernel is exercised in fp64")
+    # config-3 recipe: 2% nonzeros, most of x on its bound; the small size is SM-resident
+    m, n = (1537, 3001) if path == "streamed" else (600, 1000)
+    inst = make_config(3, m=m, n=n, seed=5)
+    rounds = 40
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("BX_NO_ZSKIP", "1")
+        else:
+            monkeypatch.delenv("BX_NO_ZSKIP", raising=False)
+        out.append(_solve(inst.a.astype(dtype), inst.y, inst.lower, inst.upper, kind, 10, 1e-9, rounds, dtype=dtype))
+    on, ref = out
+    assert on.rounds == ref.rounds == rounds
+    assert np.count_nonzero(on.x) < on.x.size                # the skip had something to skip
+    for r_on, r_ref in zip(on.trace, ref.trace):
+        assert r_on.primal == r_ref.primal and r_on.dual == r_ref.dual and r_on.gap == r_ref.gap
+        assert r_on.preserved_count == r_ref.preserved_count
+    assert np.array_equal(on.x, ref.x) and np.array_equal(on.theta, ref.theta)
