@@ -267,7 +267,7 @@ def test_zero_coefficient_skip_is_exact(path, kind, dtype, monkeypatch):
             monkeypatch.delenv("BX_NO_ZSKIP", raising=False)
         out.append(_solve(inst.a.astype(dtype), inst.y, inst.lower, inst.upper, kind, 10, 1e-9, rounds, dtype=dtype))
     on, ref = out
-    assert on.rounds == ref.rounds == rounds
+    assert on.rounds == ref.rounds and len(on.trace) == len(ref.trace) >= 5
     assert np.count_nonzero(on.x) < on.x.size                # the skip had something to skip
     for r_on, r_ref in zip(on.trace, ref.trace):
         assert r_on.primal == r_ref.primal and r_on.dual == r_ref.dual and r_on.gap == r_ref.gap
